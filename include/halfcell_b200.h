@@ -1,0 +1,143 @@
+/*
+ * halfcell_b200 — C ABI of the B200-native full-order implicit step of the
+ * microstructure-resolved half-cell model (arXiv 1704.04139).
+ *
+ * Every entry point replaces one Python entry point of the reference package
+ * `halfcell` (reference tree `pkg/src/halfcell/...`, cited as file:line).  The
+ * ABI uses plain pointers and sizes only; device pointers are CUDA global
+ * memory (e.g. `torch.Tensor.data_ptr()`), `stream` is a `cudaStream_t`
+ * (NULL = legacy default stream).  All functions return HC_OK or an error code;
+ * `hc_last_error()` returns the message of the last failure on the calling
+ * thread.  Errors map 1:1 onto the reference exception classes
+ * (`src/halfcell/errors.py:1-37`).
+ *
+ * Packed state layout follows the reference exactly (`fvm/operator.py:3-7`,
+ * `fvm/dofmap.py:1-7`): x = [c-block (graphite + electrolyte voxels in flat
+ * order), phi-block (all non-grounded voxels in flat order)], fp64.
+ */
+#ifndef HALFCELL_B200_H
+#define HALFCELL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes (reference errors.py) ---- */
+#define HC_OK 0
+#define HC_ERR_CUDA 1          /* CUDA runtime failure / no device            */
+#define HC_ERR_MODEL 2         /* ModelError                                   */
+#define HC_ERR_NUMERICS 3      /* NumericsError (non-finite operator value)    */
+#define HC_ERR_NONCONVERGENCE 4/* NonConvergence (Newton / Krylov budget)      */
+#define HC_ERR_ARGUMENT 5      /* ValueError / ConfigError                     */
+#define HC_ERR_SIMULATION 6    /* SimulationError (time step underflow)        */
+#define HC_ERR_REDUCTION 7     /* ReductionError (POD)                         */
+
+#define HC_MAX_OCP 32
+
+/* MaterialParams (echem/params.py:50-113) + PhysConstants (params.py:26-29). */
+typedef struct hc_params {
+  double temperature, d_gr, sigma_gr, sigma_li, sigma_cc, sigma_pl, d_el, kappa_el,
+         t_plus, dlnf_dlnc, i00_grel, i00_ceel, i00_plel, c_gr_max,
+         n_const_thickness, c_li_metal, faraday, gas_constant;
+  int32_t n_ocp, pad_;
+  double ocp_soc[HC_MAX_OCP];
+  double ocp_v[HC_MAX_OCP];
+} hc_params;
+
+/* Sizes of an operator: Dofmap counts (dofmap.py:20-36) and face-list lengths
+ * of SystemOperator (operator.py:186-219). */
+typedef struct hc_info {
+  int64_t nx, ny, nz, n_vox;
+  int64_t n_c, n_p, n_plated, n_dirichlet;
+  int64_t n_bv, n_ce, n_strip, n_elel, n_drive_faces;
+  double h, face_area, voxel_volume, n_const, scale;
+} hc_info;
+
+/* SolverConfig (fvm/newton.py:20-51). */
+typedef struct hc_solver_config {
+  double newton_rtol, newton_atol;
+  int32_t newton_max_iter, krylov_max_iter;
+  double linear_rtol;
+  double dt_init, dt_min, dt_max, grow_factor, shrink_factor;
+  int32_t easy_iter_threshold, implicit_plated;
+} hc_solver_config;
+
+/* Result record of one Newton solve / accepted time step. */
+typedef struct hc_newton_stats {
+  int32_t n_iter, krylov_iters, retries, pad_;
+  double norm0, norm_final, tol, dt_used, dt_next, clamped_loss;
+} hc_newton_stats;
+
+typedef struct hc_operator hc_operator;
+
+const char* hc_last_error(void);
+int hc_device_count(int* out);
+
+/* build_dofmap (fvm/dofmap.py:71-101) + SystemOperator.__init__/_build
+ * (fvm/operator.py:109-242): uploads labels [z][y][x] (uint8, host), numbers
+ * the DOFs, classifies and compacts every voxel face on the device.  Raises the
+ * reference's ModelErrors (no graphite, no foil, no electrolyte path, no
+ * counter collector to ground, forbidden adjacency, kinetics on a grounded face). */
+int hc_operator_create(const uint8_t* labels_host, int32_t nx, int32_t ny, int32_t nz,
+                       double voxel_size_um, const hc_params* params, hc_operator** out);
+int hc_operator_destroy(hc_operator* op);
+int hc_operator_info(const hc_operator* op, hc_info* out);
+
+/* Export index arrays in the reference's layout into host int64 buffers.
+ * what: 0 c_dof[n_vox], 1 p_dof[n_vox], 2 plated_voxels[n_plated], 3 dirichlet[n_dirichlet],
+ *       4 bv (4 x n_bv: xc_gr, xc_el, xp_gr, xp_el), 5 ce (3 x n_ce: xp_fo, xc_el, xp_el),
+ *       6 strip (4 x n_strip: xp_pl, xc_el, xp_el, slot), 7 elel (4 x n_elel: xc_i, xc_j, xp_i, xp_j)
+ * (operator.py:188-219 attribute names). */
+int hc_operator_export(const hc_operator* op, int32_t what, int64_t* host_out);
+
+/* SystemOperator.apply and its parts (operator.py:331-389).  part:
+ * 0 apply (full), 1 apply_bv, 2 apply_one_over_c, 3 apply_lin, 4 apply_const, 5 apply_bnd.
+ * x, n_pl, out: device fp64, packed layout. */
+int hc_apply(hc_operator* op, int32_t part, const double* x, const double* n_pl, double mu,
+             double beta, double* out, void* stream);
+
+/* Matrix-free Jacobian-vector product (jacobian(x) + diag(inv_dt on c rows)) @ v,
+ * i.e. the matrix newton.py:126 factorizes, applied to v (operator.py:458-471). */
+int hc_jvp(hc_operator* op, const double* x, const double* n_pl, double beta, double inv_dt,
+           const double* v, double* out, void* stream);
+
+/* Sparse Jacobian pattern (operator.py:458-471, CSR after duplicate summation)
+ * for sparsity parity: fills *nnz when row_ptr == NULL, else row_ptr[n_total+1],
+ * col_idx[nnz] (host int64) and optionally values (host fp64, at state x/n_pl/beta). */
+int hc_jacobian_csr(hc_operator* op, const double* x, const double* n_pl, double beta,
+                    int64_t* nnz, int64_t* row_ptr, int64_t* col_idx, double* values);
+
+/* newton_solve (fvm/newton.py:86-168): solves m (x - x_prev)/dt + A(x; mu) = 0
+ * from x_guess; x_out receives the converged packed state (device). */
+int hc_newton_solve(hc_operator* op, const double* x_guess, double dt, const double* x_prev,
+                    const double* n_pl, double mu, const hc_solver_config* cfg, double* x_out,
+                    hc_newton_stats* stats, void* stream);
+
+/* solve_initial_potential (fvm/newton.py:171-206): phi block at frozen c. */
+int hc_solve_initial_potential(hc_operator* op, const double* x0, const double* n_pl, double mu,
+                               const hc_solver_config* cfg, double* x_out, hc_newton_stats* stats,
+                               void* stream);
+
+/* step (fvm/timestepping.py:270-312): one accepted implicit-Euler step with
+ * retry-on-failure, explicit plated-inventory update.  x and n_pl are updated
+ * in place (device); stats carries dt_used / dt_next / retries / clamped loss. */
+int hc_step(hc_operator* op, double* x, double* n_pl, double t, double dt_suggest, double mu,
+            const hc_solver_config* cfg, hc_newton_stats* stats, void* stream);
+
+/* Same step with HOST state buffers: copies in, steps on the device, copies out
+ * (the reference-facing end-to-end call used by bench.py's e2e leg). */
+int hc_step_host(hc_operator* op, double* x_host, double* n_pl_host, double t, double dt_suggest,
+                 double mu, const hc_solver_config* cfg, hc_newton_stats* stats);
+
+/* POD snapshot Gram G = S^T diag(w) S for S (n_dof x n_snap, column-major,
+ * device fp64) — the method-of-snapshots correlation matrix (SPEC mor.pod);
+ * G is n_snap x n_snap column-major on the device.  w may be NULL (identity). */
+int hc_pod_gram(const double* S, const double* w, int64_t n_dof, int64_t n_snap, double* G,
+                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HALFCELL_B200_H */

@@ -1,0 +1,446 @@
+// extern "C" entry points of libhalfcell_b200 (include/halfcell_b200.h).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "hc_amg.cuh"
+#include "hc_solver.cuh"
+
+namespace hc {
+Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
+                          const hc_params& hp);
+void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
+              cudaStream_t s);
+
+Operator::~Operator() {
+  delete amg;
+  delete work;
+}
+}  // namespace hc
+
+using namespace hc;
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return HC_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HC_ERR_CUDA;
+  }
+}
+
+static cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+namespace {
+__global__ void k_first_nonfinite(long long n, const double* __restrict__ a,
+                                  unsigned long long* __restrict__ first) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n && !isfinite(a[i])) atomicMin(first, (unsigned long long)i);
+}
+}  // namespace
+
+extern "C" {
+
+const char* hc_last_error(void) { return g_err.c_str(); }
+
+int hc_device_count(int* out) {
+  return guarded([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    *out = n;
+  });
+}
+
+int hc_operator_create(const uint8_t* labels_host, int32_t nx, int32_t ny, int32_t nz,
+                       double voxel_size_um, const hc_params* params, hc_operator** out) {
+  return guarded([&] {
+    if (!labels_host || !params || !out) throw Error(HC_ERR_ARGUMENT, "null argument");
+    *out = (hc_operator*)create_operator(labels_host, nx, ny, nz, voxel_size_um, *params);
+  });
+}
+
+int hc_operator_destroy(hc_operator* op) {
+  return guarded([&] { delete (Operator*)op; });
+}
+
+int hc_operator_info(const hc_operator* op, hc_info* out) {
+  return guarded([&] { *out = ((const Operator*)op)->info; });
+}
+
+int hc_operator_export(const hc_operator* opq, int32_t what, int64_t* out) {
+  return guarded([&] {
+    const Operator& op = *(const Operator*)opq;
+    const long long nvox = op.P.nvox, nc = op.info.n_c;
+    auto get = [](const DBuf<int32_t>& b, long long n) {
+      std::vector<int32_t> h(n);
+      if (n) HC_CUDA(cudaMemcpy(h.data(), b.p, n * 4, cudaMemcpyDeviceToHost));
+      return h;
+    };
+    if (what == 0 || what == 1) {
+      auto h = get(what == 0 ? op.cdof : op.pdof, nvox);
+      for (long long i = 0; i < nvox; ++i) out[i] = h[i];
+      return;
+    }
+    if (what == 2) {
+      auto h = get(op.plated_vox, op.info.n_plated);
+      for (size_t i = 0; i < h.size(); ++i) out[i] = h[i];
+      return;
+    }
+    auto cd = get(op.cdof, nvox), pd = get(op.pdof, nvox);
+    if (what == 3) {
+      long long k = 0;
+      for (long long i = 0; i < nvox; ++i)
+        if (pd[i] < 0) out[k++] = i;
+      return;
+    }
+    if (what >= 4 && what <= 6) {
+      long long off = what == 4 ? 0 : (what == 5 ? op.info.n_bv : op.info.n_bv + op.info.n_ce);
+      long long n = what == 4 ? op.info.n_bv : (what == 5 ? op.info.n_ce : op.info.n_strip);
+      std::vector<int32_t> so(n), el(n), slot(n);
+      if (n) {
+        HC_CUDA(cudaMemcpy(so.data(), op.if_solid.p + off, n * 4, cudaMemcpyDeviceToHost));
+        HC_CUDA(cudaMemcpy(el.data(), op.if_el.p + off, n * 4, cudaMemcpyDeviceToHost));
+        HC_CUDA(cudaMemcpy(slot.data(), op.if_slot.p + off, n * 4, cudaMemcpyDeviceToHost));
+      }
+      for (long long i = 0; i < n; ++i) {
+        if (what == 4) {  // xc_gr, xc_el, xp_gr, xp_el
+          out[i] = cd[so[i]];
+          out[n + i] = cd[el[i]];
+          out[2 * n + i] = nc + pd[so[i]];
+          out[3 * n + i] = nc + pd[el[i]];
+        } else if (what == 5) {  // xp_fo, xc_el, xp_el
+          out[i] = nc + pd[so[i]];
+          out[n + i] = cd[el[i]];
+          out[2 * n + i] = nc + pd[el[i]];
+        } else {  // xp_pl, xc_el, xp_el, slot
+          out[i] = nc + pd[so[i]];
+          out[n + i] = cd[el[i]];
+          out[2 * n + i] = nc + pd[el[i]];
+          out[3 * n + i] = slot[i];
+        }
+      }
+      return;
+    }
+    if (what == 7) {
+      long long n = op.info.n_elel;
+      auto lo = get(op.elel_lo, n), hi = get(op.elel_hi, n);
+      for (long long i = 0; i < n; ++i) {
+        out[i] = cd[lo[i]];
+        out[n + i] = cd[hi[i]];
+        out[2 * n + i] = nc + pd[lo[i]];
+        out[3 * n + i] = nc + pd[hi[i]];
+      }
+      return;
+    }
+    throw Error(HC_ERR_ARGUMENT, "unknown export selector");
+  });
+}
+
+int hc_apply(hc_operator* opq, int32_t part, const double* x, const double* n_pl, double mu,
+             double beta, double* out, void* stream) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    cudaStream_t s = S(stream);
+    const long long ntot = op.info.n_c + op.info.n_p;
+    int parts = 0;
+    switch (part) {
+      case 0: parts = PART_LIN | PART_BV | PART_1C | PART_BND; break;
+      case 1: parts = PART_BV; break;
+      case 2: parts = PART_1C; break;
+      case 3: parts = PART_LIN; break;
+      case 4: parts = 0; break;
+      case 5: parts = PART_BND; mu = 1.0; break;
+      default: throw Error(HC_ERR_ARGUMENT, "unknown operator part");
+    }
+    scatter_packed(op, x, op.xg.p, true, s);
+    residual_grid(op, op.xg.p, n_pl, mu, beta, parts, nullptr, 0.0, op.outg.p, s);
+    gather_packed(op, op.outg.p, out, s);
+    if (part == 0 && ntot) {
+      DBuf<unsigned long long> first(1);
+      HC_CUDA(cudaMemsetAsync(first.p, 0xff, sizeof(unsigned long long), s));
+      k_first_nonfinite<<<(int)((ntot + 255) / 256), 256, 0, s>>>(ntot, out, first.p);
+      HC_CHECK_LAUNCH();
+      unsigned long long f = 0;
+      HC_CUDA(cudaMemcpyAsync(&f, first.p, sizeof(f), cudaMemcpyDeviceToHost, s));
+      HC_CUDA(cudaStreamSynchronize(s));
+      if (f != ~0ULL) {
+        int32_t vox = 0;
+        const DBuf<int32_t>& m = (long long)f < op.info.n_c ? op.c_vox : op.p_vox;
+        long long k = (long long)f < op.info.n_c ? (long long)f : (long long)f - op.info.n_c;
+        HC_CUDA(cudaMemcpy(&vox, m.p + k, 4, cudaMemcpyDeviceToHost));
+        long long z = vox / op.P.nxy, rem = vox % op.P.nxy, y = rem / op.P.nx, xx = rem % op.P.nx;
+        char msg[128];
+        snprintf(msg, sizeof msg, "operator produced a non-finite value at voxel (%lld, %lld, %lld)",
+                 xx, y, z);
+        throw Error(HC_ERR_NUMERICS, msg);
+      }
+    }
+  });
+}
+
+int hc_jvp(hc_operator* opq, const double* x, const double* n_pl, double beta, double inv_dt,
+           const double* v, double* out, void* stream) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    cudaStream_t s = S(stream);
+    scatter_packed(op, x, op.xg.p, true, s);
+    linearize(op, op.xg.p, n_pl, beta, s);
+    scatter_packed(op, v, op.vg.p, false, s);
+    jvp_grid(op, op.vg.p, inv_dt, 1 | 4, op.outg.p, s);
+    gather_packed(op, op.outg.p, out, s);
+  });
+}
+
+// Host assembly of the analytic Jacobian in the reference's CSR convention:
+// duplicates summed, exact zeros of the sum dropped (scipy csr + csr).
+int hc_jacobian_csr(hc_operator* opq, const double* x, const double* n_pl, double beta,
+                    int64_t* nnz_out, int64_t* row_ptr, int64_t* col_idx, double* values) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    const DevParams& P = op.P;
+    const long long nvox = P.nvox, nc = op.info.n_c, n = op.info.n_c + op.info.n_p;
+    scatter_packed(op, x, op.xg.p, true, 0);
+    linearize(op, op.xg.p, n_pl, beta, 0);
+    HC_CUDA(cudaDeviceSynchronize());
+    std::vector<uint8_t> lab(nvox);
+    std::vector<int32_t> cd(nvox), pd(nvox), so(op.n_if), el(op.n_if);
+    std::vector<int8_t> kd(op.n_if);
+    std::vector<double> coef(3 * op.n_if), w(nvox);
+    HC_CUDA(cudaMemcpy(lab.data(), op.labels.p, nvox, cudaMemcpyDeviceToHost));
+    HC_CUDA(cudaMemcpy(cd.data(), op.cdof.p, nvox * 4, cudaMemcpyDeviceToHost));
+    HC_CUDA(cudaMemcpy(pd.data(), op.pdof.p, nvox * 4, cudaMemcpyDeviceToHost));
+    HC_CUDA(cudaMemcpy(w.data(), op.inv_c.p, nvox * 8, cudaMemcpyDeviceToHost));
+    if (op.n_if) {
+      HC_CUDA(cudaMemcpy(so.data(), op.if_solid.p, op.n_if * 4, cudaMemcpyDeviceToHost));
+      HC_CUDA(cudaMemcpy(el.data(), op.if_el.p, op.n_if * 4, cudaMemcpyDeviceToHost));
+      HC_CUDA(cudaMemcpy(kd.data(), op.if_kind.p, op.n_if, cudaMemcpyDeviceToHost));
+      HC_CUDA(cudaMemcpy(coef.data(), op.if_coef.p, 3 * op.n_if * 8, cudaMemcpyDeviceToHost));
+    }
+    std::vector<std::map<int64_t, double>> rows(n);
+    auto add = [&](long long r, long long c, double v) { rows[r][c] += v; };
+    auto xc = [&](long long v) { return (long long)cd[v]; };
+    auto xp = [&](long long v) { return nc + pd[v]; };
+    const double gF2 = P.gF2, gM = P.t_plus * P.kappa * gF2;
+    auto gnd = [&](long long v) { return pd[v] < 0; };
+    long long nx = P.nx, ny = P.ny, nz = P.nz;
+    for (int axis = 0; axis < 3; ++axis) {
+      for (long long z = 0; z < nz; ++z)
+        for (long long y = 0; y < ny; ++y)
+          for (long long xx = 0; xx < nx; ++xx) {
+            if ((axis == 0 && z + 1 >= nz) || (axis == 1 && y + 1 >= ny) || (axis == 2 && xx + 1 >= nx))
+              continue;
+            long long lo = (z * ny + y) * nx + xx;
+            long long hi = lo + (axis == 0 ? nx * ny : (axis == 1 ? nx : 1));
+            uint8_t a = lab[lo], b = lab[hi];
+            uint8_t k = kind_of(a, b);
+            bool gl = gnd(lo), gh = gnd(hi);
+            if (gl && gh) continue;
+            if (gl || gh) {
+              if (k == K_CONT || k == K_CONTACT) {
+                long long live = gl ? hi : lo;
+                add(xp(live), xp(live), 2.0 * P.sig[a] * P.sig[b] / (P.sig[a] + P.sig[b]) * gF2);
+              }
+              continue;
+            }
+            auto sym = [&](long long i, long long j, double g) {
+              add(i, i, g); add(i, j, -g); add(j, j, g); add(j, i, -g);
+            };
+            if (k == K_CONT) {
+              if (a == GR) {
+                sym(xc(lo), xc(hi), P.d_gr * P.inv_h2);
+                sym(xp(lo), xp(hi), P.sigma_gr * gF2);
+              } else if (a == EL) {
+                sym(xc(lo), xc(hi), P.d_el * P.inv_h2);
+                sym(xp(lo), xp(hi), P.kappa * gF2);
+                add(xc(lo), xp(lo), gM); add(xc(lo), xp(hi), -gM);
+                add(xc(hi), xp(hi), gM); add(xc(hi), xp(lo), -gM);
+              } else {
+                sym(xp(lo), xp(hi), P.sig[a] * gF2);
+              }
+            } else if (k == K_CONTACT) {
+              sym(xp(lo), xp(hi), 2.0 * P.sig[a] * P.sig[b] / (P.sig[a] + P.sig[b]) * gF2);
+            }
+          }
+    }
+    // A_lin done: snapshot as its own summed matrix, then add the nonlinear part
+    std::vector<std::map<int64_t, double>> nl(n);
+    auto addn = [&](long long r, long long c, double v) { nl[r][c] += v; };
+    for (long long f = 0; f < op.n_if; ++f) {
+      long long s_ = so[f], e = el[f];
+      double ca = coef[f], cb = coef[op.n_if + f], cg = coef[2 * op.n_if + f];
+      if (kd[f] == IF_BV) {
+        const long long rs[4] = {xc(s_), xp(s_), xc(e), xp(e)};
+        const double sg[4] = {1, 1, -1, -1};
+        for (int q = 0; q < 4; ++q) {
+          addn(rs[q], xc(s_), sg[q] * ca);
+          addn(rs[q], xc(e), sg[q] * cb);
+          addn(rs[q], xp(s_), sg[q] * cg);
+          addn(rs[q], xp(e), -sg[q] * cg);
+        }
+      } else if (kd[f] == IF_CE) {
+        const long long rs[3] = {xp(s_), xc(e), xp(e)};
+        const double sg[3] = {1, -1, -1};
+        for (int q = 0; q < 3; ++q) {
+          addn(rs[q], xp(s_), sg[q] * cg);
+          addn(rs[q], xp(e), -sg[q] * cg);
+        }
+      } else {
+        const long long rs[3] = {xp(s_), xc(e), xp(e)};
+        const double sg[3] = {1, -1, -1};
+        for (int q = 0; q < 3; ++q) {
+          addn(rs[q], xc(e), sg[q] * cb);
+          addn(rs[q], xp(s_), sg[q] * cg);
+          addn(rs[q], xp(e), -sg[q] * cg);
+        }
+      }
+    }
+    {
+      std::vector<int32_t> lo(op.info.n_elel), hi(op.info.n_elel);
+      if (op.info.n_elel) {
+        HC_CUDA(cudaMemcpy(lo.data(), op.elel_lo.p, lo.size() * 4, cudaMemcpyDeviceToHost));
+        HC_CUDA(cudaMemcpy(hi.data(), op.elel_hi.p, hi.size() * 4, cudaMemcpyDeviceToHost));
+      }
+      for (size_t f = 0; f < lo.size(); ++f) {
+        long long i = lo[f], j = hi[f];
+        double dqi = -w[i], dqj = w[j];   // -gX/c_i, gX/c_j
+        const long long rs[4] = {xp(i), xp(j), xc(i), xc(j)};
+        const double sg[4] = {-1.0, 1.0, -P.t_plus, P.t_plus};
+        for (int q = 0; q < 4; ++q) {
+          addn(rs[q], xc(i), sg[q] * dqi);
+          addn(rs[q], xc(j), sg[q] * dqj);
+        }
+      }
+    }
+    long long nnz = 0;
+    for (long long r = 0; r < n; ++r) {
+      for (auto& kv : nl[r]) rows[r][kv.first] += kv.second;
+      for (auto it = rows[r].begin(); it != rows[r].end();) {
+        if (it->second == 0.0) it = rows[r].erase(it); else ++it;
+      }
+      nnz += (long long)rows[r].size();
+    }
+    *nnz_out = nnz;
+    if (!row_ptr) return;
+    long long k = 0;
+    row_ptr[0] = 0;
+    for (long long r = 0; r < n; ++r) {
+      for (auto& kv : rows[r]) {
+        col_idx[k] = kv.first;
+        if (values) values[k] = kv.second;
+        ++k;
+      }
+      row_ptr[r + 1] = k;
+    }
+  });
+}
+
+static void load_prev(Operator& op, const double* x_prev, cudaStream_t s);
+
+int hc_newton_solve(hc_operator* opq, const double* x_guess, double dt, const double* x_prev,
+                    const double* n_pl, double mu, const hc_solver_config* cfg, double* x_out,
+                    hc_newton_stats* stats, void* stream) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    cudaStream_t s = S(stream);
+    Work& W = work(op);
+    hc_newton_stats st{};
+    load_prev(op, x_prev, s);
+    scatter_packed(op, x_guess, W.x.p, true, s);
+    newton_grid(op, n_pl, dt, mu, *cfg, st, s);
+    gather_packed(op, W.x.p, x_out, s);
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (stats) *stats = st;
+  });
+}
+
+int hc_solve_initial_potential(hc_operator* opq, const double* x0, const double* n_pl, double mu,
+                               const hc_solver_config* cfg, double* x_out, hc_newton_stats* stats,
+                               void* stream) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    cudaStream_t s = S(stream);
+    Work& W = work(op);
+    hc_newton_stats st{};
+    scatter_packed(op, x0, W.x.p, true, s);
+    initial_potential_grid(op, n_pl, mu, *cfg, st, s);
+    gather_packed(op, W.x.p, x_out, s);
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (stats) *stats = st;
+  });
+}
+
+int hc_step(hc_operator* opq, double* x, double* n_pl, double t, double dt_suggest, double mu,
+            const hc_solver_config* cfg, hc_newton_stats* stats, void* stream) {
+  (void)t;
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    cudaStream_t s = S(stream);
+    Work& W = work(op);
+    hc_newton_stats st{};
+    scatter_packed(op, x, W.x.p, true, s);
+    step_grid(op, n_pl, dt_suggest, mu, *cfg, st, s);
+    gather_packed(op, W.x.p, x, s);
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (stats) *stats = st;
+  });
+}
+
+int hc_step_host(hc_operator* opq, double* x_host, double* n_pl_host, double t, double dt_suggest,
+                 double mu, const hc_solver_config* cfg, hc_newton_stats* stats) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    const long long ntot = op.info.n_c + op.info.n_p, npl = op.info.n_plated;
+    if (op.host_x.n < (size_t)ntot) op.host_x.alloc(std::max<long long>(ntot, 1));
+    if (op.host_npl.n < (size_t)std::max<long long>(npl, 1)) op.host_npl.alloc(std::max<long long>(npl, 1));
+    cudaStream_t s = 0;
+    HC_CUDA(cudaMemcpyAsync(op.host_x.p, x_host, ntot * 8, cudaMemcpyHostToDevice, s));
+    if (npl) HC_CUDA(cudaMemcpyAsync(op.host_npl.p, n_pl_host, npl * 8, cudaMemcpyHostToDevice, s));
+    Work& W = work(op);
+    hc_newton_stats st{};
+    scatter_packed(op, op.host_x.p, W.x.p, true, s);
+    step_grid(op, op.host_npl.p, dt_suggest, mu, *cfg, st, s);
+    gather_packed(op, W.x.p, op.host_x.p, s);
+    HC_CUDA(cudaMemcpyAsync(x_host, op.host_x.p, ntot * 8, cudaMemcpyDeviceToHost, s));
+    if (npl) HC_CUDA(cudaMemcpyAsync(n_pl_host, op.host_npl.p, npl * 8, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (stats) *stats = st;
+    (void)t;
+  });
+}
+
+int hc_pod_gram(const double* Sm, const double* w, int64_t n_dof, int64_t n_snap, double* G,
+                void* stream) {
+  return guarded([&] {
+    if (n_dof < 0 || n_snap < 0) throw Error(HC_ERR_ARGUMENT, "negative size");
+    pod_gram(Sm, w, n_dof, n_snap, G, S(stream));
+  });
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void k_extract_c2(long long n, const double2* __restrict__ x, double* __restrict__ c) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) c[i] = x[i].x;
+}
+}  // namespace
+
+static void load_prev(Operator& op, const double* x_prev, cudaStream_t s) {
+  Work& W = work(op);
+  scatter_packed(op, x_prev, op.xg2.p, true, s);
+  long long n = op.P.nvox;
+  k_extract_c2<<<(int)((n + 255) / 256), 256, 0, s>>>(n, op.xg2.p, W.cprev.p);
+  HC_CHECK_LAUNCH();
+}

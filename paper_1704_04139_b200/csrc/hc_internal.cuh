@@ -1,0 +1,241 @@
+// Internal definitions shared by the halfcell_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/halfcell_b200.h"
+
+namespace hc {
+
+// ---- phases (reference microgen/phases.py:18-26) --------------------------------
+enum : uint8_t { EL = 0, GR = 1, PL = 2, FOIL = 3, CW = 4, CC = 5, N_PHASES = 6 };
+
+// ---- interface kinds (reference echem/interfaces.py:23-61, operator.py:39-52) ---
+enum : uint8_t { K_CONT = 0, K_BV = 1, K_CE = 2, K_STRIP = 3, K_BLOCK = 4, K_CONTACT = 5, K_FORBID = 6 };
+
+__host__ __device__ inline uint8_t kind_of(uint8_t a, uint8_t b) {
+  if (a == b) return K_CONT;
+  uint8_t lo = a < b ? a : b, hi = a < b ? b : a;
+  // lo < hi
+  if (lo == EL) {
+    if (hi == GR) return K_BV;
+    if (hi == FOIL) return K_CE;
+    if (hi == PL) return K_STRIP;
+    return K_BLOCK;  // CW, CC
+  }
+  if (hi == FOIL && (lo == GR || lo == PL)) return K_FORBID;
+  return K_CONTACT;
+}
+
+// ---- exceptions carried to the C ABI -------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define HC_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::hc::Error(HC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+#define HC_CHECK_LAUNCH() HC_CUDA(cudaGetLastError())
+
+// ---- device-side parameter block (passed by value to kernels) -------------------
+struct DevParams {
+  int nx, ny, nz;
+  long long nxy, nvox;
+  double h;            // m
+  double gF2;          // 1 / (F h^2)
+  double sc;           // 1 / (F h)
+  double inv_h2;       // 1 / h^2
+  double d_gr, d_el, t_plus, kappa, sigma_gr;
+  double sig[N_PHASES];
+  double gX;           // chemical-potential face coefficient (operator.py:225-226)
+  double vt;           // 2RT/F
+  double i00_grel, i00_ceel, i00_plel, c_gr_max, n_const;
+  double drive;        // -1/(F h): b_bnd entry (operator.py:231-233)
+  int n_ocp;
+  double ocp_soc[HC_MAX_OCP];
+  double ocp_v[HC_MAX_OCP];
+};
+
+// np.interp on the OCP table (echem/kinetics.py:25-32), clamped at the ends.
+__device__ __host__ inline double ocp_dev(double c, const DevParams& P) {
+  double s = c / P.c_gr_max;
+  int n = P.n_ocp;
+  if (!(s >= P.ocp_soc[0])) return (s != s) ? s : P.ocp_v[0];
+  if (s >= P.ocp_soc[n - 1]) return P.ocp_v[n - 1];
+  int j = 0;
+  while (j + 1 < n - 1 && P.ocp_soc[j + 1] <= s) ++j;
+  double slope = (P.ocp_v[j + 1] - P.ocp_v[j]) / (P.ocp_soc[j + 1] - P.ocp_soc[j]);
+  return slope * (s - P.ocp_soc[j]) + P.ocp_v[j];
+}
+
+// d OCP / d c (echem/kinetics.py:35-42): segment by searchsorted(side=right)-1,
+// clipped; zero outside the table range.
+__device__ __host__ inline double ocp_slope_dev(double c, const DevParams& P) {
+  double s = c / P.c_gr_max;
+  int n = P.n_ocp;
+  if (s < P.ocp_soc[0] || s > P.ocp_soc[n - 1]) return 0.0;
+  int k = 0;  // number of knots <= s
+  while (k < n && P.ocp_soc[k] <= s) ++k;
+  int seg = k - 1;
+  if (seg < 0) seg = 0;
+  if (seg > n - 2) seg = n - 2;
+  return (P.ocp_v[seg + 1] - P.ocp_v[seg]) / (P.ocp_soc[seg + 1] - P.ocp_soc[seg]) / P.c_gr_max;
+}
+
+// f_pre and its derivative (echem/kinetics.py:71-87).
+__device__ __host__ inline double f_pre_dev(double n, double nc) {
+  double n4 = (n * n) * (n * n);
+  double nc4 = (nc * nc) * (nc * nc);
+  return n4 / (nc4 + n4);
+}
+__device__ __host__ inline double f_pre_deriv_dev(double n, double nc) {
+  double nc4 = (nc * nc) * (nc * nc);
+  double d = nc4 + (n * n) * (n * n);
+  return 4.0 * (n * n * n) * nc4 / (d * d);
+}
+
+// Stripping current with the implicit-inventory regularization
+// (operator.py:271-320).  Returns i; optionally the two Jacobian entries.
+__device__ __host__ inline double strip_current_dev(double c_el, double phi_pl, double phi_el,
+                                                    double n_face, double beta, const DevParams& P,
+                                                    double* di_dce, double* di_dpp) {
+  double vt = P.vt;
+  double arg = (phi_pl - phi_el) / vt;
+  double ex = exp(arg), emx = exp(-arg);
+  double E = P.i00_plel * sqrt(c_el);
+  if (beta == 0.0) {
+    double fp = f_pre_dev(n_face, P.n_const);
+    double i = E * (fp * ex - emx);
+    if (di_dce) {
+      *di_dce = 0.5 * i / c_el;
+      *di_dpp = E * (fp * ex + emx) / vt;
+    }
+    return i;
+  }
+  double lo = -E * emx, hi = E * (ex - emx);
+  double fp0 = f_pre_dev(n_face, P.n_const);
+  double i = fmin(fmax(E * (fp0 * ex - emx), lo), hi);
+  for (int it = 0; it < 60; ++it) {
+    double n_end = fmax(n_face - beta * i, 0.0);
+    double f = f_pre_dev(n_end, P.n_const);
+    double fd = n_end > 0.0 ? f_pre_deriv_dev(n_end, P.n_const) : 0.0;
+    double g = i - E * (f * ex - emx);
+    double gi = 1.0 + E * ex * fd * beta;
+    double i_new = fmin(fmax(i - g / gi, lo), hi);
+    bool done = fabs(i_new - i) <= 1e-14 * (1.0 + fabs(i_new));
+    i = i_new;
+    if (done) break;
+  }
+  if (di_dce) {
+    double n_end = fmax(n_face - beta * i, 0.0);
+    double f = f_pre_dev(n_end, P.n_const);
+    double fd = n_end > 0.0 ? f_pre_deriv_dev(n_end, P.n_const) : 0.0;
+    double gi = 1.0 + E * ex * fd * beta;
+    *di_dce = (0.5 / c_el) * E * (f * ex - emx) / gi;
+    *di_dpp = E * (f * ex + emx) / vt / gi;
+  }
+  return i;
+}
+
+// Interface face record kinds in the compacted list.
+enum : int8_t { IF_BV = 0, IF_CE = 1, IF_STRIP = 2 };
+
+// Device buffer RAII.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) HC_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+};
+
+struct Amg;   // hc_amg.cu
+struct Work;  // hc_solver.cu
+
+// The device-resident operator: geometry, DOF numbering, compacted face lists
+// and the work space of the implicit step.
+struct Operator {
+  DevParams P;
+  hc_params host_params;
+  hc_info info;
+  int n_sm = 148;
+
+  DBuf<uint8_t> labels;        // [nvox]
+  DBuf<int32_t> cdof, pdof;    // [nvox], -1 where absent
+  DBuf<int32_t> c_vox, p_vox;  // packed index -> voxel
+  DBuf<int32_t> plated_vox;    // [n_plated] ascending
+  // interface faces, reference order within each family; unified SoA list
+  // (bv first, then ce, then strip) for the kernels
+  DBuf<int32_t> if_solid, if_el, if_slot;  // slot: plated slot for strip, -1 else
+  DBuf<int8_t> if_kind;
+  int64_t n_if = 0;
+  DBuf<int32_t> elel_lo, elel_hi;          // only materialised for export
+  DBuf<int32_t> if_rank;                   // [nvox] rank among interface voxels or -1
+  DBuf<int32_t> if_dir;                    // [6 * n_if_vox] face id per direction or -1
+
+  // grid-layout work space (double2 = (c, phi) per voxel)
+  DBuf<double2> xg, xg2, vg, outg;
+  DBuf<double> cprev;          // c_prev * inv_dt per voxel (time term)
+  DBuf<double> npl;            // plated inventory per slot
+  DBuf<double> if_coef;        // 3 x n_if Jacobian coefficients (linearized)
+  DBuf<double> inv_c;          // gX / c per electrolyte voxel (linearized)
+  DBuf<double> red;            // reduction scratch
+  DBuf<double> host_x, host_npl;  // staging for the host-buffer entry point
+  Amg* amg = nullptr;
+  Work* work = nullptr;
+  // optional callback after every accepted Newton iterate (grid layout)
+  void (*iterate_hook)(Operator&, const double2*) = nullptr;
+  void* hook_ctx = nullptr;
+
+  ~Operator();
+};
+
+// kernels / helpers implemented in hc_operator.cu
+void scatter_packed(const Operator& op, const double* x, double2* xg, bool c_fill_one,
+                    cudaStream_t s);
+void gather_packed(const Operator& op, const double2* xg, double* x, cudaStream_t s);
+// residual in grid layout: parts bitmask
+enum : int { PART_LIN = 1, PART_BV = 2, PART_1C = 4, PART_BND = 8, PART_TIME = 16 };
+void residual_grid(Operator& op, const double2* xg, const double* npl, double mu, double beta,
+                   int parts, const double* cprev_scaled, double inv_dt, double2* out,
+                   cudaStream_t s);
+void linearize(Operator& op, const double2* xg, const double* npl, double beta, cudaStream_t s);
+// J v with the linearization stored in op.  flags: 1 add mass (inv_dt on c rows),
+// 2 row transform T (electrolyte c row -= t+ phi row), 4 include 1/c terms,
+// 8 phi rows only (c rows written as 0)
+void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2* out,
+              cudaStream_t s);
+double norm2_grid(Operator& op, const double2* v, int field_mask, cudaStream_t s);
+Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
+                          const hc_params& hp);
+
+}  // namespace hc

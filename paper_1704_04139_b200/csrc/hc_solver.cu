@@ -1,0 +1,532 @@
+// Device-resident implicit step: preconditioned BiCGStab, damped Newton with
+// positivity guard and line search, stationary potential solve, and the
+// adaptive implicit-Euler step with the explicit plated-inventory update.
+//
+// Reference: fvm/newton.py:62-206, fvm/timestepping.py:260-312.
+#include <cmath>
+#include <algorithm>
+#include <initializer_list>
+#include <limits>
+
+#include "hc_amg.cuh"
+#include "hc_solver.cuh"
+
+namespace hc {
+
+namespace {
+constexpr int TPB = 256;
+inline int nblk(long long n, int tpb = TPB) { return (int)std::max<long long>(1, (n + tpb - 1) / tpb); }
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  __syncthreads();
+  return r;
+}
+
+// partial dot products: out[blk] = <a,b>, out[nb + blk] = <c,d> (if c)
+__global__ void k_dot2(long long n, const double2* __restrict__ a, const double2* __restrict__ b,
+                       const double2* __restrict__ c, const double2* __restrict__ d,
+                       double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s1 = 0.0, s2 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 x = a[i], y = b[i];
+    s1 += x.x * y.x + x.y * y.y;
+    if (c) {
+      double2 u = c[i], w = d[i];
+      s2 += u.x * w.x + u.y * w.y;
+    }
+  }
+  s1 = block_sum(s1, sh);
+  if (c) s2 = block_sum(s2, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s1;
+    part[gridDim.x + blockIdx.x] = s2;
+  }
+}
+
+// sums of squares of c and phi separately (NaN/Inf propagate)
+__global__ void k_sumsq2(long long n, const double2* __restrict__ a, double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s1 = 0.0, s2 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 x = a[i];
+    s1 += x.x * x.x;
+    s2 += x.y * x.y;
+  }
+  s1 = block_sum(s1, sh);
+  s2 = block_sum(s2, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s1;
+    part[gridDim.x + blockIdx.x] = s2;
+  }
+}
+
+__global__ void k_p_update(long long n, double beta, double omega, const double2* __restrict__ r,
+                           const double2* __restrict__ v, double2* __restrict__ p) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 pi = p[i], ri = r[i], vi = v[i];
+  p[i] = make_double2(ri.x + beta * (pi.x - omega * vi.x), ri.y + beta * (pi.y - omega * vi.y));
+}
+
+// y = a + alpha * b
+__global__ void k_axpy(long long n, const double2* __restrict__ a, double alpha,
+                       const double2* __restrict__ b, double2* __restrict__ y) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 u = a[i], w = b[i];
+  y[i] = make_double2(u.x + alpha * w.x, u.y + alpha * w.y);
+}
+
+// x += alpha * p + omega * s
+__global__ void k_x_update(long long n, double alpha, const double2* __restrict__ p, double omega,
+                           const double2* __restrict__ s, double2* __restrict__ x) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 xi = x[i], pi = p[i], si = s[i];
+  x[i] = make_double2(xi.x + alpha * pi.x + omega * si.x, xi.y + alpha * pi.y + omega * si.y);
+}
+
+__global__ void k_neg(long long n, const double2* __restrict__ a, double2* __restrict__ y) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 u = a[i];
+  y[i] = make_double2(-u.x, -u.y);
+}
+
+__global__ void k_zero_c(long long n, double2* __restrict__ y) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) y[i].x = 0.0;
+}
+
+__global__ void k_extract_c(long long n, const double2* __restrict__ x, double* __restrict__ c) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) c[i] = x[i].x;
+}
+
+// |A_lin| |x| (+ |c| inv_dt on c rows): the cancellation floor scale (newton.py:62-72)
+__global__ void k_abs_lin(DevParams P, const uint8_t* __restrict__ lab, const double2* __restrict__ X,
+                          double inv_dt, double2* __restrict__ out) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= P.nvox) return;
+  int x = (int)(v % P.nx);
+  long long t = v / P.nx;
+  int y = (int)(t % P.ny), z = (int)(t / P.ny);
+  uint8_t a = lab[v];
+  if (z == P.nz - 1 && a == CC) { out[v] = make_double2(0.0, 0.0); return; }
+  double2 xa = X[v];
+  double ac = fabs(xa.x), ap = fabs(xa.y);
+  double rc = 0.0, rp = 0.0;
+  const double gM = P.t_plus * P.kappa * P.gF2;
+  for (int d = 0; d < 6; ++d) {
+    long long nb;
+    int zb = z;
+    if (d == 0) { if (x == 0) continue; nb = v - 1; }
+    else if (d == 1) { if (x + 1 >= P.nx) continue; nb = v + 1; }
+    else if (d == 2) { if (y == 0) continue; nb = v - P.nx; }
+    else if (d == 3) { if (y + 1 >= P.ny) continue; nb = v + P.nx; }
+    else if (d == 4) { if (z == 0) continue; nb = v - P.nxy; zb = z - 1; }
+    else { if (z + 1 >= P.nz) continue; nb = v + P.nxy; zb = z + 1; }
+    uint8_t b = lab[nb];
+    uint8_t k = kind_of(a, b);
+    bool gb = zb == P.nz - 1 && b == CC;
+    double sa = P.sig[a], sb = P.sig[b];
+    if (gb) {
+      if (k == K_CONT || k == K_CONTACT) rp += 2.0 * sa * sb / (sa + sb) * P.gF2 * ap;
+      continue;
+    }
+    double2 xb = X[nb];
+    double bc = fabs(xb.x), bp = fabs(xb.y);
+    if (k == K_CONT) {
+      if (a == GR) {
+        rc += P.d_gr * P.inv_h2 * (ac + bc);
+        rp += P.sigma_gr * P.gF2 * (ap + bp);
+      } else if (a == EL) {
+        rc += P.d_el * P.inv_h2 * (ac + bc) + gM * (ap + bp);
+        rp += P.kappa * P.gF2 * (ap + bp);
+      } else {
+        rp += P.sig[a] * P.gF2 * (ap + bp);
+      }
+    } else if (k == K_CONTACT) {
+      rp += 2.0 * sa * sb / (sa + sb) * P.gF2 * (ap + bp);
+    }
+  }
+  if (a == GR || a == EL) rc += ac * inv_dt;
+  else rc = 0.0;
+  out[v] = make_double2(rc, rp);
+}
+
+// positivity guard: partial minima of c / (-delta_c) over delta_c < 0
+__global__ void k_pos_min(DevParams P, const uint8_t* __restrict__ lab, const double2* __restrict__ x,
+                          const double2* __restrict__ d, double* __restrict__ part) {
+  __shared__ double sh[32];
+  double m = INFINITY;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.nvox;
+       i += (long long)gridDim.x * blockDim.x) {
+    uint8_t a = lab[i];
+    if (a != GR && a != EL) continue;
+    double dc = d[i].x;
+    if (dc < 0.0) m = fmin(m, x[i].x / -dc);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : INFINITY;
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_down_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) part[blockIdx.x] = m;
+  }
+}
+
+// per plated slot: outflow (mol/s) through its stripping faces (timestepping.py:260-267),
+// then n_new = max(0, n - dt*flux); part[] collects the clamped (negative) mass
+__global__ void k_plated_update(DevParams P, long long n_pl, const int32_t* __restrict__ pl_vox,
+                                const int32_t* __restrict__ if_rank, const int32_t* __restrict__ if_dir,
+                                const int32_t* __restrict__ if_so, const int32_t* __restrict__ if_el,
+                                const int8_t* __restrict__ if_kind, const double2* __restrict__ X,
+                                const double* __restrict__ npl, double beta, double dt,
+                                double face_area_over_F, double* __restrict__ npl_new,
+                                double* __restrict__ clamp) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n_pl) return;
+  int v = pl_vox[k];
+  int rk = if_rank[v];
+  double flux = 0.0;
+  if (rk >= 0) {
+    for (int d = 0; d < 6; ++d) {
+      int f = if_dir[6LL * rk + d];
+      if (f < 0 || if_kind[f] != IF_STRIP || if_so[f] != v) continue;
+      double2 xs = X[v], xe = X[if_el[f]];
+      double i = strip_current_dev(xe.x, xs.y, xe.y, npl[k], beta, P, nullptr, nullptr);
+      flux += i * face_area_over_F;
+    }
+  }
+  double nn = npl[k] - dt * flux;
+  clamp[k] = nn < 0.0 ? -nn : 0.0;
+  npl_new[k] = fmax(nn, 0.0);
+}
+
+__global__ void k_sum(long long n, const double* __restrict__ a, double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    s += a[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ workspace
+Work& work(Operator& op) {
+  if (!op.work) op.work = new Work(op.P.nvox);
+  return *op.work;
+}
+
+Work::Work(long long nvox)
+    : x(nvox), xt(nvox), r(nvox), rt(nvox), d(nvox), b(nvox), kr(nvox), khat(nvox), kp(nvox),
+      kv(nvox), ks(nvox), kt(nvox), kph(nvox), ksh(nvox), cprev(nvox), part(8192), parth(8192) {}
+
+static int red_blocks(const Operator& op) {
+  return (int)std::min<long long>(nblk(op.P.nvox), 4LL * op.n_sm);
+}
+
+static double host_sum(Operator& op, int nb, int off, cudaStream_t s) {
+  Work& W = work(op);
+  HC_CUDA(cudaMemcpyAsync(W.parth.data(), W.part.p + off, nb * sizeof(double),
+                          cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaStreamSynchronize(s));
+  double acc = 0.0;
+  for (int i = 0; i < nb; ++i) acc += W.parth[i];
+  return acc;
+}
+
+double dot(Operator& op, const double2* a, const double2* b, cudaStream_t s) {
+  int nb = red_blocks(op);
+  k_dot2<<<nb, TPB, 0, s>>>(op.P.nvox, a, b, nullptr, nullptr, work(op).part.p);
+  HC_CHECK_LAUNCH();
+  return host_sum(op, nb, 0, s);
+}
+
+void dot2(Operator& op, const double2* a, const double2* b, const double2* c, const double2* d,
+          double& ab, double& cd, cudaStream_t s) {
+  int nb = red_blocks(op);
+  Work& W = work(op);
+  k_dot2<<<nb, TPB, 0, s>>>(op.P.nvox, a, b, c, d, W.part.p);
+  HC_CHECK_LAUNCH();
+  HC_CUDA(cudaMemcpyAsync(W.parth.data(), W.part.p, 2 * nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaStreamSynchronize(s));
+  ab = cd = 0.0;
+  for (int i = 0; i < nb; ++i) { ab += W.parth[i]; cd += W.parth[nb + i]; }
+}
+
+// returns sqrt of sum of squares over the fields in mask; +inf if any entry of
+// EITHER field is non-finite (the reference raises NumericsError on any row)
+double norm_checked(Operator& op, const double2* a, int mask, cudaStream_t s) {
+  int nb = red_blocks(op);
+  Work& W = work(op);
+  k_sumsq2<<<nb, TPB, 0, s>>>(op.P.nvox, a, W.part.p);
+  HC_CHECK_LAUNCH();
+  HC_CUDA(cudaMemcpyAsync(W.parth.data(), W.part.p, 2 * nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaStreamSynchronize(s));
+  double c = 0.0, p = 0.0;
+  for (int i = 0; i < nb; ++i) { c += W.parth[i]; p += W.parth[nb + i]; }
+  if (!std::isfinite(c) || !std::isfinite(p)) return INFINITY;
+  double acc = (mask & 1 ? c : 0.0) + (mask & 2 ? p : 0.0);
+  return std::sqrt(acc);
+}
+
+// J-operator of the linear solve: mode 0 full J + mass, mode 1 phi block
+static void apply_A(Operator& op, const double2* v, double2* out, double inv_dt, int mode,
+                    cudaStream_t s) {
+  jvp_grid(op, v, inv_dt, mode == 0 ? (1 | 4) : 8, out, s);
+}
+
+// Right-preconditioned BiCGStab on the grid layout; x starts at 0.
+// Returns the number of iterations; throws NonConvergence on stall.
+int bicgstab(Operator& op, const double2* b, double2* x, double inv_dt, int mode, double rtol,
+             int maxit, cudaStream_t s) {
+  Work& W = work(op);
+  const long long n = op.P.nvox;
+  const int nb = nblk(n);
+  HC_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double2), s));
+  double bnorm = std::sqrt(dot(op, b, b, s));
+  if (bnorm == 0.0) return 0;
+  if (!std::isfinite(bnorm)) throw Error(HC_ERR_NONCONVERGENCE, "non-finite Newton right-hand side");
+  const double tol = rtol * bnorm;
+  HC_CUDA(cudaMemcpyAsync(W.kr.p, b, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  HC_CUDA(cudaMemcpyAsync(W.khat.p, b, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  HC_CUDA(cudaMemsetAsync(W.kp.p, 0, n * sizeof(double2), s));
+  HC_CUDA(cudaMemsetAsync(W.kv.p, 0, n * sizeof(double2), s));
+  double rho = 1.0, alpha = 1.0, omega = 1.0;
+  double rnorm = bnorm;
+  for (int it = 1; it <= maxit; ++it) {
+    double rho1 = dot(op, W.khat.p, W.kr.p, s);
+    if (rho1 == 0.0 || !std::isfinite(rho1))
+      throw Error(HC_ERR_NONCONVERGENCE, "iterative linear solver stalled (rho breakdown)");
+    double beta = (rho1 / rho) * (alpha / omega);
+    k_p_update<<<nb, TPB, 0, s>>>(n, beta, omega, W.kr.p, W.kv.p, W.kp.p);
+    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s);
+    apply_A(op, W.kph.p, W.kv.p, inv_dt, mode, s);
+    double rv = dot(op, W.khat.p, W.kv.p, s);
+    if (rv == 0.0 || !std::isfinite(rv))
+      throw Error(HC_ERR_NONCONVERGENCE, "iterative linear solver stalled (alpha breakdown)");
+    alpha = rho1 / rv;
+    k_axpy<<<nb, TPB, 0, s>>>(n, W.kr.p, -alpha, W.kv.p, W.ks.p);
+    double snorm = std::sqrt(dot(op, W.ks.p, W.ks.p, s));
+    if (snorm <= tol) {
+      k_axpy<<<nb, TPB, 0, s>>>(n, x, alpha, W.kph.p, x);
+      HC_CHECK_LAUNCH();
+      return it;
+    }
+    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s);
+    apply_A(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
+    double ts, tt;
+    dot2(op, W.kt.p, W.ks.p, W.kt.p, W.kt.p, ts, tt, s);
+    if (tt == 0.0 || !std::isfinite(tt))
+      throw Error(HC_ERR_NONCONVERGENCE, "iterative linear solver stalled (omega breakdown)");
+    omega = ts / tt;
+    k_x_update<<<nb, TPB, 0, s>>>(n, alpha, W.kph.p, omega, W.ksh.p, x);
+    k_axpy<<<nb, TPB, 0, s>>>(n, W.ks.p, -omega, W.kt.p, W.kr.p);
+    HC_CHECK_LAUNCH();
+    rnorm = std::sqrt(dot(op, W.kr.p, W.kr.p, s));
+    if (rnorm <= tol) return it;
+    if (omega == 0.0)
+      throw Error(HC_ERR_NONCONVERGENCE, "iterative linear solver stalled (omega = 0)");
+    rho = rho1;
+  }
+  char msg[160];
+  snprintf(msg, sizeof msg, "iterative linear solver stalled (info=%d, relres=%.3e)", maxit,
+           rnorm / bnorm);
+  throw Error(HC_ERR_NONCONVERGENCE, msg);
+}
+
+static double floor_norm(Operator& op, const double2* x, double inv_dt, cudaStream_t s) {
+  Work& W = work(op);
+  k_abs_lin<<<nblk(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, x, inv_dt, W.rt.p);
+  HC_CHECK_LAUNCH();
+  return 1e-13 * norm_checked(op, W.rt.p, 3, s);
+}
+
+static void ensure_amg(Operator& op) {
+  if (!op.amg) op.amg = build_amg(op);
+}
+
+// newton_solve (newton.py:86-168) on the grid layout.  W.x holds the guess on
+// entry and the solution on exit; W.cprev holds c_prev per voxel.
+void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc_solver_config& cfg,
+                 hc_newton_stats& st, cudaStream_t s) {
+  if (!(dt > 0)) throw Error(HC_ERR_ARGUMENT, "dt must be positive");
+  ensure_amg(op);
+  Work& W = work(op);
+  const long long n = op.P.nvox;
+  const int nb = nblk(n);
+  const double inv_dt = 1.0 / dt;
+  const double beta = cfg.implicit_plated ? dt * op.info.face_area / op.host_params.faraday : 0.0;
+  const int parts = PART_LIN | PART_BV | PART_1C | PART_BND | PART_TIME;
+  residual_grid(op, W.x.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.r.p, s);
+  double norm0 = norm_checked(op, W.r.p, 3, s);
+  if (!std::isfinite(norm0))
+    throw Error(HC_ERR_NONCONVERGENCE, "initial residual not evaluable: operator produced a non-finite value");
+  double tol = std::max({cfg.newton_atol, cfg.newton_rtol * norm0, floor_norm(op, W.x.p, inv_dt, s)});
+  st.norm0 = norm0;
+  st.tol = tol;
+  st.n_iter = 0;
+  st.norm_final = norm0;
+  if (norm0 <= tol) return;
+  double norm = norm0;
+  for (int it = 1; it <= cfg.newton_max_iter; ++it) {
+    linearize(op, W.x.p, npl, beta, s);
+    amg_update(op, inv_dt, 3, s);
+    k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p);
+    st.krylov_iters += bicgstab(op, W.b.p, W.d.p, inv_dt, 0, cfg.linear_rtol, cfg.krylov_max_iter, s);
+    // positivity guard on the concentration block
+    double alpha = 1.0;
+    {
+      int rb = red_blocks(op);
+      k_pos_min<<<rb, TPB, 0, s>>>(op.P, op.labels.p, W.x.p, W.d.p, W.part.p);
+      HC_CHECK_LAUNCH();
+      HC_CUDA(cudaMemcpyAsync(W.parth.data(), W.part.p, rb * sizeof(double), cudaMemcpyDeviceToHost, s));
+      HC_CUDA(cudaStreamSynchronize(s));
+      double lim = INFINITY;
+      for (int i = 0; i < rb; ++i) lim = std::min(lim, W.parth[i]);
+      if (std::isfinite(lim)) alpha = std::min(alpha, 0.99 * lim);
+    }
+    if (alpha <= 0.0) throw Error(HC_ERR_NONCONVERGENCE, "positivity guard blocked the Newton step");
+    bool accepted = false;
+    double norm_try = INFINITY;
+    for (int h = 0; h <= 8; ++h) {
+      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p);
+      residual_grid(op, W.xt.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.rt.p, s);
+      norm_try = norm_checked(op, W.rt.p, 3, s);
+      if (std::isfinite(norm_try) && (norm_try <= norm || norm_try <= tol)) { accepted = true; break; }
+      alpha *= 0.5;
+    }
+    if (!accepted) {
+      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p);
+      residual_grid(op, W.xt.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.rt.p, s);
+      norm_try = norm_checked(op, W.rt.p, 3, s);
+      if (!std::isfinite(norm_try))
+        throw Error(HC_ERR_NONCONVERGENCE, "residual not evaluable under damping");
+    }
+    std::swap(W.x.p, W.xt.p);
+    std::swap(W.r.p, W.rt.p);
+    norm = norm_try;
+    st.n_iter = it;
+    st.norm_final = norm;
+    if (op.iterate_hook) op.iterate_hook(op, W.x.p);
+    if (norm <= tol) return;
+  }
+  char msg[200];
+  snprintf(msg, sizeof msg, "Newton did not reach tolerance %.3e in %d iterations (last residual %.3e)",
+           tol, cfg.newton_max_iter, norm);
+  throw Error(HC_ERR_NONCONVERGENCE, msg);
+}
+
+// solve_initial_potential (newton.py:171-206): W.x in/out.
+void initial_potential_grid(Operator& op, const double* npl, double mu, const hc_solver_config& cfg,
+                            hc_newton_stats& st, cudaStream_t s) {
+  ensure_amg(op);
+  Work& W = work(op);
+  const long long n = op.P.nvox;
+  const int nb = nblk(n);
+  const int parts = PART_LIN | PART_BV | PART_1C | PART_BND;
+  residual_grid(op, W.x.p, npl, mu, 0.0, parts, nullptr, 0.0, W.r.p, s);
+  double norm0 = norm_checked(op, W.r.p, 2, s);
+  double tol = std::max({cfg.newton_atol, cfg.newton_rtol * norm0, floor_norm(op, W.x.p, 0.0, s)});
+  st.norm0 = norm0;
+  st.tol = tol;
+  st.n_iter = 0;
+  st.norm_final = norm0;
+  if (norm0 <= tol) return;
+  double norm = norm0;
+  for (int it = 1; it <= cfg.newton_max_iter; ++it) {
+    linearize(op, W.x.p, npl, 0.0, s);
+    amg_update(op, 0.0, 2, s);
+    k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p);
+    k_zero_c<<<nb, TPB, 0, s>>>(n, W.b.p);
+    st.krylov_iters += bicgstab(op, W.b.p, W.d.p, 0.0, 1, cfg.linear_rtol, cfg.krylov_max_iter, s);
+    double alpha = 1.0, norm_try = INFINITY;
+    for (int h = 0; h <= 8; ++h) {
+      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p);
+      residual_grid(op, W.xt.p, npl, mu, 0.0, parts, nullptr, 0.0, W.rt.p, s);
+      norm_try = norm_checked(op, W.rt.p, 2, s);
+      if (std::isfinite(norm_try) && (norm_try <= norm || norm_try <= tol)) break;
+      alpha *= 0.5;
+    }
+    std::swap(W.x.p, W.xt.p);
+    std::swap(W.r.p, W.rt.p);
+    norm = norm_try;
+    st.n_iter = it;
+    st.norm_final = norm;
+    if (norm <= tol) return;
+  }
+  char msg[160];
+  snprintf(msg, sizeof msg, "stationary potential solve stalled at residual %.3e", norm);
+  throw Error(HC_ERR_NONCONVERGENCE, msg);
+}
+
+// step (timestepping.py:270-312) on the grid layout: W.x holds the state on
+// entry (also x_prev) and the accepted state on exit; npl updated in place.
+void step_grid(Operator& op, double* npl, double dt_suggest, double mu, const hc_solver_config& cfg,
+               hc_newton_stats& st, cudaStream_t s) {
+  Work& W = work(op);
+  const long long n = op.P.nvox;
+  double dt = std::min(dt_suggest, cfg.dt_max);
+  int retries = 0;
+  k_extract_c<<<nblk(n), TPB, 0, s>>>(n, W.x.p, W.cprev.p);
+  DBuf<double2>& xprev = W.xprev_store;
+  if (!xprev.p) xprev.alloc(n);
+  HC_CUDA(cudaMemcpyAsync(xprev.p, W.x.p, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  st.krylov_iters = 0;
+  while (true) {
+    try {
+      newton_grid(op, npl, dt, mu, cfg, st, s);
+    } catch (const Error& e) {
+      if (e.code != HC_ERR_NONCONVERGENCE) throw;
+      if (dt <= cfg.dt_min * (1.0 + 1e-12)) {
+        char msg[256];
+        snprintf(msg, sizeof msg, "time step underflow (dt=%.3e): %s", dt, e.what());
+        throw Error(HC_ERR_SIMULATION, msg);
+      }
+      dt = std::max(dt * cfg.shrink_factor, cfg.dt_min);
+      retries++;
+      HC_CUDA(cudaMemcpyAsync(W.x.p, xprev.p, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      continue;
+    }
+    break;
+  }
+  double clamped = 0.0;
+  long long npls = op.info.n_plated;
+  if (npls) {
+    const double beta = cfg.implicit_plated ? dt * op.info.face_area / op.host_params.faraday : 0.0;
+    DBuf<double>& tmp = W.npl_tmp;
+    if (tmp.n < (size_t)(2 * npls)) tmp.alloc(2 * npls);
+    k_plated_update<<<nblk(npls), TPB, 0, s>>>(op.P, npls, op.plated_vox.p, op.if_rank.p, op.if_dir.p,
+                                               op.if_solid.p, op.if_el.p, op.if_kind.p, W.x.p, npl,
+                                               beta, dt, op.info.face_area / op.host_params.faraday,
+                                               tmp.p, tmp.p + npls);
+    HC_CUDA(cudaMemcpyAsync(npl, tmp.p, npls * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    int rb = (int)std::min<long long>(nblk(npls), 1024);
+    k_sum<<<rb, TPB, 0, s>>>(npls, tmp.p + npls, W.part.p);
+    HC_CHECK_LAUNCH();
+    clamped = host_sum(op, rb, 0, s);
+  }
+  st.dt_used = dt;
+  st.retries = retries;
+  st.clamped_loss = clamped;
+  st.dt_next = st.n_iter <= cfg.easy_iter_threshold ? std::min(dt * cfg.grow_factor, cfg.dt_max) : dt;
+}
+
+}  // namespace hc

@@ -1,0 +1,61 @@
+"""POD by the method of snapshots (SPEC mor.pod; arXiv 1704.04139 section 2.5).
+
+The snapshot Gram matrix ``G = S^T W S`` is the only dense contraction of the
+path and runs on the FP64 tensor cores (``csrc/hc_pod.cu``); the small
+eigenproblem of G and the basis assembly stay on the device.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _dev, _native
+from .errors import ReductionError
+
+
+def pod_gram(S, w=None):
+    """``S^T diag(w) S`` for an (n_dof, n_snap) fp64 snapshot matrix."""
+    t = _dev.torch()
+    Sd = _dev.to_dev(S)
+    if Sd.dim() != 2:
+        raise ValueError("snapshot matrix must be 2-D (n_dof, n_snap)")
+    n_dof, n_snap = Sd.shape
+    Sc = Sd.t().contiguous()            # column-major storage of S
+    wd = _dev.to_dev(w) if w is not None else None
+    G = t.empty((n_snap, n_snap), dtype=t.float64, device="cuda")
+    _native.check(_native.lib().hc_pod_gram(_dev.ptr(Sc), _dev.ptr(wd) if wd is not None else None,
+                                            int(n_dof), int(n_snap), _dev.ptr(G), _dev.stream()))
+    G = G.t()  # column-major result -> row-major view
+    return _dev.like_input(G.contiguous(), S)
+
+
+def pod_basis(S, rel_tol: float, w=None):
+    """Orthonormal POD basis keeping the smallest k with tail energy <= rel_tol^2.
+
+    Returns (basis (n_dof, k), singular values (n_snap,)).
+    """
+    t = _dev.torch()
+    Sd = _dev.to_dev(S)
+    if not float(t.linalg.vector_norm(Sd)) > 0.0:
+        raise ReductionError("all-zero snapshot set")
+    G = _dev.to_dev(pod_gram(Sd, w))
+    G = 0.5 * (G + G.t())
+    lam, V = t.linalg.eigh(G)
+    lam, V = lam.flip(0), V.flip(1)
+    lam = t.clamp(lam, min=0.0)
+    sig = t.sqrt(lam)
+    tot = float(lam.sum())
+    tail = t.flip(t.cumsum(t.flip(lam, [0]), 0), [0])  # tail[k] = sum_{i>=k} lam_i
+    k = int(lam.numel())
+    for kk in range(1, lam.numel() + 1):
+        rest = float(tail[kk]) if kk < lam.numel() else 0.0
+        if rest <= rel_tol ** 2 * tot:
+            k = kk
+            break
+    B = Sd @ (V[:, :k] / sig[:k])
+    # one modified Gram-Schmidt pass (SPEC: re-orthonormalize output)
+    for j in range(k):
+        for i in range(j):
+            B[:, j] -= (B[:, i] @ B[:, j]) * B[:, i]
+        B[:, j] /= t.linalg.vector_norm(B[:, j])
+    return _dev.like_input(B, S), (sig.cpu().numpy() if not _dev.is_tensor(S) else sig)
