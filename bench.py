@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the full-order implicit time step (BASELINE.json north_star).
+
+Workload (BASELINE configs[1], "medium"): 64x64x128 voxel half cell, 2C
+constant-current charge, dt = 0.5 s, plating/stripping on, fp64.  One bench
+step = one accepted implicit-Euler step (Newton + preconditioned Krylov +
+plated-inventory update) through the C ABI (``hc_step``) on device-resident
+state.  ``value`` = implicit steps/s over all ranks (each rank steps its own
+cell: replicas, no data-path collective).  ``e2e`` = the same step through
+``hc_step_host`` with pinned host state buffers (H2D + D2H inside the timed
+region).  The residual and J v kernels are timed separately (CUDA events,
+L2 flushed before every launch) for the GDOF/s figures and the roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+``--impl reference`` times the CPU oracle port of the reference algorithm
+(oracle/fvm_oracle.py, SuperLU-based Newton like fvm/newton.py:75-77) on a
+bounded sample of the same workload with all host cores (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "implicit time steps/s and residual+J*v GDOF/s; % of B200 HBM roofline"
+FALLBACK_HBM_GBS = 6650.0
+L2_FLUSH_BYTES = 256 << 20
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cell_for(config: str, rank: int):
+    from paper_1704_04139_b200.configs import CONFIGS
+    rs = CONFIGS[config]
+    spec = dataclasses.replace(rs.cell, seed=rs.cell.seed + 1000 * rank) if rank else rs.cell
+    return rs, spec
+
+
+def drive_mu(labels, voxel_um, c_rate, params):
+    """Charge current density (A/m^2, negative = lithiation) for a C-rate of the graphite."""
+    h = voxel_um * 1e-6
+    vol_gr = float(np.count_nonzero(labels == 1)) * h ** 3
+    area = labels.shape[1] * labels.shape[2] * h * h
+    return -c_rate * params.c_gr_max * params.constants.F * vol_gr / 3600.0 / area
+
+
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU baseline
+def _oracle_column_step(args):
+    """One implicit step of the CPU oracle on a w x w column of the workload cell."""
+    config, w, seed = args
+    from oracle import fvm_oracle as O
+    from paper_1704_04139_b200.configs import CONFIGS
+    from paper_1704_04139_b200.microgen import generate_cell
+    rs = CONFIGS[config]
+    spec = dataclasses.replace(rs.cell, nx=w, ny=w, seed=seed)
+    grid = generate_cell(spec)
+    p = O.Params(soc_init=rs.soc_init, i00_plel=rs.i00_plel_exchange / np.sqrt(1000.0))
+    op = O.OracleOperator(grid.labels, grid.voxel_size, p)
+    h = grid.voxel_size * 1e-6
+    mu = -rs.c_rate * p.c_gr_max * p.F * np.count_nonzero(grid.labels == 1) * h ** 3 / 3600 / (w * w * h * h)
+    x, npl = O.initial_fields(op)
+    x = O.solve_initial_potential(op, x, npl, mu)
+    t0 = time.perf_counter()
+    O.step(op, x, npl, rs.dt, mu)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(config: str, rounds: int, warmup: int = 0):
+    """Parallel oracle column steps on all host cores; returns per-round cell-steps/s."""
+    import multiprocessing as mp
+    from paper_1704_04139_b200.configs import CONFIGS
+    rs = CONFIGS[config]
+    w = 16
+    frac = (w * w) / (rs.cell.nx * rs.cell.ny)
+    cores = max(1, min(os.cpu_count() or 1, 16))
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    vals = []
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        for r in range(warmup + rounds):
+            t0 = time.perf_counter()
+            pool.map(_oracle_column_step, [(config, w, 7000 + 97 * r + k) for k in range(cores)])
+            wall = time.perf_counter() - t0
+            if r >= warmup:
+                vals.append(cores * frac / wall)
+    sample = (f"{cores} concurrent implicit steps of the CPU oracle (SuperLU Newton) on "
+              f"{w}x{w}x{rs.cell.nz} columns of the {config} cell ({frac:.4f} of its voxels each), "
+              "scaled linearly by voxel count (favourable to the CPU: LU cost is superlinear)")
+    return vals, cores, sample
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_1704_04139_b200 as P
+    from paper_1704_04139_b200 import _dev, _native
+    from paper_1704_04139_b200.microgen import generate_cell
+    import ctypes
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rs, spec = cell_for(args.config, rank)
+    grid = generate_cell(spec)
+    params = P.MaterialParams(soc_init=rs.soc_init, i00_plel=rs.i00_plel_exchange / np.sqrt(1000.0))
+    dof = P.build_dofmap(grid)
+    op = P.SystemOperator(dof, params)
+    mu = drive_mu(grid.labels, grid.voxel_size, rs.c_rate, params)
+    cfg = P.SolverConfig(dt_init=min(0.05, rs.dt), dt_max=rs.dt)
+    state = P.prepare_initial_state(op, params, mu, cfg)
+    L = _native.lib()
+    x = _dev.to_dev(state.x).clone()
+    npl = _dev.to_dev(state.n_pl if state.n_pl.size else np.zeros(1)).clone()
+    c = cfg.to_c()
+    st = _native.HcNewtonStats()
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream or None
+
+    def one_step():
+        _native.check(L.hc_step(op.native.handle, _dev.ptr(x), _dev.ptr(npl), 0.0, rs.dt, mu,
+                                ctypes.byref(c), ctypes.byref(st), sp))
+        return st.n_iter, st.krylov_iters
+
+    for _ in range(args.warmup):
+        one_step()
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    newton, krylov = [], []
+    n0 = ctypes.c_int64(0)
+    _native.check(L.hc_launch_count(ctypes.byref(n0)))
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for k in range(args.steps):
+            flush.zero_()                                  # L2 flush between timed steps
+            evs[k][0].record(stream)
+            it, kr = one_step()
+            evs[k][1].record(stream)
+            newton.append(it)
+            krylov.append(kr)
+        torch.cuda.synchronize()
+    n1 = ctypes.c_int64(0)
+    _native.check(L.hc_launch_count(ctypes.byref(n1)))
+    # subtract the flush kernels (torch's, not ours): none counted by hc_launch_count
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    if ws > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+        torch.distributed.barrier()
+
+    # ---- kernel timings: residual and J v at the current state
+    beta = rs.dt * op.face_area / params.constants.F
+    ms = (ctypes.c_double * 4)()
+    _native.check(L.hc_time_kernels(op.native.handle, _dev.ptr(x), _dev.ptr(npl), beta,
+                                    1.0 / rs.dt, 20, L2_FLUSH_BYTES, ms, sp))
+    nvox = int(op.native.info.n_vox)
+    n_el = int(np.count_nonzero(grid.labels == 0))
+    n_c = int(np.count_nonzero(np.isin(grid.labels, (0, 1))))
+    ndof = dof.n_total
+    res_ms, jv_ms = ms[0] + ms[1], ms[2] + ms[3]
+    jv_bytes = nvox * (1 + 16 + 16) + n_el * 8          # labels + v (c,phi) + out + gX/c (electrolyte)
+    res_bytes = nvox * (1 + 16 + 16) + n_c * 8          # labels + x + out + c_prev
+    peak, peak_kind = measured_peaks()
+    achieved = jv_bytes / (ms[2] * 1e-3) / 1e9
+
+    # ---- e2e: the same step through the host-buffer entry point
+    e2e_val = None
+    bi = (dof.n_total + max(dof.n_plated, 0)) * 8
+    if rank == 0 or ws > 1:
+        xh = torch.empty(dof.n_total, dtype=torch.float64).pin_memory()
+        nh = torch.empty(max(dof.n_plated, 1), dtype=torch.float64).pin_memory()
+        xh.copy_(x.cpu())
+        nh.copy_(npl.cpu())
+        stp = _native.HcNewtonStats()
+        k_e2e = max(1, min(args.steps, 5))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            _native.check(L.hc_step_host(op.native.handle, xh.data_ptr(), nh.data_ptr(), 0.0,
+                                         rs.dt, mu, ctypes.byref(c), ctypes.byref(stp)))
+        e2e_s = time.perf_counter() - t0
+        e2e_val = k_e2e / e2e_s
+        if ws > 1:
+            t = torch.tensor([e2e_s / k_e2e], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_val = ws / float(t.item())
+
+    out = None
+    if rank == 0:
+        value = ws * args.steps / (total_ms * 1e-3)
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            vals, cores, sample = cpu_sample(args.config, rounds=1)
+            cpu = {"value": vals[0], "unit": "steps/s", "cores": cores, "kind": "port",
+                   "sample": sample}
+        out = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded ball-union microstructure, BASELINE config shapes)",
+            "config": {"workload": f"{args.config}: {spec.nx}x{spec.ny}x{spec.nz} voxels, "
+                       f"{rs.c_rate}C charge, dt={rs.dt}s, plating on; one replica cell per GPU",
+                       "n_dof": ndof, "n_voxels": nvox, "l2": "flushed (256 MiB write) before "
+                       "every timed step and every timed kernel launch",
+                       "parallelism": f"replicas x{ws}"},
+            "newton_iters_per_step": float(np.mean(newton)),
+            "krylov_iters_per_step": float(np.mean(krylov)),
+            "gdof_per_s": {"residual": ndof / (res_ms * 1e-3) / 1e9,
+                           "jvp": ndof / (jv_ms * 1e-3) / 1e9},
+            "kernel_ms": {"residual_stencil": ms[0], "residual_iface": ms[1],
+                          "jvp_stencil": ms[2], "jvp_iface": ms[3]},
+            "roofline": {"kernel": "k_jvp_stencil", "bound": "hbm", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "bytes_per_launch": jv_bytes,
+                         "residual_achieved": res_bytes / (ms[0] * 1e-3) / 1e9},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "steps/s", "h2d_bytes_per_step": bi,
+                    "d2h_bytes_per_step": bi},
+            "gpu_launches": int(n1.value - n0.value),
+            "clocks": clk.summary(),
+        }
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return out
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    vals, cores, sample = cpu_sample(args.config, rounds=args.steps, warmup=args.warmup)
+    total_s = sum(1.0 / v for v in vals)
+    value = len(vals) / total_s
+    return {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded ball-union microstructure, BASELINE config shapes)",
+            "config": {"workload": f"{args.config} (CPU sample)", "parallelism": f"{cores} host processes"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="medium")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        out = run_reference(args, ws, rank)
+    else:
+        out = run_ours(args, ws, rank, local)
+    if out is not None:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

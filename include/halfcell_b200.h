@@ -137,6 +137,17 @@ int hc_step_host(hc_operator* op, double* x_host, double* n_pl_host, double t, d
 int hc_pod_gram(const double* S, const double* w, int64_t n_dof, int64_t n_snap, double* G,
                 void* stream);
 
+/* Number of CUDA kernels this library has launched in the process (bench.py). */
+int hc_launch_count(int64_t* out);
+
+/* Average device time (ms, CUDA events on `stream`) of one launch of each
+ * kernel of the residual and of J v at state x, with an L2 flush of
+ * `flush_bytes` before every launch: ms_out = {residual stencil, residual
+ * interface faces, J v stencil, J v interface faces}. */
+int hc_time_kernels(hc_operator* op, const double* x, const double* n_pl, double beta,
+                    double inv_dt, int32_t iters, int64_t flush_bytes, double* ms_out,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,23 +1,34 @@
-// Field-split, phase-aware aggregation multigrid preconditioner.
+// Field-split, phase-aware smoothed-aggregation multigrid preconditioner.
 //
-// The reference factorizes the Newton Jacobian with SuperLU or ILU+LGMRES
-// (fvm/newton.py:75-83).  On the device the Jacobian stays matrix-free and the
-// linear solve is a Krylov method preconditioned by:
+// The reference factorizes the Newton Jacobian with SuperLU, or uses ILU +
+// LGMRES (fvm/newton.py:75-83).  On the device the Jacobian stays matrix-free
+// and the linear solve is BiCGStab preconditioned by:
 //   1. the row transform T (electrolyte c row -= t+ * phi row of the same voxel),
 //      which cancels the migration and chemical-potential couplings exactly;
 //   2. a block lower-triangular split of T J: phi block first, then c block;
-//   3. one V-cycle per block of an unsmoothed-aggregation multigrid whose
-//      aggregates are (2^l x 2^l x 2^l block, phase) pairs — aggregation never
-//      mixes phases, so weakly coupled conductor clusters keep their own coarse
-//      unknowns (their near-null constant modes survive coarsening).
-// Level-1 Galerkin rows are gathered per coarse unknown from the matrix-free
-// fine stencil (deterministic, no atomics); deeper levels are CSR.
+//   3. one V-cycle per block of a smoothed-aggregation multigrid whose tentative
+//      aggregates are (2^l x 2^l x 2^l block, phase) pairs.  Aggregation never mixes
+//      phases, so weakly coupled conductor clusters (graphite / electrolyte networks
+//      joined only by Butler-Volmer faces, the metal counter stack) keep their own
+//      coarse unknowns; the prolongator smoothing P = (I - w D^-1 A) P0 removes the
+//      interpolation-energy defect of plain aggregation, which otherwise grows with
+//      the electrode thickness.
+// Sparsity patterns (A_l, P_l, P_l^T, A_l+1 = P_l^T A_l P_l) depend on the labels
+// only and are built once on the host; the values are recomputed on the device for
+// every linearization by deterministic per-row kernels (no atomics).  The fine level
+// is applied matrix-free (jvp kernels); its CSR copy only feeds the first Galerkin
+// product.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <memory>
 #include <numeric>
+#include <chrono>
+#include <cstdio>
+#include <thread>
 
 #include "hc_amg.cuh"
+#include "hc_stencil.cuh"
 
 namespace hc {
 
@@ -32,9 +43,7 @@ __device__ __forceinline__ double harm_d(const DevParams& P, uint8_t a, uint8_t 
   double sa = P.sig[a], sb = P.sig[b];
   return 2.0 * sa * sb / (sa + sb) * P.gF2;
 }
-
 __device__ __forceinline__ int find_col(const int32_t* col, int lo, int hi, int32_t c) {
-  // binary search in [lo, hi)
   while (lo < hi) {
     int mid = (lo + hi) >> 1;
     if (col[mid] < c) lo = mid + 1; else hi = mid;
@@ -42,118 +51,141 @@ __device__ __forceinline__ int find_col(const int32_t* col, int lo, int hi, int3
   return lo;
 }
 
-// ---- level-1 Galerkin rows gathered from the fine matrix-free operator ------
-// field 1 (phi block, J_pp) or 0 (c block of T J incl. mass).  Also writes the
-// fine-level inverse diagonal of every child voxel.
-__global__ void k_galerkin1(DevParams P, int field, int n1, const int32_t* __restrict__ ch_ptr,
-                            const int32_t* __restrict__ ch_vox, const uint8_t* __restrict__ lab,
-                            const int32_t* __restrict__ agg1, const int32_t* __restrict__ if_rank,
-                            const int32_t* __restrict__ if_dir, const int32_t* __restrict__ if_so,
-                            const int8_t* __restrict__ if_kind, const double* __restrict__ coef,
-                            long long n_if, double inv_dt, const int32_t* __restrict__ rowptr,
-                            const int32_t* __restrict__ col, double* __restrict__ val,
-                            double* __restrict__ fine_dinv) {
-  int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= n1) return;
-  int r0 = rowptr[I], r1 = rowptr[I + 1];
+// ---- level 0: assemble the field block of the fine operator into CSR --------
+// field 1: J_pp; field 0: (T J)_cc + mass.  One thread per voxel row.
+__global__ void k_assemble0(DevParams P, int field, const uint8_t* __restrict__ lab,
+                            const int32_t* __restrict__ if_rank, const int32_t* __restrict__ if_dir,
+                            const int32_t* __restrict__ if_so, const int8_t* __restrict__ if_kind,
+                            const double* __restrict__ coef, long long n_if, double inv_dt,
+                            const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            double* __restrict__ val, double* __restrict__ dinv) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= P.nvox) return;
+  int r0 = rp[v], r1 = rp[v + 1];
+  if (r0 == r1) { dinv[v] = 0.0; return; }
   for (int k = r0; k < r1; ++k) val[k] = 0.0;
-  int dpos = find_col(col, r0, r1, I);
+  int x = (int)(v % P.nx);
+  long long t = v / P.nx;
+  int y = (int)(t % P.ny), z = (int)(t / P.ny);
+  uint8_t a = lab[v];
   const double tp = P.t_plus;
-  for (int q = ch_ptr[I]; q < ch_ptr[I + 1]; ++q) {
-    long long v = ch_vox[q];
-    int x = (int)(v % P.nx);
-    long long t = v / P.nx;
-    int y = (int)(t % P.ny), z = (int)(t / P.ny);
-    uint8_t a = lab[v];
-    double diag = 0.0;
-    if (field == 0) diag += inv_dt;
-    int rk = if_rank[v];
-    for (int d = 0; d < 6; ++d) {
-      long long nb;
-      int zb = z;
-      if (d == 0) { if (x == 0) continue; nb = v - 1; }
-      else if (d == 1) { if (x + 1 >= P.nx) continue; nb = v + 1; }
-      else if (d == 2) { if (y == 0) continue; nb = v - P.nx; }
-      else if (d == 3) { if (y + 1 >= P.ny) continue; nb = v + P.nx; }
-      else if (d == 4) { if (z == 0) continue; nb = v - P.nxy; zb = z - 1; }
-      else { if (z + 1 >= P.nz) continue; nb = v + P.nxy; zb = z + 1; }
-      uint8_t b = lab[nb];
-      uint8_t kd = kind_of(a, b);
-      bool gb = grounded_d(P, b, zb);
-      double off = 0.0;  // coupling A[v, nb]
-      bool has = false;
-      if (field == 1) {
-        if (gb) {
-          if (kd == K_CONT || kd == K_CONTACT) diag += harm_d(P, a, b);
-          continue;
-        }
-        if (kd == K_CONT) {
-          double g = (a == GR ? P.sigma_gr : (a == EL ? P.kappa : P.sig[a])) * P.gF2;
-          diag += g; off = -g; has = true;
-        } else if (kd == K_CONTACT) {
-          double g = harm_d(P, a, b);
-          diag += g; off = -g; has = true;
-        } else if (kd == K_BV || kd == K_CE || kd == K_STRIP) {
-          int f = if_dir[6LL * rk + d];
-          double g = coef[2 * n_if + f];
-          diag += g; off = -g; has = true;
-        }
-      } else {
-        if (gb) continue;
-        if (kd == K_CONT && (a == GR || a == EL)) {
-          double g = (a == GR ? P.d_gr : P.d_el) * P.inv_h2;
-          diag += g; off = -g; has = true;
-        } else if (kd == K_BV || kd == K_CE || kd == K_STRIP) {
-          int f = if_dir[6LL * rk + d];
-          double ca = coef[f], cb = coef[n_if + f];
-          bool solid = if_so[f] == (int32_t)v;
-          if (solid) {            // graphite c row: dv = ca vc_s + cb vc_e + ...
-            if (if_kind[f] == IF_BV) { diag += ca; off = cb; has = true; }
-          } else {                // electrolyte c row: -(1-t+) dv
-            diag += -(1.0 - tp) * cb;
-            if (if_kind[f] == IF_BV) { off = -(1.0 - tp) * ca; has = true; }
-          }
+  double diag = field == 0 ? inv_dt : 0.0;
+  int rk = if_rank[v];
+  for (int d = 0; d < 6; ++d) {
+    long long nb;
+    int zb = z;
+    if (d == 0) { if (x == 0) continue; nb = v - 1; }
+    else if (d == 1) { if (x + 1 >= P.nx) continue; nb = v + 1; }
+    else if (d == 2) { if (y == 0) continue; nb = v - P.nx; }
+    else if (d == 3) { if (y + 1 >= P.ny) continue; nb = v + P.nx; }
+    else if (d == 4) { if (z == 0) continue; nb = v - P.nxy; zb = z - 1; }
+    else { if (z + 1 >= P.nz) continue; nb = v + P.nxy; zb = z + 1; }
+    uint8_t b = lab[nb];
+    uint8_t kd = kind_of(a, b);
+    bool gb = grounded_d(P, b, zb);
+    double off = 0.0;
+    bool has = false;
+    if (field == 1) {
+      if (gb) {
+        if (kd == K_CONT || kd == K_CONTACT) diag += harm_d(P, a, b);
+        continue;
+      }
+      if (kd == K_CONT) {
+        double g = (a == GR ? P.sigma_gr : (a == EL ? P.kappa : P.sig[a])) * P.gF2;
+        diag += g; off = -g; has = true;
+      } else if (kd == K_CONTACT) {
+        double g = harm_d(P, a, b);
+        diag += g; off = -g; has = true;
+      } else if (kd == K_BV || kd == K_CE || kd == K_STRIP) {
+        double g = coef[2 * n_if + if_dir[6LL * rk + d]];
+        diag += g; off = -g; has = true;
+      }
+    } else {
+      if (gb) continue;
+      if (kd == K_CONT && (a == GR || a == EL)) {
+        double g = (a == GR ? P.d_gr : P.d_el) * P.inv_h2;
+        diag += g; off = -g; has = true;
+      } else if (kd == K_BV || kd == K_CE || kd == K_STRIP) {
+        int f = if_dir[6LL * rk + d];
+        double ca = coef[f], cb = coef[n_if + f];
+        if (if_so[f] == (int32_t)v) {              // graphite c row
+          if (if_kind[f] == IF_BV) { diag += ca; off = cb; has = true; }
+        } else {                                   // electrolyte c row: -(1 - t+) dv
+          diag += -(1.0 - tp) * cb;
+          if (if_kind[f] == IF_BV) { off = -(1.0 - tp) * ca; has = true; }
         }
       }
-      if (has) {
-        int J = agg1[nb];
-        if (J < 0) continue;
-        if (J == I) val[dpos] += off;
-        else val[find_col(col, r0, r1, J)] += off;
-      }
     }
-    val[dpos] += diag;
-    fine_dinv[v] = diag != 0.0 ? 1.0 / diag : 0.0;
+    if (has) val[find_col(ci, r0, r1, (int32_t)nb)] += off;
   }
+  val[find_col(ci, r0, r1, (int32_t)v)] += diag;
+  dinv[v] = diag != 0.0 ? 1.0 / diag : 0.0;
 }
 
-// ---- level l -> l+1 Galerkin (unsmoothed aggregation, R = P^T) --------------
-__global__ void k_galerkin_up(int n_up, const int32_t* __restrict__ ch_ptr,
-                              const int32_t* __restrict__ ch, const int32_t* __restrict__ rp,
-                              const int32_t* __restrict__ cl, const double* __restrict__ vl,
-                              const int32_t* __restrict__ parent, const int32_t* __restrict__ rpu,
-                              const int32_t* __restrict__ clu, double* __restrict__ vu) {
-  int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= n_up) return;
-  int r0 = rpu[I], r1 = rpu[I + 1];
-  for (int k = r0; k < r1; ++k) vu[k] = 0.0;
-  for (int q = ch_ptr[I]; q < ch_ptr[I + 1]; ++q) {
-    int i = ch[q];
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
-      int J = parent[cl[k]];
-      vu[find_col(clu, r0, r1, J)] += vl[k];
-    }
-  }
-}
-
-__global__ void k_dinv(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ cl,
+__global__ void k_dinv(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                        const double* __restrict__ v, double* __restrict__ dinv) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double d = 0.0;
-  for (int k = rp[i]; k < rp[i + 1]; ++k)
-    if (cl[k] == i) d = v[k];
+  int r0 = rp[i], r1 = rp[i + 1];
+  if (r0 < r1) {
+    int k = find_col(ci, r0, r1, i);
+    if (k < r1 && ci[k] == i) d = v[k];
+  }
   dinv[i] = d != 0.0 ? 1.0 / d : 0.0;
+}
+
+// P = (I - w D^-1 A) P0 (smoothed) or P0 (tentative) — one thread per row
+__global__ void k_smooth_P(int n, int smooth, double w, const int32_t* __restrict__ arp,
+                           const int32_t* __restrict__ aci, const double* __restrict__ av,
+                           const double* __restrict__ dinv, const int32_t* __restrict__ parent,
+                           const int32_t* __restrict__ prp, const int32_t* __restrict__ pci,
+                           double* __restrict__ pv) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int p0 = prp[i], p1 = prp[i + 1];
+  if (p0 == p1) return;
+  for (int k = p0; k < p1; ++k) pv[k] = 0.0;
+  pv[find_col(pci, p0, p1, parent[i])] += 1.0;
+  if (!smooth) return;
+  double s = -w * dinv[i];
+  for (int k = arp[i]; k < arp[i + 1]; ++k)
+    pv[find_col(pci, p0, p1, parent[aci[k]])] += s * av[k];
+}
+
+// AP = A P (row-wise), then A_next = P^T (AP): two per-row passes, no atomics
+__global__ void k_ap(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                     const double* __restrict__ av, const int32_t* __restrict__ prp,
+                     const int32_t* __restrict__ pci, const double* __restrict__ pv,
+                     const int32_t* __restrict__ qrp, const int32_t* __restrict__ qci,
+                     double* __restrict__ qv) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int r0 = qrp[i], r1 = qrp[i + 1];
+  if (r0 == r1) return;
+  for (int k = r0; k < r1; ++k) qv[k] = 0.0;
+  for (int k = arp[i]; k < arp[i + 1]; ++k) {
+    int j = aci[k];
+    double a = av[k];
+    for (int m = prp[j]; m < prp[j + 1]; ++m) qv[find_col(qci, r0, r1, pci[m])] += a * pv[m];
+  }
+}
+
+__global__ void k_ptap(int n_next, const int32_t* __restrict__ pt_ptr,
+                       const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
+                       const double* __restrict__ pv, const int32_t* __restrict__ qrp,
+                       const int32_t* __restrict__ qci, const double* __restrict__ qv,
+                       const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
+                       double* __restrict__ nv) {
+  int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= n_next) return;
+  int r0 = nrp[I], r1 = nrp[I + 1];
+  for (int k = r0; k < r1; ++k) nv[k] = 0.0;
+  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) {
+    int i = pt_row[q];
+    double p = pv[pt_idx[q]];
+    for (int m = qrp[i]; m < qrp[i + 1]; ++m) nv[find_col(nci, r0, r1, qci[m])] += p * qv[m];
+  }
 }
 
 // ---- coarsest level: dense LU with partial pivoting in one CTA --------------
@@ -165,85 +197,76 @@ __global__ void k_dense_from_csr(int n, const int32_t* __restrict__ rp, const in
   for (int k = rp[i]; k < rp[i + 1]; ++k) A[(long long)i * n + cl[k]] = v[k];
 }
 
-__global__ void k_dense_lu(int n, double* __restrict__ A, int* __restrict__ piv) {
-  __shared__ double smax[1024];
-  __shared__ int sidx[1024];
+// coarsest level: LU with partial pivoting in shared memory, then the explicit
+// inverse (one thread per column), so every coarse solve is one dense mat-vec
+__global__ void k_dense_inverse(int n, const double* __restrict__ A, double* __restrict__ Ainv) {
+  extern __shared__ double sm[];
+  double* M = sm;                         // n x n
+  int* perm = (int*)(sm + (size_t)n * n);
+  __shared__ int piv_row;
   int tid = threadIdx.x;
+  for (int e = tid; e < n * n; e += blockDim.x) M[e] = A[e];
+  for (int i = tid; i < n; i += blockDim.x) perm[i] = i;
+  __syncthreads();
   for (int k = 0; k < n; ++k) {
-    double best = -1.0;
-    int bi = k;
-    for (int i = k + tid; i < n; i += blockDim.x) {
-      double a = fabs(A[(long long)i * n + k]);
-      if (a > best) { best = a; bi = i; }
+    if (tid == 0) {
+      int p = k;
+      double best = fabs(M[k * n + k]);
+      for (int i = k + 1; i < n; ++i)
+        if (fabs(M[i * n + k]) > best) { best = fabs(M[i * n + k]); p = i; }
+      piv_row = p;
+      if (p != k) { int t = perm[k]; perm[k] = perm[p]; perm[p] = t; }
     }
-    smax[tid] = best;
-    sidx[tid] = bi;
     __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-      if (tid < s) {
-        if (smax[tid + s] > smax[tid] || (smax[tid + s] == smax[tid] && sidx[tid + s] < sidx[tid])) {
-          smax[tid] = smax[tid + s];
-          sidx[tid] = sidx[tid + s];
-        }
-      }
-      __syncthreads();
-    }
-    int p = sidx[0];
-    if (tid == 0) piv[k] = p;
+    int p = piv_row;
     if (p != k)
       for (int j = tid; j < n; j += blockDim.x) {
-        double t = A[(long long)k * n + j];
-        A[(long long)k * n + j] = A[(long long)p * n + j];
-        A[(long long)p * n + j] = t;
+        double t = M[k * n + j]; M[k * n + j] = M[p * n + j]; M[p * n + j] = t;
       }
     __syncthreads();
-    double akk = A[(long long)k * n + k];
-    double inv = akk != 0.0 ? 1.0 / akk : 0.0;
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) A[(long long)i * n + k] *= inv;
+    double d = M[k * n + k];
+    double inv = d != 0.0 ? 1.0 / d : 0.0;
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) M[i * n + k] *= inv;
     __syncthreads();
     int m = n - k - 1;
     for (int e = tid; e < m * m; e += blockDim.x) {
       int i = k + 1 + e / m, j = k + 1 + e % m;
-      A[(long long)i * n + j] -= A[(long long)i * n + k] * A[(long long)k * n + j];
+      M[i * n + j] -= M[i * n + k] * M[k * n + j];
     }
     __syncthreads();
+  }
+  // column j of the inverse: solve L U x = e_{perm^-1 ...}: (P A) = L U, A^-1 = U^-1 L^-1 P
+  for (int j = tid; j < n; j += blockDim.x) {
+    double y[HC_COARSE_MAX];
+    for (int i = 0; i < n; ++i) {
+      double s = perm[i] == j ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= M[i * n + k] * y[k];
+      y[i] = s;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < n; ++k) s -= M[i * n + k] * y[k];
+      double d = M[i * n + i];
+      y[i] = d != 0.0 ? s / d : 0.0;
+    }
+    for (int i = 0; i < n; ++i) Ainv[i * n + j] = y[i];
   }
 }
 
-__global__ void k_dense_solve(int n, const double* __restrict__ A, const int* __restrict__ piv,
-                              const double* __restrict__ b, double* __restrict__ x) {
-  extern __shared__ double y[];
-  int tid = threadIdx.x;
-  for (int i = tid; i < n; i += blockDim.x) y[i] = b[i];
-  __syncthreads();
-  if (tid == 0)
-    for (int k = 0; k < n; ++k) {
-      int p = piv[k];
-      if (p != k) { double t = y[k]; y[k] = y[p]; y[p] = t; }
-    }
-  __syncthreads();
-  for (int k = 0; k < n; ++k) {  // L (unit) forward
-    double yk = y[k];
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) y[i] -= A[(long long)i * n + k] * yk;
-    __syncthreads();
-  }
-  for (int k = n - 1; k >= 0; --k) {  // U backward
-    if (tid == 0) {
-      double d = A[(long long)k * n + k];
-      y[k] = d != 0.0 ? y[k] / d : 0.0;
-    }
-    __syncthreads();
-    double yk = y[k];
-    for (int i = tid; i < k; i += blockDim.x) y[i] -= A[(long long)i * n + k] * yk;
-    __syncthreads();
-  }
-  for (int i = tid; i < n; i += blockDim.x) x[i] = y[i];
+// x = Ainv b, one warp per row
+__global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const double* __restrict__ b,
+                               double* __restrict__ x) {
+  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32) s += Ainv[row * n + j] * b[j];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) x[row] = s;
 }
 
-// ---- V-cycle kernels --------------------------------------------------------
+// ---- cycle kernels ------------------------------------------------------------
 __device__ __forceinline__ double fld(const double2& a, int f) { return f ? a.y : a.x; }
 
-// e = w dinv r (field f), other component zero
 __global__ void k_fine_smooth0(long long n, int f, double w, const double* __restrict__ dinv,
                                const double2* __restrict__ r, double2* __restrict__ e) {
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -252,7 +275,6 @@ __global__ void k_fine_smooth0(long long n, int f, double w, const double* __res
   e[v] = f ? make_double2(0.0, val) : make_double2(val, 0.0);
 }
 
-// e += w dinv (r - t) on field f
 __global__ void k_fine_smooth(long long n, int f, double w, const double* __restrict__ dinv,
                               const double2* __restrict__ r, const double2* __restrict__ t,
                               double2* __restrict__ e) {
@@ -262,27 +284,32 @@ __global__ void k_fine_smooth(long long n, int f, double w, const double* __rest
   if (f) e[v].y += d; else e[v].x += d;
 }
 
-// level-1 rhs: b1[I] = sum over children of (r - t)
-__global__ void k_fine_restrict(int n1, int f, const int32_t* __restrict__ ch_ptr,
-                                const int32_t* __restrict__ ch_vox, const double2* __restrict__ r,
+// b1 = P0^T (r - t) on field f
+__global__ void k_fine_restrict(int n1, int f, const int32_t* __restrict__ pt_ptr,
+                                const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
+                                const double* __restrict__ pv, const double2* __restrict__ r,
                                 const double2* __restrict__ t, double* __restrict__ b1) {
   int I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= n1) return;
   double s = 0.0;
-  for (int q = ch_ptr[I]; q < ch_ptr[I + 1]; ++q) {
-    int v = ch_vox[q];
-    s += fld(r[v], f) - fld(t[v], f);
+  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) {
+    int v = pt_row[q];
+    s += pv[pt_idx[q]] * (fld(r[v], f) - fld(t[v], f));
   }
   b1[I] = s;
 }
 
-__global__ void k_fine_prolong(long long n, int f, const int32_t* __restrict__ agg1,
+// e += alpha P0 x1 on field f
+__global__ void k_fine_prolong(long long n, int f, double alpha, const int32_t* __restrict__ prp,
+                               const int32_t* __restrict__ pci, const double* __restrict__ pv,
                                const double* __restrict__ x1, double2* __restrict__ e) {
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= n) return;
-  int I = agg1[v];
-  if (I < 0) return;
-  if (f) e[v].y += x1[I]; else e[v].x += x1[I];
+  int p0 = prp[v], p1 = prp[v + 1];
+  if (p0 == p1) return;
+  double s = 0.0;
+  for (int m = p0; m < p1; ++m) s += pv[m] * x1[pci[m]];
+  if (f) e[v].y += alpha * s; else e[v].x += alpha * s;
 }
 
 __global__ void k_csr_smooth0(int n, double w, const double* __restrict__ dinv,
@@ -291,7 +318,22 @@ __global__ void k_csr_smooth0(int n, double w, const double* __restrict__ dinv,
   if (i < n) x[i] = w * dinv[i] * b[i];
 }
 
-// y = x + w dinv (b - A x)
+// VS lanes per row (VS = 1, 8 or 32), chosen per level from the mean row length
+template <int VS>
+__global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
+                               const int32_t* __restrict__ cl, const double* __restrict__ v,
+                               const double* __restrict__ dinv, const double* __restrict__ b,
+                               const double* __restrict__ x, double* __restrict__ y, int resid) {
+  long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int i = (int)(gt / VS), lane = (int)(gt % VS);
+  if (i >= n) return;
+  double s = 0.0;
+  for (int k = rp[i] + lane; k < rp[i + 1]; k += VS) s += v[k] * x[cl[k]];
+#pragma unroll
+  for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
+  if (lane == 0) y[i] = resid ? b[i] - s : x[i] + w * dinv[i] * (b[i] - s);
+}
+
 __global__ void k_csr_jacobi(int n, double w, const int32_t* __restrict__ rp,
                              const int32_t* __restrict__ cl, const double* __restrict__ v,
                              const double* __restrict__ dinv, const double* __restrict__ b,
@@ -303,7 +345,6 @@ __global__ void k_csr_jacobi(int n, double w, const int32_t* __restrict__ rp,
   y[i] = x[i] + w * dinv[i] * s;
 }
 
-// res = b - A x
 __global__ void k_csr_resid(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ cl,
                             const double* __restrict__ v, const double* __restrict__ b,
                             const double* __restrict__ x, double* __restrict__ res) {
@@ -314,20 +355,30 @@ __global__ void k_csr_resid(int n, const int32_t* __restrict__ rp, const int32_t
   res[i] = s;
 }
 
-__global__ void k_csr_restrict(int n_up, const int32_t* __restrict__ ch_ptr,
-                               const int32_t* __restrict__ ch, const double* __restrict__ res,
-                               double* __restrict__ b_up) {
+__global__ void k_csr_restrict(int n_next, const int32_t* __restrict__ pt_ptr,
+                               const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
+                               const double* __restrict__ pv, const double* __restrict__ res,
+                               double* __restrict__ b_next) {
   int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= n_up) return;
+  if (I >= n_next) return;
   double s = 0.0;
-  for (int q = ch_ptr[I]; q < ch_ptr[I + 1]; ++q) s += res[ch[q]];
-  b_up[I] = s;
+  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) s += pv[pt_idx[q]] * res[pt_row[q]];
+  b_next[I] = s;
 }
 
-__global__ void k_csr_prolong(int n, const int32_t* __restrict__ parent,
-                              const double* __restrict__ xu, double* __restrict__ x) {
+__global__ void k_csr_prolong(int n, double alpha, const int32_t* __restrict__ prp,
+                              const int32_t* __restrict__ pci, const double* __restrict__ pv,
+                              const double* __restrict__ xn, double* __restrict__ x) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] += xu[parent[i]];
+  if (i >= n) return;
+  double s = 0.0;
+  for (int m = prp[i]; m < prp[i + 1]; ++m) s += pv[m] * xn[pci[m]];
+  x[i] += alpha * s;
+}
+
+__global__ void k_vec_add(int n, const double* __restrict__ a, double* __restrict__ x) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] += a[i];
 }
 
 template <class T>
@@ -336,325 +387,538 @@ void upload(DBuf<T>& d, const std::vector<T>& h) {
   if (!h.empty()) HC_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
 }
 
+// host CSR pattern
+struct HPat {
+  std::vector<int32_t> rp, ci;
+  int n() const { return (int)rp.size() - 1; }
+};
+
+template <class F>
+void parallel_for(int n, F&& f) {
+  int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < 4096) nt = 1;
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      int lo = (int)((long long)n * t / nt), hi = (int)((long long)n * (t + 1) / nt);
+      for (int i = lo; i < hi; ++i) f(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+// rows given as per-row vectors -> CSR (sorted, unique)
+HPat finish(std::vector<std::vector<int32_t>>& rows) {
+  HPat p;
+  p.rp.assign(rows.size() + 1, 0);
+  parallel_for((int)rows.size(), [&](int i) {
+    auto& r = rows[i];
+    std::sort(r.begin(), r.end());
+    r.erase(std::unique(r.begin(), r.end()), r.end());
+  });
+  for (size_t i = 0; i < rows.size(); ++i) p.rp[i + 1] = p.rp[i] + (int32_t)rows[i].size();
+  p.ci.resize(p.rp.back());
+  parallel_for((int)rows.size(), [&](int i) {
+    std::copy(rows[i].begin(), rows[i].end(), p.ci.begin() + p.rp[i]);
+  });
+  return p;
+}
+
+void upload_csr(Csr& c, const HPat& p) {
+  c.n = p.n();
+  c.nnz = (long long)p.ci.size();
+  upload(c.rp, p.rp);
+  upload(c.ci, p.ci);
+  c.v.alloc(std::max<size_t>(p.ci.size(), 1));
+}
+
 }  // namespace
 
-// ============================================================== host: pattern
-// Build the aggregation hierarchy of one field from the host copy of the labels.
-static void build_block(const Operator& op, const std::vector<uint8_t>& lab,
-                        const std::vector<int32_t>& if_rank, const std::vector<int32_t>& if_dir,
-                        const std::vector<int8_t>& if_kind, int field, int coarse_max,
-                        AmgBlock& B) {
+// ============================================================== host: patterns
+static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int field,
+                        const Amg& cfg, AmgBlock& B) {
   const int nx = op.P.nx, ny = op.P.ny, nz = op.P.nz;
   const long long nxy = (long long)nx * ny, nvox = nxy * nz;
   B.field = field;
+  B.alpha = cfg.alpha;
+  B.levels.clear();
   auto in_field = [&](long long v) {
     uint8_t a = lab[v];
     if (field == 0) return a == GR || a == EL;
     return !((v / nxy) == nz - 1 && a == CC);
   };
-  // ---- level 1 unknowns: (2x2x2 block, phase)
-  int bx = (nx + 1) / 2, by = (ny + 1) / 2, bz = (nz + 1) / 2;
-  long long nkeys = (long long)bx * by * bz * N_PHASES;
-  std::vector<int32_t> keynum(nkeys, -1);
-  for (long long v = 0; v < nvox; ++v) {
-    if (!in_field(v)) continue;
-    long long x = v % nx, y = (v / nx) % ny, z = v / nxy;
-    long long key = (((z / 2) * by + y / 2) * bx + x / 2) * N_PHASES + lab[v];
-    keynum[key] = 1;
-  }
-  int n1 = 0;
-  std::vector<int32_t> ubx, uby, ubz, uph;
-  for (long long k = 0; k < nkeys; ++k)
-    if (keynum[k] >= 0) {
-      keynum[k] = n1++;
-      long long blk = k / N_PHASES;
-      uph.push_back((int32_t)(k % N_PHASES));
-      ubx.push_back((int32_t)(blk % bx));
-      uby.push_back((int32_t)((blk / bx) % by));
-      ubz.push_back((int32_t)(blk / ((long long)bx * by)));
-    }
-  std::vector<int32_t> agg1(nvox, -1);
-  std::vector<int32_t> cnt(n1 + 1, 0);
-  for (long long v = 0; v < nvox; ++v) {
-    if (!in_field(v)) continue;
-    long long x = v % nx, y = (v / nx) % ny, z = v / nxy;
-    long long key = (((z / 2) * by + y / 2) * bx + x / 2) * N_PHASES + lab[v];
-    agg1[v] = keynum[key];
-    cnt[agg1[v] + 1]++;
-  }
-  std::vector<int32_t> chp(n1 + 1, 0), chv;
-  for (int i = 0; i < n1; ++i) chp[i + 1] = chp[i] + cnt[i + 1];
-  chv.resize(chp[n1]);
+  // ---- level 0 pattern from the fine couplings (same rules as k_assemble0)
+  HPat A, G;
   {
-    std::vector<int32_t> fill(chp.begin(), chp.end() - 1);
-    for (long long v = 0; v < nvox; ++v)
-      if (agg1[v] >= 0) chv[fill[agg1[v]]++] = (int32_t)v;
-  }
-  // level-1 pattern from fine couplings
-  std::vector<std::vector<int32_t>> rows(n1);
-  for (int I = 0; I < n1; ++I) rows[I].push_back(I);
-  for (long long v = 0; v < nvox; ++v) {
-    int I = agg1[v];
-    if (I < 0) continue;
-    long long x = v % nx, y = (v / nx) % ny, z = v / nxy;
-    uint8_t a = lab[v];
-    for (int d = 0; d < 6; ++d) {
-      long long nb;
-      if (d == 0) { if (x == 0) continue; nb = v - 1; }
-      else if (d == 1) { if (x + 1 >= nx) continue; nb = v + 1; }
-      else if (d == 2) { if (y == 0) continue; nb = v - nx; }
-      else if (d == 3) { if (y + 1 >= ny) continue; nb = v + nx; }
-      else if (d == 4) { if (z == 0) continue; nb = v - nxy; }
-      else { if (z + 1 >= nz) continue; nb = v + nxy; }
-      int J = agg1[nb];
-      if (J < 0 || J == I) continue;
-      uint8_t b = lab[nb];
-      uint8_t kd = kind_of(a, b);
-      bool has;
-      if (field == 1) has = kd == K_CONT || kd == K_CONTACT || kd == K_BV || kd == K_CE || kd == K_STRIP;
-      else has = (kd == K_CONT) || (kd == K_BV);
-      if (has) rows[I].push_back(J);
-    }
-  }
-  auto finish_rows = [](std::vector<std::vector<int32_t>>& rws, std::vector<int32_t>& rp,
-                        std::vector<int32_t>& cl) {
-    rp.assign(rws.size() + 1, 0);
-    cl.clear();
-    for (size_t i = 0; i < rws.size(); ++i) {
-      auto& r = rws[i];
-      std::sort(r.begin(), r.end());
-      r.erase(std::unique(r.begin(), r.end()), r.end());
-      rp[i + 1] = rp[i] + (int32_t)r.size();
-      cl.insert(cl.end(), r.begin(), r.end());
-    }
-  };
-  B.levels.clear();
-  B.levels.emplace_back();
-  {
-    AmgLevel& L = B.levels.back();
-    L.n = n1;
-    std::vector<int32_t> rp, cl;
-    finish_rows(rows, rp, cl);
-    upload(L.rowptr, rp);
-    upload(L.col, cl);
-    L.val.alloc(std::max<size_t>(cl.size(), 1));
-    upload(L.ch_ptr, chp);
-    upload(L.ch, chv);
-    L.nnz = (long long)cl.size();
-    L.h_rowptr = rp;
-    L.h_col = cl;
-  }
-  upload(B.agg1, agg1);
-  B.fine_dinv.alloc(nvox);
-  HC_CUDA(cudaMemset(B.fine_dinv.p, 0, nvox * sizeof(double)));
-  // ---- deeper levels
-  int sx = bx, sy = by, sz = bz;
-  std::vector<int32_t> cbx = ubx, cby = uby, cbz = ubz, cph = uph;
-  while (B.levels.back().n > coarse_max && (sx > 1 || sy > 1 || sz > 1)) {
-    AmgLevel& L = B.levels.back();
-    int nx2 = (sx + 1) / 2, ny2 = (sy + 1) / 2, nz2 = (sz + 1) / 2;
-    long long nk = (long long)nx2 * ny2 * nz2 * N_PHASES;
-    std::vector<int32_t> kn(nk, -1);
-    std::vector<long long> keyof(L.n);
-    for (int i = 0; i < L.n; ++i) {
-      long long key = (((long long)(cbz[i] / 2) * ny2 + cby[i] / 2) * nx2 + cbx[i] / 2) * N_PHASES + cph[i];
-      keyof[i] = key;
-      kn[key] = 1;
-    }
-    int nu = 0;
-    std::vector<int32_t> nbx, nby, nbz, nph;
-    for (long long k = 0; k < nk; ++k)
-      if (kn[k] >= 0) {
-        kn[k] = nu++;
-        long long blk = k / N_PHASES;
-        nph.push_back((int32_t)(k % N_PHASES));
-        nbx.push_back((int32_t)(blk % nx2));
-        nby.push_back((int32_t)((blk / nx2) % ny2));
-        nbz.push_back((int32_t)(blk / ((long long)nx2 * ny2)));
+    std::vector<std::vector<int32_t>> rows(nvox), grows(nvox);
+    parallel_for((int)nvox, [&](int vi) {
+      long long v = vi;
+      if (!in_field(v)) return;
+      auto& r = rows[v];
+      r.push_back((int32_t)v);
+      long long x = v % nx, y = (v / nx) % ny, z = v / nxy;
+      uint8_t a = lab[v];
+      for (int d = 0; d < 6; ++d) {
+        long long nb;
+        if (d == 0) { if (x == 0) continue; nb = v - 1; }
+        else if (d == 1) { if (x + 1 >= nx) continue; nb = v + 1; }
+        else if (d == 2) { if (y == 0) continue; nb = v - nx; }
+        else if (d == 3) { if (y + 1 >= ny) continue; nb = v + nx; }
+        else if (d == 4) { if (z == 0) continue; nb = v - nxy; }
+        else { if (z + 1 >= nz) continue; nb = v + nxy; }
+        if (!in_field(nb)) continue;
+        uint8_t kd = kind_of(a, lab[nb]);
+        if (kd == K_CONT) grows[v].push_back((int32_t)nb);   // same-phase conduction: strong
+        bool has = field == 1 ? (kd == K_CONT || kd == K_CONTACT || kd == K_BV || kd == K_CE ||
+                                 kd == K_STRIP)
+                              : ((kd == K_CONT) || kd == K_BV);
+        if (has) r.push_back((int32_t)nb);
       }
-    std::vector<int32_t> parent(L.n);
-    for (int i = 0; i < L.n; ++i) parent[i] = kn[keyof[i]];
-    std::vector<int32_t> c2(nu + 1, 0);
-    for (int i = 0; i < L.n; ++i) c2[parent[i] + 1]++;
-    std::vector<int32_t> cp(nu + 1, 0), cv(L.n);
-    for (int i = 0; i < nu; ++i) cp[i + 1] = cp[i] + c2[i + 1];
-    {
-      std::vector<int32_t> fill(cp.begin(), cp.end() - 1);
-      for (int i = 0; i < L.n; ++i) cv[fill[parent[i]]++] = i;
-    }
-    std::vector<std::vector<int32_t>> rws(nu);
-    for (int i = 0; i < L.n; ++i)
-      for (int k = L.h_rowptr[i]; k < L.h_rowptr[i + 1]; ++k)
-        rws[parent[i]].push_back(parent[L.h_col[k]]);
-    upload(L.parent, parent);
-    AmgLevel U;
-    U.n = nu;
-    std::vector<int32_t> rp, cl;
-    finish_rows(rws, rp, cl);
-    upload(U.rowptr, rp);
-    upload(U.col, cl);
-    U.val.alloc(std::max<size_t>(cl.size(), 1));
-    upload(U.ch_ptr, cp);
-    upload(U.ch, cv);
-    U.nnz = (long long)cl.size();
-    U.h_rowptr = rp;
-    U.h_col = cl;
-    B.levels.push_back(std::move(U));
-    sx = nx2; sy = ny2; sz = nz2;
-    cbx = nbx; cby = nby; cbz = nbz; cph = nph;
+    });
+    A = finish(rows);
+    G = finish(grows);
   }
-  for (auto& L : B.levels) {
-    L.dinv.alloc(std::max(L.n, 1));
-    L.x.alloc(std::max(L.n, 1));
-    L.x2.alloc(std::max(L.n, 1));
-    L.b.alloc(std::max(L.n, 1));
-    L.res.alloc(std::max(L.n, 1));
-    L.h_rowptr.clear(); L.h_rowptr.shrink_to_fit();
-    L.h_col.clear(); L.h_col.shrink_to_fit();
+  // per-row geometry for aggregation: block coordinates and phase (-1 = empty row)
+  std::vector<int32_t> bx(nvox), by(nvox), bz(nvox), ph(nvox);
+  for (long long v = 0; v < nvox; ++v) {
+    bx[v] = (int32_t)(v % nx);
+    by[v] = (int32_t)((v / nx) % ny);
+    bz[v] = (int32_t)(v / nxy);
+    ph[v] = in_field(v) ? lab[v] : -1;
+  }
+  int sx = nx, sy = ny, sz = nz;
+  int level = 0;
+  while (true) {
+    B.levels.emplace_back();
+    AmgLevel& L = B.levels.back();
+    const int n = A.n();
+    L.n = n;
+    upload_csr(L.A, A);
+    L.dinv.alloc(std::max(n, 1));
+    int active = 0;
+    for (int i = 0; i < n; ++i) active += A.rp[i + 1] > A.rp[i];
+    bool can = sx > 1 || sy > 1 || sz > 1;
+    if (active <= cfg.coarse_max || !can) break;
+    // tentative aggregation: connected components (in the strong same-phase graph G)
+    // of the unknowns sharing a (2x2x2 block, phase) key
+    int nx2 = (sx + 1) / 2, ny2 = (sy + 1) / 2, nz2 = (sz + 1) / 2;
+    std::vector<long long> key(n, -1);
+    for (int i = 0; i < n; ++i)
+      if (ph[i] >= 0)
+        key[i] = (((long long)(bz[i] / 2) * ny2 + by[i] / 2) * nx2 + bx[i] / 2) * N_PHASES + ph[i];
+    std::vector<int32_t> uf(n);
+    std::iota(uf.begin(), uf.end(), 0);
+    // connectivity splitting keeps disconnected same-phase pieces apart; at the top of
+    // the hierarchy (few blocks left) pieces are merged so the coarsest level stays small
+    const bool split = (long long)nx2 * ny2 * nz2 > 64;
+    auto find = [&](int32_t i) {
+      while (uf[i] != i) { uf[i] = uf[uf[i]]; i = uf[i]; }
+      return i;
+    };
+    for (int i = 0; i < n; ++i) {
+      if (key[i] < 0) continue;
+      for (int k = G.rp[i]; k < G.rp[i + 1]; ++k) {
+        int j = G.ci[k];
+        if (key[j] != key[i]) continue;
+        int a_ = find(i), b_ = find(j);
+        if (!split) continue;
+        if (a_ != b_) uf[std::max(a_, b_)] = std::min(a_, b_);
+      }
+    }
+    std::vector<std::pair<long long, int32_t>> order;
+    order.reserve(n);
+    for (int i = 0; i < n; ++i)
+      if (key[i] >= 0) order.emplace_back(key[i], split ? find(i) : 0);
+    std::vector<int32_t> parent(n, -1);
+    int nn = 0;
+    std::vector<int32_t> nbx, nby, nbz, nph;
+    {
+      std::vector<std::pair<std::pair<long long, int32_t>, int32_t>> tup;
+      tup.reserve(order.size());
+      for (int i = 0, q = 0; i < n; ++i)
+        if (key[i] >= 0) tup.push_back({order[q++], i});
+      std::sort(tup.begin(), tup.end());
+      for (size_t q = 0; q < tup.size(); ++q) {
+        if (q == 0 || tup[q].first != tup[q - 1].first) {
+          long long k = tup[q].first.first;
+          long long blk = k / N_PHASES;
+          nph.push_back((int32_t)(k % N_PHASES));
+          nbx.push_back((int32_t)(blk % nx2));
+          nby.push_back((int32_t)((blk / nx2) % ny2));
+          nbz.push_back((int32_t)(blk / ((long long)nx2 * ny2)));
+          ++nn;
+        }
+        parent[tup[q].second] = nn - 1;
+      }
+    }
+    // strong graph of the next level: quotient of G by the aggregation
+    HPat Gn;
+    {
+      std::vector<std::vector<int32_t>> rows(nn);
+      for (int i = 0; i < n; ++i) {
+        if (parent[i] < 0) continue;
+        for (int k = G.rp[i]; k < G.rp[i + 1]; ++k) {
+          int pj = parent[G.ci[k]];
+          if (pj >= 0 && pj != parent[i]) rows[parent[i]].push_back(pj);
+        }
+      }
+      Gn = finish(rows);
+    }
+    upload(L.parent, parent);
+    // prolongator pattern: parent(i) plus (smoothed) the parents of row i's columns
+    const bool smooth = level < cfg.sa_levels;
+    HPat Pp;
+    {
+      std::vector<std::vector<int32_t>> rows(n);
+      parallel_for(n, [&](int i) {
+        if (parent[i] < 0) return;
+        rows[i].push_back(parent[i]);
+        if (smooth)
+          for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) rows[i].push_back(parent[A.ci[k]]);
+      });
+      Pp = finish(rows);
+    }
+    upload_csr(L.P, Pp);
+    // transpose lists of P
+    std::vector<int32_t> tp(nn + 1, 0), trow(Pp.ci.size()), tidx(Pp.ci.size());
+    for (int32_t c : Pp.ci) tp[c + 1]++;
+    for (int I = 0; I < nn; ++I) tp[I + 1] += tp[I];
+    {
+      std::vector<int32_t> fill(tp.begin(), tp.end() - 1);
+      for (int i = 0; i < n; ++i)
+        for (int m = Pp.rp[i]; m < Pp.rp[i + 1]; ++m) {
+          int q = fill[Pp.ci[m]]++;
+          trow[q] = i;
+          tidx[q] = m;
+        }
+    }
+    upload(L.pt_ptr, tp);
+    upload(L.pt_row, trow);
+    upload(L.pt_idx, tidx);
+    // AP = A P pattern, then next-level pattern P^T (AP)
+    HPat AP;
+    {
+      std::vector<std::vector<int32_t>> rows(n);
+      parallel_for(n, [&](int i) {
+        auto& r = rows[i];
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+          int j = A.ci[k];
+          for (int m = Pp.rp[j]; m < Pp.rp[j + 1]; ++m) r.push_back(Pp.ci[m]);
+        }
+      });
+      AP = finish(rows);
+    }
+    upload_csr(L.AP, AP);
+    HPat An;
+    {
+      std::vector<std::vector<int32_t>> rows(nn);
+      parallel_for(nn, [&](int I) {
+        auto& r = rows[I];
+        for (int q = tp[I]; q < tp[I + 1]; ++q) {
+          int i = trow[q];
+          r.insert(r.end(), AP.ci.begin() + AP.rp[i], AP.ci.begin() + AP.rp[i + 1]);
+        }
+      });
+      An = finish(rows);
+    }
+    if (getenv("HC_AMG_VERBOSE"))
+      fprintf(stderr, "amg field %d level %d: n=%d active=%d nnz=%zu P.nnz=%zu -> next n=%d nnz=%zu\n",
+              field, level, n, active, A.ci.size(), Pp.ci.size(), nn, An.ci.size());
+    A = std::move(An);
+    G = std::move(Gn);
+    bx = nbx; by = nby; bz = nbz; ph = nph;
+    sx = nx2; sy = ny2; sz = nz2;
+    ++level;
+  }
+  for (size_t l = 1; l < B.levels.size(); ++l) {
+    AmgLevel& L = B.levels[l];
+    int m = std::max(L.n, 1);
+    L.x.alloc(m); L.x2.alloc(m); L.b.alloc(m); L.res.alloc(m); L.acc.alloc(m);
   }
   int nc = B.levels.back().n;
-  B.dense.alloc((size_t)nc * nc);
-  B.piv.alloc(nc);
+  if (nc > HC_COARSE_MAX)
+    throw Error(HC_ERR_CUDA, "aggregation hierarchy left " + std::to_string(nc) +
+                                 " coarsest unknowns (limit " + std::to_string(HC_COARSE_MAX) + ")");
+  B.dense.alloc((size_t)std::max(nc, 1) * std::max(nc, 1));
+  B.dense_inv.alloc((size_t)std::max(nc, 1) * std::max(nc, 1));
 }
 
 Amg* build_amg(const Operator& op) {
   long long nvox = op.P.nvox;
   std::vector<uint8_t> lab(nvox);
   HC_CUDA(cudaMemcpy(lab.data(), op.labels.p, nvox, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> if_rank(nvox), if_dir(op.if_dir.n);
-  std::vector<int8_t> if_kind(op.n_if);
-  HC_CUDA(cudaMemcpy(if_rank.data(), op.if_rank.p, nvox * 4, cudaMemcpyDeviceToHost));
-  if (op.if_dir.n) HC_CUDA(cudaMemcpy(if_dir.data(), op.if_dir.p, op.if_dir.n * 4, cudaMemcpyDeviceToHost));
-  if (op.n_if) HC_CUDA(cudaMemcpy(if_kind.data(), op.if_kind.p, op.n_if, cudaMemcpyDeviceToHost));
   auto amg = std::make_unique<Amg>();
-  build_block(op, lab, if_rank, if_dir, if_kind, 0, amg->coarse_max, amg->blk[0]);
-  build_block(op, lab, if_rank, if_dir, if_kind, 1, amg->coarse_max, amg->blk[1]);
-  amg->t.alloc(nvox);
-  amg->e.alloc(nvox);
-  amg->zp.alloc(nvox);
-  amg->rr.alloc(nvox);
+  if (const char* e = getenv("HC_AMG_NU")) amg->nu = atoi(e);
+  if (const char* e = getenv("HC_AMG_OMEGA")) amg->omega = atof(e);
+  if (const char* e = getenv("HC_AMG_OMEGA_P")) amg->omega_p = atof(e);
+  if (const char* e = getenv("HC_AMG_SA_LEVELS")) amg->sa_levels = atoi(e);
+  if (const char* e = getenv("HC_AMG_ALPHA")) amg->alpha = atof(e);
+  if (const char* e = getenv("HC_AMG_COARSE_MAX")) amg->coarse_max = atoi(e);
+  if (const char* e = getenv("HC_AMG_GAMMA")) amg->gamma = atoi(e);
+  if (const char* e = getenv("HC_AMG_WDEPTH")) amg->wdepth = atoi(e);
+  if (const char* e = getenv("HC_GRAPHS")) amg->use_graphs = atoi(e) != 0;
+  auto t0 = std::chrono::steady_clock::now();
+  build_block(op, lab, 0, *amg, amg->blk[0]);
+  build_block(op, lab, 1, *amg, amg->blk[1]);
+  if (getenv("HC_AMG_VERBOSE"))
+    fprintf(stderr, "amg setup %.3f s\n",
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  for (int f = 0; f < 2; ++f) {
+    amg->rs[f].alloc(nvox);
+    amg->ea[f].alloc(nvox);
+    amg->eb[f].alloc(nvox);
+  }
+  amg->res.alloc(nvox);
+  amg->rc2.alloc(nvox);
   return amg.release();
 }
 
-// Numeric Galerkin products for the current linearization (op.if_coef) and dt.
+// Numeric setup for the current linearization (op.if_coef) and dt.
 void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
   Amg& A = *op.amg;
   for (int f = 0; f < 2; ++f) {
     if (!(blocks & (1 << f))) continue;
     AmgBlock& B = A.blk[f];
-    AmgLevel& L1 = B.levels[0];
-    k_galerkin1<<<nblk(L1.n), TPB, 0, s>>>(op.P, f, L1.n, L1.ch_ptr.p, L1.ch.p, op.labels.p,
-                                           B.agg1.p, op.if_rank.p, op.if_dir.p, op.if_solid.p,
-                                           op.if_kind.p, op.if_coef.p, op.n_if, inv_dt,
-                                           L1.rowptr.p, L1.col.p, L1.val.p, B.fine_dinv.p);
+    AmgLevel& L0 = B.levels[0];
+    k_assemble0<<<nblk(op.P.nvox), TPB, 0, s>>>(op.P, f, op.labels.p, op.if_rank.p, op.if_dir.p,
+                                                op.if_solid.p, op.if_kind.p, op.if_coef.p, op.n_if,
+                                                inv_dt, L0.A.rp.p, L0.A.ci.p, L0.A.v.p, L0.dinv.p); HC_COUNT();
     for (size_t l = 0; l + 1 < B.levels.size(); ++l) {
       AmgLevel& L = B.levels[l];
       AmgLevel& U = B.levels[l + 1];
-      k_galerkin_up<<<nblk(U.n), TPB, 0, s>>>(U.n, U.ch_ptr.p, U.ch.p, L.rowptr.p, L.col.p,
-                                              L.val.p, L.parent.p, U.rowptr.p, U.col.p, U.val.p);
+      if (l > 0) {
+        k_dinv<<<nblk(L.n), TPB, 0, s>>>(L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p); HC_COUNT();
+      }
+      k_smooth_P<<<nblk(L.n), TPB, 0, s>>>(L.n, (int)l < A.sa_levels, A.omega_p, L.A.rp.p, L.A.ci.p,
+                                           L.A.v.p, L.dinv.p, L.parent.p, L.P.rp.p, L.P.ci.p,
+                                           L.P.v.p); HC_COUNT();
+      k_ap<<<nblk(L.n), TPB, 0, s>>>(L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.P.rp.p, L.P.ci.p, L.P.v.p,
+                                     L.AP.rp.p, L.AP.ci.p, L.AP.v.p); HC_COUNT();
+      k_ptap<<<nblk(U.n, 128), 128, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p, L.P.v.p,
+                                            L.AP.rp.p, L.AP.ci.p, L.AP.v.p, U.A.rp.p, U.A.ci.p,
+                                            U.A.v.p); HC_COUNT();
     }
-    for (auto& L : B.levels)
-      k_dinv<<<nblk(L.n), TPB, 0, s>>>(L.n, L.rowptr.p, L.col.p, L.val.p, L.dinv.p);
     AmgLevel& C = B.levels.back();
-    k_dense_from_csr<<<nblk(C.n), TPB, 0, s>>>(C.n, C.rowptr.p, C.col.p, C.val.p, B.dense.p);
-    k_dense_lu<<<1, 1024, 0, s>>>(C.n, B.dense.p, B.piv.p);
+    if (B.levels.size() > 1) {
+      k_dinv<<<nblk(C.n), TPB, 0, s>>>(C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, C.dinv.p); HC_COUNT();
+    }
+    k_dense_from_csr<<<nblk(C.n), TPB, 0, s>>>(C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, B.dense.p); HC_COUNT();
+    size_t smem = (size_t)C.n * C.n * sizeof(double) + (size_t)C.n * sizeof(int);
+    static bool attr = false;
+    if (!attr) {
+      HC_CUDA(cudaFuncSetAttribute(k_dense_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((size_t)HC_COARSE_MAX * HC_COARSE_MAX * 8 + HC_COARSE_MAX * 4)));
+      attr = true;
+    }
+    k_dense_inverse<<<1, 256, smem, s>>>(C.n, B.dense.p, B.dense_inv.p); HC_COUNT();
     HC_CHECK_LAUNCH();
   }
 }
 
-// V-cycle on CSR levels l.. (level index into B.levels); rhs in L.b, result in L.x
-static void vcycle_csr(AmgBlock& B, size_t l, int nu, double w, cudaStream_t s) {
-  AmgLevel& L = B.levels[l];
-  if (l + 1 == B.levels.size()) {
-    k_dense_solve<<<1, 256, L.n * sizeof(double), s>>>(L.n, B.dense.p, B.piv.p, L.b.p, L.x.p);
-    return;
+static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s);
+
+// y = x + w D^-1 (b - A x)  or  (resid) y = b - A x, with lanes-per-row from the density
+static void csr_sweep(const AmgLevel& L, double w, const double* b, const double* x, double* y,
+                      int resid, cudaStream_t s) {
+  double avg = L.n ? (double)L.A.nnz / L.n : 0.0;
+  if (avg <= 12.0) {
+    k_csr_jacobi_v<1><<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p, b, x, y, resid); HC_COUNT();
+  } else if (avg <= 48.0) {
+    k_csr_jacobi_v<8><<<nblk(8LL * L.n), TPB, 0, s>>>(L.n, w, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p, b, x, y, resid); HC_COUNT();
+  } else {
+    k_csr_jacobi_v<32><<<nblk(32LL * L.n), TPB, 0, s>>>(L.n, w, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p, b, x, y, resid); HC_COUNT();
   }
+}
+
+// one cycle at CSR level l >= 1: rhs in L.b, result in L.x
+static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
+  AmgLevel& L = B.levels[l];
   AmgLevel& U = B.levels[l + 1];
-  k_csr_smooth0<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.dinv.p, L.b.p, L.x.p);
-  for (int k = 1; k < nu; ++k) {
-    k_csr_jacobi<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.rowptr.p, L.col.p, L.val.p, L.dinv.p, L.b.p,
-                                           L.x.p, L.x2.p);
+  const double w = A.omega;
+  k_csr_smooth0<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
+  for (int k = 1; k < A.nu; ++k) {
+    csr_sweep(L, w, L.b.p, L.x.p, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
   }
-  k_csr_resid<<<nblk(L.n), TPB, 0, s>>>(L.n, L.rowptr.p, L.col.p, L.val.p, L.b.p, L.x.p, L.res.p);
-  k_csr_restrict<<<nblk(U.n), TPB, 0, s>>>(U.n, U.ch_ptr.p, U.ch.p, L.res.p, U.b.p);
-  vcycle_csr(B, l + 1, nu, w, s);
-  k_csr_prolong<<<nblk(L.n), TPB, 0, s>>>(L.n, L.parent.p, U.x.p, L.x.p);
-  for (int k = 0; k < nu; ++k) {
-    k_csr_jacobi<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.rowptr.p, L.col.p, L.val.p, L.dinv.p, L.b.p,
-                                           L.x.p, L.x2.p);
+  csr_sweep(L, 0.0, L.b.p, L.x.p, L.res.p, 1, s);
+  k_csr_restrict<<<nblk(U.n), TPB, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p, L.P.v.p,
+                                           L.res.p, U.b.p); HC_COUNT();
+  solve_level(A, B, l + 1, s);
+  k_csr_prolong<<<nblk(L.n), TPB, 0, s>>>(L.n, B.alpha, L.P.rp.p, L.P.ci.p, L.P.v.p, U.x.p,
+                                          L.x.p); HC_COUNT();
+  for (int k = 0; k < A.nu; ++k) {
+    csr_sweep(L, w, L.b.p, L.x.p, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
   }
 }
 
-// one V-cycle for field f on the fine grid: e = M_f^{-1} r (field component only)
-static void vcycle_fine(Operator& op, int f, const double2* r, double2* e, double inv_dt,
-                        cudaStream_t s) {
-  Amg& A = *op.amg;
-  AmgBlock& B = A.blk[f];
-  AmgLevel& L1 = B.levels[0];
-  const long long nv = op.P.nvox;
-  const int flags = f ? 0 : (1 | 2);
-  const double w = A.omega;
-  k_fine_smooth0<<<nblk(nv), TPB, 0, s>>>(nv, f, w, B.fine_dinv.p, r, e);
-  for (int k = 1; k < A.nu; ++k) {
-    jvp_grid(op, e, inv_dt, flags, A.t.p, s);
-    k_fine_smooth<<<nblk(nv), TPB, 0, s>>>(nv, f, w, B.fine_dinv.p, r, A.t.p, e);
+// approximate solve at level l >= 1 (rhs L.b -> L.x): gamma cycles on the first
+// wdepth levels, one below, dense LU at the coarsest level
+static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
+  AmgLevel& L = B.levels[l];
+  if (l + 1 == B.levels.size()) {
+    k_dense_matvec<<<nblk(L.n, 8), 256, 0, s>>>(L.n, B.dense_inv.p, L.b.p, L.x.p); HC_COUNT();
+    return;
   }
-  jvp_grid(op, e, inv_dt, flags, A.t.p, s);
-  k_fine_restrict<<<nblk(L1.n), TPB, 0, s>>>(L1.n, f, L1.ch_ptr.p, L1.ch.p, r, A.t.p, L1.b.p);
-  vcycle_csr(B, 0, A.nu, w, s);
-  k_fine_prolong<<<nblk(nv), TPB, 0, s>>>(nv, f, B.agg1.p, L1.x.p, e);
-  for (int k = 0; k < A.nu; ++k) {
-    jvp_grid(op, e, inv_dt, flags, A.t.p, s);
-    k_fine_smooth<<<nblk(nv), TPB, 0, s>>>(nv, f, w, B.fine_dinv.p, r, A.t.p, e);
+  cycle_once(A, B, l, s);
+  int g = (int)l <= A.wdepth ? A.gamma : 1;
+  for (int k = 1; k < g; ++k) {
+    HC_CUDA(cudaMemcpyAsync(L.acc.p, L.x.p, L.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    csr_sweep(L, 0.0, L.b.p, L.acc.p, L.res.p, 1, s);
+    std::swap(L.b.p, L.res.p);
+    cycle_once(A, B, l, s);
+    std::swap(L.b.p, L.res.p);
+    k_vec_add<<<nblk(L.n), TPB, 0, s>>>(L.n, L.acc.p, L.x.p); HC_COUNT();
   }
-  HC_CHECK_LAUNCH();
 }
 
 namespace {
-// rr = T r : electrolyte c row -= t+ * phi row
-__global__ void k_apply_T(DevParams P, const uint8_t* __restrict__ lab, const double2* __restrict__ r,
-                          double2* __restrict__ out) {
+__global__ void k_smooth0_s(long long n, double w, const double* __restrict__ dinv,
+                            const double* __restrict__ r, double* __restrict__ e) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v < n) e[v] = w * dinv[v] * r[v];
+}
+__global__ void k_restrict0_s(int n1, const int32_t* __restrict__ pt_ptr,
+                              const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
+                              const double* __restrict__ pv, const double* __restrict__ res,
+                              double* __restrict__ b1) {
+  int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= n1) return;
+  double s = 0.0;
+  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) s += pv[pt_idx[q]] * res[pt_row[q]];
+  b1[I] = s;
+}
+__global__ void k_prolong0_s(long long n, double alpha, const int32_t* __restrict__ prp,
+                             const int32_t* __restrict__ pci, const double* __restrict__ pv,
+                             const double* __restrict__ x1, double* __restrict__ e) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  int p0 = prp[v], p1 = prp[v + 1];
+  if (p0 == p1) return;
+  double s = 0.0;
+  for (int m = p0; m < p1; ++m) s += pv[m] * x1[pci[m]];
+  e[v] += alpha * s;
+}
+// T r split into scalar field right-hand sides
+__global__ void k_split_T(DevParams P, const uint8_t* __restrict__ lab, const double2* __restrict__ r,
+                          double* __restrict__ rc, double* __restrict__ rp) {
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= P.nvox) return;
   double2 a = r[v];
-  if (lab[v] == EL) a.x -= P.t_plus * a.y;
-  out[v] = a;
+  rc[v] = lab[v] == EL ? a.x - P.t_plus * a.y : a.x;
+  rp[v] = a.y;
 }
-// rc = rr.c - t.c (coupling), stored in .x of out; phi part from zp
-__global__ void k_combine(long long n, const double2* __restrict__ rr, const double2* __restrict__ t,
-                          double2* __restrict__ out) {
+__global__ void k_merge_s(long long n, const double* __restrict__ ec, const double* __restrict__ ep,
+                          double2* __restrict__ z) {
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= n) return;
-  out[v] = make_double2(rr[v].x - t[v].x, 0.0);
-}
-__global__ void k_merge(long long n, const double2* __restrict__ zc, const double2* __restrict__ zp,
-                        double2* __restrict__ z) {
-  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= n) return;
-  z[v] = make_double2(zc[v].x, zp[v].y);
+  if (v < n) z[v] = make_double2(ec ? ec[v] : 0.0, ep[v]);
 }
 }  // namespace
 
+// one V-cycle for block f on the fine grid, scalar vectors: e = M_f^{-1} r.
+// Returns the buffer holding e (one of the block's two ping-pong vectors).
+static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, cudaStream_t s) {
+  Amg& A = *op.amg;
+  AmgBlock& B = A.blk[f];
+  AmgLevel& L0 = B.levels[0];
+  const long long nv = op.P.nvox;
+  const double w = A.omega;
+  const int nb = nblk(nv);
+  FineArgs F{op.labels.p, op.if_rank.p, op.if_dir.p, op.if_coef.p, op.n_if, op.inv_c.p};
+  double* e = A.ea[f].p;
+  double* e2 = A.eb[f].p;
+  auto sweep = [&](int epi, const double* in, double* out) {
+    if (f == 1) {
+      if (epi == EP_SMOOTH)
+        k_fine_op<SM_PHI, EP_SMOOTH><<<nb, TPB, 0, s>>>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out);
+      else
+        k_fine_op<SM_PHI, EP_RESID><<<nb, TPB, 0, s>>>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out);
+    } else {
+      if (epi == EP_SMOOTH)
+        k_fine_op<SM_CONC, EP_SMOOTH><<<nb, TPB, 0, s>>>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out);
+      else
+        k_fine_op<SM_CONC, EP_RESID><<<nb, TPB, 0, s>>>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out);
+    }
+    HC_COUNT();
+  };
+  k_smooth0_s<<<nb, TPB, 0, s>>>(nv, w, L0.dinv.p, r, e); HC_COUNT();
+  if (B.levels.size() == 1) return e;
+  AmgLevel& L1 = B.levels[1];
+  for (int k = 1; k < A.nu; ++k) {
+    sweep(EP_SMOOTH, e, e2);
+    std::swap(e, e2);
+  }
+  sweep(EP_RESID, e, A.res.p);
+  k_restrict0_s<<<nblk(L1.n), TPB, 0, s>>>(L1.n, L0.pt_ptr.p, L0.pt_row.p, L0.pt_idx.p, L0.P.v.p,
+                                           A.res.p, L1.b.p); HC_COUNT();
+  solve_level(A, B, 1, s);
+  k_prolong0_s<<<nb, TPB, 0, s>>>(nv, B.alpha, L0.P.rp.p, L0.P.ci.p, L0.P.v.p, L1.x.p, e); HC_COUNT();
+  for (int k = 0; k < A.nu; ++k) {
+    sweep(EP_SMOOTH, e, e2);
+    std::swap(e, e2);
+  }
+  HC_CHECK_LAUNCH();
+  return e;
+}
+
 // z = M^{-1} r for the full (c, phi) system; mode 0 full, 1 phi block only
-void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mode,
-               cudaStream_t s) {
+static void amg_apply_impl(Operator& op, const double2* r, double2* z, double inv_dt, int mode,
+                           cudaStream_t s) {
   Amg& A = *op.amg;
   const long long nv = op.P.nvox;
+  const int nb = nblk(nv);
+  k_split_T<<<nb, TPB, 0, s>>>(op.P, op.labels.p, r, A.rs[0].p, A.rs[1].p); HC_COUNT();
+  double* ep = vcycle_fine(op, 1, A.rs[1].p, inv_dt, s);
   if (mode == 1) {
-    vcycle_fine(op, 1, r, z, inv_dt, s);
+    k_merge_s<<<nb, TPB, 0, s>>>(nv, nullptr, ep, z); HC_COUNT();
     return;
   }
-  k_apply_T<<<nblk(nv), TPB, 0, s>>>(op.P, op.labels.p, r, A.rr.p);
-  vcycle_fine(op, 1, A.rr.p, A.zp.p, inv_dt, s);     // zp.y = phi correction, zp.x = 0
-  jvp_grid(op, A.zp.p, inv_dt, 2, A.t.p, s);        // t.x = (T J)_cp zp
-  k_combine<<<nblk(nv), TPB, 0, s>>>(nv, A.rr.p, A.t.p, A.e.p);
-  vcycle_fine(op, 0, A.e.p, z, inv_dt, s);           // z.x = c correction
-  k_merge<<<nblk(nv), TPB, 0, s>>>(nv, z, A.zp.p, z);
+  // c-block right-hand side: T r_c - (T J)_cp e_phi
+  FineArgs F{op.labels.p, op.if_rank.p, op.if_dir.p, op.if_coef.p, op.n_if, op.inv_c.p};
+  k_fine_op<SM_CP, EP_RESID><<<nb, TPB, 0, s>>>(op.P, F, nullptr, ep, A.rs[0].p, nullptr, 0.0,
+                                                inv_dt, 0, nullptr, A.rc2.p); HC_COUNT();
+  double* ec = vcycle_fine(op, 0, A.rc2.p, inv_dt, s);
+  k_merge_s<<<nb, TPB, 0, s>>>(nv, ec, ep, z); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 
+// The preconditioner is a fixed kernel sequence for fixed (r, z, mode, dt): it is
+// captured once into a CUDA graph and replayed (the Galerkin values it reads
+// live in device memory, so re-linearization does not invalidate the graph).
+void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mode,
+               cudaStream_t s) {
+  Amg& A = *op.amg;
+  if (!A.use_graphs || s == 0) {
+    amg_apply_impl(op, r, z, inv_dt, mode, s);
+    return;
+  }
+  for (auto& g : A.graphs)
+    if (g.r == r && g.z == z && g.mode == mode && g.inv_dt == inv_dt) {
+      HC_CUDA(cudaGraphLaunch(g.exec, s));
+      g_launch_count += g.n_kernels;
+      return;
+    }
+  AmgGraph g;
+  g.r = r; g.z = z; g.mode = mode; g.inv_dt = inv_dt;
+  unsigned long long c0 = g_launch_count;
+  cudaGraph_t graph;
+  HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  amg_apply_impl(op, r, z, inv_dt, mode, s);
+  HC_CUDA(cudaStreamEndCapture(s, &graph));
+  g.n_kernels = g_launch_count - c0;
+  g_launch_count = c0;
+  HC_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+  HC_CUDA(cudaGraphDestroy(graph));
+  if (A.graphs.size() >= 16) {
+    cudaGraphExecDestroy(A.graphs.front().exec);
+    A.graphs.erase(A.graphs.begin());
+  }
+  A.graphs.push_back(g);
+  HC_CUDA(cudaGraphLaunch(g.exec, s));
+  g_launch_count += g.n_kernels;
+}
 
+Amg::~Amg() {
+  for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+}
 
 }  // namespace hc

@@ -3,34 +3,58 @@
 
 #include "hc_internal.cuh"
 
+#define HC_COARSE_MAX 160
+
 namespace hc {
 
-struct AmgLevel {
+struct Csr {
   int n = 0;
   long long nnz = 0;
-  DBuf<int32_t> rowptr, col;
-  DBuf<double> val, dinv;
-  DBuf<int32_t> ch_ptr, ch;   // children (previous level unknowns, or fine voxels for level 1)
-  DBuf<int32_t> parent;       // unknown -> next coarser unknown
-  DBuf<double> x, x2, b, res;
-  std::vector<int32_t> h_rowptr, h_col;  // setup only
+  DBuf<int32_t> rp, ci;
+  DBuf<double> v;
+};
+
+struct AmgLevel {
+  int n = 0;                             // rows (level 0: one per voxel, empty outside the field)
+  Csr A;                                 // level operator (level 0 only feeds the Galerkin product)
+  DBuf<double> dinv;
+  DBuf<int32_t> parent;                  // tentative aggregate of each row, -1 if empty
+  Csr P;                                 // prolongator to the next level (smoothed aggregation)
+  Csr AP;                                // A P (Galerkin intermediate)
+  DBuf<int32_t> pt_ptr, pt_row, pt_idx;  // P^T: for each coarse unknown, (row, value index) pairs
+  DBuf<double> x, x2, b, res, acc;       // cycle vectors (levels >= 1)
 };
 
 struct AmgBlock {
   int field = 0;                  // 0: c block of T J, 1: phi block of J
-  std::vector<AmgLevel> levels;   // levels[0] is aggregation level 1
-  DBuf<int32_t> agg1;             // fine voxel -> level-1 unknown, -1 outside the field
-  DBuf<double> fine_dinv;         // fine inverse diagonal
-  DBuf<double> dense;             // coarsest LU
-  DBuf<int> piv;
+  double alpha = 1.0;             // coarse-correction scaling
+  std::vector<AmgLevel> levels;   // levels[0] is the fine grid
+  DBuf<double> dense, dense_inv;  // coarsest matrix and its inverse
+};
+
+struct AmgGraph {
+  const double2* r = nullptr;
+  double2* z = nullptr;
+  int mode = 0;
+  double inv_dt = 0.0;
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long n_kernels = 0;
 };
 
 struct Amg {
+  ~Amg();
+  bool use_graphs = true;
+  std::vector<AmgGraph> graphs;
   AmgBlock blk[2];
-  int coarse_max = 256;
+  int coarse_max = 128;       // <= HC_COARSE_MAX (the coarsest inverse lives in shared memory)
   int nu = 2;
-  double omega = 0.6;
-  DBuf<double2> t, e, zp, rr;
+  double omega = 0.6;        // Jacobi smoothing weight
+  double omega_p = 2.0 / 3;  // prolongator smoothing weight
+  int sa_levels = 2;         // smoothed prolongators on the first sa_levels transfers
+  double alpha = 1.0;
+  int gamma = 1;             // cycles per coarse-level solve (2 = W-cycle)
+  int wdepth = 3;
+  DBuf<double> rs[2], ea[2], eb[2], res, rc2;   // fine-level scalar vectors per block
 };
 
 Amg* build_amg(const Operator& op);

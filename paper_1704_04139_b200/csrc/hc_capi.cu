@@ -11,6 +11,7 @@
 #include "hc_solver.cuh"
 
 namespace hc {
+unsigned long long g_launch_count = 0;
 Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
                           const hc_params& hp);
 void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
@@ -19,7 +20,25 @@ void pod_gram(const double* S, const double* w, long long n_dof, long long n_sna
 Operator::~Operator() {
   delete amg;
   delete work;
+  if (stream) cudaStreamDestroy(stream);
+  if (ev_in) cudaEventDestroy(ev_in);
+  if (ev_out) cudaEventDestroy(ev_out);
 }
+
+// Runs solver work on the operator's private stream, ordered after the
+// caller's stream and before anything the caller enqueues afterwards.
+struct StreamJoin {
+  Operator& op;
+  cudaStream_t caller;
+  StreamJoin(Operator& o, cudaStream_t c) : op(o), caller(c) {
+    HC_CUDA(cudaEventRecord(op.ev_in, caller));
+    HC_CUDA(cudaStreamWaitEvent(op.stream, op.ev_in, 0));
+  }
+  ~StreamJoin() {
+    cudaEventRecord(op.ev_out, op.stream);
+    cudaStreamWaitEvent(caller, op.ev_out, 0);
+  }
+};
 }  // namespace hc
 
 using namespace hc;
@@ -170,7 +189,7 @@ int hc_apply(hc_operator* opq, int32_t part, const double* x, const double* n_pl
     if (part == 0 && ntot) {
       DBuf<unsigned long long> first(1);
       HC_CUDA(cudaMemsetAsync(first.p, 0xff, sizeof(unsigned long long), s));
-      k_first_nonfinite<<<(int)((ntot + 255) / 256), 256, 0, s>>>(ntot, out, first.p);
+      k_first_nonfinite<<<(int)((ntot + 255) / 256), 256, 0, s>>>(ntot, out, first.p); HC_COUNT();
       HC_CHECK_LAUNCH();
       unsigned long long f = 0;
       HC_CUDA(cudaMemcpyAsync(&f, first.p, sizeof(f), cudaMemcpyDeviceToHost, s));
@@ -353,7 +372,8 @@ int hc_newton_solve(hc_operator* opq, const double* x_guess, double dt, const do
                     hc_newton_stats* stats, void* stream) {
   return guarded([&] {
     Operator& op = *(Operator*)opq;
-    cudaStream_t s = S(stream);
+    StreamJoin join(op, S(stream));
+    cudaStream_t s = op.stream;
     Work& W = work(op);
     hc_newton_stats st{};
     load_prev(op, x_prev, s);
@@ -370,7 +390,8 @@ int hc_solve_initial_potential(hc_operator* opq, const double* x0, const double*
                                void* stream) {
   return guarded([&] {
     Operator& op = *(Operator*)opq;
-    cudaStream_t s = S(stream);
+    StreamJoin join(op, S(stream));
+    cudaStream_t s = op.stream;
     Work& W = work(op);
     hc_newton_stats st{};
     scatter_packed(op, x0, W.x.p, true, s);
@@ -386,7 +407,8 @@ int hc_step(hc_operator* opq, double* x, double* n_pl, double t, double dt_sugge
   (void)t;
   return guarded([&] {
     Operator& op = *(Operator*)opq;
-    cudaStream_t s = S(stream);
+    StreamJoin join(op, S(stream));
+    cudaStream_t s = op.stream;
     Work& W = work(op);
     hc_newton_stats st{};
     scatter_packed(op, x, W.x.p, true, s);
@@ -404,7 +426,7 @@ int hc_step_host(hc_operator* opq, double* x_host, double* n_pl_host, double t, 
     const long long ntot = op.info.n_c + op.info.n_p, npl = op.info.n_plated;
     if (op.host_x.n < (size_t)ntot) op.host_x.alloc(std::max<long long>(ntot, 1));
     if (op.host_npl.n < (size_t)std::max<long long>(npl, 1)) op.host_npl.alloc(std::max<long long>(npl, 1));
-    cudaStream_t s = 0;
+    cudaStream_t s = op.stream;
     HC_CUDA(cudaMemcpyAsync(op.host_x.p, x_host, ntot * 8, cudaMemcpyHostToDevice, s));
     if (npl) HC_CUDA(cudaMemcpyAsync(op.host_npl.p, n_pl_host, npl * 8, cudaMemcpyHostToDevice, s));
     Work& W = work(op);
@@ -417,6 +439,49 @@ int hc_step_host(hc_operator* opq, double* x_host, double* n_pl_host, double t, 
     HC_CUDA(cudaStreamSynchronize(s));
     if (stats) *stats = st;
     (void)t;
+  });
+}
+
+int hc_launch_count(int64_t* out) {
+  return guarded([&] { *out = (int64_t)g_launch_count; });
+}
+
+int hc_time_kernels(hc_operator* opq, const double* x, const double* n_pl, double beta,
+                    double inv_dt, int32_t iters, int64_t flush_bytes, double* ms_out,
+                    void* stream) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    cudaStream_t s = S(stream);
+    scatter_packed(op, x, op.xg.p, true, s);
+    linearize(op, op.xg.p, n_pl, beta, s);
+    Work& W = work(op);
+    HC_CUDA(cudaMemcpyAsync(W.cprev.p, op.inv_c.p, op.P.nvox * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));  // any finite c_prev will do
+    DBuf<uint8_t> scratch(flush_bytes > 0 ? (size_t)flush_bytes : 0);
+    cudaEvent_t e0, e1;
+    HC_CUDA(cudaEventCreate(&e0));
+    HC_CUDA(cudaEventCreate(&e1));
+    const int parts = PART_LIN | PART_BV | PART_1C | PART_BND | PART_TIME;
+    for (int k = 0; k < 4; ++k) {
+      double acc = 0.0;
+      for (int it = 0; it < iters; ++it) {
+        if (scratch.n) HC_CUDA(cudaMemsetAsync(scratch.p, it & 0xff, scratch.n, s));
+        HC_CUDA(cudaEventRecord(e0, s));
+        if (k < 2)
+          residual_grid(op, op.xg.p, n_pl, -1.0, beta, parts, W.cprev.p, inv_dt, op.outg.p, s,
+                        k == 0 ? 1 : 2);
+        else
+          jvp_grid(op, op.xg.p, inv_dt, 1 | 4, op.outg.p, s, k == 2 ? 1 : 2);
+        HC_CUDA(cudaEventRecord(e1, s));
+        HC_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        HC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        acc += ms;
+      }
+      ms_out[k] = iters ? acc / iters : 0.0;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   });
 }
 
@@ -441,6 +506,6 @@ static void load_prev(Operator& op, const double* x_prev, cudaStream_t s) {
   Work& W = work(op);
   scatter_packed(op, x_prev, op.xg2.p, true, s);
   long long n = op.P.nvox;
-  k_extract_c2<<<(int)((n + 255) / 256), 256, 0, s>>>(n, op.xg2.p, W.cprev.p);
+  k_extract_c2<<<(int)((n + 255) / 256), 256, 0, s>>>(n, op.xg2.p, W.cprev.p); HC_COUNT();
   HC_CHECK_LAUNCH();
 }

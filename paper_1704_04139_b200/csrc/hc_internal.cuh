@@ -48,6 +48,10 @@ struct Error : std::runtime_error {
 
 #define HC_CHECK_LAUNCH() HC_CUDA(cudaGetLastError())
 
+// process-wide count of kernels launched by this library (bench.py's gpu_launches)
+extern unsigned long long g_launch_count;
+#define HC_COUNT() (++::hc::g_launch_count)
+
 // ---- device-side parameter block (passed by value to kernels) -------------------
 struct DevParams {
   int nx, ny, nz;
@@ -212,6 +216,9 @@ struct Operator {
   DBuf<double> host_x, host_npl;  // staging for the host-buffer entry point
   Amg* amg = nullptr;
   Work* work = nullptr;
+  int krylov_log = 0;
+  cudaStream_t stream = nullptr;   // private non-blocking stream (graph capture needs one)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   // optional callback after every accepted Newton iterate (grid layout)
   void (*iterate_hook)(Operator&, const double2*) = nullptr;
   void* hook_ctx = nullptr;
@@ -227,13 +234,13 @@ void gather_packed(const Operator& op, const double2* xg, double* x, cudaStream_
 enum : int { PART_LIN = 1, PART_BV = 2, PART_1C = 4, PART_BND = 8, PART_TIME = 16 };
 void residual_grid(Operator& op, const double2* xg, const double* npl, double mu, double beta,
                    int parts, const double* cprev_scaled, double inv_dt, double2* out,
-                   cudaStream_t s);
+                   cudaStream_t s, int which = 3);  // which: 1 stencil kernel, 2 interface kernel
 void linearize(Operator& op, const double2* xg, const double* npl, double beta, cudaStream_t s);
 // J v with the linearization stored in op.  flags: 1 add mass (inv_dt on c rows),
 // 2 row transform T (electrolyte c row -= t+ phi row), 4 include 1/c terms,
 // 8 phi rows only (c rows written as 0)
 void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2* out,
-              cudaStream_t s);
+              cudaStream_t s, int which = 3);
 double norm2_grid(Operator& op, const double2* v, int field_mask, cudaStream_t s);
 Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
                           const hc_params& hp);

@@ -13,6 +13,7 @@
 #include <cstring>
 
 #include "hc_internal.cuh"
+#include "hc_stencil.cuh"
 
 namespace hc {
 
@@ -513,28 +514,29 @@ __global__ void k_sumsq(long long n, const double2* __restrict__ v, int field_ma
 void scatter_packed(const Operator& op, const double* x, double2* xg, bool c_fill_one,
                     cudaStream_t s) {
   long long nv = op.P.nvox;
-  k_fill<<<blocks_for(nv), TPB, 0, s>>>(nv, xg, c_fill_one ? 1.0 : 0.0, 0.0);
+  k_fill<<<blocks_for(nv), TPB, 0, s>>>(nv, xg, c_fill_one ? 1.0 : 0.0, 0.0); HC_COUNT();
   long long n = std::max(op.info.n_c, op.info.n_p);
   if (n) k_scatter<<<blocks_for(n), TPB, 0, s>>>(op.P, (int)op.info.n_c, (int)op.info.n_p,
-                                                 op.c_vox.p, op.p_vox.p, x, xg);
+                                                 op.c_vox.p, op.p_vox.p, x, xg); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 
 void gather_packed(const Operator& op, const double2* xg, double* x, cudaStream_t s) {
   long long n = std::max(op.info.n_c, op.info.n_p);
   if (n) k_gather<<<blocks_for(n), TPB, 0, s>>>((int)op.info.n_c, (int)op.info.n_p, op.c_vox.p,
-                                                op.p_vox.p, xg, x);
+                                                op.p_vox.p, xg, x); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 
 void residual_grid(Operator& op, const double2* xg, const double* npl, double mu, double beta,
-                   int parts, const double* cprev, double inv_dt, double2* out, cudaStream_t s) {
-  k_residual_stencil<<<blocks_for(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, xg, mu, parts,
-                                                           cprev, inv_dt, out);
-  if ((parts & PART_BV) && op.n_if)
+                   int parts, const double* cprev, double inv_dt, double2* out, cudaStream_t s,
+                   int which) {
+  if (which & 1) k_residual_stencil<<<blocks_for(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, xg, mu, parts,
+                                                           cprev, inv_dt, out); HC_COUNT();
+  if ((which & 2) && (parts & PART_BV) && op.n_if)
     k_residual_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p,
                                                          op.if_el.p, op.if_slot.p, op.if_kind.p,
-                                                         xg, npl, beta, out);
+                                                         xg, npl, beta, out); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 
@@ -542,24 +544,27 @@ void linearize(Operator& op, const double2* xg, const double* npl, double beta, 
   if (op.n_if)
     k_lin_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
                                                     op.if_slot.p, op.if_kind.p, xg, npl, beta,
-                                                    op.if_coef.p);
-  k_lin_invc<<<blocks_for(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, xg, op.inv_c.p);
+                                                    op.if_coef.p); HC_COUNT();
+  k_lin_invc<<<blocks_for(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, xg, op.inv_c.p); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 
 void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2* out,
-              cudaStream_t s) {
-  k_jvp_stencil<<<blocks_for(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, op.inv_c.p, vg, inv_dt,
-                                                      flags, out);
-  if (op.n_if)
+              cudaStream_t s, int which) {
+  if (which & 1) {
+    FineArgs F{op.labels.p, op.if_rank.p, op.if_dir.p, op.if_coef.p, op.n_if, op.inv_c.p};
+    k_fine_op<SM_FULL, EP_STORE><<<blocks_for(op.P.nvox), TPB, 0, s>>>(
+        op.P, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out, nullptr); HC_COUNT();
+  }
+  if (false)
     k_jvp_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
-                                                    op.if_kind.p, op.if_coef.p, vg, flags, out);
+                                                    op.if_kind.p, op.if_coef.p, vg, flags, out); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 
 double norm2_grid(Operator& op, const double2* v, int field_mask, cudaStream_t s) {
   int nb = std::min<long long>(blocks_for(op.P.nvox), 4 * op.n_sm);
-  k_sumsq<<<nb, TPB, 0, s>>>(op.P.nvox, v, field_mask, op.red.p);
+  k_sumsq<<<nb, TPB, 0, s>>>(op.P.nvox, v, field_mask, op.red.p); HC_COUNT();
   HC_CHECK_LAUNCH();
   std::vector<double> h(nb);
   HC_CUDA(cudaMemcpyAsync(h.data(), op.red.p, nb * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -629,7 +634,7 @@ static long long number_mask(const DBuf<int32_t>& mask, DBuf<int32_t>& num, DBuf
   HC_CUDA(cudaStreamSynchronize(s));
   long long count = (long long)last_num + last_mask;
   if (inv) inv->alloc(count);
-  k_finalize_numbering<<<blocks_for(n), TPB, 0, s>>>(n, mask.p, num.p, inv ? inv->p : nullptr);
+  k_finalize_numbering<<<blocks_for(n), TPB, 0, s>>>(n, mask.p, num.p, inv ? inv->p : nullptr); HC_COUNT();
   HC_CHECK_LAUNCH();
   return count;
 }
@@ -680,6 +685,10 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
   cudaStream_t s = 0;
   const DevParams& P = op->P;
 
+  HC_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
+  if (const char* e = getenv("HC_KRYLOV_LOG")) op->krylov_log = atoi(e);
+  HC_CUDA(cudaEventCreateWithFlags(&op->ev_in, cudaEventDisableTiming));
+  HC_CUDA(cudaEventCreateWithFlags(&op->ev_out, cudaEventDisableTiming));
   op->labels.alloc(nvox);
   HC_CUDA(cudaMemcpy(op->labels.p, labels_host, nvox, cudaMemcpyHostToDevice));
 
@@ -690,10 +699,10 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
     DBuf<int> ok(1);
     HC_CUDA(cudaMemsetAsync(touch.p, 0, touch.n, s));
     HC_CUDA(cudaMemsetAsync(ok.p, 0, sizeof(int), s));
-    k_uf_init<<<blocks_for(nvox), TPB, 0, s>>>(P, op->labels.p, par.p);
-    k_uf_merge<<<blocks_for(nvox), TPB, 0, s>>>(P, op->labels.p, par.p);
-    k_uf_touch<<<blocks_for(nvox), TPB, 0, s>>>(P, op->labels.p, par.p, touch.p);
-    k_uf_both<<<blocks_for(nvox), TPB, 0, s>>>(nvox, touch.p, ok.p);
+    k_uf_init<<<blocks_for(nvox), TPB, 0, s>>>(P, op->labels.p, par.p); HC_COUNT();
+    k_uf_merge<<<blocks_for(nvox), TPB, 0, s>>>(P, op->labels.p, par.p); HC_COUNT();
+    k_uf_touch<<<blocks_for(nvox), TPB, 0, s>>>(P, op->labels.p, par.p, touch.p); HC_COUNT();
+    k_uf_both<<<blocks_for(nvox), TPB, 0, s>>>(nvox, touch.p, ok.p); HC_COUNT();
     HC_CHECK_LAUNCH();
     int okh = 0;
     HC_CUDA(cudaMemcpy(&okh, ok.p, sizeof(int), cudaMemcpyDeviceToHost));
@@ -711,7 +720,7 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
 
   // DOF numbering (dofmap.py:84-97)
   DBuf<int32_t> cmask(nvox), pmask(nvox), plmask(nvox), plslot;
-  k_masks<<<blocks_for(nvox), TPB, 0, s>>>(P, op->labels.p, cmask.p, pmask.p, plmask.p);
+  k_masks<<<blocks_for(nvox), TPB, 0, s>>>(P, op->labels.p, cmask.p, pmask.p, plmask.p); HC_COUNT();
   HC_CHECK_LAUNCH();
   op->info.n_c = number_mask(cmask, op->cdof, &op->c_vox, nvox, s);
   op->info.n_p = number_mask(pmask, op->pdof, &op->p_vox, nvox, s);
@@ -727,7 +736,7 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
     HC_CUDA(cudaMemset(err.p, 0, sizeof(int)));
     HC_CUDA(cudaMemset(bad.p, 0xff, sizeof(unsigned long long)));
     if (n_faces)
-      k_face_check<<<blocks_for(n_faces), TPB, 0, s>>>(P, op->labels.p, n_faces, err.p, bad.p);
+      k_face_check<<<blocks_for(n_faces), TPB, 0, s>>>(P, op->labels.p, n_faces, err.p, bad.p); HC_COUNT();
     HC_CHECK_LAUNCH();
     int e = 0;
     unsigned long long fb = 0;
@@ -775,7 +784,7 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
       k_orient<<<blocks_for(ns[k]), TPB, 0, s>>>(P, op->labels.p, lists[k]->p, ns[k], (int8_t)k,
                                                  plslot.p, op->if_solid.p + off,
                                                  op->if_el.p + off, op->if_slot.p + off,
-                                                 op->if_kind.p + off);
+                                                 op->if_kind.p + off); HC_COUNT();
     off += ns[k];
   }
   HC_CHECK_LAUNCH();
@@ -785,14 +794,14 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
     HC_CUDA(cudaMemsetAsync(mark.p, 0, nvox * sizeof(int32_t), s));
     if (op->n_if)
       k_if_mark<<<blocks_for(op->n_if), TPB, 0, s>>>(op->n_if, op->if_solid.p, op->if_el.p,
-                                                      mark.p);
+                                                      mark.p); HC_COUNT();
     HC_CHECK_LAUNCH();
     long long n_ifv = number_mask(mark, op->if_rank, nullptr, nvox, s);
     op->if_dir.alloc(std::max<long long>(6 * n_ifv, 1));
     HC_CUDA(cudaMemsetAsync(op->if_dir.p, 0xff, op->if_dir.n * sizeof(int32_t), s));
     if (op->n_if)
       k_if_dirs<<<blocks_for(op->n_if), TPB, 0, s>>>(P, op->n_if, op->if_solid.p, op->if_el.p,
-                                                      op->if_rank.p, op->if_dir.p);
+                                                      op->if_rank.p, op->if_dir.p); HC_COUNT();
     HC_CHECK_LAUNCH();
   }
   // electrolyte-electrolyte faces (operator.py:187-191), kept for export
@@ -804,7 +813,7 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
     op->elel_hi.alloc(n_elel);
     if (n_elel)
       k_elel_pairs<<<blocks_for(n_elel), TPB, 0, s>>>(P, fel.p, n_elel, op->elel_lo.p,
-                                                      op->elel_hi.p);
+                                                      op->elel_hi.p); HC_COUNT();
     HC_CHECK_LAUNCH();
   }
   // drive faces: working-collector voxels in the z = 0 layer (operator.py:229-235)

@@ -102,10 +102,10 @@ void pod_gram(const double* S, const double* w, long long n_dof, long long n_sna
   int nz = (int)std::max<long long>(1, (n_dof + k_per - 1) / k_per);
   DBuf<double> part((size_t)nz * n * n);
   dim3 grid(tiles, tiles, nz);
-  k_gram<<<grid, NW * 32, 0, s>>>(S, w, n_dof, n, k_per, part.p);
+  k_gram<<<grid, NW * 32, 0, s>>>(S, w, n_dof, n, k_per, part.p); HC_COUNT();
   HC_CHECK_LAUNCH();
   long long nn = (long long)n * n;
-  k_reduce_parts<<<(int)((nn + 255) / 256), 256, 0, s>>>(nn, nz, part.p, G);
+  k_reduce_parts<<<(int)((nn + 255) / 256), 256, 0, s>>>(nn, nz, part.p, G); HC_COUNT();
   HC_CHECK_LAUNCH();
   HC_CUDA(cudaStreamSynchronize(s));
 }

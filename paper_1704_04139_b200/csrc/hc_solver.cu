@@ -254,7 +254,7 @@ static double host_sum(Operator& op, int nb, int off, cudaStream_t s) {
 
 double dot(Operator& op, const double2* a, const double2* b, cudaStream_t s) {
   int nb = red_blocks(op);
-  k_dot2<<<nb, TPB, 0, s>>>(op.P.nvox, a, b, nullptr, nullptr, work(op).part.p);
+  k_dot2<<<nb, TPB, 0, s>>>(op.P.nvox, a, b, nullptr, nullptr, work(op).part.p); HC_COUNT();
   HC_CHECK_LAUNCH();
   return host_sum(op, nb, 0, s);
 }
@@ -263,7 +263,7 @@ void dot2(Operator& op, const double2* a, const double2* b, const double2* c, co
           double& ab, double& cd, cudaStream_t s) {
   int nb = red_blocks(op);
   Work& W = work(op);
-  k_dot2<<<nb, TPB, 0, s>>>(op.P.nvox, a, b, c, d, W.part.p);
+  k_dot2<<<nb, TPB, 0, s>>>(op.P.nvox, a, b, c, d, W.part.p); HC_COUNT();
   HC_CHECK_LAUNCH();
   HC_CUDA(cudaMemcpyAsync(W.parth.data(), W.part.p, 2 * nb * sizeof(double), cudaMemcpyDeviceToHost, s));
   HC_CUDA(cudaStreamSynchronize(s));
@@ -276,7 +276,7 @@ void dot2(Operator& op, const double2* a, const double2* b, const double2* c, co
 double norm_checked(Operator& op, const double2* a, int mask, cudaStream_t s) {
   int nb = red_blocks(op);
   Work& W = work(op);
-  k_sumsq2<<<nb, TPB, 0, s>>>(op.P.nvox, a, W.part.p);
+  k_sumsq2<<<nb, TPB, 0, s>>>(op.P.nvox, a, W.part.p); HC_COUNT();
   HC_CHECK_LAUNCH();
   HC_CUDA(cudaMemcpyAsync(W.parth.data(), W.part.p, 2 * nb * sizeof(double), cudaMemcpyDeviceToHost, s));
   HC_CUDA(cudaStreamSynchronize(s));
@@ -316,17 +316,17 @@ int bicgstab(Operator& op, const double2* b, double2* x, double inv_dt, int mode
     if (rho1 == 0.0 || !std::isfinite(rho1))
       throw Error(HC_ERR_NONCONVERGENCE, "iterative linear solver stalled (rho breakdown)");
     double beta = (rho1 / rho) * (alpha / omega);
-    k_p_update<<<nb, TPB, 0, s>>>(n, beta, omega, W.kr.p, W.kv.p, W.kp.p);
+    k_p_update<<<nb, TPB, 0, s>>>(n, beta, omega, W.kr.p, W.kv.p, W.kp.p); HC_COUNT();
     amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s);
     apply_A(op, W.kph.p, W.kv.p, inv_dt, mode, s);
     double rv = dot(op, W.khat.p, W.kv.p, s);
     if (rv == 0.0 || !std::isfinite(rv))
       throw Error(HC_ERR_NONCONVERGENCE, "iterative linear solver stalled (alpha breakdown)");
     alpha = rho1 / rv;
-    k_axpy<<<nb, TPB, 0, s>>>(n, W.kr.p, -alpha, W.kv.p, W.ks.p);
+    k_axpy<<<nb, TPB, 0, s>>>(n, W.kr.p, -alpha, W.kv.p, W.ks.p); HC_COUNT();
     double snorm = std::sqrt(dot(op, W.ks.p, W.ks.p, s));
     if (snorm <= tol) {
-      k_axpy<<<nb, TPB, 0, s>>>(n, x, alpha, W.kph.p, x);
+      k_axpy<<<nb, TPB, 0, s>>>(n, x, alpha, W.kph.p, x); HC_COUNT();
       HC_CHECK_LAUNCH();
       return it;
     }
@@ -337,10 +337,11 @@ int bicgstab(Operator& op, const double2* b, double2* x, double inv_dt, int mode
     if (tt == 0.0 || !std::isfinite(tt))
       throw Error(HC_ERR_NONCONVERGENCE, "iterative linear solver stalled (omega breakdown)");
     omega = ts / tt;
-    k_x_update<<<nb, TPB, 0, s>>>(n, alpha, W.kph.p, omega, W.ksh.p, x);
-    k_axpy<<<nb, TPB, 0, s>>>(n, W.ks.p, -omega, W.kt.p, W.kr.p);
+    k_x_update<<<nb, TPB, 0, s>>>(n, alpha, W.kph.p, omega, W.ksh.p, x); HC_COUNT();
+    k_axpy<<<nb, TPB, 0, s>>>(n, W.ks.p, -omega, W.kt.p, W.kr.p); HC_COUNT();
     HC_CHECK_LAUNCH();
     rnorm = std::sqrt(dot(op, W.kr.p, W.kr.p, s));
+    if (op.krylov_log) fprintf(stderr, "krylov mode=%d it=%d relres=%.3e alpha=%.3e omega=%.3e\n", mode, it, rnorm / bnorm, alpha, omega);
     if (rnorm <= tol) return it;
     if (omega == 0.0)
       throw Error(HC_ERR_NONCONVERGENCE, "iterative linear solver stalled (omega = 0)");
@@ -354,7 +355,7 @@ int bicgstab(Operator& op, const double2* b, double2* x, double inv_dt, int mode
 
 static double floor_norm(Operator& op, const double2* x, double inv_dt, cudaStream_t s) {
   Work& W = work(op);
-  k_abs_lin<<<nblk(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, x, inv_dt, W.rt.p);
+  k_abs_lin<<<nblk(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, x, inv_dt, W.rt.p); HC_COUNT();
   HC_CHECK_LAUNCH();
   return 1e-13 * norm_checked(op, W.rt.p, 3, s);
 }
@@ -389,13 +390,13 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
   for (int it = 1; it <= cfg.newton_max_iter; ++it) {
     linearize(op, W.x.p, npl, beta, s);
     amg_update(op, inv_dt, 3, s);
-    k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p);
+    k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
     st.krylov_iters += bicgstab(op, W.b.p, W.d.p, inv_dt, 0, cfg.linear_rtol, cfg.krylov_max_iter, s);
     // positivity guard on the concentration block
     double alpha = 1.0;
     {
       int rb = red_blocks(op);
-      k_pos_min<<<rb, TPB, 0, s>>>(op.P, op.labels.p, W.x.p, W.d.p, W.part.p);
+      k_pos_min<<<rb, TPB, 0, s>>>(op.P, op.labels.p, W.x.p, W.d.p, W.part.p); HC_COUNT();
       HC_CHECK_LAUNCH();
       HC_CUDA(cudaMemcpyAsync(W.parth.data(), W.part.p, rb * sizeof(double), cudaMemcpyDeviceToHost, s));
       HC_CUDA(cudaStreamSynchronize(s));
@@ -407,14 +408,14 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
     bool accepted = false;
     double norm_try = INFINITY;
     for (int h = 0; h <= 8; ++h) {
-      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p);
+      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p); HC_COUNT();
       residual_grid(op, W.xt.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.rt.p, s);
       norm_try = norm_checked(op, W.rt.p, 3, s);
       if (std::isfinite(norm_try) && (norm_try <= norm || norm_try <= tol)) { accepted = true; break; }
       alpha *= 0.5;
     }
     if (!accepted) {
-      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p);
+      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p); HC_COUNT();
       residual_grid(op, W.xt.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.rt.p, s);
       norm_try = norm_checked(op, W.rt.p, 3, s);
       if (!std::isfinite(norm_try))
@@ -454,12 +455,12 @@ void initial_potential_grid(Operator& op, const double* npl, double mu, const hc
   for (int it = 1; it <= cfg.newton_max_iter; ++it) {
     linearize(op, W.x.p, npl, 0.0, s);
     amg_update(op, 0.0, 2, s);
-    k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p);
-    k_zero_c<<<nb, TPB, 0, s>>>(n, W.b.p);
+    k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
+    k_zero_c<<<nb, TPB, 0, s>>>(n, W.b.p); HC_COUNT();
     st.krylov_iters += bicgstab(op, W.b.p, W.d.p, 0.0, 1, cfg.linear_rtol, cfg.krylov_max_iter, s);
     double alpha = 1.0, norm_try = INFINITY;
     for (int h = 0; h <= 8; ++h) {
-      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p);
+      k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p); HC_COUNT();
       residual_grid(op, W.xt.p, npl, mu, 0.0, parts, nullptr, 0.0, W.rt.p, s);
       norm_try = norm_checked(op, W.rt.p, 2, s);
       if (std::isfinite(norm_try) && (norm_try <= norm || norm_try <= tol)) break;
@@ -485,7 +486,7 @@ void step_grid(Operator& op, double* npl, double dt_suggest, double mu, const hc
   const long long n = op.P.nvox;
   double dt = std::min(dt_suggest, cfg.dt_max);
   int retries = 0;
-  k_extract_c<<<nblk(n), TPB, 0, s>>>(n, W.x.p, W.cprev.p);
+  k_extract_c<<<nblk(n), TPB, 0, s>>>(n, W.x.p, W.cprev.p); HC_COUNT();
   DBuf<double2>& xprev = W.xprev_store;
   if (!xprev.p) xprev.alloc(n);
   HC_CUDA(cudaMemcpyAsync(xprev.p, W.x.p, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
@@ -516,10 +517,10 @@ void step_grid(Operator& op, double* npl, double dt_suggest, double mu, const hc
     k_plated_update<<<nblk(npls), TPB, 0, s>>>(op.P, npls, op.plated_vox.p, op.if_rank.p, op.if_dir.p,
                                                op.if_solid.p, op.if_el.p, op.if_kind.p, W.x.p, npl,
                                                beta, dt, op.info.face_area / op.host_params.faraday,
-                                               tmp.p, tmp.p + npls);
+                                               tmp.p, tmp.p + npls); HC_COUNT();
     HC_CUDA(cudaMemcpyAsync(npl, tmp.p, npls * sizeof(double), cudaMemcpyDeviceToDevice, s));
     int rb = (int)std::min<long long>(nblk(npls), 1024);
-    k_sum<<<rb, TPB, 0, s>>>(npls, tmp.p + npls, W.part.p);
+    k_sum<<<rb, TPB, 0, s>>>(npls, tmp.p + npls, W.part.p); HC_COUNT();
     HC_CHECK_LAUNCH();
     clamped = host_sum(op, rb, 0, s);
   }

@@ -149,9 +149,11 @@ def ball_union_solid(shape_zyx, radius_mean, gamma_shape, porosity, rng) -> np.n
     nz, ny, nx = shape_zyx
     theta = radius_mean / gamma_shape
     er3 = theta ** 3 * gamma_shape * (gamma_shape + 1) * (gamma_shape + 2)
-    n_mean = -np.log(porosity) * nz * ny * nx / (4.0 / 3.0 * np.pi * er3)
+    m = float(radius_mean)               # centres also fall in a margin around the box
+    ext = np.array([nx + 2 * m, ny + 2 * m, nz + 2 * m])
+    n_mean = -np.log(porosity) * float(np.prod(ext)) / (4.0 / 3.0 * np.pi * er3)
     n = int(rng.poisson(n_mean))
-    centres = rng.random((n, 3)) * np.array([nx, ny, nz], dtype=float)
+    centres = rng.random((n, 3)) * ext - m
     radii = rng.gamma(gamma_shape, theta, size=n)
     f = np.full(shape_zyx, -np.inf)
     for (cx, cy, cz), r in zip(centres, radii):
