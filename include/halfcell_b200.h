@@ -137,6 +137,10 @@ int hc_step_host(hc_operator* op, double* x_host, double* n_pl_host, double t, d
 int hc_pod_gram(const double* S, const double* w, int64_t n_dof, int64_t n_snap, double* G,
                 void* stream);
 
+/* Evict L2 by streaming a `bytes`-sized buffer through it (reads only, so no dirty
+ * lines are left behind); used between timed iterations. */
+int hc_flush_l2(int64_t bytes, void* stream);
+
 /* Number of CUDA kernels this library has launched in the process (bench.py). */
 int hc_launch_count(int64_t* out);
 

@@ -83,6 +83,7 @@ _SIGS = {
                                     ctypes.POINTER(HcSolverConfig),
                                     ctypes.POINTER(HcNewtonStats)]),
     "hc_launch_count": (ctypes.c_int, [c_int64_p]),
+    "hc_flush_l2": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p]),
     "hc_time_kernels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                                        ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),

@@ -59,14 +59,11 @@ __global__ void k_assemble0(DevParams P, int field, const uint8_t* __restrict__ 
                             const double* __restrict__ coef, long long n_if, double inv_dt,
                             const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             double* __restrict__ val, double* __restrict__ dinv) {
-  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= P.nvox) return;
+  int x, y, z, v;
+  if (!vox_index(P, x, y, z, v)) return;
   int r0 = rp[v], r1 = rp[v + 1];
   if (r0 == r1) { dinv[v] = 0.0; return; }
   for (int k = r0; k < r1; ++k) val[k] = 0.0;
-  int x = (int)(v % P.nx);
-  long long t = v / P.nx;
-  int y = (int)(t % P.ny), z = (int)(t / P.ny);
   uint8_t a = lab[v];
   const double tp = P.t_plus;
   double diag = field == 0 ? inv_dt : 0.0;
@@ -381,6 +378,25 @@ __global__ void k_vec_add(int n, const double* __restrict__ a, double* __restric
   if (i < n) x[i] += a[i];
 }
 
+// b[I] = sum_q ptv[q] res[pt_row[q]] (P^T res), 8 lanes per coarse row
+__global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
+                             const int32_t* __restrict__ pt_row, const double* __restrict__ ptv,
+                             const double* __restrict__ res, double* __restrict__ b1) {
+  long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int I = (int)(gt >> 3), lane = (int)(gt & 7);
+  if (I >= n1) return;
+  double s = 0.0;
+  for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += 8) s += ptv[q] * res[pt_row[q]];
+  s += __shfl_down_sync(0xffffffffu, s, 4, 8);
+  s += __shfl_down_sync(0xffffffffu, s, 2, 8);
+  s += __shfl_down_sync(0xffffffffu, s, 1, 8);
+  if (lane == 0) b1[I] = s;
+}
+__global__ void k_gather_ptv(long long n, const int32_t* __restrict__ pt_idx,
+                             const double* __restrict__ pv, double* __restrict__ ptv) {
+  long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q < n) ptv[q] = pv[pt_idx[q]];
+}
 template <class T>
 void upload(DBuf<T>& d, const std::vector<T>& h) {
   d.alloc(h.size());
@@ -565,7 +581,7 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     }
     upload(L.parent, parent);
     // prolongator pattern: parent(i) plus (smoothed) the parents of row i's columns
-    const bool smooth = level < cfg.sa_levels;
+    const bool smooth = level < (field == 0 ? cfg.sa_levels_c : cfg.sa_levels);
     HPat Pp;
     {
       std::vector<std::vector<int32_t>> rows(n);
@@ -594,6 +610,7 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     upload(L.pt_ptr, tp);
     upload(L.pt_row, trow);
     upload(L.pt_idx, tidx);
+    L.ptv.alloc(std::max<size_t>(tidx.size(), 1));
     // AP = A P pattern, then next-level pattern P^T (AP)
     HPat AP;
     {
@@ -648,6 +665,9 @@ Amg* build_amg(const Operator& op) {
   HC_CUDA(cudaMemcpy(lab.data(), op.labels.p, nvox, cudaMemcpyDeviceToHost));
   auto amg = std::make_unique<Amg>();
   if (const char* e = getenv("HC_AMG_NU")) amg->nu = atoi(e);
+  amg->nu_c = amg->nu;
+  if (const char* e = getenv("HC_AMG_NU_C")) amg->nu_c = atoi(e);
+  if (const char* e = getenv("HC_AMG_SA_C")) amg->sa_levels_c = atoi(e);
   if (const char* e = getenv("HC_AMG_OMEGA")) amg->omega = atof(e);
   if (const char* e = getenv("HC_AMG_OMEGA_P")) amg->omega_p = atof(e);
   if (const char* e = getenv("HC_AMG_SA_LEVELS")) amg->sa_levels = atoi(e);
@@ -656,6 +676,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_GAMMA")) amg->gamma = atoi(e);
   if (const char* e = getenv("HC_AMG_WDEPTH")) amg->wdepth = atoi(e);
   if (const char* e = getenv("HC_GRAPHS")) amg->use_graphs = atoi(e) != 0;
+  if (const char* e = getenv("HC_AMG_REFRESH")) amg->refresh = atoi(e);
   auto t0 = std::chrono::steady_clock::now();
   build_block(op, lab, 0, *amg, amg->blk[0]);
   build_block(op, lab, 1, *amg, amg->blk[1]);
@@ -679,7 +700,7 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
     if (!(blocks & (1 << f))) continue;
     AmgBlock& B = A.blk[f];
     AmgLevel& L0 = B.levels[0];
-    k_assemble0<<<nblk(op.P.nvox), TPB, 0, s>>>(op.P, f, op.labels.p, op.if_rank.p, op.if_dir.p,
+    k_assemble0<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, f, op.labels.p, op.if_rank.p, op.if_dir.p,
                                                 op.if_solid.p, op.if_kind.p, op.if_coef.p, op.n_if,
                                                 inv_dt, L0.A.rp.p, L0.A.ci.p, L0.A.v.p, L0.dinv.p); HC_COUNT();
     for (size_t l = 0; l + 1 < B.levels.size(); ++l) {
@@ -688,9 +709,11 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
       if (l > 0) {
         k_dinv<<<nblk(L.n), TPB, 0, s>>>(L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p); HC_COUNT();
       }
-      k_smooth_P<<<nblk(L.n), TPB, 0, s>>>(L.n, (int)l < A.sa_levels, A.omega_p, L.A.rp.p, L.A.ci.p,
+      k_smooth_P<<<nblk(L.n), TPB, 0, s>>>(L.n, (int)l < (f == 0 ? A.sa_levels_c : A.sa_levels), A.omega_p, L.A.rp.p, L.A.ci.p,
                                            L.A.v.p, L.dinv.p, L.parent.p, L.P.rp.p, L.P.ci.p,
                                            L.P.v.p); HC_COUNT();
+      k_gather_ptv<<<nblk((long long)L.P.nnz), TPB, 0, s>>>((long long)L.P.nnz, L.pt_idx.p, L.P.v.p,
+                                                           L.ptv.p); HC_COUNT();
       k_ap<<<nblk(L.n), TPB, 0, s>>>(L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.P.rp.p, L.P.ci.p, L.P.v.p,
                                      L.AP.rp.p, L.AP.ci.p, L.AP.v.p); HC_COUNT();
       k_ptap<<<nblk(U.n, 128), 128, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p, L.P.v.p,
@@ -735,17 +758,17 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   AmgLevel& U = B.levels[l + 1];
   const double w = A.omega;
   k_csr_smooth0<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
-  for (int k = 1; k < A.nu; ++k) {
+  for (int k = 1; k < A.nu_c; ++k) {
     csr_sweep(L, w, L.b.p, L.x.p, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
   }
   csr_sweep(L, 0.0, L.b.p, L.x.p, L.res.p, 1, s);
-  k_csr_restrict<<<nblk(U.n), TPB, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p, L.P.v.p,
-                                           L.res.p, U.b.p); HC_COUNT();
+  k_restrict_v<<<nblk(8LL * U.n), TPB, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.ptv.p, L.res.p,
+                                               U.b.p); HC_COUNT();
   solve_level(A, B, l + 1, s);
   k_csr_prolong<<<nblk(L.n), TPB, 0, s>>>(L.n, B.alpha, L.P.rp.p, L.P.ci.p, L.P.v.p, U.x.p,
                                           L.x.p); HC_COUNT();
-  for (int k = 0; k < A.nu; ++k) {
+  for (int k = 0; k < A.nu_c; ++k) {
     csr_sweep(L, w, L.b.p, L.x.p, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
   }
@@ -776,16 +799,6 @@ __global__ void k_smooth0_s(long long n, double w, const double* __restrict__ di
                             const double* __restrict__ r, double* __restrict__ e) {
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v < n) e[v] = w * dinv[v] * r[v];
-}
-__global__ void k_restrict0_s(int n1, const int32_t* __restrict__ pt_ptr,
-                              const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
-                              const double* __restrict__ pv, const double* __restrict__ res,
-                              double* __restrict__ b1) {
-  int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= n1) return;
-  double s = 0.0;
-  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) s += pv[pt_idx[q]] * res[pt_row[q]];
-  b1[I] = s;
 }
 __global__ void k_prolong0_s(long long n, double alpha, const int32_t* __restrict__ prp,
                              const int32_t* __restrict__ pci, const double* __restrict__ pv,
@@ -823,20 +836,21 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   const long long nv = op.P.nvox;
   const double w = A.omega;
   const int nb = nblk(nv);
-  FineArgs F{op.labels.p, op.if_rank.p, op.if_dir.p, op.if_coef.p, op.n_if, op.inv_c.p};
+  FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p};
+  const dim3 vg = vox_grid(op.P), vb = vox_block();
   double* e = A.ea[f].p;
   double* e2 = A.eb[f].p;
   auto sweep = [&](int epi, const double* in, double* out) {
     if (f == 1) {
       if (epi == EP_SMOOTH)
-        k_fine_op<SM_PHI, EP_SMOOTH><<<nb, TPB, 0, s>>>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out);
+        fine_launch_t<SM_PHI, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
       else
-        k_fine_op<SM_PHI, EP_RESID><<<nb, TPB, 0, s>>>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out);
+        fine_launch_t<SM_PHI, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
     } else {
       if (epi == EP_SMOOTH)
-        k_fine_op<SM_CONC, EP_SMOOTH><<<nb, TPB, 0, s>>>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out);
+        fine_launch_t<SM_CONC, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
       else
-        k_fine_op<SM_CONC, EP_RESID><<<nb, TPB, 0, s>>>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out);
+        fine_launch_t<SM_CONC, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
     }
     HC_COUNT();
   };
@@ -848,8 +862,8 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
     std::swap(e, e2);
   }
   sweep(EP_RESID, e, A.res.p);
-  k_restrict0_s<<<nblk(L1.n), TPB, 0, s>>>(L1.n, L0.pt_ptr.p, L0.pt_row.p, L0.pt_idx.p, L0.P.v.p,
-                                           A.res.p, L1.b.p); HC_COUNT();
+  k_restrict_v<<<nblk(8LL * L1.n), TPB, 0, s>>>(L1.n, L0.pt_ptr.p, L0.pt_row.p, L0.ptv.p, A.res.p,
+                                                L1.b.p); HC_COUNT();
   solve_level(A, B, 1, s);
   k_prolong0_s<<<nb, TPB, 0, s>>>(nv, B.alpha, L0.P.rp.p, L0.P.ci.p, L0.P.v.p, L1.x.p, e); HC_COUNT();
   for (int k = 0; k < A.nu; ++k) {
@@ -873,9 +887,9 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
     return;
   }
   // c-block right-hand side: T r_c - (T J)_cp e_phi
-  FineArgs F{op.labels.p, op.if_rank.p, op.if_dir.p, op.if_coef.p, op.n_if, op.inv_c.p};
-  k_fine_op<SM_CP, EP_RESID><<<nb, TPB, 0, s>>>(op.P, F, nullptr, ep, A.rs[0].p, nullptr, 0.0,
-                                                inv_dt, 0, nullptr, A.rc2.p); HC_COUNT();
+  FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p};
+  fine_launch_t<SM_CP, EP_RESID>(op.P, F, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0, nullptr,
+                               A.rc2.p, op.n_sm, s); HC_COUNT();
   double* ec = vcycle_fine(op, 0, A.rc2.p, inv_dt, s);
   k_merge_s<<<nb, TPB, 0, s>>>(nv, ec, ep, z); HC_COUNT();
   HC_CHECK_LAUNCH();

@@ -22,6 +22,7 @@ struct AmgLevel {
   Csr P;                                 // prolongator to the next level (smoothed aggregation)
   Csr AP;                                // A P (Galerkin intermediate)
   DBuf<int32_t> pt_ptr, pt_row, pt_idx;  // P^T: for each coarse unknown, (row, value index) pairs
+  DBuf<double> ptv;                      // P^T values (gathered after every setup)
   DBuf<double> x, x2, b, res, acc;       // cycle vectors (levels >= 1)
 };
 
@@ -48,12 +49,15 @@ struct Amg {
   AmgBlock blk[2];
   int coarse_max = 128;       // <= HC_COARSE_MAX (the coarsest inverse lives in shared memory)
   int nu = 2;
+  int nu_c = 2;              // smoothing sweeps on the CSR levels
+  int sa_levels_c = 0;       // smoothed transfers of the c block (plain aggregation suffices)
   double omega = 0.6;        // Jacobi smoothing weight
   double omega_p = 2.0 / 3;  // prolongator smoothing weight
   int sa_levels = 2;         // smoothed prolongators on the first sa_levels transfers
   double alpha = 1.0;
   int gamma = 1;             // cycles per coarse-level solve (2 = W-cycle)
   int wdepth = 3;
+  int refresh = 0;          // numeric setup every Newton iteration (1) or once per solve (0)
   DBuf<double> rs[2], ea[2], eb[2], res, rc2;   // fine-level scalar vectors per block
 };
 

@@ -69,7 +69,29 @@ struct DevParams {
   int n_ocp;
   double ocp_soc[HC_MAX_OCP];
   double ocp_v[HC_MAX_OCP];
+  // face-coefficient tables indexed [a * 6 + b] (a: row phase, b: neighbour phase);
+  // grounded neighbours hold phi = 0, so their closure is the ordinary face formula
+  double gP[36];      // phi-row conduction (same phase: sigma_a, contact: harmonic mean) * gF2
+  double gC[36];      // c-row diffusion (graphite / electrolyte same-phase faces)
+  double gMig[36];    // c-row migration coupling to phi (electrolyte-electrolyte)
+  unsigned char ifc[36];  // 1 for interface-kinetics pairs (BV, counter exchange, stripping)
 };
+
+// 3-D launch shape of the per-voxel stencil kernels: a warp spans 32 consecutive
+// x, a block 32 x 8 in the xy plane, blockIdx.z = z.  No 64-bit index division.
+constexpr int VX = 32, VY = 8;
+inline dim3 vox_grid(const DevParams& P) {
+  return dim3((unsigned)((P.nx + VX - 1) / VX), (unsigned)((P.ny + VY - 1) / VY), (unsigned)P.nz);
+}
+inline dim3 vox_block() { return dim3(VX, VY, 1); }
+__device__ __forceinline__ bool vox_index(const DevParams& P, int& x, int& y, int& z, int& v) {
+  x = blockIdx.x * VX + threadIdx.x;
+  y = blockIdx.y * VY + threadIdx.y;
+  z = blockIdx.z;
+  if (x >= P.nx || y >= P.ny) return false;
+  v = (z * P.ny + y) * P.nx + x;
+  return true;
+}
 
 // np.interp on the OCP table (echem/kinetics.py:25-32), clamped at the ends.
 __device__ __host__ inline double ocp_dev(double c, const DevParams& P) {
@@ -211,6 +233,7 @@ struct Operator {
   DBuf<double> cprev;          // c_prev * inv_dt per voxel (time term)
   DBuf<double> npl;            // plated inventory per slot
   DBuf<double> if_coef;        // 3 x n_if Jacobian coefficients (linearized)
+  DBuf<double> if_vcoef;       // the same per interface voxel and direction: [3][6 n_if_vox]
   DBuf<double> inv_c;          // gX / c per electrolyte voxel (linearized)
   DBuf<double> red;            // reduction scratch
   DBuf<double> host_x, host_npl;  // staging for the host-buffer entry point

@@ -273,10 +273,8 @@ __global__ void k_gather(int n_c, int n_p, const int32_t* __restrict__ c_vox,
 __global__ void __launch_bounds__(TPB) k_residual_stencil(
     DevParams P, const uint8_t* __restrict__ lab, const double2* __restrict__ X, double mu,
     int parts, const double* __restrict__ cprev, double inv_dt, double2* __restrict__ out) {
-  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= P.nvox) return;
-  int x, y, z;
-  coords(P, v, x, y, z);
+  int x, y, z, v;
+  if (!vox_index(P, x, y, z, v)) return;
   uint8_t a = lab[v];
   if (grounded(P, a, z)) {
     out[v] = make_double2(0.0, 0.0);
@@ -389,6 +387,21 @@ __global__ void k_lin_iface(DevParams P, long long n_if, const int32_t* __restri
   coef[f] = P.sc * a;
   coef[n_if + f] = P.sc * b;
   coef[2 * n_if + f] = P.sc * g;
+}
+
+// per interface voxel and direction: copy of the face's three coefficients
+// (layout [3][6 * n_if_vox]) so the stencil kernels read them with one load
+__global__ void k_lin_scatter(DevParams P, long long n_if, const int32_t* __restrict__ so,
+                              const int32_t* __restrict__ el, const int32_t* __restrict__ rank,
+                              const double* __restrict__ coef, long long nslot,
+                              double* __restrict__ ifv) {
+  long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (f >= n_if) return;
+  const int s = so[f], e = el[f];
+  const double ca = coef[f], cb = coef[n_if + f], cg = coef[2 * n_if + f];
+  const long long is = 6LL * rank[s] + dir_to(P, s, e), ie = 6LL * rank[e] + dir_to(P, e, s);
+  ifv[is] = ca; ifv[nslot + is] = cb; ifv[2 * nslot + is] = cg;
+  ifv[ie] = ca; ifv[nslot + ie] = cb; ifv[2 * nslot + ie] = cg;
 }
 
 __global__ void k_lin_invc(DevParams P, const uint8_t* __restrict__ lab,
@@ -531,7 +544,7 @@ void gather_packed(const Operator& op, const double2* xg, double* x, cudaStream_
 void residual_grid(Operator& op, const double2* xg, const double* npl, double mu, double beta,
                    int parts, const double* cprev, double inv_dt, double2* out, cudaStream_t s,
                    int which) {
-  if (which & 1) k_residual_stencil<<<blocks_for(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, xg, mu, parts,
+  if (which & 1) k_residual_stencil<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, op.labels.p, xg, mu, parts,
                                                            cprev, inv_dt, out); HC_COUNT();
   if ((which & 2) && (parts & PART_BV) && op.n_if)
     k_residual_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p,
@@ -541,10 +554,15 @@ void residual_grid(Operator& op, const double2* xg, const double* npl, double mu
 }
 
 void linearize(Operator& op, const double2* xg, const double* npl, double beta, cudaStream_t s) {
-  if (op.n_if)
+  if (op.n_if) {
     k_lin_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
                                                     op.if_slot.p, op.if_kind.p, xg, npl, beta,
                                                     op.if_coef.p); HC_COUNT();
+    long long nslot = (long long)op.if_dir.n;
+    k_lin_scatter<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
+                                                      op.if_rank.p, op.if_coef.p, nslot,
+                                                      op.if_vcoef.p); HC_COUNT();
+  }
   k_lin_invc<<<blocks_for(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, xg, op.inv_c.p); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
@@ -552,9 +570,9 @@ void linearize(Operator& op, const double2* xg, const double* npl, double beta, 
 void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2* out,
               cudaStream_t s, int which) {
   if (which & 1) {
-    FineArgs F{op.labels.p, op.if_rank.p, op.if_dir.p, op.if_coef.p, op.n_if, op.inv_c.p};
-    k_fine_op<SM_FULL, EP_STORE><<<blocks_for(op.P.nvox), TPB, 0, s>>>(
-        op.P, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out, nullptr); HC_COUNT();
+    FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p};
+    fine_launch_t<SM_FULL, EP_STORE>(op.P, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out,
+                                   nullptr, op.n_sm, s); HC_COUNT();
   }
   if (false)
     k_jvp_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
@@ -613,6 +631,23 @@ static DevParams make_dev_params(const hc_params& hp, int nx, int ny, int nz, do
     P.ocp_soc[k] = hp.ocp_soc[k];
     P.ocp_v[k] = hp.ocp_v[k];
   }
+  for (int a = 0; a < N_PHASES; ++a)
+    for (int b = 0; b < N_PHASES; ++b) {
+      int i = a * N_PHASES + b;
+      uint8_t k = kind_of((uint8_t)a, (uint8_t)b);
+      P.gP[i] = P.gC[i] = P.gMig[i] = 0.0;
+      P.ifc[i] = (k == K_BV || k == K_CE || k == K_STRIP) ? 1 : 0;
+      if (k == K_CONT) {
+        P.gP[i] = (a == GR ? P.sigma_gr : (a == EL ? P.kappa : P.sig[a])) * P.gF2;
+        if (a == GR) P.gC[i] = P.d_gr * P.inv_h2;
+        if (a == EL) {
+          P.gC[i] = P.d_el * P.inv_h2;
+          P.gMig[i] = P.t_plus * P.kappa * P.gF2;
+        }
+      } else if (k == K_CONTACT) {
+        P.gP[i] = 2.0 * P.sig[a] * P.sig[b] / (P.sig[a] + P.sig[b]) * P.gF2;
+      }
+    }
   return P;
 }
 
@@ -840,6 +875,8 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
   op->cprev.alloc(nvox);
   op->inv_c.alloc(nvox);
   op->if_coef.alloc(std::max<long long>(3 * op->n_if, 1));
+  op->if_vcoef.alloc(3 * op->if_dir.n);
+  HC_CUDA(cudaMemset(op->if_vcoef.p, 0, op->if_vcoef.n * sizeof(double)));
   op->npl.alloc(std::max<long long>(op->info.n_plated, 1));
   op->red.alloc(4096);
   HC_CUDA(cudaDeviceSynchronize());

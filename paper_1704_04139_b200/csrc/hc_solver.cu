@@ -117,11 +117,8 @@ __global__ void k_extract_c(long long n, const double2* __restrict__ x, double* 
 // |A_lin| |x| (+ |c| inv_dt on c rows): the cancellation floor scale (newton.py:62-72)
 __global__ void k_abs_lin(DevParams P, const uint8_t* __restrict__ lab, const double2* __restrict__ X,
                           double inv_dt, double2* __restrict__ out) {
-  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= P.nvox) return;
-  int x = (int)(v % P.nx);
-  long long t = v / P.nx;
-  int y = (int)(t % P.ny), z = (int)(t / P.ny);
+  int x, y, z, v;
+  if (!vox_index(P, x, y, z, v)) return;
   uint8_t a = lab[v];
   if (z == P.nz - 1 && a == CC) { out[v] = make_double2(0.0, 0.0); return; }
   double2 xa = X[v];
@@ -355,7 +352,7 @@ int bicgstab(Operator& op, const double2* b, double2* x, double inv_dt, int mode
 
 static double floor_norm(Operator& op, const double2* x, double inv_dt, cudaStream_t s) {
   Work& W = work(op);
-  k_abs_lin<<<nblk(op.P.nvox), TPB, 0, s>>>(op.P, op.labels.p, x, inv_dt, W.rt.p); HC_COUNT();
+  k_abs_lin<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, op.labels.p, x, inv_dt, W.rt.p); HC_COUNT();
   HC_CHECK_LAUNCH();
   return 1e-13 * norm_checked(op, W.rt.p, 3, s);
 }
@@ -389,7 +386,9 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
   double norm = norm0;
   for (int it = 1; it <= cfg.newton_max_iter; ++it) {
     linearize(op, W.x.p, npl, beta, s);
-    amg_update(op, inv_dt, 3, s);
+    // the preconditioner is rebuilt at the first Newton iteration of every solve; later
+    // iterations reuse it (the Krylov solver sees the exact current Jacobian)
+    if (it == 1 || op.amg->refresh) amg_update(op, inv_dt, 3, s);
     k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
     st.krylov_iters += bicgstab(op, W.b.p, W.d.p, inv_dt, 0, cfg.linear_rtol, cfg.krylov_max_iter, s);
     // positivity guard on the concentration block
@@ -454,7 +453,7 @@ void initial_potential_grid(Operator& op, const double* npl, double mu, const hc
   double norm = norm0;
   for (int it = 1; it <= cfg.newton_max_iter; ++it) {
     linearize(op, W.x.p, npl, 0.0, s);
-    amg_update(op, 0.0, 2, s);
+    if (it == 1 || op.amg->refresh) amg_update(op, 0.0, 2, s);
     k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
     k_zero_c<<<nb, TPB, 0, s>>>(n, W.b.p); HC_COUNT();
     st.krylov_iters += bicgstab(op, W.b.p, W.d.p, 0.0, 1, cfg.linear_rtol, cfg.krylov_max_iter, s);
