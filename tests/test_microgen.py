@@ -1,0 +1,80 @@
+"""Geometry setup: BASELINE ball-union cells and the germ-grain plated layer."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+from scipy import ndimage
+
+from paper_1704_04139_b200.configs import CONFIGS
+from paper_1704_04139_b200.microgen import (CellSpec, ball_union_solid, generate_cell, plate_germs,
+                                           sample_germs)
+from paper_1704_04139_b200.phases import Phase, PhaseGrid
+
+
+def flat_anode_grid(nx=24, ny=24, nz=16, h=1.0, surf_z=7):
+    labels = np.zeros((nz, ny, nx), dtype=np.uint8)
+    labels[: surf_z + 1] = Phase.GRAPHITE
+    return PhaseGrid(labels, h)
+
+
+def test_zero_intensity_no_plating():
+    grid = flat_anode_grid()
+    out = plate_germs(grid, 0.0, 2.2, np.random.default_rng(0))
+    assert np.array_equal(out.labels, grid.labels)
+
+
+def test_plated_voxels_respect_construction_contract():
+    # same contract as the reference test (tests/test_plating.py): every plated voxel
+    # lies within r_s of a germ projection, was electrolyte, and touches graphite
+    grid = flat_anode_grid()
+    out = plate_germs(grid, 0.02, 2.2, np.random.default_rng(11))
+    plated = np.argwhere(out.labels == Phase.PLATED_LI)
+    assert plated.shape[0] > 0
+    germs = sample_germs(24.0, 24.0, 0.02, np.random.default_rng(11))
+    stars = np.array([[gx, gy, 8.0] for gx, gy in germs])
+    for z, y, x in plated:
+        c = (np.array([x, y, z]) + 0.5)
+        assert np.min(np.linalg.norm(stars - c, axis=1)) <= 2.2 + 1e-9
+        assert grid.labels[z, y, x] == Phase.ELECTROLYTE
+        nb = [out.labels[z + dz, y + dy, x + dx]
+              for dz, dy, dx in [(0, 0, 1), (0, 0, -1), (0, 1, 0), (0, -1, 0), (1, 0, 0), (-1, 0, 0)]
+              if 0 <= z + dz < 16 and 0 <= y + dy < 24 and 0 <= x + dx < 24]
+        assert Phase.GRAPHITE in nb
+
+
+def test_germ_count_statistics():
+    counts = [sample_germs(44.0, 44.0, 0.01, np.random.default_rng(1905 + k)).shape[0]
+              for k in range(200)]
+    assert abs(np.mean(counts) - 19.36) <= 3.0 * np.sqrt(19.36) / np.sqrt(200.0)
+
+
+def test_ball_union_hits_porosity_exactly():
+    solid = ball_union_solid((40, 32, 32), 4.0, 4.0, 0.35, np.random.default_rng(0))
+    assert abs(1.0 - solid.mean() - 0.35) < 1.0 / solid.size + 1e-12
+
+
+@pytest.mark.parametrize("name", ["tiny", "medium"])
+def test_config_cells_are_valid_half_cells(name):
+    spec = CONFIGS[name].cell
+    g = generate_cell(spec)
+    lab = g.labels
+    assert lab.shape == (spec.nz, spec.ny, spec.nx)
+    assert np.all(lab[0] == Phase.COLLECTOR_WORKING)
+    assert np.all(lab[-1] == Phase.COLLECTOR_COUNTER)
+    f0 = spec.n_anode + spec.n_separator
+    assert np.all(lab[f0:-1] == Phase.LI_FOIL)
+    assert np.all(lab[spec.n_anode:f0] == Phase.ELECTROLYTE)
+    gr = lab == Phase.GRAPHITE
+    comp, n = ndimage.label(gr, structure=ndimage.generate_binary_structure(3, 1))
+    touching = set(np.unique(comp[1][comp[1] > 0]))
+    assert set(range(1, n + 1)) <= touching        # every graphite piece reaches the collector
+    assert (lab == Phase.PLATED_LI).sum() > 0
+
+
+def test_generation_is_deterministic_and_seeded():
+    spec = CONFIGS["tiny"].cell
+    a, b = generate_cell(spec), generate_cell(spec)
+    assert np.array_equal(a.labels, b.labels)
+    c = generate_cell(dataclasses.replace(spec, seed=spec.seed + 1))
+    assert not np.array_equal(a.labels, c.labels)
