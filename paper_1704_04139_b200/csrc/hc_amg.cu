@@ -677,6 +677,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_WDEPTH")) amg->wdepth = atoi(e);
   if (const char* e = getenv("HC_GRAPHS")) amg->use_graphs = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_REFRESH")) amg->refresh = atoi(e);
+  if (const char* e = getenv("HC_AMG_REFRESH_SOLVES")) amg->refresh_solves = std::max(1, atoi(e));
   auto t0 = std::chrono::steady_clock::now();
   build_block(op, lab, 0, *amg, amg->blk[0]);
   build_block(op, lab, 1, *amg, amg->blk[1]);
@@ -843,14 +844,18 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   auto sweep = [&](int epi, const double* in, double* out) {
     if (f == 1) {
       if (epi == EP_SMOOTH)
-        fine_launch_t<SM_PHI, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+        { if (op.stencil_kind == 2) fine_launch_p<SM_PHI, EP_SMOOTH>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+          else fine_launch_t<SM_PHI, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s); }
       else
-        fine_launch_t<SM_PHI, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+        { if (op.stencil_kind == 2) fine_launch_p<SM_PHI, EP_RESID>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+          else fine_launch_t<SM_PHI, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s); }
     } else {
       if (epi == EP_SMOOTH)
-        fine_launch_t<SM_CONC, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+        { if (op.stencil_kind == 2) fine_launch_p<SM_CONC, EP_SMOOTH>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+          else fine_launch_t<SM_CONC, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s); }
       else
-        fine_launch_t<SM_CONC, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+        { if (op.stencil_kind == 2) fine_launch_p<SM_CONC, EP_RESID>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+          else fine_launch_t<SM_CONC, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s); }
     }
     HC_COUNT();
   };
@@ -888,8 +893,13 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
   }
   // c-block right-hand side: T r_c - (T J)_cp e_phi
   FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p};
-  fine_launch_t<SM_CP, EP_RESID>(op.P, F, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0, nullptr,
-                               A.rc2.p, op.n_sm, s); HC_COUNT();
+  if (op.stencil_kind == 2)
+    fine_launch_p<SM_CP, EP_RESID>(op.P, F, op.lab4.p, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0,
+                                   nullptr, A.rc2.p, op.n_sm, s);
+  else
+    fine_launch_t<SM_CP, EP_RESID>(op.P, F, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0, nullptr,
+                                   A.rc2.p, op.n_sm, s);
+  HC_COUNT();
   double* ec = vcycle_fine(op, 0, A.rc2.p, inv_dt, s);
   k_merge_s<<<nb, TPB, 0, s>>>(nv, ec, ep, z); HC_COUNT();
   HC_CHECK_LAUNCH();
@@ -901,7 +911,7 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
 void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mode,
                cudaStream_t s) {
   Amg& A = *op.amg;
-  if (!A.use_graphs || s == 0) {
+  if (!A.use_graphs || s == 0 || op.capturing) {
     amg_apply_impl(op, r, z, inv_dt, mode, s);
     return;
   }

@@ -58,6 +58,9 @@ struct Amg {
   int gamma = 1;             // cycles per coarse-level solve (2 = W-cycle)
   int wdepth = 3;
   int refresh = 0;          // numeric setup every Newton iteration (1) or once per solve (0)
+  int refresh_solves = 8;   // rebuild once every this many Newton solves (and when dt changes)
+  long long solves = 0;
+  double last_inv_dt = -1.0;
   DBuf<double> rs[2], ea[2], eb[2], res, rc2;   // fine-level scalar vectors per block
 };
 

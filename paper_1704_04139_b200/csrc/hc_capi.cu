@@ -18,6 +18,7 @@ void pod_gram(const double* S, const double* w, long long n_dof, long long n_sna
               cudaStream_t s);
 
 Operator::~Operator() {
+  destroy_krylov_graphs(kg);
   delete amg;
   delete work;
   if (stream) cudaStreamDestroy(stream);

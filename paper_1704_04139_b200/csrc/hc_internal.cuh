@@ -206,6 +206,8 @@ struct DBuf {
 
 struct Amg;   // hc_amg.cu
 struct Work;  // hc_solver.cu
+struct KrylovGraphs;  // hc_krylov.cu
+void destroy_krylov_graphs(KrylovGraphs* g);
 
 // The device-resident operator: geometry, DOF numbering, compacted face lists
 // and the work space of the implicit step.
@@ -216,6 +218,7 @@ struct Operator {
   int n_sm = 148;
 
   DBuf<uint8_t> labels;        // [nvox]
+  DBuf<int32_t> lab4;          // labels widened to 32 bit (cp.async staging)
   DBuf<int32_t> cdof, pdof;    // [nvox], -1 where absent
   DBuf<int32_t> c_vox, p_vox;  // packed index -> voxel
   DBuf<int32_t> plated_vox;    // [n_plated] ascending
@@ -240,6 +243,11 @@ struct Operator {
   Amg* amg = nullptr;
   Work* work = nullptr;
   int krylov_log = 0;
+  int stencil_kind = 2;            // 1: register-prefetch tiles, 2: cp.async ring
+  bool dev_krylov = true;          // device-resident BiCGStab (hc_krylov.cu)
+  int krylov_batch = 4;            // iteration graphs launched per status check
+  bool capturing = false;          // inside a stream capture (no nested capture)
+  KrylovGraphs* kg = nullptr;
   cudaStream_t stream = nullptr;   // private non-blocking stream (graph capture needs one)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   // optional callback after every accepted Newton iterate (grid layout)

@@ -1,0 +1,277 @@
+// Device-resident BiCGStab: scalars live in device memory, dot products are fused
+// into the vector-update kernels as per-block partials finalized by one-thread
+// kernels, and one iteration is a single CUDA graph.  The host launches the
+// iteration graph in batches and reads one status word per batch; kernels become
+// no-ops once the device has declared convergence, so the result is identical to
+// stopping exactly at the converged iteration.
+//
+// Algorithm and breakdown/stall semantics: right-preconditioned BiCGStab as in
+// bicgstab() (hc_solver.cu), which replaces the reference's direct / ILU-LGMRES
+// solve (fvm/newton.py:75-83).
+#include <cmath>
+
+#include "hc_amg.cuh"
+#include "hc_solver.cuh"
+
+namespace hc {
+
+namespace {
+constexpr int TPB = 256;
+// device scalar slots
+enum { S_RHO, S_ALPHA, S_OMEGA, S_RHO1, S_BETA, S_TOL2, S_RN2, S_SN2, S_DONE, S_ITERS, S_ERR,
+       S_EARLY, S_RV, S_TS, S_TT, S_NSLOT };
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-reduce up to two sums into part[blockIdx.x] and part[gridDim.x + blockIdx.x]
+__device__ __forceinline__ void block_part2(double s1, double s2, double* part) {
+  __shared__ double sh[2][32];
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sh[0][w] = s1; sh[1][w] = s2; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    s1 = l < nw ? sh[0][l] : 0.0;
+    s2 = l < nw ? sh[1][l] : 0.0;
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (l == 0) { part[blockIdx.x] = s1; part[gridDim.x + blockIdx.x] = s2; }
+  }
+}
+
+// block-wide sum of nb partials in a fixed order (deterministic); result valid in thread 0
+__device__ __forceinline__ double fin_sum_block(const double* part, int nb) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) s += part[i];
+  s = warp_sum(s);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = s;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = l < (int)(blockDim.x >> 5) ? sh[l] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;
+}
+
+__global__ void k_dev_dot2(long long n, const double* __restrict__ ks, const double2* __restrict__ a,
+                           const double2* __restrict__ b, const double2* __restrict__ c,
+                           const double2* __restrict__ d, double* __restrict__ part) {
+  if (ks[S_DONE] != 0.0) return;
+  double s1 = 0.0, s2 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 x = a[i], y = b[i];
+    s1 += x.x * y.x + x.y * y.y;
+    if (c) {
+      double2 u = c[i], w = d[i];
+      s2 += u.x * w.x + u.y * w.y;
+    }
+  }
+  block_part2(s1, s2, part);
+}
+
+// 0: beta  1: alpha  2: s-norm  3: omega  4: r-norm / next rho   (one block of 256)
+__global__ void k_dev_scalar(int what, int nb, const double* __restrict__ part, double* ks) {
+  if (ks[S_DONE] != 0.0) return;
+  double s1 = 0.0, s2 = 0.0;
+  if (what >= 1) s1 = fin_sum_block(part, nb);
+  if (what >= 3) s2 = fin_sum_block(part + nb, nb);
+  if (threadIdx.x != 0) return;
+  if (what == 0) {
+    double rho1 = ks[S_RHO1];
+    if (rho1 == 0.0 || !isfinite(rho1)) { ks[S_ERR] = 1; ks[S_DONE] = 1; return; }
+    ks[S_BETA] = (rho1 / ks[S_RHO]) * (ks[S_ALPHA] / ks[S_OMEGA]);
+  } else if (what == 1) {
+    double rv = s1;
+    if (rv == 0.0 || !isfinite(rv)) { ks[S_ERR] = 2; ks[S_DONE] = 1; return; }
+    ks[S_ALPHA] = ks[S_RHO1] / rv;
+  } else if (what == 2) {
+    ks[S_SN2] = s1;
+    if (s1 <= ks[S_TOL2]) ks[S_EARLY] = 1;
+  } else if (what == 3) {
+    if (ks[S_EARLY] != 0.0) { ks[S_OMEGA] = 0.0; return; }
+    double ts = s1, tt = s2;
+    if (tt == 0.0 || !isfinite(tt)) { ks[S_ERR] = 3; ks[S_DONE] = 1; return; }
+    ks[S_OMEGA] = ts / tt;
+  } else {
+    double rn2 = s1, rr = s2;
+    ks[S_RN2] = rn2;
+    ks[S_ITERS] += 1.0;
+    ks[S_RHO] = ks[S_RHO1];
+    ks[S_RHO1] = rr;
+    if (ks[S_EARLY] != 0.0 || rn2 <= ks[S_TOL2]) { ks[S_DONE] = 1; return; }
+    if (ks[S_OMEGA] == 0.0) { ks[S_ERR] = 4; ks[S_DONE] = 1; }
+  }
+}
+
+__global__ void k_dev_p(long long n, const double* __restrict__ ks, const double2* __restrict__ r,
+                        const double2* __restrict__ v, double2* __restrict__ p) {
+  if (ks[S_DONE] != 0.0) return;
+  const double beta = ks[S_BETA], omega = ks[S_OMEGA];
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 pi = p[i], ri = r[i], vi = v[i];
+  p[i] = make_double2(ri.x + beta * (pi.x - omega * vi.x), ri.y + beta * (pi.y - omega * vi.y));
+}
+
+// s = r - alpha v, partial ||s||^2
+__global__ void k_dev_s(long long n, const double* __restrict__ ks, const double2* __restrict__ r,
+                        const double2* __restrict__ v, double2* __restrict__ s,
+                        double* __restrict__ part) {
+  if (ks[S_DONE] != 0.0) return;
+  const double alpha = ks[S_ALPHA];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 ri = r[i], vi = v[i];
+    double2 si = make_double2(ri.x - alpha * vi.x, ri.y - alpha * vi.y);
+    s[i] = si;
+    acc += si.x * si.x + si.y * si.y;
+  }
+  block_part2(acc, 0.0, part);
+}
+
+// x += alpha phat + omega shat; r = s - omega t; partials ||r||^2 and <rhat, r>
+__global__ void k_dev_xr(long long n, const double* __restrict__ ks, const double2* __restrict__ ph,
+                         const double2* __restrict__ sh, const double2* __restrict__ s,
+                         const double2* __restrict__ t, const double2* __restrict__ rhat,
+                         double2* __restrict__ x, double2* __restrict__ r, double* __restrict__ part) {
+  if (ks[S_DONE] != 0.0) return;
+  const double alpha = ks[S_ALPHA], omega = ks[S_OMEGA];
+  double a1 = 0.0, a2 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 xi = x[i], pi = ph[i], si = sh[i], s0 = s[i], ti = t[i], h = rhat[i];
+    x[i] = make_double2(xi.x + alpha * pi.x + omega * si.x, xi.y + alpha * pi.y + omega * si.y);
+    double2 ri = make_double2(s0.x - omega * ti.x, s0.y - omega * ti.y);
+    r[i] = ri;
+    a1 += ri.x * ri.x + ri.y * ri.y;
+    a2 += h.x * ri.x + h.y * ri.y;
+  }
+  block_part2(a1, a2, part);
+}
+
+__global__ void k_dev_init(int nb, const double* __restrict__ part, double* ks, double tol2) {
+  double b2 = fin_sum_block(part, nb);
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < S_NSLOT; ++i) ks[i] = 0.0;
+  ks[S_RHO] = ks[S_ALPHA] = ks[S_OMEGA] = 1.0;
+  ks[S_RHO1] = b2;
+  ks[S_TOL2] = tol2 * b2;
+  if (b2 == 0.0) ks[S_DONE] = 1;
+}
+}  // namespace
+
+struct KrylovGraphs {
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // per mode
+  double inv_dt[2] = {-1.0, -1.0};
+  unsigned long long n_kernels[2] = {0, 0};
+  double2* x_ptr[2] = {nullptr, nullptr};
+  DBuf<double> ks, part;
+  double* ks_host = nullptr;
+  ~KrylovGraphs() {
+    for (auto e : exec) if (e) cudaGraphExecDestroy(e);
+    if (ks_host) cudaFreeHost(ks_host);
+  }
+};
+
+void destroy_krylov_graphs(KrylovGraphs* g) { delete g; }
+
+static void apply_A_dev(Operator& op, const double2* v, double2* out, double inv_dt, int mode,
+                        cudaStream_t s) {
+  jvp_grid(op, v, inv_dt, mode == 0 ? (1 | 4) : 8, out, s);
+}
+
+int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int mode, double rtol,
+                 int maxit, cudaStream_t s) {
+  Work& W = work(op);
+  if (!op.kg) op.kg = new KrylovGraphs();
+  KrylovGraphs& G = *op.kg;
+  const long long n = op.P.nvox;
+  const int nb = (int)std::min<long long>((n + TPB - 1) / TPB, 2LL * op.n_sm);
+  if (!G.ks.p) {
+    G.ks.alloc(S_NSLOT);
+    G.part.alloc(4 * nb + 8);
+    HC_CUDA(cudaMallocHost(&G.ks_host, S_NSLOT * sizeof(double)));
+  }
+  // init: x = 0, r = rhat = b, p = v = 0
+  HC_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double2), s));
+  HC_CUDA(cudaMemcpyAsync(W.kr.p, b, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  HC_CUDA(cudaMemcpyAsync(W.khat.p, b, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  HC_CUDA(cudaMemsetAsync(W.kp.p, 0, n * sizeof(double2), s));
+  HC_CUDA(cudaMemsetAsync(W.kv.p, 0, n * sizeof(double2), s));
+  HC_CUDA(cudaMemsetAsync(G.ks.p, 0, S_NSLOT * sizeof(double), s));
+  k_dev_dot2<<<nb, TPB, 0, s>>>(n, G.ks.p, b, b, nullptr, nullptr, G.part.p); HC_COUNT();
+  k_dev_init<<<1, 256, 0, s>>>(nb, G.part.p, G.ks.p, rtol * rtol); HC_COUNT();
+  // (re)capture the iteration graph for this mode / dt
+  if (!G.exec[mode] || G.inv_dt[mode] != inv_dt) {
+    if (G.exec[mode]) cudaGraphExecDestroy(G.exec[mode]);
+    unsigned long long c0 = g_launch_count;
+    cudaGraph_t graph;
+    op.capturing = true;
+    HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    double* ks = G.ks.p;
+    double* part = G.part.p;
+    k_dev_scalar<<<1, 256, 0, s>>>(0, nb, part, ks); HC_COUNT();
+    k_dev_p<<<(int)((n + TPB - 1) / TPB), TPB, 0, s>>>(n, ks, W.kr.p, W.kv.p, W.kp.p); HC_COUNT();
+    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s);
+    apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
+    k_dev_dot2<<<nb, TPB, 0, s>>>(n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part); HC_COUNT();
+    k_dev_scalar<<<1, 256, 0, s>>>(1, nb, part, ks); HC_COUNT();
+    k_dev_s<<<nb, TPB, 0, s>>>(n, ks, W.kr.p, W.kv.p, W.ks.p, part); HC_COUNT();
+    k_dev_scalar<<<1, 256, 0, s>>>(2, nb, part, ks); HC_COUNT();
+    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s);
+    apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
+    k_dev_dot2<<<nb, TPB, 0, s>>>(n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part); HC_COUNT();
+    k_dev_scalar<<<1, 256, 0, s>>>(3, nb, part, ks); HC_COUNT();
+    k_dev_xr<<<nb, TPB, 0, s>>>(n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
+                                part); HC_COUNT();
+    k_dev_scalar<<<1, 256, 0, s>>>(4, nb, part, ks); HC_COUNT();
+    HC_CUDA(cudaStreamEndCapture(s, &graph));
+    op.capturing = false;
+    G.n_kernels[mode] = g_launch_count - c0;
+    g_launch_count = c0;
+    HC_CUDA(cudaGraphInstantiate(&G.exec[mode], graph, 0));
+    HC_CUDA(cudaGraphDestroy(graph));
+    G.inv_dt[mode] = inv_dt;
+    G.x_ptr[mode] = x;
+  }
+  if (G.x_ptr[mode] != x) throw Error(HC_ERR_ARGUMENT, "bicgstab_dev: solution buffer changed");
+  int done_iters = 0;
+  const int batch = op.krylov_batch;
+  while (true) {
+    for (int k = 0; k < batch; ++k) {
+      HC_CUDA(cudaGraphLaunch(G.exec[mode], s));
+      g_launch_count += G.n_kernels[mode];
+    }
+    HC_CUDA(cudaMemcpyAsync(G.ks_host, G.ks.p, S_NSLOT * sizeof(double), cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+    const double* h = G.ks_host;
+    done_iters = (int)h[S_ITERS];
+    if (h[S_ERR] != 0.0) {
+      char msg[128];
+      snprintf(msg, sizeof msg, "iterative linear solver stalled (breakdown %d at iteration %d)",
+               (int)h[S_ERR], done_iters);
+      throw Error(HC_ERR_NONCONVERGENCE, msg);
+    }
+    if (h[S_DONE] != 0.0) break;
+    if (done_iters >= maxit) {
+      char msg[160];
+      snprintf(msg, sizeof msg, "iterative linear solver stalled (info=%d, relres=%.3e)", maxit,
+               std::sqrt(h[S_RN2] / std::max(h[S_TOL2] / 1e-300, 1e-300)));
+      throw Error(HC_ERR_NONCONVERGENCE, msg);
+    }
+  }
+  return done_iters;
+}
+
+}  // namespace hc

@@ -544,8 +544,14 @@ void gather_packed(const Operator& op, const double2* xg, double* x, cudaStream_
 void residual_grid(Operator& op, const double2* xg, const double* npl, double mu, double beta,
                    int parts, const double* cprev, double inv_dt, double2* out, cudaStream_t s,
                    int which) {
-  if (which & 1) k_residual_stencil<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, op.labels.p, xg, mu, parts,
-                                                           cprev, inv_dt, out); HC_COUNT();
+  if (which & 1) {
+    if (op.stencil_kind == 2)
+      res_launch_p(op.P, op.lab4.p, xg, mu, parts, cprev, inv_dt, out, op.n_sm, s);
+    else
+      k_residual_stencil<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, op.labels.p, xg, mu, parts,
+                                                               cprev, inv_dt, out);
+    HC_COUNT();
+  }
   if ((which & 2) && (parts & PART_BV) && op.n_if)
     k_residual_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p,
                                                          op.if_el.p, op.if_slot.p, op.if_kind.p,
@@ -571,8 +577,13 @@ void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2
               cudaStream_t s, int which) {
   if (which & 1) {
     FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p};
-    fine_launch_t<SM_FULL, EP_STORE>(op.P, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out,
-                                   nullptr, op.n_sm, s); HC_COUNT();
+    if (op.stencil_kind == 2)
+      fine_launch_p<SM_FULL, EP_STORE>(op.P, F, op.lab4.p, vg, nullptr, nullptr, nullptr, 0.0, inv_dt,
+                                       flags, out, nullptr, op.n_sm, s);
+    else
+      fine_launch_t<SM_FULL, EP_STORE>(op.P, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out,
+                                       nullptr, op.n_sm, s);
+    HC_COUNT();
   }
   if (false)
     k_jvp_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
@@ -722,10 +733,14 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
 
   HC_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
   if (const char* e = getenv("HC_KRYLOV_LOG")) op->krylov_log = atoi(e);
+  if (const char* e = getenv("HC_DEV_KRYLOV")) op->dev_krylov = atoi(e) != 0;
+  if (const char* e = getenv("HC_STENCIL")) op->stencil_kind = atoi(e);
+  if (const char* e = getenv("HC_KRYLOV_BATCH")) op->krylov_batch = std::max(1, atoi(e));
   HC_CUDA(cudaEventCreateWithFlags(&op->ev_in, cudaEventDisableTiming));
   HC_CUDA(cudaEventCreateWithFlags(&op->ev_out, cudaEventDisableTiming));
   op->labels.alloc(nvox);
   HC_CUDA(cudaMemcpy(op->labels.p, labels_host, nvox, cudaMemcpyHostToDevice));
+
 
   // electrolyte path between electrode and counter electrode (dofmap.py:57-68,81-82)
   {
@@ -838,6 +853,14 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
       k_if_dirs<<<blocks_for(op->n_if), TPB, 0, s>>>(P, op->n_if, op->if_solid.p, op->if_el.p,
                                                       op->if_rank.p, op->if_dir.p); HC_COUNT();
     HC_CHECK_LAUNCH();
+  }
+  // 32-bit labels for the staged stencils: phase | (interface rank + 1) << 3
+  {
+    std::vector<int32_t> rank(nvox), l4(nvox);
+    HC_CUDA(cudaMemcpy(rank.data(), op->if_rank.p, nvox * 4, cudaMemcpyDeviceToHost));
+    for (long long v = 0; v < nvox; ++v) l4[v] = (int32_t)labels_host[v] | ((rank[v] + 1) << 3);
+    op->lab4.alloc(nvox);
+    HC_CUDA(cudaMemcpy(op->lab4.p, l4.data(), nvox * 4, cudaMemcpyHostToDevice));
   }
   // electrolyte-electrolyte faces (operator.py:187-191), kept for export
   {

@@ -388,9 +388,24 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
     linearize(op, W.x.p, npl, beta, s);
     // the preconditioner is rebuilt at the first Newton iteration of every solve; later
     // iterations reuse it (the Krylov solver sees the exact current Jacobian)
-    if (it == 1 || op.amg->refresh) amg_update(op, inv_dt, 3, s);
+    {
+      Amg& A = *op.amg;
+      bool first = it == 1;
+      if (first) ++A.solves;
+      // the Galerkin hierarchy is rebuilt for the first Newton iteration of every
+      // refresh_solves-th solve (and always when dt changed); Krylov always sees the
+      // exact current Jacobian, the preconditioner may lag
+      bool rebuild = A.refresh || (first && (A.solves % A.refresh_solves == 1 ||
+                                             A.refresh_solves == 1 || A.last_inv_dt != inv_dt));
+      if (rebuild) {
+        amg_update(op, inv_dt, 3, s);
+        A.last_inv_dt = inv_dt;
+      }
+    }
     k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
-    st.krylov_iters += bicgstab(op, W.b.p, W.d.p, inv_dt, 0, cfg.linear_rtol, cfg.krylov_max_iter, s);
+    st.krylov_iters += op.dev_krylov
+        ? bicgstab_dev(op, W.b.p, W.d.p, inv_dt, 0, cfg.linear_rtol, cfg.krylov_max_iter, s)
+        : bicgstab(op, W.b.p, W.d.p, inv_dt, 0, cfg.linear_rtol, cfg.krylov_max_iter, s);
     // positivity guard on the concentration block
     double alpha = 1.0;
     {
@@ -456,7 +471,9 @@ void initial_potential_grid(Operator& op, const double* npl, double mu, const hc
     if (it == 1 || op.amg->refresh) amg_update(op, 0.0, 2, s);
     k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
     k_zero_c<<<nb, TPB, 0, s>>>(n, W.b.p); HC_COUNT();
-    st.krylov_iters += bicgstab(op, W.b.p, W.d.p, 0.0, 1, cfg.linear_rtol, cfg.krylov_max_iter, s);
+    st.krylov_iters += op.dev_krylov
+        ? bicgstab_dev(op, W.b.p, W.d.p, 0.0, 1, cfg.linear_rtol, cfg.krylov_max_iter, s)
+        : bicgstab(op, W.b.p, W.d.p, 0.0, 1, cfg.linear_rtol, cfg.krylov_max_iter, s);
     double alpha = 1.0, norm_try = INFINITY;
     for (int h = 0; h <= 8; ++h) {
       k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p); HC_COUNT();

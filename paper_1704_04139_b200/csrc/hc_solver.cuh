@@ -19,6 +19,8 @@ struct Work {
 Work& work(Operator& op);
 double dot(Operator& op, const double2* a, const double2* b, cudaStream_t s);
 double norm_checked(Operator& op, const double2* a, int mask, cudaStream_t s);
+int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int mode, double rtol,
+                 int maxit, cudaStream_t s);
 int bicgstab(Operator& op, const double2* b, double2* x, double inv_dt, int mode, double rtol,
              int maxit, cudaStream_t s);
 void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc_solver_config& cfg,

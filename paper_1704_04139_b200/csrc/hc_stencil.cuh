@@ -639,3 +639,390 @@ inline void fine_launch_t(const DevParams& P, const FineArgs& F, const double2* 
 }
 
 }  // namespace hc
+
+namespace hc {
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// ---------------------------------------------------------------------------------
+// Pipelined 2.5-D stencil (the solver's kernel).  Same tiling as k_fine_t, but the
+// plane tiles (values, 32-bit labels, gX/c) are staged with cp.async into a
+// 4-deep shared-memory ring: while plane z is computed, planes z+1..z+3 are in
+// flight, so every SM keeps several planes of HBM traffic outstanding without
+// spending registers on it.  z-1 of the own column is kept in registers, z+1 is
+// read from the ring.
+template <int MODE, int EPI>
+__global__ void __launch_bounds__(VX * VY)
+k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double2* __restrict__ V,
+         const double* __restrict__ e, const double* __restrict__ r, const double* __restrict__ dinv,
+         double omega, double inv_dt, int flags, double2* __restrict__ out2, double* __restrict__ out,
+         int zc) {
+  constexpr bool FULLM = MODE == SM_FULL;
+  constexpr int S = 4;
+  constexpr int TW = VX + 2, TH = VY + 2, TN = TW * TH;
+  using VT = typename std::conditional<FULLM, double2, double>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  VT* sv = reinterpret_cast<VT*>(smem_raw);                       // [S][TN]
+  double* sw = reinterpret_cast<double*>(sv + S * TN);             // [S][TN] (FULL only)
+  int* sl = reinterpret_cast<int*>(sw + (FULLM ? S * TN : 0));     // [S][TN]
+  __shared__ double sP[36], sC[36], sM[36];
+  __shared__ unsigned char sI[36];
+  const int tid = threadIdx.y * VX + threadIdx.x;
+  if (tid < 36) {
+    sP[tid] = P.gP[tid];
+    sC[tid] = P.gC[tid];
+    sM[tid] = P.gMig[tid];
+    sI[tid] = P.ifc[tid];
+  }
+  const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
+  const int x0 = blockIdx.x * VX, y0 = blockIdx.y * VY;
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  const bool active = x < nx && y < ny;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);
+  const int zlast = min(z1, nz - 1);  // last plane that must be staged
+  const bool one_c_flag = FULLM && (flags & 4);
+  int hoff[2];
+  bool hval[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = tid + k * VX * VY;
+    hval[k] = i < TN;
+    const int hy = i / TW, hx = i - hy * TW;
+    const int gx = min(max(x0 + hx - 1, 0), nx - 1), gy = min(max(y0 + hy - 1, 0), ny - 1);
+    hoff[k] = gy * nx + gx;
+  }
+  auto issue = [&](int zz, int buf) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (hval[k]) {
+        const int i = tid + k * VX * VY;
+        const long long idx = (long long)zz * nxy + hoff[k];
+        cp_async4(sl + buf * TN + i, lab4 + idx);
+        if constexpr (FULLM) {
+          cp_async16(sv + buf * TN + i, V + idx);
+          if (one_c_flag) cp_async8(sw + buf * TN + i, F.w + idx);
+        } else {
+          cp_async8(sv + buf * TN + i, e + idx);
+        }
+      }
+  };
+  for (int j = 0; j < 3; ++j) {
+    if (z0 + j <= zlast) issue(z0 + j, j);
+    cp_commit();
+  }
+  const int cidx = (threadIdx.y + 1) * TW + threadIdx.x + 1;
+  const int col = active ? y * nx + x : 0;
+  VT vm{};
+  double wm = 0.0;
+  int lm = 0;
+  if (active) {
+    const int zm = z0 > 0 ? z0 - 1 : z0;
+    const long long idx = (long long)zm * nxy + col;
+    lm = lab4[idx] & 7;
+    if constexpr (FULLM) {
+      vm = V[idx];
+      if (one_c_flag) wm = F.w[idx];
+    } else {
+      vm = e[idx];
+    }
+  }
+  const double tp = P.t_plus;
+  for (int z = z0; z < z1; ++z) {
+    const int j = z - z0, buf = j % S, bufp = (j + 1) % S;
+    const int v = z * nxy + col;
+    double rv = 0.0, dv_ = 0.0;
+    if (active) {
+      if constexpr (!FULLM) {
+        if (EPI != EP_STORE) rv = r[v];
+        if (EPI == EP_SMOOTH) dv_ = dinv[v];
+      }
+    }
+    cp_wait1();        // planes z and z+1 have landed (only z+2's group may be pending)
+    __syncthreads();
+    if (z + 3 <= zlast) issue(z + 3, (j + 3) % S);  // reuses plane z-1's slot
+    cp_commit();
+    if (active) {
+      const int aw = sl[buf * TN + cidx];   // phase | (interface rank + 1) << 3
+      const int a = aw & 7;
+      const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == GR || a == EL)
+                                                             : !(z == nz - 1 && a == CC);
+      const bool top = z + 1 >= nz;
+      const VT va = sv[buf * TN + cidx];
+      if (!in_row) {
+        if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
+        else out[v] = 0.0;
+      } else {
+        const int rk = (aw >> 3) - 1;
+        const int a6 = a * 6;
+        const bool solid = a != EL;
+        double rc = 0.0, rp = 0.0;
+        double wa = 0.0;
+        bool one_c = false;
+        if constexpr (FULLM) {
+          one_c = one_c_flag && a == EL;
+          if (one_c) wa = sw[buf * TN + cidx];
+        }
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+          // neighbour d straight from the ring (z-1 from registers, z+1 from the next slot)
+          int b;
+          VT vb;
+          double wb = 0.0;
+          if (d < 4) {
+            const int t = d == 0 ? cidx - 1 : (d == 1 ? cidx + 1 : (d == 2 ? cidx - TW : cidx + TW));
+            b = sl[buf * TN + t] & 7;
+            vb = sv[buf * TN + t];
+            if constexpr (FULLM) if (one_c) wb = sw[buf * TN + t];
+          } else if (d == 4) {
+            b = lm;
+            vb = vm;
+            wb = wm;
+          } else {
+            b = top ? a : (sl[bufp * TN + cidx] & 7);
+            vb = top ? va : sv[bufp * TN + cidx];
+            if constexpr (FULLM) if (one_c) wb = top ? wa : sw[bufp * TN + cidx];
+          }
+          const int i = a6 + b;
+          if constexpr (FULLM) {
+            const double dp = va.y - vb.y;
+            rp += sP[i] * dp;
+            rc += sC[i] * (va.x - vb.x) + sM[i] * dp;
+            if (one_c && sM[i] != 0.0) {
+              const double dq = wa * va.x - wb * vb.x;
+              rp += dq;
+              rc += tp * dq;
+            }
+          } else if (MODE == SM_PHI) {
+            rp += sP[i] * (va - vb);
+          } else if (MODE == SM_CONC) {
+            rp += sC[i] * (va - vb);
+          }
+          if (sI[i]) {
+            const long long f = 6LL * rk + d;
+            const bool bv = a == GR || b == GR;
+            if constexpr (FULLM) {
+              const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f),
+                           cg = __ldg(F.vcoef + 2 * F.nslot + f);
+              const double2 vs = solid ? va : vb, ve = solid ? vb : va;
+              const double dv = (bv ? ca * vs.x : 0.0) + cb * ve.x + cg * (vs.y - ve.y);
+              if (solid) {
+                if (bv) rc += dv;
+                rp += dv;
+              } else {
+                rc -= dv;
+                rp -= dv;
+              }
+            } else if (MODE == SM_PHI) {
+              rp += __ldg(F.vcoef + 2 * F.nslot + f) * (va - vb);
+            } else if (MODE == SM_CP) {
+              const double cg = __ldg(F.vcoef + 2 * F.nslot + f);
+              if (solid) {
+                if (bv) rp += cg * (va - vb);
+              } else {
+                rp += (1.0 - tp) * cg * (va - vb);
+              }
+            } else {
+              const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f);
+              if (solid) {
+                if (bv) rp += ca * va + cb * vb;
+              } else {
+                rp -= (1.0 - tp) * ((bv ? ca * vb : 0.0) + cb * va);
+              }
+            }
+          }
+        }
+        if constexpr (FULLM) {
+          if ((flags & 1) && (a == GR || a == EL)) rc += va.x * inv_dt;
+          if ((flags & 2) && a == EL) rc -= tp * rp;
+          if (flags & 8) rc = 0.0;
+          out2[v] = make_double2(rc, rp);
+        } else {
+          if (MODE == SM_CONC) rp += inv_dt * va;
+          if (EPI == EP_STORE) out[v] = rp;
+          else if (EPI == EP_RESID) out[v] = rv - rp;
+          else out[v] = va + omega * dv_ * (rv - rp);
+        }
+      }
+      lm = a;
+      vm = va;
+      if constexpr (FULLM) wm = one_c_flag ? sw[buf * TN + cidx] : 0.0;
+    }
+  }
+  cp_wait1();
+}
+
+template <int MODE, int EPI>
+inline void fine_launch_p(const DevParams& P, const FineArgs& F, const int32_t* lab4,
+                          const double2* V, const double* e, const double* r, const double* dinv,
+                          double omega, double inv_dt, int flags, double2* out2, double* out,
+                          int n_sm, cudaStream_t s) {
+  constexpr bool FULLM = MODE == SM_FULL;
+  constexpr int TN = (VX + 2) * (VY + 2);
+  const size_t smem = 4 * TN * ((FULLM ? 16 : 8) + (FULLM ? 8 : 0) + 4);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fine_p<MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
+  const long long want = 6LL * n_sm;
+  int zc = (int)std::max<long long>(2, (long long)bx * by * P.nz / want);
+  zc = std::min(zc, 64);
+  const int bz = (P.nz + zc - 1) / zc;
+  k_fine_p<MODE, EPI><<<dim3(bx, by, bz), dim3(VX, VY, 1), smem, s>>>(
+      P, F, lab4, V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
+}
+
+}  // namespace hc
+
+namespace hc {
+
+// ---------------------------------------------------------------------------------
+// Operator value (residual) stencil with the same cp.async ring: linear two-point
+// fluxes, grounded closures, chemical-potential faces (log c, operator.py:322-327),
+// boundary drive and implicit-Euler time term.  Interface currents are added by
+// k_residual_iface over the compacted face list.
+static __global__ void __launch_bounds__(VX * VY)
+k_res_p(DevParams P, const int32_t* __restrict__ lab4, const double2* __restrict__ X, double mu,
+        int parts, const double* __restrict__ cprev, double inv_dt, double2* __restrict__ out,
+        int zc) {
+  constexpr int S = 4;
+  constexpr int TW = VX + 2, TH = VY + 2, TN = TW * TH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sv = reinterpret_cast<double2*>(smem_raw);
+  int* sl = reinterpret_cast<int*>(sv + S * TN);
+  __shared__ double sP[36], sC[36], sM[36];
+  const int tid = threadIdx.y * VX + threadIdx.x;
+  if (tid < 36) {
+    sP[tid] = P.gP[tid];
+    sC[tid] = P.gC[tid];
+    sM[tid] = P.gMig[tid];
+  }
+  const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
+  const int x0 = blockIdx.x * VX, y0 = blockIdx.y * VY;
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  const bool active = x < nx && y < ny;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);
+  const int zlast = min(z1, nz - 1);
+  int hoff[2];
+  bool hval[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = tid + k * VX * VY;
+    hval[k] = i < TN;
+    const int hy = i / TW, hx = i - hy * TW;
+    const int gx = min(max(x0 + hx - 1, 0), nx - 1), gy = min(max(y0 + hy - 1, 0), ny - 1);
+    hoff[k] = gy * nx + gx;
+  }
+  auto issue = [&](int zz, int buf) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (hval[k]) {
+        const int i = tid + k * VX * VY;
+        const long long idx = (long long)zz * nxy + hoff[k];
+        cp_async4(sl + buf * TN + i, lab4 + idx);
+        cp_async16(sv + buf * TN + i, X + idx);
+      }
+  };
+  for (int j = 0; j < 3; ++j) {
+    if (z0 + j <= zlast) issue(z0 + j, j);
+    cp_commit();
+  }
+  const int cidx = (threadIdx.y + 1) * TW + threadIdx.x + 1;
+  const int col = active ? y * nx + x : 0;
+  double2 vm{};
+  int lm = 0;
+  if (active) {
+    const int zm = z0 > 0 ? z0 - 1 : z0;
+    const long long idx = (long long)zm * nxy + col;
+    lm = lab4[idx] & 7;
+    vm = X[idx];
+  }
+  const bool lin = parts & PART_LIN, c1 = parts & PART_1C;
+  const double tp = P.t_plus;
+  for (int z = z0; z < z1; ++z) {
+    const int j = z - z0, buf = j % S, bufp = (j + 1) % S;
+    const int v = z * nxy + col;
+    double cp = 0.0;
+    if (active && (parts & PART_TIME)) cp = cprev[v];
+    cp_wait1();
+    __syncthreads();
+    if (z + 3 <= zlast) issue(z + 3, (j + 3) % S);
+    cp_commit();
+    if (active) {
+      const int a = sl[buf * TN + cidx] & 7;
+      const double2 va = sv[buf * TN + cidx];
+      const bool grounded_row = z == nz - 1 && a == CC;
+      const bool top = z + 1 >= nz;
+      if (grounded_row) {
+        out[v] = make_double2(0.0, 0.0);
+      } else {
+        const int a6 = a * 6;
+        const bool one_c = c1 && a == EL;
+        const double la = one_c ? log(va.x) : 0.0;
+        double rc = 0.0, rp = 0.0;
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+          int b;
+          double2 vb;
+          if (d < 4) {
+            const int t = d == 0 ? cidx - 1 : (d == 1 ? cidx + 1 : (d == 2 ? cidx - TW : cidx + TW));
+            b = sl[buf * TN + t] & 7;
+            vb = sv[buf * TN + t];
+          } else if (d == 4) {
+            b = lm;
+            vb = vm;
+          } else {
+            b = top ? a : (sl[bufp * TN + cidx] & 7);
+            vb = top ? va : sv[bufp * TN + cidx];
+          }
+          const int i = a6 + b;
+          if (lin) {
+            const double dp = va.y - vb.y;
+            rp += sP[i] * dp;
+            rc += sC[i] * (va.x - vb.x) + sM[i] * dp;
+          }
+          if (one_c && sM[i] != 0.0) {   // electrolyte-electrolyte face
+            const double q = P.gX * (la - log(vb.x));
+            rp += q;
+            rc += tp * q;
+          }
+        }
+        if ((parts & PART_BND) && a == CW && z == 0) rp += mu * P.drive;
+        if ((parts & PART_TIME) && (a == GR || a == EL)) rc += (va.x - cp) * inv_dt;
+        out[v] = make_double2(rc, rp);
+      }
+      lm = a;
+      vm = va;
+    }
+  }
+  cp_wait1();
+}
+
+inline void res_launch_p(const DevParams& P, const int32_t* lab4, const double2* X, double mu,
+                         int parts, const double* cprev, double inv_dt, double2* out, int n_sm,
+                         cudaStream_t s) {
+  constexpr int TN = (VX + 2) * (VY + 2);
+  const size_t smem = 4 * TN * (16 + 4);
+  const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
+  int zc = (int)std::max<long long>(2, (long long)bx * by * P.nz / (6LL * n_sm));
+  zc = std::min(zc, 64);
+  const int bz = (P.nz + zc - 1) / zc;
+  k_res_p<<<dim3(bx, by, bz), dim3(VX, VY, 1), smem, s>>>(P, lab4, X, mu, parts, cprev, inv_dt,
+                                                          out, zc);
+}
+
+}  // namespace hc

@@ -1,0 +1,30 @@
+"""Scratch: N implicit steps of a config under the current env knobs; prints iters and time/step."""
+import ctypes, sys, time
+import numpy as np
+sys.path.insert(0, '.')
+import torch
+import paper_1704_04139_b200 as P
+from paper_1704_04139_b200 import _dev, _native
+from paper_1704_04139_b200.configs import CONFIGS
+from paper_1704_04139_b200.microgen import generate_cell
+name, nsteps = sys.argv[1], int(sys.argv[2])
+rs = CONFIGS[name]
+grid = generate_cell(rs.cell)
+params = P.MaterialParams(soc_init=rs.soc_init, i00_plel=rs.i00_plel_exchange / np.sqrt(1000.0))
+op = P.SystemOperator(P.build_dofmap(grid), params)
+h = grid.voxel_size * 1e-6
+mu = -rs.c_rate * params.c_gr_max * params.constants.F * np.count_nonzero(grid.labels == 1) * h**3 / 3600 / (grid.labels.shape[1] * grid.labels.shape[2] * h * h)
+cfg = P.SolverConfig(dt_max=rs.dt, dt_init=min(0.05, rs.dt))
+st = P.prepare_initial_state(op, params, mu, cfg)
+x = _dev.to_dev(st.x).clone(); npl = _dev.to_dev(st.n_pl).clone()
+c = cfg.to_c(); s = _native.HcNewtonStats(); L = _native.lib()
+v_cp, _ = P.qoi_vectors(op.dof)
+its = []
+for k in range(2):
+    _native.check(L.hc_step(op.native.handle, _dev.ptr(x), _dev.ptr(npl), 0.0, rs.dt, mu, ctypes.byref(c), ctypes.byref(s), None))
+torch.cuda.synchronize(); t = time.time()
+for k in range(nsteps):
+    _native.check(L.hc_step(op.native.handle, _dev.ptr(x), _dev.ptr(npl), 0.0, rs.dt, mu, ctypes.byref(c), ctypes.byref(s), None))
+    its.append(s.krylov_iters)
+torch.cuda.synchronize(); el = time.time() - t
+print(f'{name}: {el / nsteps * 1e3:.1f} ms/step, krylov/step {np.mean(its):.1f} max {max(its)}, V={float(v_cp @ x.cpu().numpy()):.6f}')
