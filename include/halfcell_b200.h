@@ -131,6 +131,14 @@ int hc_step(hc_operator* op, double* x, double* n_pl, double t, double dt_sugges
 int hc_step_host(hc_operator* op, double* x_host, double* n_pl_host, double t, double dt_suggest,
                  double mu, const hc_solver_config* cfg, hc_newton_stats* stats);
 
+/* Batched parameter study (BASELINE config 3): one accepted step for each of n
+ * independent cells (own operator, state, dt, applied current) on the device;
+ * cells run concurrently on their operators' private streams, driven by
+ * n_threads host threads.  x[i], n_pl[i] are device pointers updated in place. */
+int hc_step_batch(hc_operator* const* ops, int32_t n, double* const* x, double* const* n_pl,
+                  const double* dt_suggest, const double* mu, const hc_solver_config* cfg,
+                  hc_newton_stats* stats, int32_t n_threads);
+
 /* POD snapshot Gram G = S^T diag(w) S for S (n_dof x n_snap, column-major,
  * device fp64) — the method-of-snapshots correlation matrix (SPEC mor.pod);
  * G is n_snap x n_snap column-major on the device.  w may be NULL (identity). */

@@ -21,6 +21,7 @@ _LAZY = {
     "prepare_initial_state": "timestepping", "run_transient": "timestepping",
     "qoi_vectors": "qoi", "qoi_cell_voltage": "qoi", "qoi_mean_solid_conc": "qoi",
     "pod_gram": "pod", "pod_basis": "pod",
+    "make_batch": "batch", "step_batch": "batch", "BatchCell": "batch",
 }
 
 

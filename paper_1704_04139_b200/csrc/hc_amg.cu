@@ -918,18 +918,18 @@ void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mo
   for (auto& g : A.graphs)
     if (g.r == r && g.z == z && g.mode == mode && g.inv_dt == inv_dt) {
       HC_CUDA(cudaGraphLaunch(g.exec, s));
-      g_launch_count += g.n_kernels;
+      count_graph_launch(g.n_kernels);
       return;
     }
   AmgGraph g;
   g.r = r; g.z = z; g.mode = mode; g.inv_dt = inv_dt;
-  unsigned long long c0 = g_launch_count;
+  unsigned long long c0 = t_launch_count;
   cudaGraph_t graph;
   HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   amg_apply_impl(op, r, z, inv_dt, mode, s);
   HC_CUDA(cudaStreamEndCapture(s, &graph));
-  g.n_kernels = g_launch_count - c0;
-  g_launch_count = c0;
+  g.n_kernels = t_launch_count - c0;
+  uncount(g.n_kernels);
   HC_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
   HC_CUDA(cudaGraphDestroy(graph));
   if (A.graphs.size() >= 16) {
@@ -938,7 +938,7 @@ void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mo
   }
   A.graphs.push_back(g);
   HC_CUDA(cudaGraphLaunch(g.exec, s));
-  g_launch_count += g.n_kernels;
+  count_graph_launch(g.n_kernels);
 }
 
 Amg::~Amg() {

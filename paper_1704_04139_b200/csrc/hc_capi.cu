@@ -3,6 +3,8 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -11,7 +13,8 @@
 #include "hc_solver.cuh"
 
 namespace hc {
-unsigned long long g_launch_count = 0;
+std::atomic<unsigned long long> g_launch_count{0};
+thread_local unsigned long long t_launch_count = 0;
 Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
                           const hc_params& hp);
 void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
@@ -456,7 +459,7 @@ int hc_step_host(hc_operator* opq, double* x_host, double* n_pl_host, double t, 
 }
 
 int hc_launch_count(int64_t* out) {
-  return guarded([&] { *out = (int64_t)g_launch_count; });
+  return guarded([&] { *out = (int64_t)g_launch_count.load(); });
 }
 
 int hc_time_kernels(hc_operator* opq, const double* x, const double* n_pl, double beta,
@@ -500,6 +503,47 @@ int hc_time_kernels(hc_operator* opq, const double* x, const double* n_pl, doubl
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+  });
+}
+
+int hc_step_batch(hc_operator* const* ops, int32_t n, double* const* x, double* const* n_pl,
+                  const double* dt_suggest, const double* mu, const hc_solver_config* cfg,
+                  hc_newton_stats* stats, int32_t n_threads) {
+  return guarded([&] {
+    if (n <= 0) return;
+    int dev = 0;
+    HC_CUDA(cudaGetDevice(&dev));
+    int nt = std::max(1, std::min<int>(n_threads > 0 ? n_threads : 16, n));
+    std::atomic<int> next{0};
+    std::mutex m;
+    int first_code = HC_OK;
+    std::string first_msg;
+    auto worker = [&] {
+      cudaSetDevice(dev);
+      for (int i; (i = next.fetch_add(1)) < n;) {
+        try {
+          Operator& op = *(Operator*)ops[i];
+          Work& W = work(op);
+          cudaStream_t s = op.stream;
+          hc_newton_stats st{};
+          scatter_packed(op, x[i], W.x.p, true, s);
+          step_grid(op, n_pl[i], dt_suggest[i], mu[i], *cfg, st, s);
+          gather_packed(op, W.x.p, x[i], s);
+          HC_CUDA(cudaStreamSynchronize(s));
+          if (stats) stats[i] = st;
+        } catch (const Error& e) {
+          std::lock_guard<std::mutex> g(m);
+          if (first_code == HC_OK) { first_code = e.code; first_msg = "cell " + std::to_string(i) + ": " + e.what(); }
+        } catch (const std::exception& e) {
+          std::lock_guard<std::mutex> g(m);
+          if (first_code == HC_OK) { first_code = HC_ERR_CUDA; first_msg = e.what(); }
+        }
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(worker);
+    for (auto& t : th) t.join();
+    if (first_code != HC_OK) throw Error(first_code, first_msg);
   });
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -49,8 +50,18 @@ struct Error : std::runtime_error {
 #define HC_CHECK_LAUNCH() HC_CUDA(cudaGetLastError())
 
 // process-wide count of kernels launched by this library (bench.py's gpu_launches)
-extern unsigned long long g_launch_count;
-#define HC_COUNT() (++::hc::g_launch_count)
+extern std::atomic<unsigned long long> g_launch_count;
+extern thread_local unsigned long long t_launch_count;   // this thread's launches (captures)
+inline void count_launch() {
+  g_launch_count.fetch_add(1, std::memory_order_relaxed);
+  ++t_launch_count;
+}
+inline void count_graph_launch(unsigned long long n) {
+  g_launch_count.fetch_add(n, std::memory_order_relaxed);
+}
+// launches recorded while capturing a graph are not kernel executions: undo them
+inline void uncount(unsigned long long n) { g_launch_count.fetch_sub(n, std::memory_order_relaxed); }
+#define HC_COUNT() (::hc::count_launch())
 
 // ---- device-side parameter block (passed by value to kernels) -------------------
 struct DevParams {

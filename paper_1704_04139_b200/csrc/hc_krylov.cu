@@ -215,7 +215,7 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   // (re)capture the iteration graph for this mode / dt
   if (!G.exec[mode] || G.inv_dt[mode] != inv_dt) {
     if (G.exec[mode]) cudaGraphExecDestroy(G.exec[mode]);
-    unsigned long long c0 = g_launch_count;
+    unsigned long long c0 = t_launch_count;
     cudaGraph_t graph;
     op.capturing = true;
     HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -238,8 +238,8 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
     k_dev_scalar<<<1, 256, 0, s>>>(4, nb, part, ks); HC_COUNT();
     HC_CUDA(cudaStreamEndCapture(s, &graph));
     op.capturing = false;
-    G.n_kernels[mode] = g_launch_count - c0;
-    g_launch_count = c0;
+    G.n_kernels[mode] = t_launch_count - c0;
+    uncount(G.n_kernels[mode]);
     HC_CUDA(cudaGraphInstantiate(&G.exec[mode], graph, 0));
     HC_CUDA(cudaGraphDestroy(graph));
     G.inv_dt[mode] = inv_dt;
@@ -251,7 +251,7 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   while (true) {
     for (int k = 0; k < batch; ++k) {
       HC_CUDA(cudaGraphLaunch(G.exec[mode], s));
-      g_launch_count += G.n_kernels[mode];
+      count_graph_launch(G.n_kernels[mode]);
     }
     HC_CUDA(cudaMemcpyAsync(G.ks_host, G.ks.p, S_NSLOT * sizeof(double), cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
