@@ -26,6 +26,7 @@
 #include <chrono>
 #include <cstdio>
 #include <thread>
+#include <type_traits>
 
 #include "hc_amg.cuh"
 #include "hc_stencil.cuh"
@@ -315,17 +316,22 @@ __global__ void k_csr_smooth0(int n, double w, const double* __restrict__ dinv,
   if (i < n) x[i] = w * dinv[i] * b[i];
 }
 
+__global__ void k_to_float(long long n, const double* __restrict__ a, float* __restrict__ b) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (float)a[i];
+}
+
 // VS lanes per row (VS = 1, 8 or 32), chosen per level from the mean row length
-template <int VS>
+template <int VS, class VT>
 __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
-                               const int32_t* __restrict__ cl, const double* __restrict__ v,
+                               const int32_t* __restrict__ cl, const VT* __restrict__ v,
                                const double* __restrict__ dinv, const double* __restrict__ b,
                                const double* __restrict__ x, double* __restrict__ y, int resid) {
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int i = (int)(gt / VS), lane = (int)(gt % VS);
   if (i >= n) return;
   double s = 0.0;
-  for (int k = rp[i] + lane; k < rp[i + 1]; k += VS) s += v[k] * x[cl[k]];
+  for (int k = rp[i] + lane; k < rp[i + 1]; k += VS) s += (double)v[k] * x[cl[k]];
 #pragma unroll
   for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
   if (lane == 0) y[i] = resid ? b[i] - s : x[i] + w * dinv[i] * (b[i] - s);
@@ -445,6 +451,7 @@ void upload_csr(Csr& c, const HPat& p) {
   upload(c.rp, p.rp);
   upload(c.ci, p.ci);
   c.v.alloc(std::max<size_t>(p.ci.size(), 1));
+  c.vf.alloc(std::max<size_t>(p.ci.size(), 1));
 }
 
 }  // namespace
@@ -677,6 +684,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_WDEPTH")) amg->wdepth = atoi(e);
   if (const char* e = getenv("HC_GRAPHS")) amg->use_graphs = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_REFRESH")) amg->refresh = atoi(e);
+  if (const char* e = getenv("HC_AMG_FP32")) amg->fp32_coarse = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_REFRESH_SOLVES")) amg->refresh_solves = std::max(1, atoi(e));
   auto t0 = std::chrono::steady_clock::now();
   build_block(op, lab, 0, *amg, amg->blk[0]);
@@ -721,6 +729,12 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
                                             L.AP.rp.p, L.AP.ci.p, L.AP.v.p, U.A.rp.p, U.A.ci.p,
                                             U.A.v.p); HC_COUNT();
     }
+    for (size_t l = 1; l < B.levels.size(); ++l) {
+      AmgLevel& L = B.levels[l];
+      if (A.fp32_coarse && L.A.nnz) {
+        k_to_float<<<nblk(L.A.nnz), TPB, 0, s>>>(L.A.nnz, L.A.v.p, L.A.vf.p); HC_COUNT();
+      }
+    }
     AmgLevel& C = B.levels.back();
     if (B.levels.size() > 1) {
       k_dinv<<<nblk(C.n), TPB, 0, s>>>(C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, C.dinv.p); HC_COUNT();
@@ -741,15 +755,26 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
 static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s);
 
 // y = x + w D^-1 (b - A x)  or  (resid) y = b - A x, with lanes-per-row from the density
-static void csr_sweep(const AmgLevel& L, double w, const double* b, const double* x, double* y,
-                      int resid, cudaStream_t s) {
+static void csr_sweep(const Amg& A, const AmgLevel& L, double w, const double* b, const double* x,
+                      double* y, int resid, cudaStream_t s) {
   double avg = L.n ? (double)L.A.nnz / L.n : 0.0;
+  const bool f32 = A.fp32_coarse;
+  auto go = [&](auto vs_tag, auto* vals) {
+    constexpr int VS = decltype(vs_tag)::value;
+    using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
+    k_csr_jacobi_v<VS, VT><<<nblk((long long)VS * L.n), TPB, 0, s>>>(L.n, w, L.A.rp.p, L.A.ci.p, vals,
+                                                                      L.dinv.p, b, x, y, resid);
+    HC_COUNT();
+  };
   if (avg <= 12.0) {
-    k_csr_jacobi_v<1><<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p, b, x, y, resid); HC_COUNT();
+    if (f32) go(std::integral_constant<int, 1>{}, (const float*)L.A.vf.p);
+    else go(std::integral_constant<int, 1>{}, (const double*)L.A.v.p);
   } else if (avg <= 48.0) {
-    k_csr_jacobi_v<8><<<nblk(8LL * L.n), TPB, 0, s>>>(L.n, w, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p, b, x, y, resid); HC_COUNT();
+    if (f32) go(std::integral_constant<int, 8>{}, (const float*)L.A.vf.p);
+    else go(std::integral_constant<int, 8>{}, (const double*)L.A.v.p);
   } else {
-    k_csr_jacobi_v<32><<<nblk(32LL * L.n), TPB, 0, s>>>(L.n, w, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p, b, x, y, resid); HC_COUNT();
+    if (f32) go(std::integral_constant<int, 32>{}, (const float*)L.A.vf.p);
+    else go(std::integral_constant<int, 32>{}, (const double*)L.A.v.p);
   }
 }
 
@@ -760,17 +785,17 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   const double w = A.omega;
   k_csr_smooth0<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
   for (int k = 1; k < A.nu_c; ++k) {
-    csr_sweep(L, w, L.b.p, L.x.p, L.x2.p, 0, s);
+    csr_sweep(A, L, w, L.b.p, L.x.p, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
   }
-  csr_sweep(L, 0.0, L.b.p, L.x.p, L.res.p, 1, s);
+  csr_sweep(A, L, 0.0, L.b.p, L.x.p, L.res.p, 1, s);
   k_restrict_v<<<nblk(8LL * U.n), TPB, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.ptv.p, L.res.p,
                                                U.b.p); HC_COUNT();
   solve_level(A, B, l + 1, s);
   k_csr_prolong<<<nblk(L.n), TPB, 0, s>>>(L.n, B.alpha, L.P.rp.p, L.P.ci.p, L.P.v.p, U.x.p,
                                           L.x.p); HC_COUNT();
   for (int k = 0; k < A.nu_c; ++k) {
-    csr_sweep(L, w, L.b.p, L.x.p, L.x2.p, 0, s);
+    csr_sweep(A, L, w, L.b.p, L.x.p, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
   }
 }
@@ -787,7 +812,7 @@ static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   int g = (int)l <= A.wdepth ? A.gamma : 1;
   for (int k = 1; k < g; ++k) {
     HC_CUDA(cudaMemcpyAsync(L.acc.p, L.x.p, L.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    csr_sweep(L, 0.0, L.b.p, L.acc.p, L.res.p, 1, s);
+    csr_sweep(A, L, 0.0, L.b.p, L.acc.p, L.res.p, 1, s);
     std::swap(L.b.p, L.res.p);
     cycle_once(A, B, l, s);
     std::swap(L.b.p, L.res.p);

@@ -12,6 +12,7 @@ struct Csr {
   long long nnz = 0;
   DBuf<int32_t> rp, ci;
   DBuf<double> v;
+  DBuf<float> vf;    // fp32 copy used by the cycle's sweeps (the preconditioner needs no fp64)
 };
 
 struct AmgLevel {
@@ -51,12 +52,13 @@ struct Amg {
   int nu = 2;
   int nu_c = 2;              // smoothing sweeps on the CSR levels
   int sa_levels_c = 0;       // smoothed transfers of the c block (plain aggregation suffices)
-  double omega = 0.6;        // Jacobi smoothing weight
+  double omega = 0.9;        // Jacobi smoothing weight
   double omega_p = 2.0 / 3;  // prolongator smoothing weight
   int sa_levels = 2;         // smoothed prolongators on the first sa_levels transfers
   double alpha = 1.0;
   int gamma = 1;             // cycles per coarse-level solve (2 = W-cycle)
   int wdepth = 3;
+  bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int refresh = 0;          // numeric setup every Newton iteration (1) or once per solve (0)
   int refresh_solves = 8;   // rebuild once every this many Newton solves (and when dt changes)
   long long solves = 0;

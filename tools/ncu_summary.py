@@ -8,7 +8,8 @@ agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[hdr_i + 1:]:
     if len(r) <= vi or r[mi] != 'gpu__time_duration.sum':
         continue
-    name = r[ki].split('(')[0].split('<')[0]
+    name = r[ki].replace('void ', '').replace('(anonymous namespace)::', '').replace('<unnamed>::', '')
+    name = name.replace('hc::', '').split('(')[0]
     v = float(r[vi].replace(',', ''))
     agg[name][0] += 1
     agg[name][1] += v
