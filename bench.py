@@ -61,6 +61,17 @@ def drive_mu(labels, voxel_um, c_rate, params):
     return -c_rate * params.c_gr_max * params.constants.F * vol_gr / 3600.0 / area
 
 
+def committed_traffic(config: str, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/traffic.json, written from the .ncu-rep of the same bench command)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d.get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
 def measured_peaks():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -229,7 +240,7 @@ def run_ours(args, ws, rank, local):
 
     # ---- kernel timings: residual and J v at the current state
     beta = rs.dt * op.face_area / params.constants.F
-    ms = (ctypes.c_double * 4)()
+    ms = (ctypes.c_double * 5)()
     _native.check(L.hc_time_kernels(op.native.handle, _dev.ptr(x), _dev.ptr(npl), beta,
                                     1.0 / rs.dt, 20, L2_FLUSH_BYTES, ms, sp))
     nvox = int(op.native.info.n_vox)
@@ -241,6 +252,8 @@ def run_ours(args, ws, rank, local):
     res_bytes = nvox * (1 + 16 + 16) + n_c * 8          # labels + x + out + c_prev
     peak, peak_kind = measured_peaks()
     achieved = jv_bytes / (ms[2] * 1e-3) / 1e9
+    copy_gbs = nvox * 32 / (ms[4] * 1e-3) / 1e9          # same-size streaming copy, same timing
+    traffic = committed_traffic(args.config, "k_fine_p<0, 0>")
 
     # ---- e2e: the same step through the host-buffer entry point
     e2e_val = None
@@ -288,11 +301,17 @@ def run_ours(args, ws, rank, local):
                            "jvp": ndof / (jv_ms * 1e-3) / 1e9},
             "kernel_ms": {"residual_stencil": ms[0], "residual_iface": ms[1],
                           "jvp_stencil": ms[2], "jvp_iface": ms[3]},
-            "roofline": {"kernel": "k_jvp_stencil", "bound": "hbm", "achieved": achieved,
-                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+            "roofline": {"kernel": "k_fine_p<SM_FULL> (J v, fused interface faces)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_launch": jv_bytes,
-                         "residual_achieved": res_bytes / (ms[0] * 1e-3) / 1e9},
+                         "bytes_per_voxel": "label 1 + v 16 + out 16 (+ gX/c 8 on electrolyte voxels)",
+                         "same_size_stream_copy_gbs": copy_gbs,
+                         "frac_of_stream_copy": achieved / copy_gbs,
+                         "residual": {"kernel": "k_res_p + k_residual_iface",
+                                      "achieved": res_bytes / (res_ms * 1e-3) / 1e9,
+                                      "frac": res_bytes / (res_ms * 1e-3) / 1e9 / peak,
+                                      "bytes_per_launch": res_bytes}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "steps/s", "h2d_bytes_per_step": bi,
                     "d2h_bytes_per_step": bi},

@@ -154,8 +154,9 @@ int hc_launch_count(int64_t* out);
 
 /* Average device time (ms, CUDA events on `stream`) of one launch of each
  * kernel of the residual and of J v at state x, with an L2 flush of
- * `flush_bytes` before every launch: ms_out = {residual stencil, residual
- * interface faces, J v stencil, J v interface faces}. */
+ * `flush_bytes` before every launch: ms_out[5] = {residual stencil, residual
+ * interface faces, J v (fused stencil incl. interface faces), 0 (no separate
+ * interface kernel), streaming copy of one double2 per voxel (calibration)}. */
 int hc_time_kernels(hc_operator* op, const double* x, const double* n_pl, double beta,
                     double inv_dt, int32_t iters, int64_t flush_bytes, double* ms_out,
                     void* stream);

@@ -331,7 +331,17 @@ __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
   int i = (int)(gt / VS), lane = (int)(gt % VS);
   if (i >= n) return;
   double s = 0.0;
-  for (int k = rp[i] + lane; k < rp[i + 1]; k += VS) s += (double)v[k] * x[cl[k]];
+  const int k1 = rp[i + 1];
+  int k = rp[i] + lane;
+  double s2 = 0.0;
+  for (; k + VS < k1; k += 2 * VS) {   // two independent gathers in flight per lane
+    const int c0 = cl[k], c1 = cl[k + VS];
+    const double a0 = (double)v[k], a1 = (double)v[k + VS];
+    s += a0 * x[c0];
+    s2 += a1 * x[c1];
+  }
+  if (k < k1) s += (double)v[k] * x[cl[k]];
+  s += s2;
 #pragma unroll
   for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
   if (lane == 0) y[i] = resid ? b[i] - s : x[i] + w * dinv[i] * (b[i] - s);
