@@ -137,9 +137,14 @@ def _oracle_column_step(args):
     from oracle import fvm_oracle as O
     from paper_1704_04139_b200.configs import CONFIGS
     from paper_1704_04139_b200.microgen import generate_cell
+    from paper_1704_04139_b200.errors import GeometryError
     rs = CONFIGS[config]
-    spec = dataclasses.replace(rs.cell, nx=w, ny=w, seed=seed)
-    grid = generate_cell(spec)
+    for attempt in range(20):   # a thin column can miss the collector; take the next seed
+        try:
+            grid = generate_cell(dataclasses.replace(rs.cell, nx=w, ny=w, seed=seed + 100000 * attempt))
+            break
+        except GeometryError:
+            continue
     p = O.Params(soc_init=rs.soc_init, i00_plel=rs.i00_plel_exchange / np.sqrt(1000.0))
     op = O.OracleOperator(grid.labels, grid.voxel_size, p)
     h = grid.voxel_size * 1e-6
