@@ -347,6 +347,36 @@ __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
   if (lane == 0) y[i] = resid ? b[i] - s : x[i] + w * dinv[i] * (b[i] - s);
 }
 
+// Generalized sweep: y = xin + w D^-1 (b - A xin)  (resid: y = b - A xin) where the
+// input vector is materialised on the fly:
+//   XM 0: xin = x                                  (plain sweep)
+//   XM 1: xin = w D^-1 b                           (first pre-sweep from a zero guess)
+//   XM 2: xin = x + alpha * xc[parent]             (first post-sweep fused with the
+//                                                   tentative-prolongator correction)
+template <int VS, class VT, int XM>
+__global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict__ rp,
+                        const int32_t* __restrict__ cl, const VT* __restrict__ v,
+                        const double* __restrict__ dinv, const double* __restrict__ b,
+                        const double* __restrict__ x, const int32_t* __restrict__ parent,
+                        const double* __restrict__ xc, double* __restrict__ y, int resid) {
+  long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int i = (int)(gt / VS), lane = (int)(gt % VS);
+  if (i >= n) return;
+  auto xin = [&](int j) -> double {
+    if (XM == 0) return x[j];
+    if (XM == 1) return w * dinv[j] * b[j];
+    return x[j] + alpha * xc[parent[j]];
+  };
+  double s = 0.0;
+  for (int k = rp[i] + lane; k < rp[i + 1]; k += VS) s += (double)v[k] * xin(cl[k]);
+#pragma unroll
+  for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
+  if (lane == 0) {
+    const double xi = xin(i);
+    y[i] = resid ? b[i] - s : xi + w * dinv[i] * (b[i] - s);
+  }
+}
+
 __global__ void k_csr_jacobi(int n, double w, const int32_t* __restrict__ rp,
                              const int32_t* __restrict__ cl, const double* __restrict__ v,
                              const double* __restrict__ dinv, const double* __restrict__ b,
@@ -692,6 +722,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_COARSE_MAX")) amg->coarse_max = atoi(e);
   if (const char* e = getenv("HC_AMG_GAMMA")) amg->gamma = atoi(e);
   if (const char* e = getenv("HC_AMG_WDEPTH")) amg->wdepth = atoi(e);
+  if (const char* e = getenv("HC_AMG_WMIN")) amg->wmin = atoi(e);
   if (const char* e = getenv("HC_GRAPHS")) amg->use_graphs = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_REFRESH")) amg->refresh = atoi(e);
   if (const char* e = getenv("HC_AMG_FP32")) amg->fp32_coarse = atoi(e) != 0;
@@ -788,24 +819,61 @@ static void csr_sweep(const Amg& A, const AmgLevel& L, double w, const double* b
   }
 }
 
+// generalized sweep launcher (see k_csr_x)
+template <int XM>
+static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha, const double* b,
+                        const double* x, const int32_t* parent, const double* xc, double* y,
+                        int resid, cudaStream_t s) {
+  double avg = L.n ? (double)L.A.nnz / L.n : 0.0;
+  const int VSsel = avg <= 12.0 ? 1 : (avg <= 48.0 ? 8 : 32);
+  auto go = [&](auto vs_tag, auto* vals) {
+    constexpr int VS = decltype(vs_tag)::value;
+    using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
+    k_csr_x<VS, VT, XM><<<nblk((long long)VS * L.n), TPB, 0, s>>>(
+        L.n, w, alpha, L.A.rp.p, L.A.ci.p, vals, L.dinv.p, b, x, parent, xc, y, resid);
+    HC_COUNT();
+  };
+  const float* vf = L.A.vf.p;
+  const double* vd = L.A.v.p;
+  if (VSsel == 1) { if (A.fp32_coarse) go(std::integral_constant<int, 1>{}, vf); else go(std::integral_constant<int, 1>{}, vd); }
+  else if (VSsel == 8) { if (A.fp32_coarse) go(std::integral_constant<int, 8>{}, vf); else go(std::integral_constant<int, 8>{}, vd); }
+  else { if (A.fp32_coarse) go(std::integral_constant<int, 32>{}, vf); else go(std::integral_constant<int, 32>{}, vd); }
+}
+
 // one cycle at CSR level l >= 1: rhs in L.b, result in L.x
 static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   AmgLevel& L = B.levels[l];
   AmgLevel& U = B.levels[l + 1];
   const double w = A.omega;
-  k_csr_smooth0<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
-  for (int k = 1; k < A.nu_c; ++k) {
-    csr_sweep(A, L, w, L.b.p, L.x.p, L.x2.p, 0, s);
-    std::swap(L.x.p, L.x2.p);
+  // pre-smoothing from a zero guess: the first sweep materialises x0 = w D^-1 b itself
+  int pre = A.nu_c;
+  if (pre >= 2) {
+    csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.x.p, 0, s);
+    for (int k = 2; k < pre; ++k) {
+      csr_sweep_x<0>(A, L, w, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.x2.p, 0, s);
+      std::swap(L.x.p, L.x2.p);
+    }
+    csr_sweep_x<0>(A, L, 0.0, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.res.p, 1, s);
+  } else {
+    k_csr_smooth0<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
+    csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.res.p, 1, s);
   }
-  csr_sweep(A, L, 0.0, L.b.p, L.x.p, L.res.p, 1, s);
   k_restrict_v<<<nblk(8LL * U.n), TPB, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.ptv.p, L.res.p,
                                                U.b.p); HC_COUNT();
   solve_level(A, B, l + 1, s);
-  k_csr_prolong<<<nblk(L.n), TPB, 0, s>>>(L.n, B.alpha, L.P.rp.p, L.P.ci.p, L.P.v.p, U.x.p,
-                                          L.x.p); HC_COUNT();
-  for (int k = 0; k < A.nu_c; ++k) {
-    csr_sweep(A, L, w, L.b.p, L.x.p, L.x2.p, 0, s);
+  const bool tentative = L.P.nnz == (long long)L.n;  // one prolongator entry per row
+  int post = A.nu_c;
+  if (tentative && post >= 1) {
+    // prolongation fused into the first post-sweep (P0 entries are all 1)
+    csr_sweep_x<2>(A, L, w, B.alpha, L.b.p, L.x.p, L.parent.p, U.x.p, L.x2.p, 0, s);
+    std::swap(L.x.p, L.x2.p);
+    --post;
+  } else {
+    k_csr_prolong<<<nblk(L.n), TPB, 0, s>>>(L.n, B.alpha, L.P.rp.p, L.P.ci.p, L.P.v.p, U.x.p,
+                                            L.x.p); HC_COUNT();
+  }
+  for (int k = 0; k < post; ++k) {
+    csr_sweep_x<0>(A, L, w, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
   }
 }
@@ -819,7 +887,7 @@ static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
     return;
   }
   cycle_once(A, B, l, s);
-  int g = (int)l <= A.wdepth ? A.gamma : 1;
+  int g = ((int)l >= A.wmin && (int)l <= A.wdepth) ? A.gamma : 1;
   for (int k = 1; k < g; ++k) {
     HC_CUDA(cudaMemcpyAsync(L.acc.p, L.x.p, L.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     csr_sweep(A, L, 0.0, L.b.p, L.acc.p, L.res.p, 1, s);
