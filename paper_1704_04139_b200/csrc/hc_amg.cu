@@ -945,29 +945,45 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   double* e = A.ea[f].p;
   double* e2 = A.eb[f].p;
   auto sweep = [&](int epi, const double* in, double* out) {
+    const bool p2 = op.stencil_kind == 2;
     if (f == 1) {
-      if (epi == EP_SMOOTH)
-        { if (op.stencil_kind == 2) fine_launch_p<SM_PHI, EP_SMOOTH>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-          else fine_launch_t<SM_PHI, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s); }
-      else
-        { if (op.stencil_kind == 2) fine_launch_p<SM_PHI, EP_RESID>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-          else fine_launch_t<SM_PHI, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s); }
+      if (epi == EP_SMOOTH0) fine_launch_p<SM_PHI, EP_SMOOTH0>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+      else if (epi == EP_SMOOTH) {
+        if (p2) fine_launch_p<SM_PHI, EP_SMOOTH>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+        else fine_launch_t<SM_PHI, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+      } else {
+        if (p2) fine_launch_p<SM_PHI, EP_RESID>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+        else fine_launch_t<SM_PHI, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+      }
     } else {
-      if (epi == EP_SMOOTH)
-        { if (op.stencil_kind == 2) fine_launch_p<SM_CONC, EP_SMOOTH>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-          else fine_launch_t<SM_CONC, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s); }
-      else
-        { if (op.stencil_kind == 2) fine_launch_p<SM_CONC, EP_RESID>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-          else fine_launch_t<SM_CONC, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s); }
+      if (epi == EP_SMOOTH0) fine_launch_p<SM_CONC, EP_SMOOTH0>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+      else if (epi == EP_SMOOTH) {
+        if (p2) fine_launch_p<SM_CONC, EP_SMOOTH>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+        else fine_launch_t<SM_CONC, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+      } else {
+        if (p2) fine_launch_p<SM_CONC, EP_RESID>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+        else fine_launch_t<SM_CONC, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
+      }
     }
     HC_COUNT();
   };
-  k_smooth0_s<<<nb, TPB, 0, s>>>(nv, w, L0.dinv.p, r, e); HC_COUNT();
-  if (B.levels.size() == 1) return e;
+  if (B.levels.size() == 1) {
+    k_smooth0_s<<<nb, TPB, 0, s>>>(nv, w, L0.dinv.p, r, e); HC_COUNT();
+    return e;
+  }
   AmgLevel& L1 = B.levels[1];
-  for (int k = 1; k < A.nu; ++k) {
-    sweep(EP_SMOOTH, e, e2);
-    std::swap(e, e2);
+  if (A.nu >= 2 && op.stencil_kind == 2) {
+    sweep(EP_SMOOTH0, nullptr, e);          // e1 from the zero guess in one pass
+    for (int k = 2; k < A.nu; ++k) {
+      sweep(EP_SMOOTH, e, e2);
+      std::swap(e, e2);
+    }
+  } else {
+    k_smooth0_s<<<nb, TPB, 0, s>>>(nv, w, L0.dinv.p, r, e); HC_COUNT();
+    for (int k = 1; k < A.nu; ++k) {
+      sweep(EP_SMOOTH, e, e2);
+      std::swap(e, e2);
+    }
   }
   sweep(EP_RESID, e, A.res.p);
   k_restrict_v<<<nblk(8LL * L1.n), TPB, 0, s>>>(L1.n, L0.pt_ptr.p, L0.pt_row.p, L0.ptv.p, A.res.p,

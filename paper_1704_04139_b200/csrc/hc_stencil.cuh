@@ -25,7 +25,7 @@
 namespace hc {
 
 enum { SM_FULL = 0, SM_PHI = 1, SM_CONC = 2, SM_CP = 3 };
-enum { EP_STORE = 0, EP_SMOOTH = 1, EP_RESID = 2 };
+enum { EP_STORE = 0, EP_SMOOTH = 1, EP_RESID = 2, EP_SMOOTH0 = 3 };  // SMOOTH0: first sweep from e0 = w D^-1 r
 
 struct FineArgs {
   const uint8_t* lab;
@@ -671,13 +671,15 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
          double omega, double inv_dt, int flags, double2* __restrict__ out2, double* __restrict__ out,
          int zc) {
   constexpr bool FULLM = MODE == SM_FULL;
+  constexpr bool X0 = EPI == EP_SMOOTH0;   // input e0 = w D^-1 r materialised from staged r, dinv
   constexpr int S = 4;
   constexpr int TW = VX + 2, TH = VY + 2, TN = TW * TH;
   using VT = typename std::conditional<FULLM, double2, double>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   VT* sv = reinterpret_cast<VT*>(smem_raw);                       // [S][TN]
   double* sw = reinterpret_cast<double*>(sv + S * TN);             // [S][TN] (FULL only)
-  int* sl = reinterpret_cast<int*>(sw + (FULLM ? S * TN : 0));     // [S][TN]
+  double* sd = sw + (FULLM ? S * TN : 0);                          // [S][TN] dinv (X0 only)
+  int* sl = reinterpret_cast<int*>(sd + (X0 ? S * TN : 0));        // [S][TN]
   __shared__ double sP[36], sC[36], sM[36];
   __shared__ unsigned char sI[36];
   const int tid = threadIdx.y * VX + threadIdx.x;
@@ -714,10 +716,18 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
         if constexpr (FULLM) {
           cp_async16(sv + buf * TN + i, V + idx);
           if (one_c_flag) cp_async8(sw + buf * TN + i, F.w + idx);
+        } else if constexpr (X0) {
+          cp_async8(sv + buf * TN + i, r + idx);
+          cp_async8(sd + buf * TN + i, dinv + idx);
         } else {
           cp_async8(sv + buf * TN + i, e + idx);
         }
       }
+  };
+  // staged value -> stencil input (e, or e0 = w dinv r for the zero-guess sweep)
+  auto val = [&](int slot) -> VT {
+    if constexpr (X0) return omega * sd[slot] * sv[slot];
+    else return sv[slot];
   };
   for (int j = 0; j < 3; ++j) {
     if (z0 + j <= zlast) issue(z0 + j, j);
@@ -735,6 +745,8 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
     if constexpr (FULLM) {
       vm = V[idx];
       if (one_c_flag) wm = F.w[idx];
+    } else if constexpr (X0) {
+      vm = omega * dinv[idx] * r[idx];
     } else {
       vm = e[idx];
     }
@@ -747,7 +759,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
     if (active) {
       if constexpr (!FULLM) {
         if (EPI != EP_STORE) rv = r[v];
-        if (EPI == EP_SMOOTH) dv_ = dinv[v];
+        if (EPI == EP_SMOOTH || EPI == EP_SMOOTH0) dv_ = dinv[v];
       }
     }
     cp_wait1();        // planes z and z+1 have landed (only z+2's group may be pending)
@@ -760,7 +772,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
       const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == GR || a == EL)
                                                              : !(z == nz - 1 && a == CC);
       const bool top = z + 1 >= nz;
-      const VT va = sv[buf * TN + cidx];
+      const VT va = val(buf * TN + cidx);
       if (!in_row) {
         if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
         else out[v] = 0.0;
@@ -784,7 +796,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
           if (d < 4) {
             const int t = d == 0 ? cidx - 1 : (d == 1 ? cidx + 1 : (d == 2 ? cidx - TW : cidx + TW));
             b = sl[buf * TN + t] & 7;
-            vb = sv[buf * TN + t];
+            vb = val(buf * TN + t);
             if constexpr (FULLM) if (one_c) wb = sw[buf * TN + t];
           } else if (d == 4) {
             b = lm;
@@ -792,7 +804,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
             wb = wm;
           } else {
             b = top ? a : (sl[bufp * TN + cidx] & 7);
-            vb = top ? va : sv[bufp * TN + cidx];
+            vb = top ? va : val(bufp * TN + cidx);
             if constexpr (FULLM) if (one_c) wb = top ? wa : sw[bufp * TN + cidx];
           }
           const int i = a6 + b;
@@ -853,7 +865,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
           if (MODE == SM_CONC) rp += inv_dt * va;
           if (EPI == EP_STORE) out[v] = rp;
           else if (EPI == EP_RESID) out[v] = rv - rp;
-          else out[v] = va + omega * dv_ * (rv - rp);
+          else out[v] = va + omega * dv_ * (rv - rp);   // SMOOTH and SMOOTH0
         }
       }
       lm = a;
@@ -871,7 +883,7 @@ inline void fine_launch_p(const DevParams& P, const FineArgs& F, const int32_t* 
                           int n_sm, cudaStream_t s) {
   constexpr bool FULLM = MODE == SM_FULL;
   constexpr int TN = (VX + 2) * (VY + 2);
-  const size_t smem = 4 * TN * ((FULLM ? 16 : 8) + (FULLM ? 8 : 0) + 4);
+  const size_t smem = 4 * TN * ((FULLM ? 16 : 8) + (FULLM ? 8 : 0) + (EPI == EP_SMOOTH0 ? 8 : 0) + 4);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fine_p<MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
