@@ -62,6 +62,9 @@ typedef struct hc_solver_config {
   double linear_rtol;
   double dt_init, dt_min, dt_max, grow_factor, shrink_factor;
   int32_t easy_iter_threshold, implicit_plated;
+  /* Krylov tolerance of Newton iteration k: max(linear_rtol, linear_safety * tol / |F_k|),
+   * i.e. never solve beyond what the nonlinear tolerance can use (0 = always linear_rtol). */
+  double linear_safety;
 } hc_solver_config;
 
 /* Result record of one Newton solve / accepted time step. */

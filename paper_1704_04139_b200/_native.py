@@ -32,7 +32,8 @@ class HcSolverConfig(ctypes.Structure):
                 ("linear_rtol", ctypes.c_double), ("dt_init", ctypes.c_double),
                 ("dt_min", ctypes.c_double), ("dt_max", ctypes.c_double),
                 ("grow_factor", ctypes.c_double), ("shrink_factor", ctypes.c_double),
-                ("easy_iter_threshold", ctypes.c_int32), ("implicit_plated", ctypes.c_int32)]
+                ("easy_iter_threshold", ctypes.c_int32), ("implicit_plated", ctypes.c_int32),
+                ("linear_safety", ctypes.c_double)]
 
 
 class HcNewtonStats(ctypes.Structure):

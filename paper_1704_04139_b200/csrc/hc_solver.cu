@@ -403,9 +403,10 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
       }
     }
     k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
+    const double lin_tol = std::min(0.1, std::max(cfg.linear_rtol, cfg.linear_safety * tol / norm));
     st.krylov_iters += op.dev_krylov
-        ? bicgstab_dev(op, W.b.p, W.d.p, inv_dt, 0, cfg.linear_rtol, cfg.krylov_max_iter, s)
-        : bicgstab(op, W.b.p, W.d.p, inv_dt, 0, cfg.linear_rtol, cfg.krylov_max_iter, s);
+        ? bicgstab_dev(op, W.b.p, W.d.p, inv_dt, 0, lin_tol, cfg.krylov_max_iter, s)
+        : bicgstab(op, W.b.p, W.d.p, inv_dt, 0, lin_tol, cfg.krylov_max_iter, s);
     // positivity guard on the concentration block
     double alpha = 1.0;
     {
@@ -471,9 +472,10 @@ void initial_potential_grid(Operator& op, const double* npl, double mu, const hc
     if (it == 1 || op.amg->refresh) amg_update(op, 0.0, 2, s);
     k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
     k_zero_c<<<nb, TPB, 0, s>>>(n, W.b.p); HC_COUNT();
+    const double lin_tol = std::min(0.1, std::max(cfg.linear_rtol, cfg.linear_safety * tol / norm));
     st.krylov_iters += op.dev_krylov
-        ? bicgstab_dev(op, W.b.p, W.d.p, 0.0, 1, cfg.linear_rtol, cfg.krylov_max_iter, s)
-        : bicgstab(op, W.b.p, W.d.p, 0.0, 1, cfg.linear_rtol, cfg.krylov_max_iter, s);
+        ? bicgstab_dev(op, W.b.p, W.d.p, 0.0, 1, lin_tol, cfg.krylov_max_iter, s)
+        : bicgstab(op, W.b.p, W.d.p, 0.0, 1, lin_tol, cfg.krylov_max_iter, s);
     double alpha = 1.0, norm_try = INFINITY;
     for (int h = 0; h <= 8; ++h) {
       k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p); HC_COUNT();

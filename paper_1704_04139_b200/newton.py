@@ -36,6 +36,9 @@ class SolverConfig:
     easy_iter_threshold: int = 5
     implicit_plated: bool = True
     krylov_max_iter: int = 1000
+    # Krylov tolerance per Newton iteration: max(linear_rtol, linear_safety * tol / |F_k|)
+    # (the linear solve never goes beyond what the Newton tolerance can use); 0 disables
+    linear_safety: float = 0.0
 
     def __post_init__(self):
         if not 0.0 < self.shrink_factor < 1.0 < self.grow_factor:
@@ -61,6 +64,7 @@ class SolverConfig:
         c.grow_factor, c.shrink_factor = self.grow_factor, self.shrink_factor
         c.easy_iter_threshold = self.easy_iter_threshold
         c.implicit_plated = 1 if self.implicit_plated else 0
+        c.linear_safety = self.linear_safety
         return c
 
 

@@ -100,11 +100,14 @@ def test_newton_solve(case):
     assert np.max(np.abs(res.x[nc:] - ref[nc:])) < 1e-8
 
 
-def test_transient_curves(case):
+@pytest.mark.parametrize("linear_safety", [0.0, 0.1])
+def test_transient_curves(case, linear_safety):
+    """Curves vs the reference; also with the inexact-Newton Krylov tolerance the bench
+    uses (linear_safety=0.1: never solve beyond what the Newton tolerance can use)."""
     g, op, dof, params, _ = case
     P, _ = _pkg()
     mu, dt = float(g["mu"]), float(g["dt"])
-    cfg = P.SolverConfig()
+    cfg = P.SolverConfig(linear_safety=linear_safety)
     state = P.prepare_initial_state(op, params, mu, cfg)
     v_cp, v_ac = P.qoi_vectors(dof)
     volts, means, npls = [v_cp @ state.x], [v_ac @ state.x], [state.n_pl.sum()]
