@@ -876,6 +876,29 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
   cp_wait1();
 }
 
+// z-chunking for a single wave: as many CTAs as can be resident at once (occupancy
+// query, cached per instantiation), each marching ceil(nz / bz) planes — no partial
+// last wave, longest possible pipelines.
+inline int ctas_per_sm_target() {
+  static int t = -1;
+  if (t < 0) {
+    const char* e = getenv("HC_ZC_TARGET");
+    t = e ? atoi(e) : 12;
+  }
+  return t;
+}
+
+// grid z-extent: about `target` CTAs per SM in total (HC_ZC_TARGET; 0 = exactly one
+// resident wave from the occupancy query), at least two planes per CTA
+inline int pick_bz(int bx, int by, int nz, int per_sm, int n_sm) {
+  const int target = ctas_per_sm_target();
+  const long long want = (long long)(target > 0 ? target : per_sm) * n_sm;
+  int bz = (int)std::max<long long>(1, want / std::max(1, bx * by));
+  bz = std::min(bz, std::max(1, nz / 2));
+  const int zc = (nz + bz - 1) / bz;
+  return (nz + zc - 1) / zc;
+}
+
 template <int MODE, int EPI>
 inline void fine_launch_p(const DevParams& P, const FineArgs& F, const int32_t* lab4,
                           const double2* V, const double* e, const double* r, const double* dinv,
@@ -884,16 +907,15 @@ inline void fine_launch_p(const DevParams& P, const FineArgs& F, const int32_t* 
   constexpr bool FULLM = MODE == SM_FULL;
   constexpr int TN = (VX + 2) * (VY + 2);
   const size_t smem = 4 * TN * ((FULLM ? 16 : 8) + (FULLM ? 8 : 0) + (EPI == EP_SMOOTH0 ? 8 : 0) + 4);
-  static bool attr = false;
-  if (!attr) {
+  static int per_sm = 0;
+  if (!per_sm) {
     cudaFuncSetAttribute(k_fine_p<MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fine_p<MODE, EPI>, VX * VY, smem);
+    if (per_sm < 1) per_sm = 1;
   }
   const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
-  const long long want = 6LL * n_sm;
-  int zc = (int)std::max<long long>(2, (long long)bx * by * P.nz / want);
-  zc = std::min(zc, 64);
-  const int bz = (P.nz + zc - 1) / zc;
+  const int bz = pick_bz(bx, by, P.nz, per_sm, n_sm);
+  const int zc = (P.nz + bz - 1) / bz;
   k_fine_p<MODE, EPI><<<dim3(bx, by, bz), dim3(VX, VY, 1), smem, s>>>(
       P, F, lab4, V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
 }
@@ -1029,10 +1051,14 @@ inline void res_launch_p(const DevParams& P, const int32_t* lab4, const double2*
                          cudaStream_t s) {
   constexpr int TN = (VX + 2) * (VY + 2);
   const size_t smem = 4 * TN * (16 + 4);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_res_p, VX * VY, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
   const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
-  int zc = (int)std::max<long long>(2, (long long)bx * by * P.nz / (6LL * n_sm));
-  zc = std::min(zc, 64);
-  const int bz = (P.nz + zc - 1) / zc;
+  const int bz = pick_bz(bx, by, P.nz, per_sm, n_sm);
+  const int zc = (P.nz + bz - 1) / bz;
   k_res_p<<<dim3(bx, by, bz), dim3(VX, VY, 1), smem, s>>>(P, lab4, X, mu, parts, cprev, inv_dt,
                                                           out, zc);
 }

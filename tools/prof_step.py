@@ -15,7 +15,8 @@ params = P.MaterialParams(soc_init=rs.soc_init, i00_plel=rs.i00_plel_exchange / 
 op = P.SystemOperator(P.build_dofmap(grid), params)
 h = grid.voxel_size * 1e-6
 mu = -rs.c_rate * params.c_gr_max * params.constants.F * np.count_nonzero(grid.labels == 1) * h**3 / 3600 / (grid.labels.shape[1] * grid.labels.shape[2] * h * h)
-cfg = P.SolverConfig(dt_max=rs.dt, dt_init=min(0.05, rs.dt))
+import os
+cfg = P.SolverConfig(dt_max=rs.dt, dt_init=min(0.05, rs.dt), linear_safety=float(os.environ.get('LS', '0.1')))
 st = P.prepare_initial_state(op, params, mu, cfg)
 x = _dev.to_dev(st.x).clone(); npl = _dev.to_dev(st.n_pl).clone()
 c = cfg.to_c(); s = _native.HcNewtonStats()
