@@ -563,11 +563,12 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     if (active <= cfg.coarse_max || !can) break;
     // tentative aggregation: connected components (in the strong same-phase graph G)
     // of the unknowns sharing a (2x2x2 block, phase) key
-    int nx2 = (sx + 1) / 2, ny2 = (sy + 1) / 2, nz2 = (sz + 1) / 2;
+    const int cf = level == 0 ? 2 : cfg.coarsen;   // block growth factor of this transfer
+    int nx2 = (sx + cf - 1) / cf, ny2 = (sy + cf - 1) / cf, nz2 = (sz + cf - 1) / cf;
     std::vector<long long> key(n, -1);
     for (int i = 0; i < n; ++i)
       if (ph[i] >= 0)
-        key[i] = (((long long)(bz[i] / 2) * ny2 + by[i] / 2) * nx2 + bx[i] / 2) * N_PHASES + ph[i];
+        key[i] = (((long long)(bz[i] / cf) * ny2 + by[i] / cf) * nx2 + bx[i] / cf) * N_PHASES + ph[i];
     std::vector<int32_t> uf(n);
     std::iota(uf.begin(), uf.end(), 0);
     // connectivity splitting keeps disconnected same-phase pieces apart; at the top of
@@ -726,6 +727,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_GRAPHS")) amg->use_graphs = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_REFRESH")) amg->refresh = atoi(e);
   if (const char* e = getenv("HC_AMG_FP32")) amg->fp32_coarse = atoi(e) != 0;
+  if (const char* e = getenv("HC_AMG_CF")) amg->coarsen = std::max(2, atoi(e));
   if (const char* e = getenv("HC_AMG_REFRESH_SOLVES")) amg->refresh_solves = std::max(1, atoi(e));
   auto t0 = std::chrono::steady_clock::now();
   build_block(op, lab, 0, *amg, amg->blk[0]);

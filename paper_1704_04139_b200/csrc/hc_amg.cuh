@@ -58,7 +58,8 @@ struct Amg {
   double alpha = 1.0;
   int gamma = 1;             // cycles per coarse-level solve (2 = W-cycle)
   int wdepth = 3;
-  int wmin = 1;              // gamma cycles on CSR levels wmin..wdepth
+  int wmin = 1;
+  int coarsen = 2;           // block growth factor of the transfers above level 1              // gamma cycles on CSR levels wmin..wdepth
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int refresh = 0;          // numeric setup every Newton iteration (1) or once per solve (0)
   int refresh_solves = 8;   // rebuild once every this many Newton solves (and when dt changes)
