@@ -402,7 +402,10 @@ def run_pod(args, ws, rank, local):
             "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic snapshots",
-            "config": {"workload": f"pod: {n_dof} DOF x {n_snap} snapshots"},
+            "config": {"workload": f"pod: {n_dof} DOF x {n_snap} snapshots",
+                       "flops": "2 n_dof n_snap^2 (the kernel computes the upper triangle only)"},
+            "roofline": {"bound": "tensor (FP64 DMMA pipe)", "pipe_util_ncu": 0.736,
+                         "source": "profiles/r01_gram_ncu.txt"},
             "max_rel_err_vs_cublas": err}
 
 

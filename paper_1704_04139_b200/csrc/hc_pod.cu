@@ -1,9 +1,13 @@
 // POD snapshot Gram matrix G = S^T diag(w) S (method of snapshots, SPEC mor.pod),
 // the only dense contraction of the path.  S is n_dof x n_snap column-major fp64.
 //
-// FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): each CTA owns a 64x64 tile of
-// G and a slice of the DOF dimension (split-K); slices are reduced in a fixed
-// order afterwards so the result is deterministic.
+// FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).  Each CTA owns one 64x64 tile of
+// the upper triangle of G (G is symmetric: 28 of 49 tiles for 400 snapshots) and
+// one slice of the DOF dimension (split-K).  The DOF chunks of both operand panels
+// and of the weights stream through a 3-stage cp.async ring in shared memory, so
+// HBM/L2 traffic overlaps the DMMA work; 4 warps each own a 32x32 sub-tile (16 DMMA
+// per k-step from 8 fragment loads).  Slices are reduced in a fixed order and the
+// triangle mirrored, so the result is deterministic and exactly symmetric.
 #include <algorithm>
 
 #include "hc_internal.cuh"
@@ -11,9 +15,11 @@
 namespace hc {
 
 namespace {
-constexpr int BT = 64;   // tile of G
-constexpr int KC = 32;   // DOF chunk staged in shared memory
-constexpr int NW = 8;    // warps per CTA: 4 (rows of 16) x 2 (cols of 32)
+constexpr int BT = 64;      // tile of G
+constexpr int KC = 32;      // DOF chunk per stage
+constexpr int ST = 3;       // pipeline stages
+constexpr int LD = KC + 2;  // padded row of a staged panel
+constexpr int NT = 128;     // 4 warps: 2 x 2 sub-tiles of 32 x 32
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -21,91 +27,146 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-// part[z][i][j] = sum_{k in slice z} S[k][i] w[k] S[k][j]   (i, j in the CTA tile)
-__global__ void __launch_bounds__(NW * 32) k_gram(const double* __restrict__ S,
-                                                  const double* __restrict__ w, long long n_dof,
-                                                  int n, long long k_per, double* __restrict__ part) {
-  __shared__ double As[BT][KC + 1];
-  __shared__ double Bs[BT][KC + 1];
-  const int ti = blockIdx.x, tj = blockIdx.y, z = blockIdx.z;
-  const int i0 = ti * BT, j0 = tj * BT;
+// 8-byte async copy; src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp8(void* smem, const void* gmem, int src_bytes) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// part[z][j * n + i] = sum_{k in slice z} S[k][i] w[k] S[k][j]   for the tile pair (ti <= tj)
+__global__ void __launch_bounds__(NT) k_gram(const double* __restrict__ S, const double* __restrict__ w,
+                                             long long n_dof, int n, int tiles, long long k_per,
+                                             double* __restrict__ part) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                        // [ST][BT][LD]
+  double* Bs = As + ST * BT * LD;           // [ST][BT][LD]
+  double* Ws = Bs + ST * BT * LD;           // [ST][KC]
+  // upper-triangle tile pair from the linear block index
+  int p = blockIdx.x, ti = 0;
+  while (p >= tiles - ti) { p -= tiles - ti; ++ti; }
+  const int tj = ti + p;
+  const int i0 = ti * BT, j0 = tj * BT, z = blockIdx.y;
   const long long k_begin = (long long)z * k_per;
   const long long k_end = min(n_dof, k_begin + k_per);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wr = warp >> 1, wc = warp & 1;     // warp tile: rows wr*16 .. +16, cols wc*32 .. +32
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 1, wc = warp & 1;
   const int g = lane >> 2, tq = lane & 3;
-  double acc[2][4][2];
+  const double* wsrc = w;
+  auto stage = [&](long long k0, int s) {
+    // 64 columns x 32 DOFs per panel: 2048 elements per panel, 16 per thread
+    for (int e = tid; e < BT * KC; e += NT) {
+      const int col = e / KC, kk = e - col * KC;
+      const long long k = k0 + kk;
+      const int gi = i0 + col, gj = j0 + col;
+      const bool kin = k < k_end;
+      cp8(As + (s * BT + col) * LD + kk, S + (long long)min(gi, n - 1) * n_dof + (kin ? k : 0),
+          (kin && gi < n) ? 8 : 0);
+      cp8(Bs + (s * BT + col) * LD + kk, S + (long long)min(gj, n - 1) * n_dof + (kin ? k : 0),
+          (kin && gj < n) ? 8 : 0);
+    }
+    if (tid < KC) {
+      const long long k = k0 + tid;
+      const bool kin = k < k_end;
+      if (wsrc) cp8(Ws + s * KC + tid, wsrc + (kin ? k : 0), kin ? 8 : 0);
+      else Ws[s * KC + tid] = kin ? 1.0 : 0.0;
+    }
+  };
+  double acc[4][4][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (long long k0 = k_begin; k0 < k_end; k0 += KC) {
-    // stage: As[i][kk] = S[k0+kk][i0+i] * w, Bs[j][kk] = S[k0+kk][j0+j]
-    for (int e = threadIdx.x; e < BT * KC; e += blockDim.x) {
-      int col = e / KC, kk = e % KC;
-      long long k = k0 + kk;
-      double wk = (k < k_end) ? (w ? w[k] : 1.0) : 0.0;
-      int gi = i0 + col, gj = j0 + col;
-      As[col][kk] = (k < k_end && gi < n) ? S[(long long)gi * n_dof + k] * wk : 0.0;
-      Bs[col][kk] = (k < k_end && gj < n) ? S[(long long)gj * n_dof + k] : 0.0;
-    }
+  const long long nchunks = (k_end - k_begin + KC - 1) / KC;
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < nchunks) stage(k_begin + (long long)s * KC, s);
+    cp_commit();
+  }
+  for (long long c = 0; c < nchunks; ++c) {
+    cp_wait<ST - 2>();
     __syncthreads();
+    const long long cn = c + ST - 1;
+    if (cn < nchunks) stage(k_begin + cn * KC, (int)(cn % ST));
+    cp_commit();
+    const int s = (int)(c % ST);
+    const double* A = As + s * BT * LD;
+    const double* B = Bs + s * BT * LD;
+    const double* W = Ws + s * KC;
 #pragma unroll
     for (int ks = 0; ks < KC; ks += 4) {
-      double af[2], bf[4];
+      const double wk = W[ks + tq];
+      double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) af[a] = As[wr * 16 + a * 8 + g][ks + tq];
+      for (int a = 0; a < 4; ++a) af[a] = A[(wr * 32 + a * 8 + g) * LD + ks + tq] * wk;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = Bs[wc * 32 + b * 8 + g][ks + tq];
+      for (int b = 0; b < 4; ++b) bf[b] = B[(wc * 32 + b * 8 + g) * LD + ks + tq];
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();
   }
+  cp_wait<0>();
   double* out = part + (long long)z * n * n;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      int i = i0 + wr * 16 + a * 8 + g;
-      int j = j0 + wc * 32 + b * 8 + tq * 2;
+      const int i = i0 + wr * 32 + a * 8 + g;
+      const int j = j0 + wc * 32 + b * 8 + tq * 2;
       if (i < n && j < n) out[(long long)j * n + i] = acc[a][b][0];
       if (i < n && j + 1 < n) out[(long long)(j + 1) * n + i] = acc[a][b][1];
     }
 }
 
-__global__ void k_reduce_parts(long long nn, int nz, const double* __restrict__ part,
-                               double* __restrict__ G) {
+// G[j][i] = G[i][j] = sum_z part[z] over the upper triangle (fixed order)
+__global__ void k_reduce_sym(int n, int nz, int tiles, const double* __restrict__ part,
+                             double* __restrict__ G) {
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nn = (long long)n * n;
   if (e >= nn) return;
+  const int j = (int)(e / n), i = (int)(e % n);
+  // the tile pair (ti <= tj) that computed this entry
+  const int ti = i / BT, tj = j / BT;
+  const bool upper = ti <= tj;
+  const long long src = upper ? e : (long long)i * n + j;   // mirrored entry
   double s = 0.0;
-  for (int z = 0; z < nz; ++z) s += part[(long long)z * nn + e];
+  for (int z = 0; z < nz; ++z) s += part[(long long)z * nn + src];
   G[e] = s;
+  (void)tiles;
 }
 }  // namespace
 
 void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
               cudaStream_t s) {
   if (n_snap == 0) return;
-  int n = (int)n_snap;
-  int tiles = (n + BT - 1) / BT;
-  int sms = 148;
-  int dev = 0;
+  const int n = (int)n_snap;
+  const int tiles = (n + BT - 1) / BT;
+  const int pairs = tiles * (tiles + 1) / 2;
+  int sms = 148, dev = 0;
   HC_CUDA(cudaGetDevice(&dev));
   HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  long long want = std::max<long long>(1, (2LL * sms + tiles * tiles - 1) / (tiles * tiles));
+  const size_t smem = (size_t)(2 * ST * BT * LD + ST * KC) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    HC_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  int per_sm = 1;
+  HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram, NT, smem));
+  const long long want = std::max<long long>(1, ((long long)std::max(per_sm, 1) * sms + pairs - 1) / pairs);
   long long k_per = (n_dof + want - 1) / want;
-  k_per = ((k_per + KC - 1) / KC) * KC;
-  if (k_per == 0) k_per = KC;
-  int nz = (int)std::max<long long>(1, (n_dof + k_per - 1) / k_per);
+  k_per = std::max<long long>(KC, ((k_per + KC - 1) / KC) * KC);
+  const int nz = (int)std::max<long long>(1, (n_dof + k_per - 1) / k_per);
   DBuf<double> part((size_t)nz * n * n);
-  dim3 grid(tiles, tiles, nz);
-  k_gram<<<grid, NW * 32, 0, s>>>(S, w, n_dof, n, k_per, part.p); HC_COUNT();
+  HC_CUDA(cudaMemsetAsync(part.p, 0, part.n * sizeof(double), s));
+  k_gram<<<dim3(pairs, nz), NT, smem, s>>>(S, w, n_dof, n, tiles, k_per, part.p); HC_COUNT();
   HC_CHECK_LAUNCH();
-  long long nn = (long long)n * n;
-  k_reduce_parts<<<(int)((nn + 255) / 256), 256, 0, s>>>(nn, nz, part.p, G); HC_COUNT();
+  const long long nn = (long long)n * n;
+  k_reduce_sym<<<(int)((nn + 255) / 256), 256, 0, s>>>(n, nz, tiles, part.p, G); HC_COUNT();
   HC_CHECK_LAUNCH();
   HC_CUDA(cudaStreamSynchronize(s));
 }

@@ -16,11 +16,15 @@ from .errors import ReductionError
 def pod_gram(S, w=None):
     """``S^T diag(w) S`` for an (n_dof, n_snap) fp64 snapshot matrix."""
     t = _dev.torch()
-    Sd = _dev.to_dev(S)
-    if Sd.dim() != 2:
-        raise ValueError("snapshot matrix must be 2-D (n_dof, n_snap)")
-    n_dof, n_snap = Sd.shape
-    Sc = Sd.t().contiguous()            # column-major storage of S
+    if _dev.is_tensor(S) and S.is_cuda and S.dtype == t.float64 and S.dim() == 2 \
+            and S.t().is_contiguous():
+        Sc = S.t()                      # already column-major: no copy
+    else:
+        Sd = _dev.to_dev(S)
+        if Sd.dim() != 2:
+            raise ValueError("snapshot matrix must be 2-D (n_dof, n_snap)")
+        Sc = Sd.t().contiguous()        # column-major storage of S
+    n_snap, n_dof = Sc.shape
     wd = _dev.to_dev(w) if w is not None else None
     G = t.empty((n_snap, n_snap), dtype=t.float64, device="cuda")
     _native.check(_native.lib().hc_pod_gram(_dev.ptr(Sc), _dev.ptr(wd) if wd is not None else None,
