@@ -663,7 +663,25 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 // 4-deep shared-memory ring: while plane z is computed, planes z+1..z+3 are in
 // flight, so every SM keeps several planes of HBM traffic outstanding without
 // spending registers on it.  z-1 of the own column is kept in registers, z+1 is
-// read from the ring.
+// read from the ring.  The z loop is unrolled by the ring depth so every ring slot
+// is a compile-time offset (no per-plane slot arithmetic), and interface faces are
+// handled in a second pass only by voxels that own interface slots (the per-voxel
+// coefficient rows are zero on non-interface faces).
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async4a(unsigned sa, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8a(unsigned sa, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16a(unsigned sa, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+template <int K>
+using SlotC = std::integral_constant<int, K>;
+
 template <int MODE, int EPI>
 __global__ void __launch_bounds__(VX * VY)
 k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double2* __restrict__ V,
@@ -674,6 +692,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
   constexpr bool X0 = EPI == EP_SMOOTH0;   // input e0 = w D^-1 r materialised from staged r, dinv
   constexpr int S = 4;
   constexpr int TW = VX + 2, TH = VY + 2, TN = TW * TH;
+  constexpr int VB = FULLM ? 16 : 8;       // bytes per staged value
   using VT = typename std::conditional<FULLM, double2, double>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   VT* sv = reinterpret_cast<VT*>(smem_raw);                       // [S][TN]
@@ -681,13 +700,11 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
   double* sd = sw + (FULLM ? S * TN : 0);                          // [S][TN] dinv (X0 only)
   int* sl = reinterpret_cast<int*>(sd + (X0 ? S * TN : 0));        // [S][TN]
   __shared__ double sP[36], sC[36], sM[36];
-  __shared__ unsigned char sI[36];
   const int tid = threadIdx.y * VX + threadIdx.x;
   if (tid < 36) {
     sP[tid] = P.gP[tid];
     sC[tid] = P.gC[tid];
     sM[tid] = P.gMig[tid];
-    sI[tid] = P.ifc[tid];
   }
   const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
   const int x0 = blockIdx.x * VX, y0 = blockIdx.y * VY;
@@ -696,8 +713,10 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);
   const int zlast = min(z1, nz - 1);  // last plane that must be staged
   const bool one_c_flag = FULLM && (flags & 4);
+  // this thread's (up to two) halo elements: global column offset + shared address
   int hoff[2];
   bool hval[2];
+  unsigned hsa_l[2], hsa_v[2], hsa_w[2], hsa_d[2];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int i = tid + k * VX * VY;
@@ -705,22 +724,27 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
     const int hy = i / TW, hx = i - hy * TW;
     const int gx = min(max(x0 + hx - 1, 0), nx - 1), gy = min(max(y0 + hy - 1, 0), ny - 1);
     hoff[k] = gy * nx + gx;
+    hsa_l[k] = smem_addr(sl + i);
+    hsa_v[k] = smem_addr(sv + i);
+    hsa_w[k] = smem_addr(sw + i);
+    hsa_d[k] = smem_addr(sd + i);
   }
-  auto issue = [&](int zz, int buf) {
+  const int col = active ? y * nx + x : 0;
+  auto issue = [&](int zz, auto slotc) {
+    constexpr int buf = decltype(slotc)::value;
 #pragma unroll
     for (int k = 0; k < 2; ++k)
       if (hval[k]) {
-        const int i = tid + k * VX * VY;
         const long long idx = (long long)zz * nxy + hoff[k];
-        cp_async4(sl + buf * TN + i, lab4 + idx);
+        cp_async4a(hsa_l[k] + buf * TN * 4, lab4 + idx);
         if constexpr (FULLM) {
-          cp_async16(sv + buf * TN + i, V + idx);
-          if (one_c_flag) cp_async8(sw + buf * TN + i, F.w + idx);
+          cp_async16a(hsa_v[k] + buf * TN * VB, V + idx);
+          if (one_c_flag) cp_async8a(hsa_w[k] + buf * TN * 8, F.w + idx);
         } else if constexpr (X0) {
-          cp_async8(sv + buf * TN + i, r + idx);
-          cp_async8(sd + buf * TN + i, dinv + idx);
+          cp_async8a(hsa_v[k] + buf * TN * 8, r + idx);
+          cp_async8a(hsa_d[k] + buf * TN * 8, dinv + idx);
         } else {
-          cp_async8(sv + buf * TN + i, e + idx);
+          cp_async8a(hsa_v[k] + buf * TN * 8, e + idx);
         }
       }
   };
@@ -729,12 +753,13 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
     if constexpr (X0) return omega * sd[slot] * sv[slot];
     else return sv[slot];
   };
-  for (int j = 0; j < 3; ++j) {
-    if (z0 + j <= zlast) issue(z0 + j, j);
-    cp_commit();
-  }
+  if (z0 <= zlast) issue(z0, SlotC<0>{});
+  cp_commit();
+  if (z0 + 1 <= zlast) issue(z0 + 1, SlotC<1>{});
+  cp_commit();
+  if (z0 + 2 <= zlast) issue(z0 + 2, SlotC<2>{});
+  cp_commit();
   const int cidx = (threadIdx.y + 1) * TW + threadIdx.x + 1;
-  const int col = active ? y * nx + x : 0;
   VT vm{};
   double wm = 0.0;
   int lm = 0;
@@ -752,8 +777,10 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
     }
   }
   const double tp = P.t_plus;
-  for (int z = z0; z < z1; ++z) {
-    const int j = z - z0, buf = j % S, bufp = (j + 1) % S;
+  const long long nslot = F.nslot;
+  auto step = [&](int z, auto slotc) {
+    constexpr int buf = decltype(slotc)::value;
+    constexpr int bufp = (buf + 1) % S;
     const int v = z * nxy + col;
     double rv = 0.0, dv_ = 0.0;
     if (active) {
@@ -764,114 +791,144 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
     }
     cp_wait1();        // planes z and z+1 have landed (only z+2's group may be pending)
     __syncthreads();
-    if (z + 3 <= zlast) issue(z + 3, (j + 3) % S);  // reuses plane z-1's slot
+    if (z + 3 <= zlast) issue(z + 3, SlotC<(buf + 3) % S>{});  // reuses plane z-1's slot
     cp_commit();
-    if (active) {
-      const int aw = sl[buf * TN + cidx];   // phase | (interface rank + 1) << 3
-      const int a = aw & 7;
-      const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == GR || a == EL)
-                                                             : !(z == nz - 1 && a == CC);
-      const bool top = z + 1 >= nz;
-      const VT va = val(buf * TN + cidx);
-      if (!in_row) {
-        if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
-        else out[v] = 0.0;
-      } else {
-        const int rk = (aw >> 3) - 1;
-        const int a6 = a * 6;
-        const bool solid = a != EL;
-        double rc = 0.0, rp = 0.0;
-        double wa = 0.0;
-        bool one_c = false;
+    if (!active) return;
+    const int aw = sl[buf * TN + cidx];   // phase | (interface rank + 1) << 3
+    const int a = aw & 7;
+    const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == GR || a == EL)
+                                                           : !(z == nz - 1 && a == CC);
+    const bool top = z + 1 >= nz;
+    const VT va = val(buf * TN + cidx);
+    double wa = 0.0;
+    if constexpr (FULLM) wa = one_c_flag ? sw[buf * TN + cidx] : 0.0;
+    if (!in_row) {
+      if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
+      else out[v] = 0.0;
+    } else {
+      const int rk = (aw >> 3) - 1;
+      const int a6 = a * 6;
+      const bool solid = a != EL;
+      double rc = 0.0, rp = 0.0;
+      bool one_c = false;
+      if constexpr (FULLM) one_c = one_c_flag && a == EL;
+      int bb[6];
+      VT vbv[6];
+#pragma unroll
+      for (int d = 0; d < 6; ++d) {
+        // neighbour d straight from the ring (z-1 from registers, z+1 from the next slot)
+        int b;
+        VT vb;
+        double wb = 0.0;
+        if (d < 4) {
+          const int t = d == 0 ? cidx - 1 : (d == 1 ? cidx + 1 : (d == 2 ? cidx - TW : cidx + TW));
+          b = sl[buf * TN + t] & 7;
+          vb = val(buf * TN + t);
+          if constexpr (FULLM) if (one_c) wb = sw[buf * TN + t];
+        } else if (d == 4) {
+          b = lm;
+          vb = vm;
+          wb = wm;
+        } else {
+          b = top ? a : (sl[bufp * TN + cidx] & 7);
+          vb = top ? va : val(bufp * TN + cidx);
+          if constexpr (FULLM) if (one_c) wb = top ? wa : sw[bufp * TN + cidx];
+        }
+        bb[d] = b;
+        vbv[d] = vb;
+        const int i = a6 + b;
         if constexpr (FULLM) {
-          one_c = one_c_flag && a == EL;
-          if (one_c) wa = sw[buf * TN + cidx];
+          const double dp = va.y - vb.y;
+          rp += sP[i] * dp;
+          rc += sC[i] * (va.x - vb.x) + sM[i] * dp;
+          if (one_c && sM[i] != 0.0) {
+            const double dq = wa * va.x - wb * vb.x;
+            rp += dq;
+            rc += tp * dq;
+          }
+        } else if (MODE == SM_PHI) {
+          rp += sP[i] * (va - vb);
+        } else if (MODE == SM_CONC) {
+          rp += sC[i] * (va - vb);
+        }
+      }
+      if (rk >= 0) {
+        // interface kinetics: this voxel's six coefficient slots (zero off-interface)
+        const long long f = 6LL * rk;
+        double cg[6], ca[6], cb[6];
+        if constexpr (FULLM || MODE == SM_PHI || MODE == SM_CP) {
+          const double2* q = reinterpret_cast<const double2*>(F.vcoef + 2 * nslot + f);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const double2 t = __ldg(q + k);
+            cg[2 * k] = t.x;
+            cg[2 * k + 1] = t.y;
+          }
+        }
+        if constexpr (FULLM || MODE == SM_CONC) {
+          const double2* qa = reinterpret_cast<const double2*>(F.vcoef + f);
+          const double2* qb = reinterpret_cast<const double2*>(F.vcoef + nslot + f);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const double2 ta = __ldg(qa + k), tb = __ldg(qb + k);
+            ca[2 * k] = ta.x;
+            ca[2 * k + 1] = ta.y;
+            cb[2 * k] = tb.x;
+            cb[2 * k + 1] = tb.y;
+          }
         }
 #pragma unroll
         for (int d = 0; d < 6; ++d) {
-          // neighbour d straight from the ring (z-1 from registers, z+1 from the next slot)
-          int b;
-          VT vb;
-          double wb = 0.0;
-          if (d < 4) {
-            const int t = d == 0 ? cidx - 1 : (d == 1 ? cidx + 1 : (d == 2 ? cidx - TW : cidx + TW));
-            b = sl[buf * TN + t] & 7;
-            vb = val(buf * TN + t);
-            if constexpr (FULLM) if (one_c) wb = sw[buf * TN + t];
-          } else if (d == 4) {
-            b = lm;
-            vb = vm;
-            wb = wm;
-          } else {
-            b = top ? a : (sl[bufp * TN + cidx] & 7);
-            vb = top ? va : val(bufp * TN + cidx);
-            if constexpr (FULLM) if (one_c) wb = top ? wa : sw[bufp * TN + cidx];
-          }
-          const int i = a6 + b;
+          const bool bv = a == GR || bb[d] == GR;
+          const VT vb = vbv[d];
           if constexpr (FULLM) {
-            const double dp = va.y - vb.y;
-            rp += sP[i] * dp;
-            rc += sC[i] * (va.x - vb.x) + sM[i] * dp;
-            if (one_c && sM[i] != 0.0) {
-              const double dq = wa * va.x - wb * vb.x;
-              rp += dq;
-              rc += tp * dq;
+            const double2 vs = solid ? va : vb, ve = solid ? vb : va;
+            const double dv = (bv ? ca[d] * vs.x : 0.0) + cb[d] * ve.x + cg[d] * (vs.y - ve.y);
+            if (solid) {
+              if (bv) rc += dv;
+              rp += dv;
+            } else {
+              rc -= dv;
+              rp -= dv;
             }
           } else if (MODE == SM_PHI) {
-            rp += sP[i] * (va - vb);
-          } else if (MODE == SM_CONC) {
-            rp += sC[i] * (va - vb);
-          }
-          if (sI[i]) {
-            const long long f = 6LL * rk + d;
-            const bool bv = a == GR || b == GR;
-            if constexpr (FULLM) {
-              const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f),
-                           cg = __ldg(F.vcoef + 2 * F.nslot + f);
-              const double2 vs = solid ? va : vb, ve = solid ? vb : va;
-              const double dv = (bv ? ca * vs.x : 0.0) + cb * ve.x + cg * (vs.y - ve.y);
-              if (solid) {
-                if (bv) rc += dv;
-                rp += dv;
-              } else {
-                rc -= dv;
-                rp -= dv;
-              }
-            } else if (MODE == SM_PHI) {
-              rp += __ldg(F.vcoef + 2 * F.nslot + f) * (va - vb);
-            } else if (MODE == SM_CP) {
-              const double cg = __ldg(F.vcoef + 2 * F.nslot + f);
-              if (solid) {
-                if (bv) rp += cg * (va - vb);
-              } else {
-                rp += (1.0 - tp) * cg * (va - vb);
-              }
+            rp += cg[d] * (va - vb);
+          } else if (MODE == SM_CP) {
+            if (solid) {
+              if (bv) rp += cg[d] * (va - vb);
             } else {
-              const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f);
-              if (solid) {
-                if (bv) rp += ca * va + cb * vb;
-              } else {
-                rp -= (1.0 - tp) * ((bv ? ca * vb : 0.0) + cb * va);
-              }
+              rp += (1.0 - tp) * cg[d] * (va - vb);
+            }
+          } else {
+            if (solid) {
+              if (bv) rp += ca[d] * va + cb[d] * vb;
+            } else {
+              rp -= (1.0 - tp) * ((bv ? ca[d] * vb : 0.0) + cb[d] * va);
             }
           }
         }
-        if constexpr (FULLM) {
-          if ((flags & 1) && (a == GR || a == EL)) rc += va.x * inv_dt;
-          if ((flags & 2) && a == EL) rc -= tp * rp;
-          if (flags & 8) rc = 0.0;
-          out2[v] = make_double2(rc, rp);
-        } else {
-          if (MODE == SM_CONC) rp += inv_dt * va;
-          if (EPI == EP_STORE) out[v] = rp;
-          else if (EPI == EP_RESID) out[v] = rv - rp;
-          else out[v] = va + omega * dv_ * (rv - rp);   // SMOOTH and SMOOTH0
-        }
       }
-      lm = a;
-      vm = va;
-      if constexpr (FULLM) wm = one_c_flag ? sw[buf * TN + cidx] : 0.0;
+      if constexpr (FULLM) {
+        if ((flags & 1) && (a == GR || a == EL)) rc += va.x * inv_dt;
+        if ((flags & 2) && a == EL) rc -= tp * rp;
+        if (flags & 8) rc = 0.0;
+        out2[v] = make_double2(rc, rp);
+      } else {
+        if (MODE == SM_CONC) rp += inv_dt * va;
+        if (EPI == EP_STORE) out[v] = rp;
+        else if (EPI == EP_RESID) out[v] = rv - rp;
+        else out[v] = va + omega * dv_ * (rv - rp);   // SMOOTH and SMOOTH0
+      }
     }
+    lm = a;
+    vm = va;
+    if constexpr (FULLM) wm = wa;
+  };
+  for (int zb = z0; zb < z1; zb += S) {
+    step(zb, SlotC<0>{});
+    if (zb + 1 < z1) step(zb + 1, SlotC<1>{});
+    if (zb + 2 < z1) step(zb + 2, SlotC<2>{});
+    if (zb + 3 < z1) step(zb + 3, SlotC<3>{});
   }
   cp_wait1();
 }
@@ -910,6 +967,7 @@ inline void fine_launch_p(const DevParams& P, const FineArgs& F, const int32_t* 
   static int per_sm = 0;
   if (!per_sm) {
     cudaFuncSetAttribute(k_fine_p<MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_fine_p<MODE, EPI>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fine_p<MODE, EPI>, VX * VY, smem);
     if (per_sm < 1) per_sm = 1;
   }
@@ -1053,6 +1111,7 @@ inline void res_launch_p(const DevParams& P, const int32_t* lab4, const double2*
   const size_t smem = 4 * TN * (16 + 4);
   static int per_sm = 0;
   if (!per_sm) {
+    cudaFuncSetAttribute(k_res_p, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_res_p, VX * VY, smem);
     if (per_sm < 1) per_sm = 1;
   }
