@@ -13,7 +13,7 @@ from .errors import (ConfigError, HalfcellError, ModelError, NativeError, NonCon
                      NumericsError, ReductionError, SimulationError)
 from .params import HcParams
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhalfcell_b200.so")
+LIB_PATH = os.environ.get("HC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhalfcell_b200.so")
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_int64_p = ctypes.POINTER(ctypes.c_int64)

@@ -30,6 +30,7 @@
 
 #include "hc_amg.cuh"
 #include "hc_stencil.cuh"
+#include "hc_tma.cuh"
 
 namespace hc {
 
@@ -942,30 +943,20 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   const long long nv = op.P.nvox;
   const double w = A.omega;
   const int nb = nblk(nv);
-  FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p};
+  FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
+             op.if_cslot.p};
   const dim3 vg = vox_grid(op.P), vb = vox_block();
   double* e = A.ea[f].p;
   double* e2 = A.eb[f].p;
   auto sweep = [&](int epi, const double* in, double* out) {
-    const bool p2 = op.stencil_kind == 2;
     if (f == 1) {
-      if (epi == EP_SMOOTH0) fine_launch_p<SM_PHI, EP_SMOOTH0>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-      else if (epi == EP_SMOOTH) {
-        if (p2) fine_launch_p<SM_PHI, EP_SMOOTH>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-        else fine_launch_t<SM_PHI, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-      } else {
-        if (p2) fine_launch_p<SM_PHI, EP_RESID>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-        else fine_launch_t<SM_PHI, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-      }
+      if (epi == EP_SMOOTH0) fine_launch_op<SM_PHI, EP_SMOOTH0>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
+      else if (epi == EP_SMOOTH) fine_launch_op<SM_PHI, EP_SMOOTH>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
+      else fine_launch_op<SM_PHI, EP_RESID>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
     } else {
-      if (epi == EP_SMOOTH0) fine_launch_p<SM_CONC, EP_SMOOTH0>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-      else if (epi == EP_SMOOTH) {
-        if (p2) fine_launch_p<SM_CONC, EP_SMOOTH>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-        else fine_launch_t<SM_CONC, EP_SMOOTH>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-      } else {
-        if (p2) fine_launch_p<SM_CONC, EP_RESID>(op.P, F, op.lab4.p, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-        else fine_launch_t<SM_CONC, EP_RESID>(op.P, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, op.n_sm, s);
-      }
+      if (epi == EP_SMOOTH0) fine_launch_op<SM_CONC, EP_SMOOTH0>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
+      else if (epi == EP_SMOOTH) fine_launch_op<SM_CONC, EP_SMOOTH>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
+      else fine_launch_op<SM_CONC, EP_RESID>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
     }
     HC_COUNT();
   };
@@ -974,7 +965,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
     return e;
   }
   AmgLevel& L1 = B.levels[1];
-  if (A.nu >= 2 && op.stencil_kind == 2) {
+  if (A.nu >= 2) {
     sweep(EP_SMOOTH0, nullptr, e);          // e1 from the zero guess in one pass
     for (int k = 2; k < A.nu; ++k) {
       sweep(EP_SMOOTH, e, e2);
@@ -1013,13 +1004,10 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
     return;
   }
   // c-block right-hand side: T r_c - (T J)_cp e_phi
-  FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p};
-  if (op.stencil_kind == 2)
-    fine_launch_p<SM_CP, EP_RESID>(op.P, F, op.lab4.p, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0,
-                                   nullptr, A.rc2.p, op.n_sm, s);
-  else
-    fine_launch_t<SM_CP, EP_RESID>(op.P, F, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0, nullptr,
-                                   A.rc2.p, op.n_sm, s);
+  FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
+             op.if_cslot.p};
+  fine_launch_op<SM_CP, EP_RESID>(op, F, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0,
+                                  nullptr, A.rc2.p, s);
   HC_COUNT();
   double* ec = vcycle_fine(op, 0, A.rc2.p, inv_dt, s);
   k_merge_s<<<nb, TPB, 0, s>>>(nv, ec, ep, z); HC_COUNT();

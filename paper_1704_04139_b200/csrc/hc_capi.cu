@@ -22,6 +22,7 @@ void pod_gram(const double* S, const double* w, long long n_dof, long long n_sna
 
 Operator::~Operator() {
   destroy_krylov_graphs(kg);
+  delete tma;
   delete amg;
   delete work;
   if (stream) cudaStreamDestroy(stream);

@@ -218,6 +218,7 @@ struct DBuf {
 struct Amg;   // hc_amg.cu
 struct Work;  // hc_solver.cu
 struct KrylovGraphs;  // hc_krylov.cu
+struct TmaCache;      // hc_tma.cuh
 void destroy_krylov_graphs(KrylovGraphs* g);
 
 // The device-resident operator: geometry, DOF numbering, compacted face lists
@@ -230,6 +231,8 @@ struct Operator {
 
   DBuf<uint8_t> labels;        // [nvox]
   DBuf<int32_t> lab4;          // labels widened to 32 bit (cp.async staging)
+  DBuf<int32_t> labt;          // TMA label word: (phase + 1) | (rank + 1) << 3, 0 = outside
+  TmaCache* tma = nullptr;     // tensor maps of the TMA stencils
   DBuf<int32_t> cdof, pdof;    // [nvox], -1 where absent
   DBuf<int32_t> c_vox, p_vox;  // packed index -> voxel
   DBuf<int32_t> plated_vox;    // [n_plated] ascending
@@ -248,13 +251,14 @@ struct Operator {
   DBuf<double> npl;            // plated inventory per slot
   DBuf<double> if_coef;        // 3 x n_if Jacobian coefficients (linearized)
   DBuf<double> if_vcoef;       // the same per interface voxel and direction: [3][6 n_if_vox]
+  DBuf<double> if_cslot;       // TMA stencil: (alpha, beta, gamma) per interface face slot
   DBuf<double> inv_c;          // gX / c per electrolyte voxel (linearized)
   DBuf<double> red;            // reduction scratch
   DBuf<double> host_x, host_npl;  // staging for the host-buffer entry point
   Amg* amg = nullptr;
   Work* work = nullptr;
   int krylov_log = 0;
-  int stencil_kind = 2;            // 1: register-prefetch tiles, 2: cp.async ring
+  int stencil_kind = 3;            // 1: register-prefetch tiles, 2: cp.async ring, 3: TMA ring (nx % 4 == 0, else 2)
   bool dev_krylov = true;          // device-resident BiCGStab (hc_krylov.cu)
   int krylov_batch = 4;            // iteration graphs launched per status check
   bool capturing = false;          // inside a stream capture (no nested capture)

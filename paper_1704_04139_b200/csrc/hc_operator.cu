@@ -14,6 +14,8 @@
 
 #include "hc_internal.cuh"
 #include "hc_stencil.cuh"
+#include "hc_tma.cuh"
+#include <cudaTypedefs.h>
 
 namespace hc {
 
@@ -389,8 +391,8 @@ __global__ void k_lin_iface(DevParams P, long long n_if, const int32_t* __restri
   coef[2 * n_if + f] = P.sc * g;
 }
 
-// per interface voxel and direction: copy of the face's three coefficients
-// (layout [3][6 * n_if_vox]) so the stencil kernels read them with one load
+// per interface voxel and direction: the face's three coefficients oriented from that
+// voxel's row (layout [3][6 * n_if_vox]) so the stencil kernels read them with one load
 __global__ void k_lin_scatter(DevParams P, long long n_if, const int32_t* __restrict__ so,
                               const int32_t* __restrict__ el, const int32_t* __restrict__ rank,
                               const double* __restrict__ coef, long long nslot,
@@ -400,8 +402,28 @@ __global__ void k_lin_scatter(DevParams P, long long n_if, const int32_t* __rest
   const int s = so[f], e = el[f];
   const double ca = coef[f], cb = coef[n_if + f], cg = coef[2 * n_if + f];
   const long long is = 6LL * rank[s] + dir_to(P, s, e), ie = 6LL * rank[e] + dir_to(P, e, s);
+  // row-oriented: the face adds alpha c_row + beta c_nbr + gamma (phi_row - phi_nbr) to the
+  // row's phi equation (solid: +i, electrolyte: -i; ca is zero except on BV faces)
   ifv[is] = ca; ifv[nslot + is] = cb; ifv[2 * nslot + is] = cg;
-  ifv[ie] = ca; ifv[nslot + ie] = cb; ifv[2 * nslot + ie] = cg;
+  ifv[ie] = -cb; ifv[nslot + ie] = -ca; ifv[2 * nslot + ie] = cg;
+}
+
+// the same, into the compact per-face slots of the TMA stencil (AoS triples; a
+// voxel's slots are consecutive in direction order, first slot in its label word)
+__global__ void k_lin_scatter_c(DevParams P, long long n_if, const int32_t* __restrict__ so,
+                                const int32_t* __restrict__ el, const int32_t* __restrict__ labt,
+                                const double* __restrict__ coef, double* __restrict__ cs) {
+  long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (f >= n_if) return;
+  const int s = so[f], e = el[f];
+  const double ca = coef[f], cb = coef[n_if + f], cg = coef[2 * n_if + f];
+  auto slot = [&](int v, int d) -> long long {
+    const unsigned w = (unsigned)labt[v];
+    return (long long)(w >> 9) + __popc(((w >> 3) & 63u) & ((1u << d) - 1u));
+  };
+  const long long is = 3 * slot(s, dir_to(P, s, e)), ie = 3 * slot(e, dir_to(P, e, s));
+  cs[is] = ca; cs[is + 1] = cb; cs[is + 2] = cg;
+  cs[ie] = -cb; cs[ie + 1] = -ca; cs[ie + 2] = cg;
 }
 
 __global__ void k_lin_invc(DevParams P, const uint8_t* __restrict__ lab,
@@ -545,7 +567,7 @@ void residual_grid(Operator& op, const double2* xg, const double* npl, double mu
                    int parts, const double* cprev, double inv_dt, double2* out, cudaStream_t s,
                    int which) {
   if (which & 1) {
-    if (op.stencil_kind == 2)
+    if (op.stencil_kind >= 2)
       res_launch_p(op.P, op.lab4.p, xg, mu, parts, cprev, inv_dt, out, op.n_sm, s);
     else
       k_residual_stencil<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, op.labels.p, xg, mu, parts,
@@ -564,6 +586,9 @@ void linearize(Operator& op, const double2* xg, const double* npl, double beta, 
     k_lin_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
                                                     op.if_slot.p, op.if_kind.p, xg, npl, beta,
                                                     op.if_coef.p); HC_COUNT();
+    if (op.tma)
+      k_lin_scatter_c<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
+                                                          op.labt.p, op.if_coef.p, op.if_cslot.p); HC_COUNT();
     long long nslot = (long long)op.if_dir.n;
     k_lin_scatter<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
                                                       op.if_rank.p, op.if_coef.p, nslot,
@@ -573,16 +598,46 @@ void linearize(Operator& op, const double2* xg, const double* npl, double beta, 
   HC_CHECK_LAUNCH();
 }
 
+bool tma_encode(CUtensorMap* m, const void* ptr, int kind, int nx, int ny, int nz) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  if (!fn || !ptr || (reinterpret_cast<uintptr_t>(ptr) & 15)) return false;
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3], es[3] = {1, 1, 1};
+  CUtensorMapDataType dt;
+  size_t ebytes;
+  if (kind == 0) {         // int32 labels, 40-wide boxes (160 B rows)
+    dt = CU_TENSOR_MAP_DATA_TYPE_INT32; ebytes = 4; dims[0] = nx; box[0] = T_LW;
+  } else if (kind == 1) {  // double2 as pairs of float64
+    dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64; ebytes = 8; dims[0] = 2 * (cuuint64_t)nx; box[0] = 2 * T_QW;
+  } else {                 // double
+    dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64; ebytes = 8; dims[0] = nx; box[0] = T_DW;
+  }
+  dims[1] = ny; dims[2] = nz;
+  box[1] = T_TH; box[2] = 1;
+  strides[0] = dims[0] * ebytes;
+  strides[1] = strides[0] * ny;
+  if (strides[0] % 16) return false;
+  CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2* out,
               cudaStream_t s, int which) {
   if (which & 1) {
-    FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p};
-    if (op.stencil_kind == 2)
-      fine_launch_p<SM_FULL, EP_STORE>(op.P, F, op.lab4.p, vg, nullptr, nullptr, nullptr, 0.0, inv_dt,
-                                       flags, out, nullptr, op.n_sm, s);
-    else
-      fine_launch_t<SM_FULL, EP_STORE>(op.P, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out,
-                                       nullptr, op.n_sm, s);
+    FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
+               op.if_cslot.p};
+    fine_launch_op<SM_FULL, EP_STORE>(op, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out,
+                                      nullptr, s);
     HC_COUNT();
   }
   if (false)
@@ -861,6 +916,30 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
     for (long long v = 0; v < nvox; ++v) l4[v] = (int32_t)labels_host[v] | ((rank[v] + 1) << 3);
     op->lab4.alloc(nvox);
     HC_CUDA(cudaMemcpy(op->lab4.p, l4.data(), nvox * 4, cudaMemcpyHostToDevice));
+    if (tma_grid_ok(P)) {
+      // TMA label word: (phase + 1) | interface-direction mask << 3 | first slot << 9 —
+      // phase + 1 so that the TMA zero fill reads as "outside"; the slots of a voxel's
+      // interface faces are consecutive in the compact coefficient array
+      std::vector<int32_t> dirs(op->if_dir.n);
+      HC_CUDA(cudaMemcpy(dirs.data(), op->if_dir.p, dirs.size() * 4, cudaMemcpyDeviceToHost));
+      long long slot = 0;
+      bool fits = true;
+      for (long long v = 0; v < nvox; ++v) {
+        int mask = 0;
+        if (rank[v] >= 0)
+          for (int d = 0; d < 6; ++d) mask |= (dirs[6LL * rank[v] + d] >= 0) << d;
+        if (slot >= (1LL << 23)) fits = false;
+        l4[v] = ((int32_t)labels_host[v] + 1) | (mask << 3) | (int32_t)((slot & ((1 << 23) - 1)) << 9);
+        slot += __builtin_popcount(mask);
+      }
+      if (fits) {
+        op->labt.alloc(nvox);
+        HC_CUDA(cudaMemcpy(op->labt.p, l4.data(), nvox * 4, cudaMemcpyHostToDevice));
+        op->if_cslot.alloc(std::max<long long>(3 * slot, 1));
+        HC_CUDA(cudaMemset(op->if_cslot.p, 0, op->if_cslot.n * sizeof(double)));
+        op->tma = new TmaCache();
+      }
+    }
   }
   // electrolyte-electrolyte faces (operator.py:187-191), kept for export
   {

@@ -1,11 +1,11 @@
 // Fused matrix-free Jacobian stencil on the voxel grid (one pass, no atomics).
 //
-// One thread per voxel row.  All neighbour labels and values are loaded up front
-// (clamped indices, masked) so every thread keeps 13+ independent loads in flight;
-// the face coefficients are derived from the phase labels, and the linearized
+// The face coefficients are derived from the phase labels, and the linearized
 // interface-face derivatives (Butler-Volmer, counter exchange, stripping) are read
-// per (interface voxel, direction) through the voxel's interface rank (if_rank),
-// so interface faces need no separate kernel and no atomics.
+// per (interface voxel, direction) through the voxel's interface rank, oriented
+// from the row's side, so interface faces need no separate kernel and no atomics.
+// This file holds the cp.async ring variant (any grid); hc_tma.cuh holds the TMA
+// variant the solver uses when the x pitch allows tensor-map tiles.
 //
 // Modes:
 //   FULL: out2 = (J + mass) V  on double2 (c, phi) vectors, with the row transform
@@ -33,610 +33,8 @@ struct FineArgs {
   const double* vcoef;    // interface derivatives per (interface voxel, direction): [3][nslot]
   long long nslot;        // 6 * number of interface voxels
   const double* w;        // gX / c per electrolyte voxel (FULL with flag 4)
+  const double* cslot;    // TMA stencil: compact row-oriented (alpha, beta, gamma) per interface face slot
 };
-
-template <int MODE, int EPI>
-__global__ void __launch_bounds__(VX * VY)
-k_fine_op(DevParams P, FineArgs F, const double2* __restrict__ V, const double* __restrict__ e,
-          const double* __restrict__ r, const double* __restrict__ dinv, double omega,
-          double inv_dt, int flags, double2* __restrict__ out2, double* __restrict__ out) {
-  // face-coefficient tables in shared memory: branch-free faces, indexed a * 6 + b
-  __shared__ double sP[36], sC[36], sM[36];
-  __shared__ unsigned char sI[36];
-  const int tid = threadIdx.y * VX + threadIdx.x;
-  if (tid < 36) {
-    sP[tid] = P.gP[tid];
-    sC[tid] = P.gC[tid];
-    sM[tid] = P.gMig[tid];
-    sI[tid] = P.ifc[tid];
-  }
-  __syncthreads();
-  int x, y, z, v;
-  if (!vox_index(P, x, y, z, v)) return;
-  const uint8_t a = __ldg(F.lab + v);
-  const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == GR || a == EL)
-                                                         : !(z == P.nz - 1 && a == CC);
-  if (!in_row) {
-    if (MODE == SM_FULL) out2[v] = make_double2(0.0, 0.0);
-    else out[v] = 0.0;
-    return;
-  }
-  // out-of-domain neighbours alias the voxel itself: same phase, zero difference,
-  // so they contribute nothing; grounded neighbours hold phi = 0 in every vector
-  const int nxy = (int)P.nxy;
-  int nb[6];
-  nb[0] = x > 0 ? v - 1 : v;
-  nb[1] = x + 1 < P.nx ? v + 1 : v;
-  nb[2] = y > 0 ? v - P.nx : v;
-  nb[3] = y + 1 < P.ny ? v + P.nx : v;
-  nb[4] = z > 0 ? v - nxy : v;
-  nb[5] = z + 1 < P.nz ? v + nxy : v;
-  uint8_t lb[6];
-#pragma unroll
-  for (int d = 0; d < 6; ++d) lb[d] = __ldg(F.lab + nb[d]);
-  const int a6 = a * 6;
-  const double tp = P.t_plus;
-  double rc = 0.0, rp = 0.0;
-  bool any_if = false;
-#pragma unroll
-  for (int d = 0; d < 6; ++d) any_if |= sI[a6 + lb[d]] != 0;
-  if (MODE == SM_FULL) {
-    const double2 Va = V[v];
-    double2 Vb[6];
-#pragma unroll
-    for (int d = 0; d < 6; ++d) Vb[d] = V[nb[d]];
-    const bool one_c = (flags & 4) && a == EL;
-    double wa = 0.0, wb[6];
-    if (one_c) {
-      wa = F.w[v];
-#pragma unroll
-      for (int d = 0; d < 6; ++d) wb[d] = F.w[nb[d]];
-    }
-#pragma unroll
-    for (int d = 0; d < 6; ++d) {
-      const int i = a6 + lb[d];
-      const double dp = Va.y - Vb[d].y;
-      rp += sP[i] * dp;
-      rc += sC[i] * (Va.x - Vb[d].x) + sM[i] * dp;
-      if (one_c && sM[i] != 0.0) {
-        double dq = wa * Va.x - wb[d] * Vb[d].x;
-        rp += dq;
-        rc += tp * dq;
-      }
-    }
-    if (any_if) {
-      const int rk = __ldg(F.if_rank + v);
-      const bool solid = a != EL;
-#pragma unroll
-      for (int d = 0; d < 6; ++d) {
-        const uint8_t b = lb[d];
-        if (!sI[a6 + b]) continue;
-        const long long f = 6LL * rk + d;
-        const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f),
-                     cg = __ldg(F.vcoef + 2 * F.nslot + f);
-        const bool bv = a == GR || b == GR;
-        const double2 vs = solid ? Va : Vb[d], ve = solid ? Vb[d] : Va;
-        // dv = ca c_s + cb c_e + cg (phi_s - phi_e)  (ca = 0 unless BV)
-        const double dv = (bv ? ca * vs.x : 0.0) + cb * ve.x + cg * (vs.y - ve.y);
-        if (solid) {
-          if (bv) rc += dv;
-          rp += dv;
-        } else {  // the row transform T is applied once below (rc -= t+ rp)
-          rc -= dv;
-          rp -= dv;
-        }
-      }
-    }
-    if ((flags & 1) && (a == GR || a == EL)) rc += Va.x * inv_dt;
-    if ((flags & 2) && a == EL) rc -= tp * rp;
-    if (flags & 8) rc = 0.0;
-    out2[v] = make_double2(rc, rp);
-    return;
-  }
-  const double ea = e[v];
-  double eb[6];
-#pragma unroll
-  for (int d = 0; d < 6; ++d) eb[d] = e[nb[d]];
-  if (MODE == SM_PHI) {
-#pragma unroll
-    for (int d = 0; d < 6; ++d) rp += sP[a6 + lb[d]] * (ea - eb[d]);
-  } else if (MODE == SM_CONC) {
-#pragma unroll
-    for (int d = 0; d < 6; ++d) rp += sC[a6 + lb[d]] * (ea - eb[d]);
-    rp += inv_dt * ea;
-  }
-  if (any_if) {
-    const int rk = __ldg(F.if_rank + v);
-    const bool solid = a != EL;
-#pragma unroll
-    for (int d = 0; d < 6; ++d) {
-      const uint8_t b = lb[d];
-      if (!sI[a6 + b]) continue;
-      const long long f = 6LL * rk + d;
-      const bool bv = a == GR || b == GR;
-      if (MODE == SM_PHI) {
-        rp += __ldg(F.vcoef + 2 * F.nslot + f) * (ea - eb[d]);
-      } else if (MODE == SM_CP) {
-        const double cg = __ldg(F.vcoef + 2 * F.nslot + f);
-        if (solid) {
-          if (bv) rp += cg * (ea - eb[d]);
-        } else {
-          rp += (1.0 - tp) * cg * (ea - eb[d]);
-        }
-      } else {
-        const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f);
-        if (solid) {
-          if (bv) rp += ca * ea + cb * eb[d];
-        } else {
-          rp -= (1.0 - tp) * ((bv ? ca * eb[d] : 0.0) + cb * ea);
-        }
-      }
-    }
-  }
-  // SM_CP with EP_RESID: out = r - (T J)_cp e (the c-block right-hand side)
-  if (EPI == EP_STORE) out[v] = rp;
-  else if (EPI == EP_RESID) out[v] = r[v] - rp;
-  else out[v] = ea + omega * dinv[v] * (r[v] - rp);
-}
-
-}  // namespace hc
-
-namespace hc {
-
-// ---------------------------------------------------------------------------------
-// z-marching variant: each thread owns one (x, y) column and walks `zc` planes,
-// keeping the z-1 / z / z+1 values and labels in registers and prefetching plane
-// z+2 one iteration ahead, so every thread has DRAM loads in flight while it
-// computes (the one-voxel-per-thread kernel above is latency bound: its unique
-// DRAM bytes per thread are too few to cover HBM latency).  x/y neighbours come
-// from L1/L2.  Same modes, epilogues and results as k_fine_op.
-template <int MODE, int EPI>
-__global__ void __launch_bounds__(VX * VY)
-k_fine_z(DevParams P, FineArgs F, const double2* __restrict__ V, const double* __restrict__ e,
-         const double* __restrict__ r, const double* __restrict__ dinv, double omega,
-         double inv_dt, int flags, double2* __restrict__ out2, double* __restrict__ out, int zc) {
-  __shared__ double sP[36], sC[36], sM[36];
-  __shared__ unsigned char sI[36];
-  const int tid = threadIdx.y * VX + threadIdx.x;
-  if (tid < 36) {
-    sP[tid] = P.gP[tid];
-    sC[tid] = P.gC[tid];
-    sM[tid] = P.gMig[tid];
-    sI[tid] = P.ifc[tid];
-  }
-  __syncthreads();
-  const int x = blockIdx.x * VX + threadIdx.x, y = blockIdx.y * VY + threadIdx.y;
-  if (x >= P.nx || y >= P.ny) return;
-  const int nxy = (int)P.nxy, nz = P.nz;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);
-  if (z0 >= z1) return;
-  const int base = y * P.nx + x;
-  const double tp = P.t_plus;
-  constexpr bool FULLM = MODE == SM_FULL;
-  const bool one_c_flag = FULLM && (flags & 4);
-  // rolling window (m: z-1, c: z, p: z+1), n: prefetched z+2
-  uint8_t lm, lc, lp, ln = 0;
-  double2 Vm = {0, 0}, Vc = {0, 0}, Vp = {0, 0}, Vn = {0, 0};
-  double em = 0, ec = 0, ep = 0, en = 0;
-  double wm = 0, wc = 0, wp = 0, wn = 0;
-  auto load = [&](int zz, uint8_t& l, double2& Vv, double& ev, double& wv) {
-    const int idx = zz * nxy + base;
-    l = __ldg(F.lab + idx);
-    if constexpr (FULLM) {
-      Vv = V[idx];
-      if (one_c_flag) wv = F.w[idx];
-    } else {
-      ev = e[idx];
-    }
-  };
-  load(z0, lc, Vc, ec, wc);
-  if (z0 > 0) load(z0 - 1, lm, Vm, em, wm);
-  else { lm = lc; Vm = Vc; em = ec; wm = wc; }
-  if (z0 + 1 < nz) load(z0 + 1, lp, Vp, ep, wp);
-  else { lp = lc; Vp = Vc; ep = ec; wp = wc; }
-  for (int z = z0; z < z1; ++z) {
-    const int v = z * nxy + base;
-    if (z + 2 < nz && z + 1 < z1) load(z + 2, ln, Vn, en, wn);
-    const uint8_t a = lc;
-    const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == GR || a == EL)
-                                                           : !(z == nz - 1 && a == CC);
-    // x/y neighbours of this plane (aliases of v at the domain edge)
-    int nb[4];
-    nb[0] = x > 0 ? v - 1 : v;
-    nb[1] = x + 1 < P.nx ? v + 1 : v;
-    nb[2] = y > 0 ? v - P.nx : v;
-    nb[3] = y + 1 < P.ny ? v + P.nx : v;
-    uint8_t lb[6];
-    double2 Vb[6];
-    double eb[6], wb[6];
-    if (in_row) {
-#pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        lb[d] = __ldg(F.lab + nb[d]);
-        if constexpr (FULLM) {
-          Vb[d] = V[nb[d]];
-          if (one_c_flag) wb[d] = F.w[nb[d]];
-        } else {
-          eb[d] = e[nb[d]];
-        }
-      }
-      lb[4] = lm; lb[5] = lp;
-      if constexpr (FULLM) {
-        Vb[4] = Vm; Vb[5] = Vp; wb[4] = wm; wb[5] = wp;
-      } else {
-        eb[4] = em; eb[5] = ep;
-      }
-      const int a6 = a * 6;
-      bool any_if = false;
-#pragma unroll
-      for (int d = 0; d < 6; ++d) any_if |= sI[a6 + lb[d]] != 0;
-      double rc = 0.0, rp = 0.0;
-      if constexpr (FULLM) {
-        const double2 Va = Vc;
-        const bool one_c = one_c_flag && a == EL;
-#pragma unroll
-        for (int d = 0; d < 6; ++d) {
-          const int i = a6 + lb[d];
-          const double dp = Va.y - Vb[d].y;
-          rp += sP[i] * dp;
-          rc += sC[i] * (Va.x - Vb[d].x) + sM[i] * dp;
-          if (one_c && sM[i] != 0.0) {
-            double dq = wc * Va.x - wb[d] * Vb[d].x;
-            rp += dq;
-            rc += tp * dq;
-          }
-        }
-        if (any_if) {
-          const int rk = __ldg(F.if_rank + v);
-          const bool solid = a != EL;
-#pragma unroll
-          for (int d = 0; d < 6; ++d) {
-            const uint8_t b = lb[d];
-            if (!sI[a6 + b]) continue;
-            const long long f = 6LL * rk + d;
-            const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f),
-                         cg = __ldg(F.vcoef + 2 * F.nslot + f);
-            const bool bv = a == GR || b == GR;
-            const double2 vs = solid ? Va : Vb[d], ve = solid ? Vb[d] : Va;
-            const double dv = (bv ? ca * vs.x : 0.0) + cb * ve.x + cg * (vs.y - ve.y);
-            if (solid) {
-              if (bv) rc += dv;
-              rp += dv;
-            } else {
-              rc -= dv;
-              rp -= dv;
-            }
-          }
-        }
-        if ((flags & 1) && (a == GR || a == EL)) rc += Va.x * inv_dt;
-        if ((flags & 2) && a == EL) rc -= tp * rp;
-        if (flags & 8) rc = 0.0;
-        out2[v] = make_double2(rc, rp);
-      } else {
-        const double ea = ec;
-        if (MODE == SM_PHI) {
-#pragma unroll
-          for (int d = 0; d < 6; ++d) rp += sP[a6 + lb[d]] * (ea - eb[d]);
-        } else if (MODE == SM_CONC) {
-#pragma unroll
-          for (int d = 0; d < 6; ++d) rp += sC[a6 + lb[d]] * (ea - eb[d]);
-          rp += inv_dt * ea;
-        }
-        if (any_if) {
-          const int rk = __ldg(F.if_rank + v);
-          const bool solid = a != EL;
-#pragma unroll
-          for (int d = 0; d < 6; ++d) {
-            const uint8_t b = lb[d];
-            if (!sI[a6 + b]) continue;
-            const long long f = 6LL * rk + d;
-            const bool bv = a == GR || b == GR;
-            if (MODE == SM_PHI) {
-              rp += __ldg(F.vcoef + 2 * F.nslot + f) * (ea - eb[d]);
-            } else if (MODE == SM_CP) {
-              const double cg = __ldg(F.vcoef + 2 * F.nslot + f);
-              if (solid) {
-                if (bv) rp += cg * (ea - eb[d]);
-              } else {
-                rp += (1.0 - tp) * cg * (ea - eb[d]);
-              }
-            } else {
-              const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f);
-              if (solid) {
-                if (bv) rp += ca * ea + cb * eb[d];
-              } else {
-                rp -= (1.0 - tp) * ((bv ? ca * eb[d] : 0.0) + cb * ea);
-              }
-            }
-          }
-        }
-        if (EPI == EP_STORE) out[v] = rp;
-        else if (EPI == EP_RESID) out[v] = r[v] - rp;
-        else out[v] = ea + omega * dinv[v] * (r[v] - rp);
-      }
-    } else {
-      if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
-      else out[v] = 0.0;
-    }
-    // advance the window
-    lm = lc; Vm = Vc; em = ec; wm = wc;
-    lc = lp; Vc = Vp; ec = ep; wc = wp;
-    if (z + 2 < nz) { lp = ln; Vp = Vn; ep = en; wp = wn; }
-    // (at the top plane z + 1 == nz - 1 the z+1 neighbour aliases the voxel itself)
-  }
-}
-
-// launch helper: z-chunk length chosen so the grid has >= 4 CTAs per SM
-template <int MODE, int EPI>
-inline void fine_launch(const DevParams& P, const FineArgs& F, const double2* V, const double* e,
-                        const double* r, const double* dinv, double omega, double inv_dt, int flags,
-                        double2* out2, double* out, int n_sm, cudaStream_t s) {
-  const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
-  const long long want = 4LL * n_sm;
-  int zc = (int)std::max<long long>(1, (long long)bx * by * P.nz / want);
-  zc = std::min(zc, 32);
-  const int bz = (P.nz + zc - 1) / zc;
-  k_fine_z<MODE, EPI><<<dim3(bx, by, bz), dim3(VX, VY, 1), 0, s>>>(P, F, V, e, r, dinv, omega,
-                                                                  inv_dt, flags, out2, out, zc);
-}
-
-}  // namespace hc
-
-namespace hc {
-
-// ---------------------------------------------------------------------------------
-// 2.5-D tiled variant (the one the solver uses).  A CTA owns a 32 x 8 column of
-// the grid and marches `zc` planes.  Each plane's tile plus its one-voxel x/y halo
-// (34 x 10 values and labels) is staged in shared memory, double-buffered: the
-// global loads of plane z+1 are issued before plane z is computed and land in the
-// other buffer afterwards, so DRAM latency overlaps the arithmetic and x/y
-// neighbours never go to L2.  z-1 / z+1 values of the own column stay in registers.
-// Halo coordinates are clamped into the domain, which aliases every missing
-// neighbour to the voxel itself (zero difference -> no face), exactly like the
-// reference's face enumeration.
-template <int MODE, int EPI>
-__global__ void __launch_bounds__(VX * VY)
-k_fine_t(DevParams P, FineArgs F, const double2* __restrict__ V, const double* __restrict__ e,
-         const double* __restrict__ r, const double* __restrict__ dinv, double omega,
-         double inv_dt, int flags, double2* __restrict__ out2, double* __restrict__ out, int zc) {
-  constexpr bool FULLM = MODE == SM_FULL;
-  constexpr int TW = VX + 2, TH = VY + 2, TN = TW * TH;  // 34 x 10 = 340
-  using VT = typename std::conditional<FULLM, double2, double>::type;
-  __shared__ VT sv[2][TN];
-  __shared__ double sw[FULLM ? 2 : 1][FULLM ? TN : 1];
-  __shared__ uint8_t sl[2][TN];
-  __shared__ double sP[36], sC[36], sM[36];
-  __shared__ unsigned char sI[36];
-  const int tid = threadIdx.y * VX + threadIdx.x;
-  if (tid < 36) {
-    sP[tid] = P.gP[tid];
-    sC[tid] = P.gC[tid];
-    sM[tid] = P.gMig[tid];
-    sI[tid] = P.ifc[tid];
-  }
-  const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
-  const int x0 = blockIdx.x * VX, y0 = blockIdx.y * VY;
-  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
-  const bool active = x < nx && y < ny;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);
-  const bool one_c_flag = FULLM && (flags & 4);
-  // the (up to) two halo elements this thread stages per plane
-  int hoff[2];
-  bool hval[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int i = tid + k * VX * VY;
-    hval[k] = i < TN;
-    const int hy = i / TW, hx = i - hy * TW;
-    const int gx = min(max(x0 + hx - 1, 0), nx - 1), gy = min(max(y0 + hy - 1, 0), ny - 1);
-    hoff[k] = gy * nx + gx;
-  }
-  VT pv[2];
-  double pw[2] = {0.0, 0.0};
-  uint8_t pl[2];
-  auto fetch = [&](int zz) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (hval[k]) {
-        const int idx = zz * nxy + hoff[k];
-        pl[k] = __ldg(F.lab + idx);
-        if constexpr (FULLM) {
-          pv[k] = V[idx];
-          if (one_c_flag) pw[k] = F.w[idx];
-        } else {
-          pv[k] = e[idx];
-        }
-      }
-  };
-  auto stash = [&](int buf) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (hval[k]) {
-        const int i = tid + k * VX * VY;
-        sl[buf][i] = pl[k];
-        sv[buf][i] = pv[k];
-        if constexpr (FULLM) sw[buf][i] = pw[k];
-      }
-  };
-  const int cidx = (threadIdx.y + 1) * TW + threadIdx.x + 1;  // own voxel in the tile
-  const int col = active ? y * nx + x : 0;
-  // own column window: z-1 (m) and z+1 (p)
-  VT vm{}, vp{};
-  double wm = 0.0, wp = 0.0;
-  uint8_t lm = 0, lp = 0;
-  if (z0 < z1) {
-    fetch(z0);
-    stash(0);
-    const int zm = z0 > 0 ? z0 - 1 : z0;
-    if (active) {
-      const int idx = zm * nxy + col;
-      lm = __ldg(F.lab + idx);
-      if constexpr (FULLM) {
-        vm = V[idx];
-        if (one_c_flag) wm = F.w[idx];
-      } else {
-        vm = e[idx];
-      }
-    }
-  }
-  const double tp = P.t_plus;
-  for (int z = z0; z < z1; ++z) {
-    const int buf = (z - z0) & 1;
-    const bool has_next = z + 1 < z1;
-    if (has_next) fetch(z + 1);
-    const int zp = z + 1 < nz ? z + 1 : z;
-    double rv = 0.0, dv_ = 0.0;
-    int rkv = -1;
-    if (active) {
-      rkv = __ldg(F.if_rank + z * nxy + col);   // prefetched: interface rows need it
-      const int idx = zp * nxy + col;
-      lp = __ldg(F.lab + idx);
-      if constexpr (FULLM) {
-        vp = V[idx];
-        if (one_c_flag) wp = F.w[idx];
-      } else {
-        vp = e[idx];
-        if (EPI != EP_STORE) rv = r[z * nxy + col];
-        if (EPI == EP_SMOOTH) dv_ = dinv[z * nxy + col];
-      }
-    }
-    __syncthreads();  // plane z staged (and the table loads on the first pass)
-    if (active) {
-      const int v = z * nxy + col;
-      const uint8_t a = sl[buf][cidx];
-      const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == GR || a == EL)
-                                                             : !(z == nz - 1 && a == CC);
-      if (!in_row) {
-        if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
-        else out[v] = 0.0;
-      } else {
-        const int ti[4] = {cidx - 1, cidx + 1, cidx - TW, cidx + TW};
-        uint8_t lb[6];
-        VT vb[6];
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-          lb[d] = sl[buf][ti[d]];
-          vb[d] = sv[buf][ti[d]];
-        }
-        lb[4] = lm; lb[5] = lp;
-        vb[4] = vm; vb[5] = vp;
-        const VT va = sv[buf][cidx];
-        const int a6 = a * 6;
-        bool any_if = false;
-#pragma unroll
-        for (int d = 0; d < 6; ++d) any_if |= sI[a6 + lb[d]] != 0;
-        double rc = 0.0, rp = 0.0;
-        if constexpr (FULLM) {
-          const bool one_c = one_c_flag && a == EL;
-          double wa = 0.0, wb[6];
-          if (one_c) {
-            wa = sw[buf][cidx];
-#pragma unroll
-            for (int d = 0; d < 4; ++d) wb[d] = sw[buf][ti[d]];
-            wb[4] = wm; wb[5] = wp;
-          }
-#pragma unroll
-          for (int d = 0; d < 6; ++d) {
-            const int i = a6 + lb[d];
-            const double dp = va.y - vb[d].y;
-            rp += sP[i] * dp;
-            rc += sC[i] * (va.x - vb[d].x) + sM[i] * dp;
-            if (one_c && sM[i] != 0.0) {
-              double dq = wa * va.x - wb[d] * vb[d].x;
-              rp += dq;
-              rc += tp * dq;
-            }
-          }
-          if (any_if) {
-            const int rk = rkv;
-            const bool solid = a != EL;
-#pragma unroll
-            for (int d = 0; d < 6; ++d) {
-              const uint8_t b = lb[d];
-              if (!sI[a6 + b]) continue;
-              const long long f = 6LL * rk + d;
-              const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f),
-                           cg = __ldg(F.vcoef + 2 * F.nslot + f);
-              const bool bv = a == GR || b == GR;
-              const double2 vs = solid ? va : vb[d], ve = solid ? vb[d] : va;
-              const double dv = (bv ? ca * vs.x : 0.0) + cb * ve.x + cg * (vs.y - ve.y);
-              if (solid) {
-                if (bv) rc += dv;
-                rp += dv;
-              } else {
-                rc -= dv;
-                rp -= dv;
-              }
-            }
-          }
-          if ((flags & 1) && (a == GR || a == EL)) rc += va.x * inv_dt;
-          if ((flags & 2) && a == EL) rc -= tp * rp;
-          if (flags & 8) rc = 0.0;
-          out2[v] = make_double2(rc, rp);
-        } else {
-          const double ea = va;
-          if (MODE == SM_PHI) {
-#pragma unroll
-            for (int d = 0; d < 6; ++d) rp += sP[a6 + lb[d]] * (ea - vb[d]);
-          } else if (MODE == SM_CONC) {
-#pragma unroll
-            for (int d = 0; d < 6; ++d) rp += sC[a6 + lb[d]] * (ea - vb[d]);
-            rp += inv_dt * ea;
-          }
-          if (any_if) {
-            const int rk = rkv;
-            const bool solid = a != EL;
-#pragma unroll
-            for (int d = 0; d < 6; ++d) {
-              const uint8_t b = lb[d];
-              if (!sI[a6 + b]) continue;
-              const long long f = 6LL * rk + d;
-              const bool bv = a == GR || b == GR;
-              if (MODE == SM_PHI) {
-                rp += __ldg(F.vcoef + 2 * F.nslot + f) * (ea - vb[d]);
-              } else if (MODE == SM_CP) {
-                const double cg = __ldg(F.vcoef + 2 * F.nslot + f);
-                if (solid) {
-                  if (bv) rp += cg * (ea - vb[d]);
-                } else {
-                  rp += (1.0 - tp) * cg * (ea - vb[d]);
-                }
-              } else {
-                const double ca = __ldg(F.vcoef + f), cb = __ldg(F.vcoef + F.nslot + f);
-                if (solid) {
-                  if (bv) rp += ca * ea + cb * vb[d];
-                } else {
-                  rp -= (1.0 - tp) * ((bv ? ca * vb[d] : 0.0) + cb * ea);
-                }
-              }
-            }
-          }
-          if (EPI == EP_STORE) out[v] = rp;
-          else if (EPI == EP_RESID) out[v] = rv - rp;
-          else out[v] = ea + omega * dv_ * (rv - rp);
-        }
-      }
-      // slide the own-column window
-      lm = sl[buf][cidx];
-      vm = sv[buf][cidx];
-      if constexpr (FULLM) wm = sw[buf][cidx];
-    }
-    if (has_next) stash(buf ^ 1);  // nobody reads buf ^ 1 after the barrier above
-  }
-}
-
-template <int MODE, int EPI>
-inline void fine_launch_t(const DevParams& P, const FineArgs& F, const double2* V, const double* e,
-                          const double* r, const double* dinv, double omega, double inv_dt,
-                          int flags, double2* out2, double* out, int n_sm, cudaStream_t s) {
-  const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
-  const long long want = 4LL * n_sm;
-  int zc = (int)std::max<long long>(1, (long long)bx * by * P.nz / want);
-  zc = std::min(zc, 64);
-  const int bz = (P.nz + zc - 1) / zc;
-  k_fine_t<MODE, EPI><<<dim3(bx, by, bz), dim3(VX, VY, 1), 0, s>>>(P, F, V, e, r, dinv, omega,
-                                                                  inv_dt, flags, out2, out, zc);
-}
 
 }  // namespace hc
 
@@ -812,7 +210,6 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
       double rc = 0.0, rp = 0.0;
       bool one_c = false;
       if constexpr (FULLM) one_c = one_c_flag && a == EL;
-      int bb[6];
       VT vbv[6];
 #pragma unroll
       for (int d = 0; d < 6; ++d) {
@@ -834,7 +231,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
           vb = top ? va : val(bufp * TN + cidx);
           if constexpr (FULLM) if (one_c) wb = top ? wa : sw[bufp * TN + cidx];
         }
-        bb[d] = b;
+
         vbv[d] = vb;
         const int i = a6 + b;
         if constexpr (FULLM) {
@@ -853,7 +250,8 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
         }
       }
       if (rk >= 0) {
-        // interface kinetics: this voxel's six coefficient slots (zero off-interface)
+        // interface kinetics: six row-oriented coefficient triples (zero off-interface),
+        // each face adds alpha c_a + beta c_b + gamma (phi_a - phi_b) to the phi row
         const long long f = 6LL * rk;
         double cg[6], ca[6], cb[6];
         if constexpr (FULLM || MODE == SM_PHI || MODE == SM_CP) {
@@ -877,35 +275,21 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
             cb[2 * k + 1] = tb.y;
           }
         }
+        double si = 0.0;
 #pragma unroll
         for (int d = 0; d < 6; ++d) {
-          const bool bv = a == GR || bb[d] == GR;
           const VT vb = vbv[d];
-          if constexpr (FULLM) {
-            const double2 vs = solid ? va : vb, ve = solid ? vb : va;
-            const double dv = (bv ? ca[d] * vs.x : 0.0) + cb[d] * ve.x + cg[d] * (vs.y - ve.y);
-            if (solid) {
-              if (bv) rc += dv;
-              rp += dv;
-            } else {
-              rc -= dv;
-              rp -= dv;
-            }
-          } else if (MODE == SM_PHI) {
-            rp += cg[d] * (va - vb);
-          } else if (MODE == SM_CP) {
-            if (solid) {
-              if (bv) rp += cg[d] * (va - vb);
-            } else {
-              rp += (1.0 - tp) * cg[d] * (va - vb);
-            }
-          } else {
-            if (solid) {
-              if (bv) rp += ca[d] * va + cb[d] * vb;
-            } else {
-              rp -= (1.0 - tp) * ((bv ? ca[d] * vb : 0.0) + cb[d] * va);
-            }
-          }
+          if constexpr (FULLM) si += ca[d] * va.x + cb[d] * vb.x + cg[d] * (va.y - vb.y);
+          else if (MODE == SM_CONC) si += ca[d] * va + cb[d] * vb;
+          else si += cg[d] * (va - vb);
+        }
+        if constexpr (FULLM) {
+          rp += si;
+          if (a == GR || a == EL) rc += si;
+        } else if (MODE == SM_PHI) {
+          rp += si;
+        } else {
+          rp += (solid ? 1.0 : 1.0 - tp) * si;   // (T J) on electrolyte c rows
         }
       }
       if constexpr (FULLM) {

@@ -1,0 +1,432 @@
+// TMA-fed 2.5-D stencil: the solver's matrix-free J v and fine-level multigrid
+// sweeps on grids whose x pitch allows tensor-map tiles (nx % 4 == 0).
+//
+// A CTA owns a 32 x 8 column of the grid and marches zc planes.  Every plane's tile
+// plus its one-voxel x/y halo is brought into a 4-deep shared-memory ring by ONE
+// thread with cp.async.bulk.tensor (labels 40 x 10 int32, values 34 x 10 double2 or
+// 36 x 10 double, gX/c 36 x 10 double), completion signalled on a per-slot mbarrier; the
+// other 255 threads issue no load instructions for the stencil operands at all.
+// Out-of-domain halo elements (x/y edges, plane -1 and plane nz) are zero-filled by
+// the TMA unit: label 0 is the "void" phase whose face coefficients are zero, so
+// missing neighbours contribute nothing — the reference's face enumeration
+// (operator.py:121-242) without a single boundary branch.
+//
+// Label word (labt): (phase + 1) | interface-direction mask << 3 | first face slot << 9,
+// 0 = outside; the slots hold row-oriented (alpha, beta, gamma) triples (cslot).
+// Face-coefficient tables are indexed (a << 3) | b in that encoding.
+#pragma once
+
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
+
+#include "hc_stencil.cuh"
+
+namespace hc {
+
+// phases in the TMA label encoding
+enum : int { TV = 0, TEL = EL + 1, TGR = GR + 1, TCC = CC + 1 };
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, int x, int y, int z,
+                                          unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
+
+// tensor maps of one launch (passed by value; __grid_constant__ keeps them in param space)
+struct TmaMaps {
+  CUtensorMap lab;   // int32 [nz][ny][nx], box 40 x 10 x 1
+  CUtensorMap val;   // values: double2 as float64 [nz][ny][2 nx] box 68 x 10, or double box 36 x 10
+  CUtensorMap aux;   // gX/c (FULL) or r (SMOOTH0), double box 36 x 10
+  CUtensorMap aux2;  // dinv (SMOOTH0)
+};
+
+#ifndef HC_TMA_STAGES
+#define HC_TMA_STAGES 4
+#endif
+constexpr int T_S = HC_TMA_STAGES;   // ring depth
+
+template <typename Fn, int... I>
+__device__ __forceinline__ void static_for_impl(Fn&& fn, std::integer_sequence<int, I...>) {
+  (fn(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename Fn>
+__device__ __forceinline__ void static_for(Fn&& fn) {
+  static_for_impl(fn, std::make_integer_sequence<int, N>{});
+}
+constexpr int T_TH = VY + 2;
+// TMA box starts must be 16-byte aligned in x, so each tile starts at the aligned
+// column at or below x0 - 1:  int32 labels at x0 - 4 (40 wide), double tiles at
+// x0 - 2 (36 wide), double2 tiles at x0 - 1 (34 wide).
+constexpr int T_LW = VX + 8, T_LOFF = 4;    // labels
+constexpr int T_DW = VX + 4, T_DOFF = 2;    // double (scalar values, gX/c, r, dinv)
+constexpr int T_QW = VX + 2, T_QOFF = 1;    // double2 values
+constexpr int T_LN = T_LW * T_TH, T_DN = T_DW * T_TH, T_QN = T_QW * T_TH;
+
+template <int MODE, int EPI>
+struct TmaLayout {
+  static constexpr bool FULLM = MODE == SM_FULL;
+  static constexpr bool X0 = EPI == EP_SMOOTH0;
+  static constexpr int VW = FULLM ? T_QW : T_DW, VOFF = FULLM ? T_QOFF : T_DOFF;
+  static constexpr int VBYTES = FULLM ? T_QN * 16 : T_DN * 8;
+  static constexpr int LAB = 0;                                         // int32 [T_LN]
+  static constexpr int VAL = ((T_LN * 4 + 127) / 128) * 128;            // value tile
+  static constexpr int AUX = VAL + (X0 ? 0 : ((VBYTES + 127) / 128) * 128);   // gX/c or r
+  static constexpr bool HAS_AUX = FULLM || X0;
+  static constexpr int AUX2 = AUX + (HAS_AUX ? ((T_DN * 8 + 127) / 128) * 128 : 0);
+  static constexpr int SLOT = AUX2 + (X0 ? ((T_DN * 8 + 127) / 128) * 128 : 0);
+};
+
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+
+// Warp-specialised: warps 0..7 compute (one voxel per thread and plane), warp 8 is
+// the producer.  full[s] completes when plane s's tiles have landed (TMA transaction
+// bytes), empty[s] when all eight compute warps are done with it, so compute warps
+// drift freely within the ring instead of meeting at a CTA barrier every plane.
+constexpr int T_WARPS = VY;                 // compute warps
+constexpr int T_THREADS = VX * (VY + 1);    // + producer warp
+
+template <int MODE, int EPI, bool ONEC>
+__global__ void __launch_bounds__(T_THREADS, 3)
+k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int32_t* __restrict__ labt,
+           const double2* __restrict__ V, const double* __restrict__ e, const double* __restrict__ r,
+           const double* __restrict__ dinv, double omega, double inv_dt, int flags,
+           double2* __restrict__ out2, double* __restrict__ out, int zc) {
+  using L = TmaLayout<MODE, EPI>;
+  constexpr bool FULLM = L::FULLM, X0 = L::X0;
+  constexpr bool OC = FULLM && ONEC;
+  using VT = typename std::conditional<FULLM, double2, double>::type;
+  extern __shared__ __align__(16) unsigned char smem_dyn[];
+  // 128-byte aligned ring (the launch adds 128 bytes of slack)
+  unsigned char* ring = smem_dyn + ((128 - ((unsigned)__cvta_generic_to_shared(smem_dyn) & 127)) & 127);
+  __shared__ __align__(16) double2 sPC[64];   // (P, C) per (a << 3 | b)
+  __shared__ __align__(8) unsigned long long full[T_S], empty[T_S];
+  const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
+  const int x0 = blockIdx.x * VX, y0 = blockIdx.y * VY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);   // planes z0 .. z1 are staged
+  const int nplane = z1 - z0;                                // computed planes
+  const unsigned full0 = (unsigned)__cvta_generic_to_shared(full);
+  const unsigned empty0 = (unsigned)__cvta_generic_to_shared(empty);
+  const int tid = threadIdx.y * VX + threadIdx.x;
+  if (tid == T_WARPS * VX) {
+#pragma unroll
+    for (int k = 0; k < T_S; ++k) {
+      mbar_init(full0 + 8 * k, 1);
+      mbar_init(empty0 + 8 * k, T_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (tid < 64) {
+    const int a = tid >> 3, b = tid & 7;
+    const bool ok = a >= 1 && a <= N_PHASES && b >= 1 && b <= N_PHASES;
+    const int i = (a - 1) * 6 + (b - 1);
+    sPC[tid] = ok ? make_double2(P.gP[i], P.gC[i]) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();   // barriers initialised, tables built (the only CTA-wide barrier)
+
+  if (threadIdx.y == T_WARPS) {   // ---------------- producer warp
+    if (threadIdx.x == 0) {
+      const unsigned sbase = (unsigned)__cvta_generic_to_shared(ring);
+      constexpr unsigned tx = T_LN * 4 + (X0 ? 2 * T_DN * 8 : L::VBYTES) + (OC ? T_DN * 8 : 0);
+      for (int j = 0; j <= nplane; ++j) {
+        const int slot = j % T_S;
+        if (j >= T_S) mbar_wait(empty0 + 8 * slot, ((j / T_S) - 1) & 1);
+        const unsigned b = full0 + 8 * slot, s = sbase + slot * L::SLOT;
+        const int zz = z0 + j;
+        mbar_expect_tx(b, tx);
+        tma_load3(s + L::LAB, &M.lab, x0 - T_LOFF, y0 - 1, zz, b);
+        if constexpr (X0) {
+          tma_load3(s + L::AUX, &M.aux, x0 - T_DOFF, y0 - 1, zz, b);
+          tma_load3(s + L::AUX2, &M.aux2, x0 - T_DOFF, y0 - 1, zz, b);
+        } else if constexpr (FULLM) {
+          tma_load3(s + L::VAL, &M.val, 2 * (x0 - T_QOFF), y0 - 1, zz, b);
+          if constexpr (OC) tma_load3(s + L::AUX, &M.aux, x0 - T_DOFF, y0 - 1, zz, b);
+        } else {
+          tma_load3(s + L::VAL, &M.val, x0 - T_DOFF, y0 - 1, zz, b);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------- compute warps
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  const bool active = x < nx && y < ny;
+  const int col = active ? y * nx + x : 0;
+  VT vm{};            // own column z - 1 (registers)
+  double wm = 0.0;
+  int lm = 0;
+  if (active && z0 > 0) {
+    const long long idx = (long long)(z0 - 1) * nxy + col;
+    lm = labt[idx] & 7;
+    if constexpr (FULLM) {
+      vm = V[idx];
+      if constexpr (OC) wm = F.w[idx];
+    } else if constexpr (X0) {
+      vm = omega * dinv[idx] * r[idx];
+    } else {
+      vm = e[idx];
+    }
+  }
+  const double tp = P.t_plus;
+  constexpr int VW = X0 ? T_DW : L::VW;
+  // byte offsets of the own voxel inside a slot
+  const int lofs = L::LAB + 4 * ((threadIdx.y + 1) * T_LW + threadIdx.x + T_LOFF);
+  const int aofs = 8 * ((threadIdx.y + 1) * T_DW + threadIdx.x + T_DOFF);
+  const int vofs = X0 ? aofs : L::VAL + (int)sizeof(VT) * ((threadIdx.y + 1) * L::VW + threadIdx.x + L::VOFF);
+  const unsigned char* base = ring;
+
+  auto step = [&](int j, auto slotc, unsigned ph0, unsigned ph1) {
+    constexpr int K = decltype(slotc)::value, K1 = (K + 1) % T_S;
+    const unsigned char* S0 = base + K * L::SLOT;
+    const unsigned char* S1 = base + K1 * L::SLOT;
+    const int z = z0 + j;
+    const int v = z * nxy + col;
+    double rv = 0.0, dv_ = 0.0;
+    if constexpr (!FULLM) {
+      if (active) {
+        if (EPI != EP_STORE) rv = r[v];
+        if (EPI == EP_SMOOTH || EPI == EP_SMOOTH0) dv_ = dinv[v];
+      }
+    }
+    mbar_wait(full0 + 8 * K, ph0);
+    mbar_wait(full0 + 8 * K1, ph1);
+    if (active) {   // pull the next plane's interface coefficients towards L1 (off the critical path)
+      const unsigned w1 = *reinterpret_cast<const unsigned*>(S1 + lofs);
+      if (w1 & (63u << 3)) {
+        const double* c = F.cslot + 3LL * (w1 >> 9);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(c));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(c + 5));
+      }
+    }
+    auto lab_at = [&](const unsigned char* Sx, int o) -> int {
+      return *reinterpret_cast<const int*>(Sx + lofs + 4 * o);
+    };
+    auto val_at = [&](const unsigned char* Sx, int o) -> VT {
+      if constexpr (X0)
+        return omega * *reinterpret_cast<const double*>(Sx + L::AUX2 + aofs + 8 * o) *
+               *reinterpret_cast<const double*>(Sx + L::AUX + aofs + 8 * o);
+      else
+        return *reinterpret_cast<const VT*>(Sx + vofs + (int)sizeof(VT) * o);
+    };
+    auto w_at = [&](const unsigned char* Sx, int o) -> double {
+      return *reinterpret_cast<const double*>(Sx + L::AUX + aofs + 8 * o);
+    };
+    // neighbour d: 0 x-1, 1 x+1, 2 y-1, 3 y+1, 4 z-1 (registers), 5 z+1 (next slot)
+    auto nb_lab = [&](int d) -> int {
+      if (d == 4) return lm;
+      if (d == 5) return lab_at(S1, 0) & 7;
+      return lab_at(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -T_LW : T_LW))) & 7;
+    };
+    auto nb_val = [&](int d) -> VT {
+      if (d == 4) return vm;
+      if (d == 5) return val_at(S1, 0);
+      return val_at(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -VW : VW)));
+    };
+    auto nb_w = [&](int d) -> double {
+      if (d == 4) return wm;
+      if (d == 5) return w_at(S1, 0);
+      return w_at(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -T_DW : T_DW)));
+    };
+    if (active) {
+      const int aw = lab_at(S0, 0);
+      const int a = aw & 7;
+      const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == TGR || a == TEL)
+                                                             : !(z == nz - 1 && a == TCC);
+      const VT va = val_at(S0, 0);
+      double wa = 0.0;
+      if constexpr (OC) wa = w_at(S0, 0);
+      if (!in_row) {
+        if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
+        else out[v] = 0.0;
+      } else {
+        const int a8 = a << 3;
+        const bool elrow = a == TEL;
+        // linear faces from the (P, C) table.  Electrolyte rows also carry migration and
+        // chemical-potential couplings, which equal t+ times their phi-row terms
+        // (operator.py:216-227), so only P and C are looked up.
+        double rc = 0.0, rp = 0.0;
+        if constexpr (FULLM) {
+          double q = 0.0;
+          int nel = 0;
+#pragma unroll
+          for (int d = 0; d < 6; ++d) {
+            const int b = nb_lab(d);
+            const double2 vb = nb_val(d);
+            const double2 pc = sPC[a8 | b];
+            rp = fma(pc.x, va.y - vb.y, rp);
+            rc = fma(pc.y, va.x - vb.x, rc);
+            if constexpr (OC) {   // gX/c is zero off the electrolyte and in the zero-filled halo
+              q = fma(-nb_w(d), vb.x, q);
+              nel += b == TEL;
+            }
+          }
+          if constexpr (OC) {
+            q = fma((double)nel, wa * va.x, q);
+            rp += elrow ? q : 0.0;
+          }
+        } else if (MODE == SM_PHI || MODE == SM_CONC) {
+#pragma unroll
+          for (int d = 0; d < 6; ++d) {
+            const double2 pc = sPC[a8 | nb_lab(d)];
+            rp = fma(MODE == SM_PHI ? pc.x : pc.y, va - nb_val(d), rp);
+          }
+        }
+        // interface kinetics: six row-oriented coefficient triples (zero off-interface);
+        // face d adds alpha c_a + beta c_b + gamma (phi_a - phi_b) to the phi row
+        double si = 0.0;
+        const unsigned mask = ((unsigned)aw >> 3) & 63u;
+        if (mask) {
+          const double* c = F.cslot + 3LL * ((unsigned)aw >> 9);
+#pragma unroll
+          for (int d = 0; d < 6; ++d) {
+            if (mask & (1u << d)) {
+              const VT vb = nb_val(d);
+              if constexpr (FULLM) si += c[0] * va.x + c[1] * vb.x + c[2] * (va.y - vb.y);
+              else if (MODE == SM_CONC) si += c[0] * va + c[1] * vb;
+              else si += c[2] * (va - vb);
+              c += 3;
+            }
+          }
+        }
+        if constexpr (FULLM) {
+          const bool crow = a == TGR || elrow;
+          if (elrow) rc = (flags & 2) ? fma(1.0 - tp, si, rc) : fma(tp, rp, rc) + si;  // T: c -= t+ phi
+          else if (crow) rc += si;
+          rp += si;
+          if ((flags & 1) && crow) rc = fma(va.x, inv_dt, rc);
+          if (flags & 8) rc = 0.0;
+          out2[v] = make_double2(rc, rp);
+        } else {
+          if (MODE == SM_PHI) rp += si;
+          else rp = fma(elrow ? 1.0 - tp : 1.0, si, rp);   // (T J) on electrolyte c rows
+          if (MODE == SM_CONC) rp = fma(inv_dt, va, rp);
+          if (EPI == EP_STORE) out[v] = rp;
+          else if (EPI == EP_RESID) out[v] = rv - rp;
+          else out[v] = va + omega * dv_ * (rv - rp);
+        }
+      }
+      lm = a;
+      vm = va;
+      if constexpr (OC) wm = wa;
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) mbar_arrive(empty0 + 8 * K);   // this warp is done with plane j
+  };
+  for (int jb = 0; jb < nplane; jb += T_S) {   // unrolled by the ring depth: slots are compile-time
+    const unsigned ph = (jb / T_S) & 1;
+    static_for<T_S>([&](auto kc) {
+      constexpr int K = decltype(kc)::value;
+      if (jb + K < nplane) step(jb + K, kc, ph, K + 1 == T_S ? ph ^ 1 : ph);
+    });
+  }
+}
+
+// ---- host side: tensor-map encoding (driver entry point, no -lcuda) and a cache
+// keyed by (pointer, element kind) so graph captures and repeated launches reuse maps.
+struct TmaCache {
+  std::mutex mu;
+  std::unordered_map<unsigned long long, CUtensorMap> maps;
+};
+
+bool tma_encode(CUtensorMap* m, const void* ptr, int kind, int nx, int ny, int nz);
+// kind: 0 int32 labels (box 40), 1 double2 values (box 68 f64), 2 double (box 36)
+inline const CUtensorMap* tma_map(TmaCache& c, const void* ptr, int kind, int nx, int ny, int nz) {
+  const unsigned long long key = reinterpret_cast<unsigned long long>(ptr) ^ ((unsigned long long)kind << 60);
+  std::lock_guard<std::mutex> g(c.mu);
+  auto it = c.maps.find(key);
+  if (it != c.maps.end()) return &it->second;
+  CUtensorMap m;
+  if (!tma_encode(&m, ptr, kind, nx, ny, nz)) return nullptr;
+  return &c.maps.emplace(key, m).first->second;
+}
+
+inline bool tma_grid_ok(const DevParams& P) { return P.nx % 4 == 0 && P.nx >= 4; }
+
+template <int MODE, int EPI>
+inline bool fine_launch_tma(TmaCache& cache, const DevParams& P, const FineArgs& F, const int32_t* labt,
+                            const double2* V, const double* e, const double* r, const double* dinv,
+                            double omega, double inv_dt, int flags, double2* out2, double* out,
+                            int n_sm, cudaStream_t s) {
+  using L = TmaLayout<MODE, EPI>;
+  if (!tma_grid_ok(P) || !labt) return false;
+  TmaMaps M;
+  std::memset(&M, 0, sizeof(M));
+  const CUtensorMap* m = tma_map(cache, labt, 0, P.nx, P.ny, P.nz);
+  if (!m) return false;
+  M.lab = *m;
+  if constexpr (L::X0) {
+    if (!(m = tma_map(cache, r, 2, P.nx, P.ny, P.nz))) return false;
+    M.aux = *m;
+    if (!(m = tma_map(cache, dinv, 2, P.nx, P.ny, P.nz))) return false;
+    M.aux2 = *m;
+  } else if constexpr (L::FULLM) {
+    if (!(m = tma_map(cache, V, 1, P.nx, P.ny, P.nz))) return false;
+    M.val = *m;
+    if (flags & 4) {
+      if (!(m = tma_map(cache, F.w, 2, P.nx, P.ny, P.nz))) return false;
+      M.aux = *m;
+    }
+  } else {
+    if (!(m = tma_map(cache, e, 2, P.nx, P.ny, P.nz))) return false;
+    M.val = *m;
+  }
+  const size_t smem = (size_t)T_S * L::SLOT + 128;
+  const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
+  auto go = [&](auto kern) {
+    static int per_sm = 0;   // one cache per instantiation (kern is a distinct type per lambda call site)
+    if (!per_sm) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T_THREADS, smem);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int bz = pick_bz(bx, by, P.nz, per_sm, n_sm);
+    const int zc = (P.nz + bz - 1) / bz;
+    kern<<<dim3(bx, by, (P.nz + zc - 1) / zc), dim3(VX, VY + 1, 1), smem, s>>>(
+        P, M, F, labt, V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
+  };
+  if (L::FULLM && (flags & 4)) go(k_fine_tma<MODE, EPI, true>);
+  else go(k_fine_tma<MODE, EPI, false>);
+  return true;
+}
+
+// the solver's dispatcher: TMA ring where the grid allows it, else the cp.async ring
+template <int MODE, int EPI>
+inline void fine_launch_op(Operator& op, const FineArgs& F, const double2* V, const double* e,
+                           const double* r, const double* dinv, double omega, double inv_dt, int flags,
+                           double2* out2, double* out, cudaStream_t s) {
+  if (op.stencil_kind == 3 && op.tma &&
+      fine_launch_tma<MODE, EPI>(*op.tma, op.P, F, op.labt.p, V, e, r, dinv, omega, inv_dt, flags, out2,
+                                 out, op.n_sm, s))
+    return;
+  fine_launch_p<MODE, EPI>(op.P, F, op.lab4.p, V, e, r, dinv, omega, inv_dt, flags, out2, out, op.n_sm, s);
+}
+
+}  // namespace hc
