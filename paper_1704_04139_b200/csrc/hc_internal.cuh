@@ -252,6 +252,8 @@ struct Operator {
   DBuf<double> if_coef;        // 3 x n_if Jacobian coefficients (linearized)
   DBuf<double> if_vcoef;       // the same per interface voxel and direction: [3][6 n_if_vox]
   DBuf<double> if_cslot;       // TMA stencil: (alpha, beta, gamma) per interface face slot
+  DBuf<int2> elz;              // TMA stencil: electrolyte z range per 32 x 8 tile column
+  DBuf<double> if_islot;       // TMA residual: interface current per face slot
   DBuf<double> inv_c;          // gX / c per electrolyte voxel (linearized)
   DBuf<double> red;            // reduction scratch
   DBuf<double> host_x, host_npl;  // staging for the host-buffer entry point

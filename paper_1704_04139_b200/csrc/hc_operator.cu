@@ -361,6 +361,37 @@ __global__ void __launch_bounds__(TPB) k_residual_iface(
   atomicAdd(&out[e].y, -q);
 }
 
+// The same currents written once per face slot, oriented from each side's row (solid
+// +i, electrolyte -i), for the TMA residual stencil to gather: no atomics.
+__global__ void __launch_bounds__(TPB) k_residual_islot(
+    DevParams P, long long n_if, const int32_t* __restrict__ so, const int32_t* __restrict__ el,
+    const int32_t* __restrict__ slot, const int8_t* __restrict__ kind, const int32_t* __restrict__ labt,
+    const double2* __restrict__ X, const double* __restrict__ npl, double beta,
+    double* __restrict__ islot) {
+  long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (f >= n_if) return;
+  int32_t s = so[f], e = el[f];
+  double2 xs = X[s], xe = X[e];
+  int8_t k = kind[f];
+  double i;
+  if (k == IF_BV) {
+    double eta = xs.y - ocp_dev(xs.x, P) - xe.y;
+    double root = sqrt(xs.x * xe.x);
+    i = 2.0 * P.i00_grel * root * sinh(eta / P.vt);
+  } else if (k == IF_CE) {
+    i = 2.0 * P.i00_ceel * sinh((xs.y - xe.y) / P.vt);
+  } else {
+    i = strip_current_dev(xe.x, xs.y, xe.y, npl[slot[f]], beta, P, nullptr, nullptr);
+  }
+  const double q = P.sc * i;
+  auto slot_of = [&](int v, int d) -> long long {
+    const unsigned w = (unsigned)labt[v];
+    return (long long)(w >> 9) + __popc(((w >> 3) & 63u) & ((1u << d) - 1u));
+  };
+  islot[slot_of(s, dir_to(P, s, e))] = q;
+  islot[slot_of(e, dir_to(P, e, s))] = -q;
+}
+
 // --------------------------------------------------------------- linearization
 __global__ void k_lin_iface(DevParams P, long long n_if, const int32_t* __restrict__ so,
                             const int32_t* __restrict__ el, const int32_t* __restrict__ slot,
@@ -566,6 +597,21 @@ void gather_packed(const Operator& op, const double2* xg, double* x, cudaStream_
 void residual_grid(Operator& op, const double2* xg, const double* npl, double mu, double beta,
                    int parts, const double* cprev, double inv_dt, double2* out, cudaStream_t s,
                    int which) {
+  if (op.tma && op.stencil_kind == 3) {
+    // deterministic: face currents into per-slot storage, gathered by the stencil
+    if ((which & 2) && (parts & PART_BV) && op.n_if)
+      k_residual_islot<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
+                                                           op.if_slot.p, op.if_kind.p, op.labt.p, xg,
+                                                           npl, beta, op.if_islot.p); HC_COUNT();
+    if ((which & 1) && res_launch_tma(op, xg, mu, parts, cprev, inv_dt, out, s)) {
+      HC_COUNT();
+      HC_CHECK_LAUNCH();
+      return;
+    }
+    if (which & 1) throw Error(HC_ERR_CUDA, "TMA residual launch failed");
+    HC_CHECK_LAUNCH();
+    return;
+  }
   if (which & 1) {
     if (op.stencil_kind >= 2)
       res_launch_p(op.P, op.lab4.p, xg, mu, parts, cprev, inv_dt, out, op.n_sm, s);
@@ -635,7 +681,7 @@ void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2
               cudaStream_t s, int which) {
   if (which & 1) {
     FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
-               op.if_cslot.p};
+               op.if_cslot.p, op.elz.p};
     fine_launch_op<SM_FULL, EP_STORE>(op, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out,
                                       nullptr, s);
     HC_COUNT();
@@ -937,6 +983,19 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
         HC_CUDA(cudaMemcpy(op->labt.p, l4.data(), nvox * 4, cudaMemcpyHostToDevice));
         op->if_cslot.alloc(std::max<long long>(3 * slot, 1));
         HC_CUDA(cudaMemset(op->if_cslot.p, 0, op->if_cslot.n * sizeof(double)));
+        op->if_islot.alloc(std::max<long long>(slot, 1));
+        HC_CUDA(cudaMemset(op->if_islot.p, 0, op->if_islot.n * sizeof(double)));
+        const int tbx = (nx + VX - 1) / VX, tby = (ny + VY - 1) / VY;
+        std::vector<int2> ez(tbx * tby, make_int2(nz, -1));
+        for (long long v = 0; v < nvox; ++v)
+          if (labels_host[v] == EL) {
+            const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((long long)nx * ny));
+            int2& t = ez[(y / VY) * tbx + x / VX];
+            t.x = std::min(t.x, z);
+            t.y = std::max(t.y, z);
+          }
+        op->elz.alloc(ez.size());
+        HC_CUDA(cudaMemcpy(op->elz.p, ez.data(), ez.size() * sizeof(int2), cudaMemcpyHostToDevice));
         op->tma = new TmaCache();
       }
     }

@@ -34,6 +34,8 @@ struct FineArgs {
   long long nslot;        // 6 * number of interface voxels
   const double* w;        // gX / c per electrolyte voxel (FULL with flag 4)
   const double* cslot;    // TMA stencil: compact row-oriented (alpha, beta, gamma) per interface face slot
+  const int2* elz;        // TMA stencil: per 32 x 8 tile column, z range holding electrolyte (lo, hi)
+  const double* islot;    // TMA residual: interface current per face slot, oriented from the row
 };
 
 }  // namespace hc

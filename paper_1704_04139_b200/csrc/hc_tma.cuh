@@ -28,7 +28,10 @@
 namespace hc {
 
 // phases in the TMA label encoding
-enum : int { TV = 0, TEL = EL + 1, TGR = GR + 1, TCC = CC + 1 };
+enum : int { TV = 0, TEL = EL + 1, TGR = GR + 1, TCC = CC + 1, TCW = CW + 1 };
+// operator value (residual) mode of the TMA stencil: parts in `flags`, mu in `omega`,
+// c_prev in `r`, interface currents per face slot in F.islot
+constexpr int SM_RES = 4;
 
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -69,6 +72,9 @@ struct TmaMaps {
 #define HC_TMA_STAGES 4
 #endif
 constexpr int T_S = HC_TMA_STAGES;   // ring depth
+#ifndef HC_TMA_MINB
+#define HC_TMA_MINB 3
+#endif
 
 template <typename Fn, int... I>
 __device__ __forceinline__ void static_for_impl(Fn&& fn, std::integer_sequence<int, I...>) {
@@ -89,7 +95,7 @@ constexpr int T_LN = T_LW * T_TH, T_DN = T_DW * T_TH, T_QN = T_QW * T_TH;
 
 template <int MODE, int EPI>
 struct TmaLayout {
-  static constexpr bool FULLM = MODE == SM_FULL;
+  static constexpr bool FULLM = MODE == SM_FULL || MODE == 4;   // double2 (c, phi) tiles
   static constexpr bool X0 = EPI == EP_SMOOTH0;
   static constexpr int VW = FULLM ? T_QW : T_DW, VOFF = FULLM ? T_QOFF : T_DOFF;
   static constexpr int VBYTES = FULLM ? T_QN * 16 : T_DN * 8;
@@ -98,7 +104,9 @@ struct TmaLayout {
   static constexpr int AUX = VAL + (X0 ? 0 : ((VBYTES + 127) / 128) * 128);   // gX/c or r
   static constexpr bool HAS_AUX = FULLM || X0;
   static constexpr int AUX2 = AUX + (HAS_AUX ? ((T_DN * 8 + 127) / 128) * 128 : 0);
-  static constexpr int SLOT = AUX2 + (X0 ? ((T_DN * 8 + 127) / 128) * 128 : 0);
+  static constexpr int LOG = AUX2 + (X0 ? ((T_DN * 8 + 127) / 128) * 128 : 0);   // log c (residual)
+  static constexpr int SLOT = LOG + (MODE == 4 ? ((T_QN * 8 + 127) / 128) * 128 : 0);
+  static constexpr int THREADS = VX * (VY + 1);   // + producer warp
 };
 
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
@@ -113,32 +121,35 @@ constexpr int T_WARPS = VY;                 // compute warps
 constexpr int T_THREADS = VX * (VY + 1);    // + producer warp
 
 template <int MODE, int EPI, bool ONEC>
-__global__ void __launch_bounds__(T_THREADS, 3)
+__global__ void __launch_bounds__(TmaLayout<MODE, EPI>::THREADS, HC_TMA_MINB)
 k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int32_t* __restrict__ labt,
            const double2* __restrict__ V, const double* __restrict__ e, const double* __restrict__ r,
            const double* __restrict__ dinv, double omega, double inv_dt, int flags,
            double2* __restrict__ out2, double* __restrict__ out, int zc) {
   using L = TmaLayout<MODE, EPI>;
   constexpr bool FULLM = L::FULLM, X0 = L::X0;
-  constexpr bool OC = FULLM && ONEC;
+  constexpr bool RES = MODE == SM_RES;
+  constexpr bool OC = MODE == SM_FULL && ONEC;
   using VT = typename std::conditional<FULLM, double2, double>::type;
   extern __shared__ __align__(16) unsigned char smem_dyn[];
   // 128-byte aligned ring (the launch adds 128 bytes of slack)
   unsigned char* ring = smem_dyn + ((128 - ((unsigned)__cvta_generic_to_shared(smem_dyn) & 127)) & 127);
   __shared__ __align__(16) double2 sPC[64];   // (P, C) per (a << 3 | b)
-  __shared__ __align__(8) unsigned long long full[T_S], empty[T_S];
+  __shared__ __align__(8) unsigned long long full[T_S], empty[T_S], ready[T_S];
   const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
   const int x0 = blockIdx.x * VX, y0 = blockIdx.y * VY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);   // planes z0 .. z1 are staged
   const int nplane = z1 - z0;                                // computed planes
   const unsigned full0 = (unsigned)__cvta_generic_to_shared(full);
   const unsigned empty0 = (unsigned)__cvta_generic_to_shared(empty);
+  const unsigned ready0 = (unsigned)__cvta_generic_to_shared(ready);
   const int tid = threadIdx.y * VX + threadIdx.x;
   if (tid == T_WARPS * VX) {
 #pragma unroll
     for (int k = 0; k < T_S; ++k) {
       mbar_init(full0 + 8 * k, 1);
       mbar_init(empty0 + 8 * k, T_WARPS);
+      if constexpr (RES) mbar_init(ready0 + 8 * k, T_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -153,20 +164,25 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
   if (threadIdx.y == T_WARPS) {   // ---------------- producer warp
     if (threadIdx.x == 0) {
       const unsigned sbase = (unsigned)__cvta_generic_to_shared(ring);
-      constexpr unsigned tx = T_LN * 4 + (X0 ? 2 * T_DN * 8 : L::VBYTES) + (OC ? T_DN * 8 : 0);
+      constexpr unsigned tx = T_LN * 4 + (X0 ? 2 * T_DN * 8 : L::VBYTES);
+      // gX/c tiles only on planes next to electrolyte in this tile column (it is zero
+      // elsewhere and only electrolyte rows read it)
+      int2 elz = make_int2(0, -1);
+      if constexpr (OC) elz = F.elz[blockIdx.y * gridDim.x + blockIdx.x];
       for (int j = 0; j <= nplane; ++j) {
         const int slot = j % T_S;
         if (j >= T_S) mbar_wait(empty0 + 8 * slot, ((j / T_S) - 1) & 1);
         const unsigned b = full0 + 8 * slot, s = sbase + slot * L::SLOT;
         const int zz = z0 + j;
-        mbar_expect_tx(b, tx);
+        const bool wtile = OC && zz >= elz.x - 1 && zz <= elz.y + 1;
+        mbar_expect_tx(b, tx + (wtile ? T_DN * 8 : 0));
         tma_load3(s + L::LAB, &M.lab, x0 - T_LOFF, y0 - 1, zz, b);
         if constexpr (X0) {
           tma_load3(s + L::AUX, &M.aux, x0 - T_DOFF, y0 - 1, zz, b);
           tma_load3(s + L::AUX2, &M.aux2, x0 - T_DOFF, y0 - 1, zz, b);
         } else if constexpr (FULLM) {
           tma_load3(s + L::VAL, &M.val, 2 * (x0 - T_QOFF), y0 - 1, zz, b);
-          if constexpr (OC) tma_load3(s + L::AUX, &M.aux, x0 - T_DOFF, y0 - 1, zz, b);
+          if (wtile) tma_load3(s + L::AUX, &M.aux, x0 - T_DOFF, y0 - 1, zz, b);
         } else {
           tma_load3(s + L::VAL, &M.val, x0 - T_DOFF, y0 - 1, zz, b);
         }
@@ -180,7 +196,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
   const bool active = x < nx && y < ny;
   const int col = active ? y * nx + x : 0;
   VT vm{};            // own column z - 1 (registers)
-  double wm = 0.0;
+  double wm = 0.0;   // gX/c (J v) or log c (residual) of the own column at z - 1
   int lm = 0;
   if (active && z0 > 0) {
     const long long idx = (long long)(z0 - 1) * nxy + col;
@@ -188,6 +204,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
     if constexpr (FULLM) {
       vm = V[idx];
       if constexpr (OC) wm = F.w[idx];
+      if constexpr (RES) wm = (lm == TEL) ? log(vm.x) : 0.0;
     } else if constexpr (X0) {
       vm = omega * dinv[idx] * r[idx];
     } else {
@@ -201,7 +218,29 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
   const int aofs = 8 * ((threadIdx.y + 1) * T_DW + threadIdx.x + T_DOFF);
   const int vofs = X0 ? aofs : L::VAL + (int)sizeof(VT) * ((threadIdx.y + 1) * L::VW + threadIdx.x + L::VOFF);
   const unsigned char* base = ring;
+  const int vidx_t = (threadIdx.y + 1) * T_QW + threadIdx.x + T_QOFF;   // own element of a double2-shaped tile
 
+  // residual: log c of the staged electrolyte elements of plane p, computed cooperatively
+  // by the eight compute warps two planes ahead (each tile element once instead of once
+  // per electrolyte face); ready[s] completes when all warps have written their share
+  auto logs_for = [&](int p) {
+    if (p > nplane) return;
+    const int slot = p % T_S;
+    mbar_wait(full0 + 8 * slot, (p / T_S) & 1);
+    unsigned char* S = ring + slot * L::SLOT;
+    for (int i = threadIdx.y * VX + threadIdx.x; i < T_QN; i += T_WARPS * VX) {
+      const int row = i / T_QW, c = i - row * T_QW;
+      const int lab = reinterpret_cast<const int*>(S + L::LAB)[row * T_LW + c + (T_LOFF - T_QOFF)];
+      if ((lab & 7) == TEL)
+        reinterpret_cast<double*>(S + L::LOG)[i] = log(reinterpret_cast<const double2*>(S + L::VAL)[i].x);
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) mbar_arrive(ready0 + 8 * slot);
+  };
+  if constexpr (RES) {
+    logs_for(0);
+    logs_for(1);
+  }
   auto step = [&](int j, auto slotc, unsigned ph0, unsigned ph1) {
     constexpr int K = decltype(slotc)::value, K1 = (K + 1) % T_S;
     const unsigned char* S0 = base + K * L::SLOT;
@@ -214,10 +253,13 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         if (EPI != EP_STORE) rv = r[v];
         if (EPI == EP_SMOOTH || EPI == EP_SMOOTH0) dv_ = dinv[v];
       }
+    } else if constexpr (RES) {
+      if (active && (flags & PART_TIME)) rv = r[v];   // c_prev
     }
-    mbar_wait(full0 + 8 * K, ph0);
-    mbar_wait(full0 + 8 * K1, ph1);
-    if (active) {   // pull the next plane's interface coefficients towards L1 (off the critical path)
+    if constexpr (RES) logs_for(j + 2);
+    mbar_wait((RES ? ready0 : full0) + 8 * K, ph0);
+    mbar_wait((RES ? ready0 : full0) + 8 * K1, ph1);
+    if (!RES && active) {   // pull the next plane's interface coefficients towards L1
       const unsigned w1 = *reinterpret_cast<const unsigned*>(S1 + lofs);
       if (w1 & (63u << 3)) {
         const double* c = F.cslot + 3LL * (w1 >> 9);
@@ -272,7 +314,33 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         // chemical-potential couplings, which equal t+ times their phi-row terms
         // (operator.py:216-227), so only P and C are looked up.
         double rc = 0.0, rp = 0.0;
-        if constexpr (FULLM) {
+        if constexpr (RES) {
+          // linear two-point fluxes and the chemical-potential faces gX (log c_a - log c_b)
+          // between electrolyte voxels (operator.py:322-327)
+          const bool lin = flags & PART_LIN, lc = (flags & PART_1C) && elrow;
+          auto lg = [&](const unsigned char* Sx, int o) -> double {
+            return reinterpret_cast<const double*>(Sx + L::LOG)[vidx_t + o];
+          };
+          const double la = lg(S0, 0);
+          double q = 0.0;
+#pragma unroll
+          for (int d = 0; d < 6; ++d) {
+            const int b = nb_lab(d);
+            const double2 vb = nb_val(d);
+            if (lin) {
+              const double2 pc = sPC[a8 | b];
+              rp = fma(pc.x, va.y - vb.y, rp);
+              rc = fma(pc.y, va.x - vb.x, rc);
+            }
+            if (lc && b == TEL) {
+              const double lb = d == 4 ? wm : (d == 5 ? lg(S1, 0)
+                                : lg(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -T_QW : T_QW))));
+              q += la - lb;
+            }
+          }
+          wa = la;
+          rp = fma(P.gX, q, rp);
+        } else if constexpr (FULLM) {
           double q = 0.0;
           int nel = 0;
 #pragma unroll
@@ -302,7 +370,14 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         // face d adds alpha c_a + beta c_b + gamma (phi_a - phi_b) to the phi row
         double si = 0.0;
         const unsigned mask = ((unsigned)aw >> 3) & 63u;
-        if (mask) {
+        if constexpr (RES) {
+          // interface currents, one per face slot, oriented from this row (k_residual_islot)
+          if (mask && (flags & PART_BV)) {
+            const double* c = F.islot + ((unsigned)aw >> 9);
+            const int n = __popc(mask);
+            for (int k = 0; k < n; ++k) si += c[k];
+          }
+        } else if (mask) {
           const double* c = F.cslot + 3LL * ((unsigned)aw >> 9);
 #pragma unroll
           for (int d = 0; d < 6; ++d) {
@@ -315,7 +390,15 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
             }
           }
         }
-        if constexpr (FULLM) {
+        if constexpr (RES) {
+          const bool crow = a == TGR || elrow;
+          if (elrow) rc = fma(tp, rp, rc);   // migration + chemical potential: t+ x phi-row terms
+          if (crow) rc += si;
+          rp += si;
+          if ((flags & PART_BND) && a == TCW && z == 0) rp = fma(omega, P.drive, rp);
+          if ((flags & PART_TIME) && crow) rc += (va.x - rv) * inv_dt;
+          out2[v] = make_double2(rc, rp);
+        } else if constexpr (FULLM) {
           const bool crow = a == TGR || elrow;
           if (elrow) rc = (flags & 2) ? fma(1.0 - tp, si, rc) : fma(tp, rp, rc) + si;  // T: c -= t+ phi
           else if (crow) rc += si;
@@ -334,7 +417,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
       }
       lm = a;
       vm = va;
-      if constexpr (OC) wm = wa;
+      if constexpr (OC || RES) wm = wa;
     }
     __syncwarp();
     if (threadIdx.x == 0) mbar_arrive(empty0 + 8 * K);   // this warp is done with plane j
@@ -389,7 +472,7 @@ inline bool fine_launch_tma(TmaCache& cache, const DevParams& P, const FineArgs&
   } else if constexpr (L::FULLM) {
     if (!(m = tma_map(cache, V, 1, P.nx, P.ny, P.nz))) return false;
     M.val = *m;
-    if (flags & 4) {
+    if (MODE == SM_FULL && (flags & 4)) {
       if (!(m = tma_map(cache, F.w, 2, P.nx, P.ny, P.nz))) return false;
       M.aux = *m;
     }
@@ -404,17 +487,28 @@ inline bool fine_launch_tma(TmaCache& cache, const DevParams& P, const FineArgs&
     if (!per_sm) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T_THREADS, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, smem);
       if (per_sm < 1) per_sm = 1;
     }
     const int bz = pick_bz(bx, by, P.nz, per_sm, n_sm);
     const int zc = (P.nz + bz - 1) / bz;
-    kern<<<dim3(bx, by, (P.nz + zc - 1) / zc), dim3(VX, VY + 1, 1), smem, s>>>(
+    kern<<<dim3(bx, by, (P.nz + zc - 1) / zc), dim3(VX, L::THREADS / VX, 1), smem, s>>>(
         P, M, F, labt, V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
   };
-  if (L::FULLM && (flags & 4)) go(k_fine_tma<MODE, EPI, true>);
+  if (MODE == SM_FULL && (flags & 4)) go(k_fine_tma<MODE, EPI, true>);
   else go(k_fine_tma<MODE, EPI, false>);
   return true;
+}
+
+// residual through the TMA stencil (parts bitmask PART_*); false if the grid or the
+// pointers do not allow tensor-map tiles
+inline bool res_launch_tma(Operator& op, const double2* X, double mu, int parts, const double* cprev,
+                           double inv_dt, double2* out, cudaStream_t s) {
+  if (op.stencil_kind != 3 || !op.tma) return false;
+  FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
+             op.if_cslot.p, op.elz.p, op.if_islot.p};
+  return fine_launch_tma<SM_RES, EP_STORE>(*op.tma, op.P, F, op.labt.p, X, nullptr, cprev, nullptr, mu,
+                                           inv_dt, parts, out, nullptr, op.n_sm, s);
 }
 
 // the solver's dispatcher: TMA ring where the grid allows it, else the cp.async ring
