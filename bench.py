@@ -182,6 +182,72 @@ def cpu_sample(config: str, rounds: int, warmup: int = 0):
 
 
 # ------------------------------------------------------------------ GPU arm
+def kernel_roofline(op, grid, params, x, npl, beta, dt, config):
+    """CUDA-event times of the residual and J v kernels (L2 read-flushed before every
+    launch) and the J v roofline: algorithmic bytes / launch time vs the measured peak."""
+    import ctypes
+    from paper_1704_04139_b200 import _dev, _native
+    L = _native.lib()
+    ms = (ctypes.c_double * 5)()
+    _native.check(L.hc_time_kernels(op.native.handle, _dev.ptr(x), _dev.ptr(npl), beta, 1.0 / dt, 20,
+                                    L2_FLUSH_BYTES, ms, _dev.stream()))
+    info = op.native.info
+    nvox = int(info.n_vox)
+    n_el = int(np.count_nonzero(grid.labels == 0))
+    n_c = int(np.count_nonzero(np.isin(grid.labels, (0, 1))))
+    n_if = int(info.n_bv + info.n_ce + info.n_strip)
+    res_ms, jv_ms = ms[0] + ms[1], ms[2] + ms[3]
+    # labels + v (c, phi) + out + gX/c on electrolyte voxels + 3 linearized coefficients per interface face
+    jv_bytes = nvox * (1 + 16 + 16) + n_el * 8 + n_if * 24
+    res_bytes = nvox * (1 + 16 + 16) + n_c * 8          # labels + x + out + c_prev
+    peak, peak_kind = measured_peaks()
+    achieved = jv_bytes / (ms[2] * 1e-3) / 1e9
+    copy_gbs = nvox * 32 / (ms[4] * 1e-3) / 1e9          # same-size streaming copy, same timing
+    traffic = committed_traffic(config, "k_fine_tma<0, 0, 1>")
+    return {
+        "res_ms": res_ms, "jv_ms": jv_ms,
+        "kernel_ms": {"residual_stencil": ms[0], "residual_iface": ms[1],
+                      "jvp_stencil": ms[2], "jvp_iface": ms[3]},
+        "roofline": {"kernel": "k_fine_tma<SM_FULL> (J v: TMA tiles, fused interface slots)",
+                     "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "bytes_per_launch": jv_bytes,
+                     "bytes_per_voxel": "label 1 + v 16 + out 16 (+ gX/c 8 per electrolyte voxel, "
+                                        "+ 24 per interface face)",
+                     "grid": f"{grid.labels.shape[2]}x{grid.labels.shape[1]}x{grid.labels.shape[0]}",
+                     "same_size_stream_copy_gbs": copy_gbs,
+                     "frac_of_stream_copy": achieved / copy_gbs,
+                     "residual": {"kernel": "k_fine_tma<SM_RES> + k_residual_islot",
+                                  "achieved": res_bytes / (res_ms * 1e-3) / 1e9,
+                                  "frac": res_bytes / (res_ms * 1e-3) / 1e9 / peak,
+                                  "bytes_per_launch": res_bytes}},
+    }
+
+
+def roofline_at_scale():
+    """J v / residual kernel roofline on the large config's grid (128x128x256) at its
+    initial state: the same kernels with an HBM-resident working set."""
+    import paper_1704_04139_b200 as P
+    from paper_1704_04139_b200 import _dev
+    from paper_1704_04139_b200.microgen import generate_cell
+    from paper_1704_04139_b200.state import initial_fields
+    rs, spec = cell_for("large", 0)
+    grid = generate_cell(spec)
+    params = P.MaterialParams(soc_init=rs.soc_init, i00_plel=rs.i00_plel_exchange / np.sqrt(1000.0))
+    dof = P.build_dofmap(grid)
+    op = P.SystemOperator(dof, params)
+    st = initial_fields(dof, params)
+    x = _dev.to_dev(st.x)
+    npl = _dev.to_dev(st.n_pl if st.n_pl.size else np.zeros(1))
+    beta = rs.dt * op.face_area / params.constants.F
+    kt = kernel_roofline(op, grid, params, x, npl, beta, rs.dt, "large")
+    out = dict(kt["roofline"])
+    out["kernel_ms"] = kt["kernel_ms"]
+    out["state"] = "initial fields of the large config"
+    del op
+    return out
+
+
 def run_ours(args, ws, rank, local):
     import torch
     import paper_1704_04139_b200 as P
@@ -248,21 +314,14 @@ def run_ours(args, ws, rank, local):
 
     # ---- kernel timings: residual and J v at the current state
     beta = rs.dt * op.face_area / params.constants.F
-    ms = (ctypes.c_double * 5)()
-    _native.check(L.hc_time_kernels(op.native.handle, _dev.ptr(x), _dev.ptr(npl), beta,
-                                    1.0 / rs.dt, 20, L2_FLUSH_BYTES, ms, sp))
-    nvox = int(op.native.info.n_vox)
-    n_el = int(np.count_nonzero(grid.labels == 0))
-    n_c = int(np.count_nonzero(np.isin(grid.labels, (0, 1))))
+    kt = kernel_roofline(op, grid, params, x, npl, beta, rs.dt, args.config)
     ndof = dof.n_total
-    res_ms, jv_ms = ms[0] + ms[1], ms[2] + ms[3]
-    jv_bytes = nvox * (1 + 16 + 16) + n_el * 8          # labels + v (c,phi) + out + gX/c (electrolyte)
-    res_bytes = nvox * (1 + 16 + 16) + n_c * 8          # labels + x + out + c_prev
-    peak, peak_kind = measured_peaks()
-    achieved = jv_bytes / (ms[2] * 1e-3) / 1e9
-    copy_gbs = nvox * 32 / (ms[4] * 1e-3) / 1e9          # same-size streaming copy, same timing
-    traffic = committed_traffic(args.config, "k_fine_p<0, 0>")
-
+    nvox = int(op.native.info.n_vox)
+    # the same kernels at the large single-GPU grid (HBM-resident working set); the medium
+    # cell's 18 MB fits in L2, so its cold-cache launches are latency- rather than HBM-bound
+    at_scale = None
+    if rank == 0 and args.config != "large" and not args.no_at_scale:
+        at_scale = roofline_at_scale()
     # ---- e2e: the same step through the host-buffer entry point
     e2e_val = None
     bi = (dof.n_total + max(dof.n_plated, 0)) * 8
@@ -307,21 +366,11 @@ def run_ours(args, ws, rank, local):
                                  "rtol_k = max(1e-10, 0.1 tol / |F_k|)"},
             "newton_iters_per_step": float(np.mean(newton)),
             "krylov_iters_per_step": float(np.mean(krylov)),
-            "gdof_per_s": {"residual": ndof / (res_ms * 1e-3) / 1e9,
-                           "jvp": ndof / (jv_ms * 1e-3) / 1e9},
-            "kernel_ms": {"residual_stencil": ms[0], "residual_iface": ms[1],
-                          "jvp_stencil": ms[2], "jvp_iface": ms[3]},
-            "roofline": {"kernel": "k_fine_p<SM_FULL> (J v, fused interface faces)", "bound": "hbm",
-                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "bytes_per_launch": jv_bytes,
-                         "bytes_per_voxel": "label 1 + v 16 + out 16 (+ gX/c 8 on electrolyte voxels)",
-                         "same_size_stream_copy_gbs": copy_gbs,
-                         "frac_of_stream_copy": achieved / copy_gbs,
-                         "residual": {"kernel": "k_res_p + k_residual_iface",
-                                      "achieved": res_bytes / (res_ms * 1e-3) / 1e9,
-                                      "frac": res_bytes / (res_ms * 1e-3) / 1e9 / peak,
-                                      "bytes_per_launch": res_bytes}},
+            "gdof_per_s": {"residual": ndof / (kt["res_ms"] * 1e-3) / 1e9,
+                           "jvp": ndof / (kt["jv_ms"] * 1e-3) / 1e9},
+            "kernel_ms": kt["kernel_ms"],
+            "roofline": kt["roofline"],
+            "roofline_at_scale": at_scale,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "steps/s", "h2d_bytes_per_step": bi,
                     "d2h_bytes_per_step": bi},
@@ -435,6 +484,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="medium")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-at-scale", action="store_true", help="skip the large-grid kernel roofline")
     ap.add_argument("--cells", type=int, default=128)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
