@@ -21,6 +21,7 @@ bounded sample of the same workload with all host cores (rank 0 only).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import dataclasses
 import json
 import os
@@ -458,6 +459,82 @@ def run_pod(args, ws, rank, local):
             "max_rel_err_vs_cublas": err}
 
 
+def run_rom(args, ws, rank, local):
+    """BASELINE config 4 end to end on the medium cell: full-order snapshots, POD (DMMA
+    Gram) per field, EI (DEIM) rows of the nonlinear sub-operators, projection, then the
+    reduced Newton solve for 500 steps in one kernel launch (timed, CUDA events)."""
+    import torch
+    import paper_1704_04139_b200 as P
+    from paper_1704_04139_b200 import mor
+    from paper_1704_04139_b200.microgen import generate_cell
+    from paper_1704_04139_b200.qoi import qoi_vectors
+    torch.cuda.set_device(local)
+    rs, spec = cell_for("medium", rank)
+    grid = generate_cell(spec)
+    params = P.MaterialParams(soc_init=rs.soc_init, i00_plel=rs.i00_plel_exchange / np.sqrt(1000.0))
+    op = P.SystemOperator(P.build_dofmap(grid), params)
+    mu = drive_mu(grid.labels, grid.voxel_size, rs.c_rate, params)
+    dt = rs.dt
+    cfg = P.SolverConfig(dt_init=min(0.05, dt), dt_max=dt, linear_safety=LINEAR_SAFETY)
+    st = P.prepare_initial_state(op, params, mu, cfg)
+    tt = {}
+    t0 = time.perf_counter()
+    snaps = mor.collect_snapshots(op, st.x, st.n_pl, mu, dt, args.rom_snapshots,
+                                  P.SolverConfig(dt_init=dt, dt_max=dt, linear_safety=LINEAR_SAFETY))
+    torch.cuda.synchronize()
+    tt["snapshots_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rom = mor.build_rom(op, snaps, args.rom_rank, args.rom_rank, args.rom_ei)
+    torch.cuda.synchronize()
+    tt["offline_build_s"] = time.perf_counter() - t0
+    xt0 = rom.project(st.x)
+    n_steps = args.rom_steps
+    for _ in range(max(1, args.warmup)):
+        mor.solve_rom(op, rom, xt0, st.n_pl, mu, dt, 2)
+    n0 = ctypes.c_int64(0)
+    from paper_1704_04139_b200 import _native
+    _native.check(_native.lib().hc_launch_count(ctypes.byref(n0)))
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        a.record()
+        tr = mor.solve_rom(op, rom, xt0, st.n_pl, mu, dt, n_steps)
+        b.record()
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    n1 = ctypes.c_int64(0)
+    _native.check(_native.lib().hc_launch_count(ctypes.byref(n1)))
+    # e2e: host reduced state in, QoI curves out, through the public API
+    xh = xt0.cpu().numpy()
+    t0 = time.perf_counter()
+    tr2 = mor.solve_rom(op, rom, xh, st.n_pl, mu, dt, n_steps)
+    v_host = np.asarray(tr2.voltage)
+    e2e_s = time.perf_counter() - t0
+    v_cp, v_ac = qoi_vectors(op.dof)
+    X = snaps.X.cpu().numpy()
+    nt = min(n_steps, X.shape[1] - 1)
+    fom_v = v_cp @ X[:, 1:nt + 1]
+    dev_v = float(np.max(np.abs(tr.voltage[:nt] - fom_v)) / np.max(np.abs(fom_v)))
+    return {"metric": "reduced implicit time steps/s (ROM online stage, config 4)",
+            "value": n_steps / (ms * 1e-3), "unit": "steps/s", "n_gpus": 1, "steps": n_steps,
+            "warmup": args.warmup, "ms_per_step": ms / n_steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (medium cell, seeded ball-union microstructure)",
+            "config": {"workload": f"rom: medium cell {spec.nx}x{spec.ny}x{spec.nz}, {args.rom_snapshots} "
+                                   f"full-order snapshots, POD rank {rom.k_c}+{rom.k_p}, {rom.m} EI rows, "
+                                   f"{n_steps} reduced steps at dt={dt}s", "n_dof": op.dof.n_total,
+                       "stencil_dofs": rom.dims["n_s"], "active_faces": rom.dims["n_f"]},
+            "newton_iters_per_step": float(np.mean(tr.newton_iters)),
+            "offline": tt,
+            "qoi_max_rel_dev_vs_fom_training_window": dev_v,
+            "e2e": {"value": n_steps / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": 8 * rom.k / n_steps,
+                    "d2h_bytes_per_step": 16.0},
+            "gpu_launches": int(n1.value - n0.value),
+            "roofline": {"bound": "latency (one CTA; k=%d dense LU per step)" % rom.k, "achieved": None,
+                         "peak": None, "unit": None, "frac": None, "traffic": None},
+            "clocks": clk.summary()}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return None
@@ -486,6 +563,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-at-scale", action="store_true", help="skip the large-grid kernel roofline")
     ap.add_argument("--cells", type=int, default=128)
+    ap.add_argument("--rom-snapshots", type=int, default=400)
+    ap.add_argument("--rom-rank", type=int, default=60)
+    ap.add_argument("--rom-ei", type=int, default=300)
+    ap.add_argument("--rom-steps", type=int, default=500)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -496,6 +577,8 @@ def main():
         out = run_batched(args, ws, rank, local)
     elif args.config == "pod":
         out = run_pod(args, ws, rank, local)
+    elif args.config == "rom":
+        out = run_rom(args, ws, rank, local)
     else:
         out = run_ours(args, ws, rank, local)
     if out is not None:

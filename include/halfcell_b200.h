@@ -35,6 +35,7 @@ extern "C" {
 #define HC_ERR_REDUCTION 7     /* ReductionError (POD)                         */
 
 #define HC_MAX_OCP 32
+#define HC_ROM_MAX_K 160       /* reduced dimension limit (dense LU in shared memory) */
 
 /* MaterialParams (echem/params.py:50-113) + PhysConstants (params.py:26-29). */
 typedef struct hc_params {
@@ -147,6 +148,47 @@ int hc_step_batch(hc_operator* const* ops, int32_t n, double* const* x, double* 
  * G is n_snap x n_snap column-major on the device.  w may be NULL (identity). */
 int hc_pod_gram(const double* S, const double* w, int64_t n_dof, int64_t n_snap, double* G,
                 void* stream);
+
+/* Reduced-order model for the online stage (SPEC mor.build_rom / solve_rom; no
+ * counterpart in the reference tree, whose mor package is not shipped).  All arrays are
+ * device memory.  x = B x~ with B = blockdiag(V_c, V_phi); the first k_c reduced
+ * coordinates belong to V_c.  Dense matrices are row-major. */
+typedef struct hc_rom {
+  int32_t k, k_c;     /* reduced dimension, c-block part                              */
+  int32_t m;          /* empirical-interpolation rows (Eq. 16 points)                 */
+  int32_t n_s;        /* stencil DOFs (full-order DOFs the EI rows and strip faces read) */
+  int32_t n_f;        /* active faces                                                 */
+  int32_t n_pl;       /* plated-lithium slots (inventory carried exactly)             */
+  const double* A;    /* [k][k]  B^T A_lin B                                          */
+  const double* Mr;   /* [k][k]  B^T diag(c rows) B (implicit-Euler mass)            */
+  const double* bnd;  /* [k]     B^T b_bnd (per unit applied current)                 */
+  const double* E;    /* [k][m]  B^T W (W_pi)^-1                                      */
+  const double* BS;   /* [n_s][k] rows of B at the stencil DOFs                       */
+  const int32_t* f_kind;  /* [n_f] 0 BV, 1 counter exchange, 2 stripping, 3 electrolyte-electrolyte */
+  const int32_t* f_dof;   /* [n_f][4] stencil indices: BV (c_gr,c_el,phi_gr,phi_el), CE
+                             (phi_fo,c_el,phi_el,-1), STRIP (phi_pl,c_el,phi_el,-1), ELEL
+                             (c_i,c_j,phi_i,phi_j)                                   */
+  const int32_t* f_slot;  /* [n_f] plated slot of a stripping face, else -1          */
+  const int32_t* row_ptr; /* [m+1] CSR: EI row -> (face, coefficient)                  */
+  const int32_t* row_face;
+  const double* row_coef;
+  const int32_t* pl_ptr;  /* [n_pl+1] CSR: plated slot -> its stripping faces         */
+  const int32_t* pl_face;
+  const double* q_v;      /* [k] B^T (cell-voltage functional)                        */
+  const double* q_ac;     /* [k] B^T (mean solid concentration functional)            */
+} hc_rom;
+
+/* Reduced implicit-Euler trajectory (SPEC mor.solve_rom): n_steps fixed steps of size
+ * dt at applied current mu from the reduced state xt[k] (updated in place) and the
+ * plated inventory n_pl[n_pl] (updated in place), chord Newton with the reduced
+ * Jacobian refreshed every step (and every `refresh` iterations), converged when each
+ * block's update is <= rtol relative.  qoi[2 n_steps] receives (cell voltage, mean
+ * solid concentration) per step, iters[n_steps] the Newton iterations (device).  One
+ * kernel launch runs the whole loop.  HC_ERR_NONCONVERGENCE carries the failing step
+ * in *failed_step. */
+int hc_rom_run(hc_operator* op, const hc_rom* rom, double* xt, double* n_pl, double mu, double dt,
+               int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, double* qoi,
+               int32_t* iters, int32_t* failed_step, void* stream);
 
 /* Evict L2 by streaming a `bytes`-sized buffer through it (reads only, so no dirty
  * lines are left behind); used between timed iterations. */

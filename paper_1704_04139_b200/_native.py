@@ -44,6 +44,13 @@ class HcNewtonStats(ctypes.Structure):
                 ("dt_next", ctypes.c_double), ("clamped_loss", ctypes.c_double)]
 
 
+class HcRom(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("k", "k_c", "m", "n_s", "n_f", "n_pl")] + [
+        (n, ctypes.c_void_p) for n in ("A", "Mr", "bnd", "E", "BS", "f_kind", "f_dof", "f_slot",
+                                       "row_ptr", "row_face", "row_coef", "pl_ptr", "pl_face",
+                                       "q_v", "q_ac")]
+
+
 _ERRORS = {1: NativeError, 2: ModelError, 3: NumericsError, 4: NonConvergence,
            5: ConfigError, 6: SimulationError, 7: ReductionError}
 
@@ -94,6 +101,10 @@ _SIGS = {
                                      ctypes.c_int32]),
     "hc_pod_gram": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                    ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "hc_rom_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HcRom), ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                  ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,0 +1,101 @@
+"""GPU: reduced-order model (BASELINE config 4 pipeline) — offline build on the device,
+online loop in one kernel, checked against the CPU restatement (oracle/rom_oracle.py)
+and against the full-order trajectory it was trained on."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+N_TRAIN = 12
+
+
+@pytest.fixture(scope="module")
+def cell():
+    import paper_1704_04139_b200 as P
+    from paper_1704_04139_b200 import mor
+    from paper_1704_04139_b200.microgen import CellSpec, generate_cell
+    from oracle import fvm_oracle as O
+    spec = CellSpec(16, 16, 32, 14, 4, seed=7, radius_mean=3.0, porosity=0.35, plating_intensity=0.05)
+    grid = generate_cell(spec)
+    params = P.MaterialParams()
+    op = P.SystemOperator(P.build_dofmap(grid), params)
+    h = grid.voxel_size * 1e-6
+    mu = -2.0 * params.c_gr_max * params.constants.F * np.count_nonzero(grid.labels == 1) * h ** 3 \
+        / 3600.0 / (grid.labels.shape[1] * grid.labels.shape[2] * h * h)
+    dt = 1.0
+    cfg = P.SolverConfig(dt_init=dt, dt_max=dt)
+    st = P.prepare_initial_state(op, params, mu, cfg)
+    snaps = mor.collect_snapshots(op, st.x, st.n_pl, mu, dt, N_TRAIN)
+    orc = O.OracleOperator(grid.labels, grid.voxel_size, O.Params())
+    return dict(op=op, orc=orc, st=st, mu=mu, dt=dt, snaps=snaps)
+
+
+def _rom(cell, k, m):
+    from paper_1704_04139_b200 import mor
+    return mor.build_rom(cell["op"], cell["snaps"], k, k, m)
+
+
+def test_pod_rank_orthonormal(cell):
+    from paper_1704_04139_b200 import mor
+    X = cell["snaps"].X
+    V, sig = mor.pod_rank(X[: cell["op"].dof.n_c], 6)
+    G = (V.t() @ V).cpu().numpy()
+    assert np.max(np.abs(G - np.eye(G.shape[0]))) < 1e-12
+    ref = np.linalg.svd(X[: cell["op"].dof.n_c].cpu().numpy(), compute_uv=False)
+    assert np.allclose(sig.cpu().numpy()[:4], ref[:4], rtol=1e-8)
+
+
+def test_deim_blocked_equals_sequential_greedy():
+    from paper_1704_04139_b200 import mor
+    from oracle import rom_oracle as R
+    rng = np.random.default_rng(5)
+    W = rng.standard_normal((3000, 37)) * 10.0 ** -(0.1 * np.arange(37))
+    assert np.array_equal(mor.deim(W, block=8), R.deim(W))
+
+
+def test_ei_exact_at_interpolation_rows(cell):
+    import torch
+    rom = _rom(cell, 6, 10)
+    snaps = cell["snaps"]
+    W, pi = rom.W, torch.as_tensor(rom.pi, device="cuda")
+    for s in (0, N_TRAIN // 2, N_TRAIN):
+        Nx = snaps.N[:, s]
+        coef = torch.linalg.solve(W[pi], Nx[pi])
+        interp = W @ coef
+        assert torch.max(torch.abs(interp[pi] - Nx[pi])) <= 1e-12 * torch.max(torch.abs(Nx[pi]))
+
+
+def test_rom_online_matches_cpu_restatement(cell):
+    from paper_1704_04139_b200 import mor
+    from oracle import rom_oracle as R
+    rom = _rom(cell, 6, 10)
+    xt0 = rom.project(cell["st"].x)
+    npl0 = cell["st"].n_pl
+    n = 6
+    tr = mor.solve_rom(cell["op"], rom, xt0, npl0, cell["mu"], cell["dt"], n)
+    xo, no, qo, io = R.rom_run(cell["orc"], rom.host(), xt0.cpu().numpy(), npl0, cell["mu"], cell["dt"], n)
+    assert np.array_equal(tr.newton_iters, io)
+    xg = tr.xt.cpu().numpy()
+    k_c = rom.k_c
+    assert np.max(np.abs(xg[:k_c] - xo[:k_c])) <= 1e-10 * np.max(np.abs(xo[:k_c]))
+    assert np.max(np.abs(xg[k_c:] - xo[k_c:])) <= 1e-10 * (np.max(np.abs(xo[k_c:])) + 1.0)
+    assert np.allclose(tr.voltage, qo[:, 0], rtol=1e-10, atol=1e-12)
+    assert np.allclose(tr.mean_solid_c, qo[:, 1], rtol=1e-10)
+    if npl0.size:
+        assert np.allclose(tr.n_pl.cpu().numpy()[: npl0.size], no, rtol=1e-10, atol=1e-30)
+
+
+def test_rom_reproduces_training_trajectory(cell):
+    """Training parameter: ROM QoI curves follow the full-order ones (SPEC mor: max
+    relative QoI deviation <= 1e-3)."""
+    from paper_1704_04139_b200 import mor
+    from paper_1704_04139_b200.qoi import qoi_vectors
+    op, snaps = cell["op"], cell["snaps"]
+    rom = _rom(cell, 10, 24)
+    tr = mor.solve_rom(op, rom, rom.project(cell["st"].x), cell["st"].n_pl, cell["mu"], cell["dt"], N_TRAIN)
+    v_cp, v_ac = qoi_vectors(op.dof)
+    X = snaps.X.cpu().numpy()
+    fom_v, fom_ac = v_cp @ X[:, 1:], v_ac @ X[:, 1:]
+    assert np.max(np.abs(tr.voltage - fom_v)) <= 1e-3 * np.max(np.abs(fom_v))
+    assert np.max(np.abs(tr.mean_solid_c - fom_ac) / np.abs(fom_ac)) <= 1e-3
