@@ -181,14 +181,15 @@ typedef struct hc_rom {
 /* Reduced implicit-Euler trajectory (SPEC mor.solve_rom): n_steps fixed steps of size
  * dt at applied current mu from the reduced state xt[k] (updated in place) and the
  * plated inventory n_pl[n_pl] (updated in place), chord Newton with the reduced
- * Jacobian refreshed every step (and every `refresh` iterations), converged when each
- * block's update is <= rtol relative.  qoi[2 n_steps] receives (cell voltage, mean
+ * Jacobian refreshed at the first iteration of every jac_steps-th step (and of a step
+ * following one that needed more than `refresh` iterations) and every `refresh`
+ * iterations inside a step, converged when each block's update is <= rtol relative.  qoi[2 n_steps] receives (cell voltage, mean
  * solid concentration) per step, iters[n_steps] the Newton iterations (device).  One
- * kernel launch runs the whole loop.  HC_ERR_NONCONVERGENCE carries the failing step
+ * kernel launch (one thread-block cluster) runs the whole loop.  HC_ERR_NONCONVERGENCE carries the failing step
  * in *failed_step. */
 int hc_rom_run(hc_operator* op, const hc_rom* rom, double* xt, double* n_pl, double mu, double dt,
-               int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, double* qoi,
-               int32_t* iters, int32_t* failed_step, void* stream);
+               int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
+               double* qoi, int32_t* iters, int32_t* failed_step, void* stream);
 
 /* Evict L2 by streaming a `bytes`-sized buffer through it (reads only, so no dirty
  * lines are left behind); used between timed iterations. */

@@ -66,7 +66,7 @@ def _faces(op, d, xs, npl, beta, need_d):
     return q, dq
 
 
-def rom_run(op, d: dict, xt, npl, mu, dt, n_steps, rtol=1e-10, max_iter=40, refresh=6):
+def rom_run(op, d: dict, xt, npl, mu, dt, n_steps, rtol=1e-10, max_iter=40, refresh=6, jac_steps=8):
     """Same loop as k_rom_run; returns (xt, n_pl, qoi (n_steps, 2), iters)."""
     k, k_c, m = d["k"], d["k_c"], d["m"]
     A, Mr, bnd, E = (d[n].reshape(k, -1) if n != "bnd" else d[n] for n in ("A", "Mr", "bnd", "E"))
@@ -81,12 +81,16 @@ def rom_run(op, d: dict, xt, npl, mu, dt, n_steps, rtol=1e-10, max_iter=40, refr
     qoi = np.zeros((n_steps, 2))
     iters = np.zeros(n_steps, np.int64)
     lu = None
+    since, prev_it = 0, 0
     for step in range(n_steps):
         xo = xt.copy()
         conv = False
         it = 0
+        step_fresh = step == 0 or since >= jac_steps or prev_it > refresh
         while it < max_iter and not conv:
-            fresh = it == 0 or (refresh > 0 and it % refresh == 0)
+            fresh = (it == 0 and step_fresh) or (refresh > 0 and it > 0 and it % refresh == 0)
+            if fresh:
+                since = 0
             xs = BS @ xt
             q, dq = _faces(op, d, xs, npl, beta, fresh)
             N = np.zeros(m)
@@ -109,6 +113,8 @@ def rom_run(op, d: dict, xt, npl, mu, dt, n_steps, rtol=1e-10, max_iter=40, refr
             it += 1
         if not conv:
             raise RuntimeError(f"reduced Newton did not converge at step {step}")
+        since += 1
+        prev_it = it
         xs = BS @ xt
         q, _ = _faces(op, d, xs, npl, beta, False)
         flux = np.zeros(npl.size)

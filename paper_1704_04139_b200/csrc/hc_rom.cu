@@ -14,16 +14,31 @@
 // the stencil, timestepping.py:260-267) and the two QoIs are recorded.  Nothing of
 // full-order length is touched online; per-step cost depends on (k, M, |S|) only.
 //
-// One CTA of 1024 threads runs the loop (there is no grid-wide dependency to
-// distribute at these sizes); every phase is separated by __syncthreads().
+// One thread-block cluster (16 CTAs of 1024 threads where the device schedules it,
+// else 8) runs the loop: the stencil gathers, face kinetics, EI rows, the G and J~ rows
+// are spread over the cluster's SMs, the dense LU / triangular solves run on CTA 0, and
+// the phases are separated by cluster barriers (barrier.cluster, release/acquire).
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "hc_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace hc {
 
 enum : int32_t { RF_BV = 0, RF_CE = 1, RF_STRIP = 2, RF_ELEL = 3 };
 constexpr int ROM_THREADS = 1024;
+constexpr int TK = 16;    // E G panel depth
+constexpr int ROM_ACC = 4; // J~ entries per thread: k <= 160 rows over >= 8 CTAs
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 struct RomDev {
   int k, k_c, m, n_s, n_f, n_pl;
@@ -65,232 +80,314 @@ __device__ void rom_face(const DevParams& P, int kind, const double* xs, const i
   }
 }
 
+struct RomWork {
+  double *x, *xs, *fq, *fdq, *nn, *rr, *G, *J, *npl, *qoi;
+  int32_t *iters, *status;
+};
+
+// acquire loads of values another CTA of the cluster wrote before the last cluster
+// barrier (bypass the non-coherent L1)
+__device__ __forceinline__ double ldc(const double* p) { return __ldcg(p); }
+
 __global__ void __launch_bounds__(ROM_THREADS, 1)
-k_rom_run(DevParams P, RomDev R, double* __restrict__ xt, double* __restrict__ npl, double mu, double dt,
-          double face_area_over_F, int n_steps, double rtol, int max_iter, int refresh,
-          double* __restrict__ xs, double* __restrict__ fq, double* __restrict__ fdq,
-          double* __restrict__ G, double* __restrict__ qoi, int32_t* __restrict__ iters,
-          int32_t* __restrict__ status) {
+k_rom_run(DevParams P, RomDev R, RomWork W, double mu, double dt, double face_area_over_F, int n_steps,
+          double rtol, int max_iter, int refresh, int jac_steps) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), ncta = (int)cl.num_blocks();
   extern __shared__ double sm[];
   const int k = R.k, m = R.m;
-  double* J = sm;                 // [k][k] LU factors
-  double* rr = J + k * k;         // [k] residual / Newton update
+  double* J = sm;                 // [k][k] LU factors (rank 0)
+  double* rr = J + k * k;         // [k] residual / Newton update (rank 0)
   double* xo = rr + k;            // [k] x~ at the start of the step
-  double* nn = xo + k;            // [m] N at the EI rows
-  double* red = nn + m;           // [64] reduction scratch
-  int* piv = reinterpret_cast<int*>(red + 64);   // [k]
+  double* red = xo + k;           // [64] reduction scratch
+  double* sx = red + 64;          // [k] x~ (this CTA's copy)
+  double* pg = sx + k;            // [TK][k] panel of G
+  int* piv = reinterpret_cast<int*>(pg + TK * k);   // [k]
+  int* ctl = piv + k;             // [4] control broadcast inside the CTA
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const int gtid = rank * nt + tid, gnt = ncta * nt;
+  const int gw = rank * nwarp + warp, gnw = ncta * nwarp;
   const double inv_dt = 1.0 / dt, beta = dt * face_area_over_F;
+  int* flag = W.status + 2;       // [2]: converged, finite (written by rank 0)
 
-  auto eval_faces = [&](bool need_d) {
-    for (int i = tid; i < R.n_s; i += nt) {   // x_S = B_S x~
-      const double* b = R.BS + (long long)i * k;
-      double s = 0.0;
-      for (int j = 0; j < k; ++j) s = fma(b[j], xt[j], s);
-      xs[i] = s;
-    }
-    __syncthreads();
-    for (int f = tid; f < R.n_f; f += nt) {
-      double q, d[4];
-      const int sl = R.f_slot[f];
-      rom_face(P, R.f_kind[f], xs, R.f_dof + 4 * f, sl >= 0 ? npl[sl] : 0.0, beta, &q, d);
-      fq[f] = q;
-      if (need_d)
-        for (int c = 0; c < 4; ++c) fdq[4 * f + c] = d[c];
-    }
-    __syncthreads();
-    for (int r = tid; r < m; r += nt) {
-      double s = 0.0;
-      for (int e = R.row_ptr[r]; e < R.row_ptr[r + 1]; ++e) s = fma(R.row_coef[e], fq[R.row_face[e]], s);
-      nn[r] = s;
-    }
+  auto load_x = [&]() {
+    for (int j = tid; j < k; j += nt) sx[j] = ldc(W.x + j);
     __syncthreads();
   };
+  // phases A-C: x_S = B_S x~, face quantities, N at the EI rows (and G when fresh)
+  auto eval = [&](bool need_d, bool need_n) {
+    for (int i = gw; i < R.n_s; i += gnw) {   // warp per row, coalesced
+      const double* b = R.BS + (long long)i * k;
+      double s = 0.0;
+      for (int j = lane; j < k; j += 32) s = fma(b[j], sx[j], s);
+      s = warp_sum(s);
+      if (lane == 0) W.xs[i] = s;
+    }
+    cl.sync();
+    for (int f = gtid; f < R.n_f; f += gnt) {
+      const int* dof = R.f_dof + 4 * f;
+      double xl[4];
+      int dl[4] = {0, 1, 2, 3};
+      for (int c = 0; c < 4; ++c) xl[c] = dof[c] >= 0 ? ldc(W.xs + dof[c]) : 1.0;
+      double q, d[4];
+      const int sl = R.f_slot[f];
+      rom_face(P, R.f_kind[f], xl, dl, sl >= 0 ? ldc(W.npl + sl) : 0.0, beta, &q, d);
+      W.fq[f] = q;
+      if (need_d)
+        for (int c = 0; c < 4; ++c) W.fdq[4 * f + c] = d[c];
+    }
+    cl.sync();
+    if (!need_n) return;
+    for (int r = gtid; r < m; r += gnt) {
+      double s = 0.0;
+      for (int e = R.row_ptr[r]; e < R.row_ptr[r + 1]; ++e) s = fma(R.row_coef[e], ldc(W.fq + R.row_face[e]), s);
+      W.nn[r] = s;
+    }
+    if (need_d)   // G = (dN/dx_S) B_S  (m x k)
+      for (int idx = gtid; idx < m * k; idx += gnt) {
+        const int r = idx / k, j = idx - r * k;
+        double s = 0.0;
+        for (int e = R.row_ptr[r]; e < R.row_ptr[r + 1]; ++e) {
+          const int f = R.row_face[e];
+          double t = 0.0;
+          for (int c = 0; c < 4; ++c) {
+            const int d = R.f_dof[4 * f + c];
+            if (d >= 0) t = fma(ldc(W.fdq + 4 * f + c), R.BS[(long long)d * k + j], t);
+          }
+          s = fma(R.row_coef[e], t, s);
+        }
+        W.G[idx] = s;
+      }
+    cl.sync();
+  };
 
+  load_x();
+  int since = 0, prev_it = 0;
   for (int step = 0; step < n_steps; ++step) {
-    for (int j = tid; j < k; j += nt) xo[j] = xt[j];
+    for (int j = tid; j < k; j += nt) xo[j] = sx[j];
     __syncthreads();
+    // chord Newton: the reduced Jacobian is refreshed at the first iteration of a step
+    // every jac_steps steps (or after a slow step), and every `refresh` iterations
+    bool step_fresh = step == 0 || since >= jac_steps || prev_it > refresh;
     bool conv = false;
     int it = 0;
     for (; it < max_iter && !conv; ++it) {
-      const bool fresh = it == 0 || (refresh > 0 && it % refresh == 0);
-      eval_faces(fresh);
-      // r~ = M~ (x~ - x~_old)/dt + A~ x~ + mu b~ + E N
-      for (int i = tid; i < k; i += nt) {
+      const bool fresh = (it == 0 && step_fresh) || (refresh > 0 && it > 0 && it % refresh == 0);
+      if (fresh) since = 0;
+      eval(fresh, true);
+      // phase D: r~ rows (warp per row) and, when fresh, J~ rows through G panels
+      for (int i = gw; i < k; i += gnw) {
         const double* a = R.A + (long long)i * k;
         const double* mr = R.Mr + (long long)i * k;
-        double s = mu * R.bnd[i];
-        for (int j = 0; j < k; ++j) s = fma(a[j], xt[j], fma(mr[j] * inv_dt, xt[j] - xo[j], s));
+        double s = 0.0;
+        for (int j = lane; j < k; j += 32) s = fma(a[j], sx[j], fma(mr[j] * inv_dt, sx[j] - xo[j], s));
         const double* e = R.E + (long long)i * m;
-        for (int r = 0; r < m; ++r) s = fma(e[r], nn[r], s);
-        rr[i] = s;
+        for (int r = lane; r < m; r += 32) s = fma(e[r], ldc(W.nn + r), s);
+        s = warp_sum(s);
+        if (lane == 0) W.rr[i] = s + mu * R.bnd[i];
       }
       if (fresh) {
-        // G = (dN/dx_S) B_S  (m x k), then J~ = M~/dt + A~ + E G, LU in shared memory
-        for (int idx = tid; idx < m * k; idx += nt) {
-          const int r = idx / k, j = idx - r * k;
-          double s = 0.0;
-          for (int e = R.row_ptr[r]; e < R.row_ptr[r + 1]; ++e) {
-            const int f = R.row_face[e];
-            double t = 0.0;
-            for (int c = 0; c < 4; ++c) {
-              const int d = R.f_dof[4 * f + c];
-              if (d >= 0) t = fma(fdq[4 * f + c], R.BS[(long long)d * k + j], t);
-            }
-            s = fma(R.row_coef[e], t, s);
+        const int my_rows = (k - rank + ncta - 1) / ncta;   // rows i = rank + t ncta
+        double acc[ROM_ACC] = {};
+        for (int r0 = 0; r0 < m; r0 += TK) {
+          const int tk = min(TK, m - r0);
+          __syncthreads();
+          for (int idx = tid; idx < TK * k; idx += nt) {
+            const int r = idx / k;
+            pg[idx] = r < tk ? ldc(W.G + (long long)(r0 + r) * k + (idx - r * k)) : 0.0;
           }
-          G[idx] = s;
+          __syncthreads();
+#pragma unroll
+          for (int h = 0; h < ROM_ACC; ++h) {
+            const int idx = tid + h * nt;
+            if (idx < my_rows * k) {
+              const int i = rank + (idx / k) * ncta, j = idx % k;
+              const double* e = R.E + (long long)i * m + r0;
+              double a2 = 0.0;
+              for (int r = 0; r < tk; ++r) a2 = fma(e[r], pg[r * k + j], a2);
+              acc[h] += a2;
+            }
+          }
         }
-        __syncthreads();
-        for (int idx = tid; idx < k * k; idx += nt) {
-          const int i = idx / k, j = idx - i * k;
-          double s = R.A[idx] + R.Mr[idx] * inv_dt;
-          const double* e = R.E + (long long)i * m;
-          for (int r = 0; r < m; ++r) s = fma(e[r], G[(long long)r * k + j], s);
-          J[idx] = s;
-        }
-        __syncthreads();
-        for (int c = 0; c < k; ++c) {   // LU with partial pivoting (column c)
-          if (tid < 32) {
-            double best = -1.0;
-            int bi = c;
-            for (int i = c + tid; i < k; i += 32) {
-              const double v = fabs(J[i * k + c]);
-              if (v > best) { best = v; bi = i; }
-            }
-            for (int o = 16; o; o >>= 1) {
-              const double ob = __shfl_down_sync(0xffffffffu, best, o);
-              const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-              if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-            }
-            if (tid == 0) piv[c] = bi;
+#pragma unroll
+        for (int h = 0; h < ROM_ACC; ++h) {
+          const int idx = tid + h * nt;
+          if (idx < my_rows * k) {
+            const int i = rank + (idx / k) * ncta, j = idx % k;
+            W.J[i * k + j] = R.A[i * k + j] + R.Mr[i * k + j] * inv_dt + acc[h];
           }
-          __syncthreads();
-          const int p = piv[c];
-          if (p != c)
-            for (int j = tid; j < k; j += nt) {
-              const double t = J[c * k + j];
-              J[c * k + j] = J[p * k + j];
-              J[p * k + j] = t;
-            }
-          __syncthreads();
-          const double d = J[c * k + c];
-          for (int idx = tid; idx < (k - c - 1) * (k - c); idx += nt) {
-            const int i = c + 1 + idx / (k - c), j = c + idx % (k - c);
-            const double l = J[i * k + c] / d;
-            if (j == c) continue;
-            J[i * k + j] = fma(-l, J[c * k + j], J[i * k + j]);
-          }
-          __syncthreads();
-          for (int i = c + 1 + tid; i < k; i += nt) J[i * k + c] /= d;
-          __syncthreads();
         }
       }
-      __syncthreads();
-      // solve J delta = r (pivots, forward, backward) on one warp, then x~ -= delta
-      if (tid < 32) {
-        for (int c = 0; c < k; ++c) {
-          const int p = piv[c];
-          if (p != c && tid == 0) {
-            const double t = rr[c];
-            rr[c] = rr[p];
-            rr[p] = t;
+      cl.sync();
+      // phase E (rank 0): LU when fresh, solve, update x~, convergence flags
+      if (rank == 0) {
+        if (fresh) {
+          for (int idx = tid; idx < k * k; idx += nt) J[idx] = ldc(W.J + idx);
+          __syncthreads();
+          for (int c = 0; c < k; ++c) {   // LU with partial pivoting (column c)
+            if (tid < 32) {
+              double best = -1.0;
+              int bi = c;
+              for (int i = c + tid; i < k; i += 32) {
+                const double v = fabs(J[i * k + c]);
+                if (v > best) { best = v; bi = i; }
+              }
+              for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_down_sync(0xffffffffu, best, o);
+                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+              }
+              if (tid == 0) piv[c] = bi;
+            }
+            __syncthreads();
+            const int p = piv[c];
+            if (p != c)
+              for (int j = tid; j < k; j += nt) {
+                const double t = J[c * k + j];
+                J[c * k + j] = J[p * k + j];
+                J[p * k + j] = t;
+              }
+            __syncthreads();
+            const double d = J[c * k + c];
+            for (int idx = tid; idx < (k - c - 1) * (k - c); idx += nt) {
+              const int i = c + 1 + idx / (k - c), j = c + idx % (k - c);
+              if (j == c) continue;
+              J[i * k + j] = fma(-(J[i * k + c] / d), J[c * k + j], J[i * k + j]);
+            }
+            __syncthreads();
+            for (int i = c + 1 + tid; i < k; i += nt) J[i * k + c] /= d;
+            __syncthreads();
           }
         }
-        __syncwarp();
-        for (int c = 0; c < k; ++c) {
-          const double v = rr[c];
-          for (int i = c + 1 + tid; i < k; i += 32) rr[i] = fma(-J[i * k + c], v, rr[i]);
+        if (tid < 32) {   // pivots, forward, backward on one warp
+          for (int j = tid; j < k; j += 32) rr[j] = ldc(W.rr + j);
           __syncwarp();
-        }
-        for (int c = k - 1; c >= 0; --c) {
-          if (tid == 0) rr[c] /= J[c * k + c];
+          if (tid == 0)
+            for (int c = 0; c < k; ++c) {
+              const int p = piv[c];
+              if (p != c) { const double t = rr[c]; rr[c] = rr[p]; rr[p] = t; }
+            }
           __syncwarp();
-          const double v = rr[c];
-          for (int i = tid; i < c; i += 32) rr[i] = fma(-J[i * k + c], v, rr[i]);
-          __syncwarp();
+          for (int c = 0; c < k; ++c) {
+            const double v = rr[c];
+            for (int i = c + 1 + tid; i < k; i += 32) rr[i] = fma(-J[i * k + c], v, rr[i]);
+            __syncwarp();
+          }
+          for (int c = k - 1; c >= 0; --c) {
+            if (tid == 0) rr[c] /= J[c * k + c];
+            __syncwarp();
+            const double v = rr[c];
+            for (int i = tid; i < c; i += 32) rr[i] = fma(-J[i * k + c], v, rr[i]);
+            __syncwarp();
+          }
+          // convergence per block: |delta_c| <= rtol |x~_c|, |delta_p| <= rtol (|x~_p| + 1)
+          double dc = 0.0, xc = 0.0, dp = 0.0, xp = 0.0;
+          for (int j = tid; j < k; j += 32) {
+            const double d = rr[j], x = sx[j] - d;
+            if (j < R.k_c) { dc += d * d; xc += x * x; } else { dp += d * d; xp += x * x; }
+          }
+          dc = warp_sum(dc); xc = warp_sum(xc); dp = warp_sum(dp); xp = warp_sum(xp);
+          for (int j = tid; j < k; j += 32) W.x[j] = sx[j] - rr[j];
+          if (tid == 0) {
+            flag[0] = sqrt(dc) <= rtol * sqrt(xc) && sqrt(dp) <= rtol * (sqrt(xp) + 1.0);
+            flag[1] = dc == dc && dp == dp;
+          }
         }
       }
-      __syncthreads();
-      // convergence per block: |delta_c| <= rtol |x~_c| and |delta_p| <= rtol (|x~_p| + 1)
-      if (tid < 32) {
-        double dc = 0.0, xc = 0.0, dp = 0.0, xp = 0.0;
-        for (int j = tid; j < k; j += 32) {
-          const double d = rr[j], x = xt[j] - d;
-          if (j < R.k_c) { dc += d * d; xc += x * x; } else { dp += d * d; xp += x * x; }
-        }
-        for (int o = 16; o; o >>= 1) {
-          dc += __shfl_down_sync(0xffffffffu, dc, o);
-          xc += __shfl_down_sync(0xffffffffu, xc, o);
-          dp += __shfl_down_sync(0xffffffffu, dp, o);
-          xp += __shfl_down_sync(0xffffffffu, xp, o);
-        }
-        if (tid == 0) {
-          const bool ok = sqrt(dc) <= rtol * sqrt(xc) && sqrt(dp) <= rtol * (sqrt(xp) + 1.0);
-          red[0] = ok ? 1.0 : 0.0;
-          red[1] = (dc == dc && dp == dp) ? 1.0 : 0.0;
-        }
+      cl.sync();
+      if (tid == 0) {
+        ctl[0] = __ldcg(flag);
+        ctl[1] = __ldcg(flag + 1);
       }
-      __syncthreads();
-      for (int j = tid; j < k; j += nt) xt[j] -= rr[j];
-      conv = red[0] != 0.0;
-      const bool finite = red[1] != 0.0;
-      __syncthreads();
-      if (!finite) {
-        if (tid == 0) { status[0] = 2; status[1] = step; }
+      load_x();   // (includes the CTA barrier that publishes ctl)
+      conv = ctl[0] != 0;
+      if (!ctl[1]) {
+        if (rank == 0 && tid == 0) { W.status[0] = 2; W.status[1] = step; }
         return;
       }
     }
     if (!conv) {
-      if (tid == 0) { status[0] = 1; status[1] = step; }
+      if (rank == 0 && tid == 0) { W.status[0] = 1; W.status[1] = step; }
       return;
     }
+    ++since;
+    prev_it = it;
     // exact plated-inventory update at the converged state (n_pl is not reduced)
-    eval_faces(false);
-    for (int s = tid; s < R.n_pl; s += nt) {
+    eval(false, false);
+    for (int s = gtid; s < R.n_pl; s += gnt) {
       double flux = 0.0;
-      for (int e = R.pl_ptr[s]; e < R.pl_ptr[s + 1]; ++e) flux += fq[R.pl_face[e]] / P.sc * face_area_over_F;
-      npl[s] = fmax(npl[s] - dt * flux, 0.0);
+      for (int e = R.pl_ptr[s]; e < R.pl_ptr[s + 1]; ++e) flux += ldc(W.fq + R.pl_face[e]) / P.sc * face_area_over_F;
+      W.npl[s] = fmax(ldc(W.npl + s) - dt * flux, 0.0);
     }
-    if (tid < 32) {   // QoIs are linear functionals of x~
+    if (rank == 0 && tid < 32) {   // QoIs are linear functionals of x~
       double v = 0.0, c = 0.0;
       for (int j = tid; j < k; j += 32) {
-        v = fma(R.q_v[j], xt[j], v);
-        c = fma(R.q_ac[j], xt[j], c);
+        v = fma(R.q_v[j], sx[j], v);
+        c = fma(R.q_ac[j], sx[j], c);
       }
-      for (int o = 16; o; o >>= 1) {
-        v += __shfl_down_sync(0xffffffffu, v, o);
-        c += __shfl_down_sync(0xffffffffu, c, o);
-      }
+      v = warp_sum(v);
+      c = warp_sum(c);
       if (tid == 0) {
-        qoi[2 * step] = v;
-        qoi[2 * step + 1] = c;
-        iters[step] = it;
+        W.qoi[2 * step] = v;
+        W.qoi[2 * step + 1] = c;
+        W.iters[step] = it;
       }
     }
-    __syncthreads();
+    cl.sync();
   }
-  if (tid == 0) { status[0] = 0; status[1] = n_steps; }
+  if (rank == 0 && tid == 0) { W.status[0] = 0; W.status[1] = n_steps; }
 }
 
 void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, double mu, double dt,
-             int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, double* qoi,
-             int32_t* iters, int32_t* status_host, cudaStream_t s) {
+             int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
+             double* qoi, int32_t* iters, int32_t* status_host, cudaStream_t s) {
   RomDev R{rom->k, rom->k_c, rom->m, rom->n_s, rom->n_f, rom->n_pl, rom->A, rom->Mr, rom->bnd,
            rom->E, rom->BS, rom->row_coef, rom->q_v, rom->q_ac, rom->f_kind, rom->f_dof, rom->f_slot,
            rom->row_ptr, rom->row_face, rom->pl_ptr, rom->pl_face};
   if (R.k < 1 || R.k > HC_ROM_MAX_K || R.m < 0 || R.n_s < 0 || R.n_f < 0 || R.k_c < 0 || R.k_c > R.k)
     throw Error(HC_ERR_ARGUMENT, "reduced model dimensions out of range");
   DBuf<double> xs(std::max(R.n_s, 1)), fq(std::max(R.n_f, 1)), fdq(4LL * std::max(R.n_f, 1)),
-      G((long long)std::max(R.m, 1) * R.k);
-  DBuf<int32_t> st(2);
-  const size_t smem = ((size_t)R.k * R.k + 2 * R.k + R.m + 64) * sizeof(double) + R.k * sizeof(int);
+      nn(std::max(R.m, 1)), rr(R.k), G((long long)std::max(R.m, 1) * R.k), J((long long)R.k * R.k);
+  DBuf<int32_t> st(4);
+  HC_CUDA(cudaMemsetAsync(st.p, 0, 4 * sizeof(int32_t), s));
+  RomWork W{xt, xs.p, fq.p, fdq.p, nn.p, rr.p, G.p, J.p, npl, qoi, iters, st.p};
+  const size_t smem = ((size_t)R.k * R.k + 3 * R.k + 64 + (size_t)TK * R.k) * sizeof(double) +
+                      (R.k + 4) * sizeof(int);
   HC_CUDA(cudaFuncSetAttribute(k_rom_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static int cluster = 0;   // largest cluster the device schedules (16 non-portable, else 8)
+  if (!cluster) {
+    cluster = 8;
+    if (cudaFuncSetAttribute(k_rom_run, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(ROM_THREADS);
+      q.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 16; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+      q.attrs = &at;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, k_rom_run, &q) == cudaSuccess && n >= 1) cluster = 16;
+    }
+    cudaGetLastError();
+    if (const char* e = getenv("HC_ROM_CLUSTER")) cluster = atoi(e) >= 16 ? 16 : 8;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(ROM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = cluster; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
   const double fa_F = op.info.face_area / op.host_params.faraday;
-  k_rom_run<<<1, ROM_THREADS, smem, s>>>(op.P, R, xt, npl, mu, dt, fa_F, n_steps, rtol, max_iter, refresh,
-                                         xs.p, fq.p, fdq.p, G.p, qoi, iters, st.p);
+  HC_CUDA(cudaLaunchKernelEx(&cfg, k_rom_run, op.P, R, W, mu, dt, fa_F, (int)n_steps, rtol, (int)max_iter,
+                             (int)refresh, (int)jac_steps));
   HC_COUNT();
-  HC_CHECK_LAUNCH();
   HC_CUDA(cudaMemcpyAsync(status_host, st.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   HC_CUDA(cudaStreamSynchronize(s));
 }

@@ -301,8 +301,10 @@ class RomTrajectory:
 
 
 def solve_rom(op, rom: ReducedModel, xt0, n_pl0, mu: float, dt: float, n_steps: int,
-              rtol: float = 1e-10, max_iter: int = 40, refresh: int = 6) -> RomTrajectory:
-    """Reduced implicit-Euler trajectory, one kernel launch (hc_rom_run)."""
+              rtol: float = 1e-10, max_iter: int = 40, refresh: int = 6,
+              jac_steps: int = 8) -> RomTrajectory:
+    """Reduced implicit-Euler trajectory, one kernel launch (hc_rom_run); the reduced
+    Jacobian is refreshed every ``jac_steps`` steps (chord Newton in between)."""
     t = _dev.torch()
     xt = _dev.to_dev(xt0).clone()
     npl = _dev.to_dev(n_pl0 if np.size(n_pl0) else np.zeros(1)).clone()
@@ -311,7 +313,8 @@ def solve_rom(op, rom: ReducedModel, xt0, n_pl0, mu: float, dt: float, n_steps: 
     failed = ctypes.c_int32(-1)
     code = _native.lib().hc_rom_run(op.native.handle, ctypes.byref(rom.struct), _dev.ptr(xt),
                                     _dev.ptr(npl), float(mu), float(dt), int(n_steps), float(rtol),
-                                    int(max_iter), int(refresh), _dev.ptr(qoi), _dev.ptr(its),
+                                    int(max_iter), int(refresh), int(jac_steps), _dev.ptr(qoi),
+                                    _dev.ptr(its),
                                     ctypes.byref(failed), _dev.stream())
     if code:
         try:
