@@ -18,6 +18,8 @@
 // every linearization by deterministic per-row kernels (no atomics).  The fine level
 // is applied matrix-free (jvp kernels); its CSR copy only feeds the first Galerkin
 // product.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -30,6 +32,8 @@
 
 #include "hc_amg.cuh"
 #include "hc_stencil.cuh"
+
+namespace cg = cooperative_groups;
 #include "hc_tma.cuh"
 
 namespace hc {
@@ -61,6 +65,7 @@ __global__ void k_assemble0(DevParams P, int field, const uint8_t* __restrict__ 
                             const double* __restrict__ coef, long long n_if, double inv_dt,
                             const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             double* __restrict__ val, double* __restrict__ dinv) {
+  pdl_wait();
   int x, y, z, v;
   if (!vox_index(P, x, y, z, v)) return;
   int r0 = rp[v], r1 = rp[v + 1];
@@ -123,6 +128,7 @@ __global__ void k_assemble0(DevParams P, int field, const uint8_t* __restrict__ 
 
 __global__ void k_dinv(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                        const double* __restrict__ v, double* __restrict__ dinv) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double d = 0.0;
@@ -140,6 +146,7 @@ __global__ void k_smooth_P(int n, int smooth, double w, const int32_t* __restric
                            const double* __restrict__ dinv, const int32_t* __restrict__ parent,
                            const int32_t* __restrict__ prp, const int32_t* __restrict__ pci,
                            double* __restrict__ pv) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int p0 = prp[i], p1 = prp[i + 1];
@@ -158,6 +165,7 @@ __global__ void k_ap(int n, const int32_t* __restrict__ arp, const int32_t* __re
                      const int32_t* __restrict__ pci, const double* __restrict__ pv,
                      const int32_t* __restrict__ qrp, const int32_t* __restrict__ qci,
                      double* __restrict__ qv) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int r0 = qrp[i], r1 = qrp[i + 1];
@@ -176,6 +184,7 @@ __global__ void k_ptap(int n_next, const int32_t* __restrict__ pt_ptr,
                        const int32_t* __restrict__ qci, const double* __restrict__ qv,
                        const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
                        double* __restrict__ nv) {
+  pdl_wait();
   int I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= n_next) return;
   int r0 = nrp[I], r1 = nrp[I + 1];
@@ -190,6 +199,7 @@ __global__ void k_ptap(int n_next, const int32_t* __restrict__ pt_ptr,
 // ---- coarsest level: dense LU with partial pivoting in one CTA --------------
 __global__ void k_dense_from_csr(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ cl,
                                  const double* __restrict__ v, double* __restrict__ A) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   for (int j = 0; j < n; ++j) A[(long long)i * n + j] = 0.0;
@@ -199,6 +209,7 @@ __global__ void k_dense_from_csr(int n, const int32_t* __restrict__ rp, const in
 // coarsest level: LU with partial pivoting in shared memory, then the explicit
 // inverse (one thread per column), so every coarse solve is one dense mat-vec
 __global__ void k_dense_inverse(int n, const double* __restrict__ A, double* __restrict__ Ainv) {
+  pdl_wait();
   extern __shared__ double sm[];
   double* M = sm;                         // n x n
   int* perm = (int*)(sm + (size_t)n * n);
@@ -255,6 +266,7 @@ __global__ void k_dense_inverse(int n, const double* __restrict__ A, double* __r
 // x = Ainv b, one warp per row
 __global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const double* __restrict__ b,
                                double* __restrict__ x) {
+  pdl_wait();
   int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
   if (row >= n) return;
   double s = 0.0;
@@ -268,6 +280,7 @@ __device__ __forceinline__ double fld(const double2& a, int f) { return f ? a.y 
 
 __global__ void k_fine_smooth0(long long n, int f, double w, const double* __restrict__ dinv,
                                const double2* __restrict__ r, double2* __restrict__ e) {
+  pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= n) return;
   double val = w * dinv[v] * fld(r[v], f);
@@ -277,6 +290,7 @@ __global__ void k_fine_smooth0(long long n, int f, double w, const double* __res
 __global__ void k_fine_smooth(long long n, int f, double w, const double* __restrict__ dinv,
                               const double2* __restrict__ r, const double2* __restrict__ t,
                               double2* __restrict__ e) {
+  pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= n) return;
   double d = w * dinv[v] * (fld(r[v], f) - fld(t[v], f));
@@ -288,6 +302,7 @@ __global__ void k_fine_restrict(int n1, int f, const int32_t* __restrict__ pt_pt
                                 const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
                                 const double* __restrict__ pv, const double2* __restrict__ r,
                                 const double2* __restrict__ t, double* __restrict__ b1) {
+  pdl_wait();
   int I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= n1) return;
   double s = 0.0;
@@ -302,6 +317,7 @@ __global__ void k_fine_restrict(int n1, int f, const int32_t* __restrict__ pt_pt
 __global__ void k_fine_prolong(long long n, int f, double alpha, const int32_t* __restrict__ prp,
                                const int32_t* __restrict__ pci, const double* __restrict__ pv,
                                const double* __restrict__ x1, double2* __restrict__ e) {
+  pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= n) return;
   int p0 = prp[v], p1 = prp[v + 1];
@@ -313,11 +329,13 @@ __global__ void k_fine_prolong(long long n, int f, double alpha, const int32_t* 
 
 __global__ void k_csr_smooth0(int n, double w, const double* __restrict__ dinv,
                               const double* __restrict__ b, double* __restrict__ x) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = w * dinv[i] * b[i];
 }
 
 __global__ void k_to_float(long long n, const double* __restrict__ a, float* __restrict__ b) {
+  pdl_wait();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) b[i] = (float)a[i];
 }
@@ -328,6 +346,7 @@ __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
                                const int32_t* __restrict__ cl, const VT* __restrict__ v,
                                const double* __restrict__ dinv, const double* __restrict__ b,
                                const double* __restrict__ x, double* __restrict__ y, int resid) {
+  pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int i = (int)(gt / VS), lane = (int)(gt % VS);
   if (i >= n) return;
@@ -360,6 +379,7 @@ __global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict
                         const double* __restrict__ dinv, const double* __restrict__ b,
                         const double* __restrict__ x, const int32_t* __restrict__ parent,
                         const double* __restrict__ xc, double* __restrict__ y, int resid) {
+  pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int i = (int)(gt / VS), lane = (int)(gt % VS);
   if (i >= n) return;
@@ -382,6 +402,7 @@ __global__ void k_csr_jacobi(int n, double w, const int32_t* __restrict__ rp,
                              const int32_t* __restrict__ cl, const double* __restrict__ v,
                              const double* __restrict__ dinv, const double* __restrict__ b,
                              const double* __restrict__ x, double* __restrict__ y) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = b[i];
@@ -392,6 +413,7 @@ __global__ void k_csr_jacobi(int n, double w, const int32_t* __restrict__ rp,
 __global__ void k_csr_resid(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ cl,
                             const double* __restrict__ v, const double* __restrict__ b,
                             const double* __restrict__ x, double* __restrict__ res) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = b[i];
@@ -403,6 +425,7 @@ __global__ void k_csr_restrict(int n_next, const int32_t* __restrict__ pt_ptr,
                                const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
                                const double* __restrict__ pv, const double* __restrict__ res,
                                double* __restrict__ b_next) {
+  pdl_wait();
   int I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= n_next) return;
   double s = 0.0;
@@ -413,6 +436,7 @@ __global__ void k_csr_restrict(int n_next, const int32_t* __restrict__ pt_ptr,
 __global__ void k_csr_prolong(int n, double alpha, const int32_t* __restrict__ prp,
                               const int32_t* __restrict__ pci, const double* __restrict__ pv,
                               const double* __restrict__ xn, double* __restrict__ x) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -421,6 +445,7 @@ __global__ void k_csr_prolong(int n, double alpha, const int32_t* __restrict__ p
 }
 
 __global__ void k_vec_add(int n, const double* __restrict__ a, double* __restrict__ x) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] += a[i];
 }
@@ -429,6 +454,7 @@ __global__ void k_vec_add(int n, const double* __restrict__ a, double* __restric
 __global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
                              const int32_t* __restrict__ pt_row, const double* __restrict__ ptv,
                              const double* __restrict__ res, double* __restrict__ b1) {
+  pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int I = (int)(gt >> 3), lane = (int)(gt & 7);
   if (I >= n1) return;
@@ -441,6 +467,7 @@ __global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
 }
 __global__ void k_gather_ptv(long long n, const int32_t* __restrict__ pt_idx,
                              const double* __restrict__ pv, double* __restrict__ ptv) {
+  pdl_wait();
   long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (q < n) ptv[q] = pv[pt_idx[q]];
 }
@@ -706,6 +733,37 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
                                  " coarsest unknowns (limit " + std::to_string(HC_COARSE_MAX) + ")");
   B.dense.alloc((size_t)std::max(nc, 1) * std::max(nc, 1));
   B.dense_inv.alloc((size_t)std::max(nc, 1) * std::max(nc, 1));
+  // cluster-fused tail of the cycle: the deepest run of CSR levels that are all small
+  // (and plain V-cycle levels), if it spans at least two levels
+  const int nl = (int)B.levels.size();
+  int from = nl - 1;
+  while (from - 1 >= 1) {
+    const AmgLevel& L = B.levels[from - 1];
+    const bool wcyc = cfg.gamma > 1 && from - 1 >= cfg.wmin && from - 1 <= cfg.wdepth;
+    if (L.n > cfg.fuse_rows || L.A.nnz > cfg.fuse_nnz || wcyc) break;
+    --from;
+  }
+  B.fuse_from = (cfg.fuse_rows > 0 && from <= nl - 2) ? from : -1;
+  if (B.fuse_from >= 1) {
+    std::vector<CoarseLev> h;
+    for (int l = B.fuse_from; l < nl; ++l) {
+      AmgLevel& L = B.levels[l];
+      CoarseLev c{};
+      c.n = L.n;
+      c.rp = L.A.rp.p; c.ci = L.A.ci.p;
+      c.vf = cfg.fp32_coarse ? L.A.vf.p : nullptr;
+      c.vd = L.A.v.p;
+      c.dinv = L.dinv.p;
+      c.b = L.b.p; c.x = L.x.p; c.x2 = L.x2.p; c.res = L.res.p;
+      c.tentative = L.P.nnz == (long long)L.n;
+      c.parent = L.parent.p;
+      c.prp = L.P.rp.p; c.pci = L.P.ci.p; c.pv = L.P.v.p;
+      c.pt_ptr = L.pt_ptr.p; c.pt_row = L.pt_row.p; c.ptv = L.ptv.p;
+      h.push_back(c);
+    }
+    B.clev.alloc(h.size());
+    HC_CUDA(cudaMemcpy(B.clev.p, h.data(), h.size() * sizeof(CoarseLev), cudaMemcpyHostToDevice));
+  }
 }
 
 Amg* build_amg(const Operator& op) {
@@ -713,8 +771,7 @@ Amg* build_amg(const Operator& op) {
   std::vector<uint8_t> lab(nvox);
   HC_CUDA(cudaMemcpy(lab.data(), op.labels.p, nvox, cudaMemcpyDeviceToHost));
   auto amg = std::make_unique<Amg>();
-  if (const char* e = getenv("HC_AMG_NU")) amg->nu = atoi(e);
-  amg->nu_c = amg->nu;
+  if (const char* e = getenv("HC_AMG_NU")) amg->nu = amg->nu_c = atoi(e);
   if (const char* e = getenv("HC_AMG_NU_C")) amg->nu_c = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_C")) amg->sa_levels_c = atoi(e);
   if (const char* e = getenv("HC_AMG_OMEGA")) amg->omega = atof(e);
@@ -730,6 +787,8 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_FP32")) amg->fp32_coarse = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_CF")) amg->coarsen = std::max(2, atoi(e));
   if (const char* e = getenv("HC_AMG_REFRESH_SOLVES")) amg->refresh_solves = std::max(1, atoi(e));
+  if (const char* e = getenv("HC_AMG_FUSE_ROWS")) amg->fuse_rows = atoi(e);
+  if (const char* e = getenv("HC_AMG_FUSE_NNZ")) amg->fuse_nnz = atoll(e);
   auto t0 = std::chrono::steady_clock::now();
   build_block(op, lab, 0, *amg, amg->blk[0]);
   build_block(op, lab, 1, *amg, amg->blk[1]);
@@ -753,37 +812,37 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
     if (!(blocks & (1 << f))) continue;
     AmgBlock& B = A.blk[f];
     AmgLevel& L0 = B.levels[0];
-    k_assemble0<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, f, op.labels.p, op.if_rank.p, op.if_dir.p,
+    launch(k_assemble0, vox_grid(op.P), vox_block(), 0, s, op.P, f, op.labels.p, op.if_rank.p, op.if_dir.p,
                                                 op.if_solid.p, op.if_kind.p, op.if_coef.p, op.n_if,
                                                 inv_dt, L0.A.rp.p, L0.A.ci.p, L0.A.v.p, L0.dinv.p); HC_COUNT();
     for (size_t l = 0; l + 1 < B.levels.size(); ++l) {
       AmgLevel& L = B.levels[l];
       AmgLevel& U = B.levels[l + 1];
       if (l > 0) {
-        k_dinv<<<nblk(L.n), TPB, 0, s>>>(L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p); HC_COUNT();
+        launch(k_dinv, nblk(L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p); HC_COUNT();
       }
-      k_smooth_P<<<nblk(L.n), TPB, 0, s>>>(L.n, (int)l < (f == 0 ? A.sa_levels_c : A.sa_levels), A.omega_p, L.A.rp.p, L.A.ci.p,
+      launch(k_smooth_P, nblk(L.n), TPB, 0, s, L.n, (int)l < (f == 0 ? A.sa_levels_c : A.sa_levels), A.omega_p, L.A.rp.p, L.A.ci.p,
                                            L.A.v.p, L.dinv.p, L.parent.p, L.P.rp.p, L.P.ci.p,
                                            L.P.v.p); HC_COUNT();
-      k_gather_ptv<<<nblk((long long)L.P.nnz), TPB, 0, s>>>((long long)L.P.nnz, L.pt_idx.p, L.P.v.p,
+      launch(k_gather_ptv, nblk((long long)L.P.nnz), TPB, 0, s, (long long)L.P.nnz, L.pt_idx.p, L.P.v.p,
                                                            L.ptv.p); HC_COUNT();
-      k_ap<<<nblk(L.n), TPB, 0, s>>>(L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.P.rp.p, L.P.ci.p, L.P.v.p,
+      launch(k_ap, nblk(L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.P.rp.p, L.P.ci.p, L.P.v.p,
                                      L.AP.rp.p, L.AP.ci.p, L.AP.v.p); HC_COUNT();
-      k_ptap<<<nblk(U.n, 128), 128, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p, L.P.v.p,
+      launch(k_ptap, nblk(U.n, 128), 128, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p, L.P.v.p,
                                             L.AP.rp.p, L.AP.ci.p, L.AP.v.p, U.A.rp.p, U.A.ci.p,
                                             U.A.v.p); HC_COUNT();
     }
     for (size_t l = 1; l < B.levels.size(); ++l) {
       AmgLevel& L = B.levels[l];
       if (A.fp32_coarse && L.A.nnz) {
-        k_to_float<<<nblk(L.A.nnz), TPB, 0, s>>>(L.A.nnz, L.A.v.p, L.A.vf.p); HC_COUNT();
+        launch(k_to_float, nblk(L.A.nnz), TPB, 0, s, L.A.nnz, L.A.v.p, L.A.vf.p); HC_COUNT();
       }
     }
     AmgLevel& C = B.levels.back();
     if (B.levels.size() > 1) {
-      k_dinv<<<nblk(C.n), TPB, 0, s>>>(C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, C.dinv.p); HC_COUNT();
+      launch(k_dinv, nblk(C.n), TPB, 0, s, C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, C.dinv.p); HC_COUNT();
     }
-    k_dense_from_csr<<<nblk(C.n), TPB, 0, s>>>(C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, B.dense.p); HC_COUNT();
+    launch(k_dense_from_csr, nblk(C.n), TPB, 0, s, C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, B.dense.p); HC_COUNT();
     size_t smem = (size_t)C.n * C.n * sizeof(double) + (size_t)C.n * sizeof(int);
     static bool attr = false;
     if (!attr) {
@@ -791,9 +850,179 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
                                    (int)((size_t)HC_COARSE_MAX * HC_COARSE_MAX * 8 + HC_COARSE_MAX * 4)));
       attr = true;
     }
-    k_dense_inverse<<<1, 256, smem, s>>>(C.n, B.dense.p, B.dense_inv.p); HC_COUNT();
+    launch(k_dense_inverse, 1, 256, smem, s, C.n, B.dense.p, B.dense_inv.p); HC_COUNT();
     HC_CHECK_LAUNCH();
   }
+}
+
+// ---- cluster-fused coarse cycle ----------------------------------------------------
+// The levels below fuse_from (a few thousand unknowns, <= ~300 k nonzeros) are far too
+// small to fill the GPU, so every sweep / restriction / prolongation there costs a
+// launch for ~1 us of work.  One launch of a 16-CTA thread-block cluster runs that whole
+// part of the V-cycle instead: rows spread over the cluster's 16 k threads (8 lanes per
+// row), phases separated by barrier.cluster (release/acquire), vectors written by other
+// CTAs read with ld.global.cg.  Same arithmetic as k_csr_x / k_restrict_v /
+// k_dense_matvec / k_csr_prolong.
+namespace {
+constexpr int CC_THREADS = 1024;
+
+template <int XM>
+__device__ void cc_sweep(const CoarseLev& L, int gt, int gn, double w, double alpha, const double* x,
+                         const double* xc, double* y, int resid) {
+  const int lane = gt & 7;
+  // warp-uniform trip count (the 8-lane shuffles need all 32 lanes of the warp)
+  for (int i0 = (gt >> 5) * 4; i0 < L.n; i0 += (gn >> 5) * 4) {
+    const int i = i0 + ((gt & 31) >> 3);
+    const bool ok = i < L.n;
+    auto xin = [&](int j) -> double {
+      if (XM == 0) return __ldcg(x + j);
+      if (XM == 1) return w * L.dinv[j] * __ldcg(L.b + j);
+      return __ldcg(x + j) + alpha * __ldcg(xc + L.parent[j]);
+    };
+    double s = 0.0;
+    if (ok)
+      for (int k = L.rp[i] + lane; k < L.rp[i + 1]; k += 8)
+        s += (L.vf ? (double)L.vf[k] : L.vd[k]) * xin(L.ci[k]);
+    s += __shfl_down_sync(0xffffffffu, s, 4, 8);
+    s += __shfl_down_sync(0xffffffffu, s, 2, 8);
+    s += __shfl_down_sync(0xffffffffu, s, 1, 8);
+    if (ok && lane == 0) {
+      const double bi = __ldcg(L.b + i);
+      y[i] = resid ? bi - s : xin(i) + w * L.dinv[i] * (bi - s);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(CC_THREADS, 1)
+k_coarse_cycle(const CoarseLev* __restrict__ levs, int nlev, const double* __restrict__ dense_inv,
+               double w, double alpha, int nu) {
+  pdl_wait();
+  cg::cluster_group cl = cg::this_cluster();
+  const int gt = (int)cl.block_rank() * blockDim.x + threadIdx.x;
+  const int gn = (int)cl.num_blocks() * blockDim.x;
+  __shared__ double* xs[16];     // current / scratch iterate per level (uniform pointer swaps)
+  __shared__ double* x2s[16];
+  if (threadIdx.x < nlev) {
+    xs[threadIdx.x] = levs[threadIdx.x].x;
+    x2s[threadIdx.x] = levs[threadIdx.x].x2;
+  }
+  __syncthreads();
+  // down: pre-smoothing from the zero guess, residual, restriction
+  for (int l = 0; l + 1 < nlev; ++l) {
+    const CoarseLev L = levs[l];
+    double*& x = xs[l];
+    double*& x2 = x2s[l];
+    if (nu >= 2) {
+      cc_sweep<1>(L, gt, gn, w, 0.0, nullptr, nullptr, x, 0);
+      cl.sync();
+      for (int k = 2; k < nu; ++k) {
+        cc_sweep<0>(L, gt, gn, w, 0.0, x, nullptr, x2, 0);
+        cl.sync();
+        if (threadIdx.x == 0) { double* t = x; x = x2; x2 = t; }
+        __syncthreads();
+      }
+      cc_sweep<0>(L, gt, gn, 0.0, 0.0, x, nullptr, L.res, 1);
+    } else {
+      for (int i = gt; i < L.n; i += gn) x[i] = w * L.dinv[i] * __ldcg(L.b + i);
+      cl.sync();
+      cc_sweep<1>(L, gt, gn, w, 0.0, nullptr, nullptr, L.res, 1);
+    }
+    cl.sync();
+    const CoarseLev U = levs[l + 1];
+    const int lane = gt & 7;
+    for (int I0 = (gt >> 5) * 4; I0 < U.n; I0 += (gn >> 5) * 4) {
+      const int I = I0 + ((gt & 31) >> 3);
+      double s = 0.0;
+      if (I < U.n)
+        for (int q = L.pt_ptr[I] + lane; q < L.pt_ptr[I + 1]; q += 8) s += L.ptv[q] * __ldcg(L.res + L.pt_row[q]);
+      s += __shfl_down_sync(0xffffffffu, s, 4, 8);
+      s += __shfl_down_sync(0xffffffffu, s, 2, 8);
+      s += __shfl_down_sync(0xffffffffu, s, 1, 8);
+      if (I < U.n && lane == 0) U.b[I] = s;
+    }
+    cl.sync();
+  }
+  {  // coarsest: x = A^-1 b (explicit inverse), warp per row
+    const CoarseLev C = levs[nlev - 1];
+    const int lane = gt & 31;
+    for (int row = gt >> 5; row < C.n; row += gn >> 5) {
+      double s = 0.0;
+      for (int j = lane; j < C.n; j += 32) s += dense_inv[row * C.n + j] * __ldcg(C.b + j);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (lane == 0) xs[nlev - 1][row] = s;
+    }
+    cl.sync();
+  }
+  // up: coarse correction (fused into the first post-sweep for tentative prolongators)
+  for (int l = nlev - 2; l >= 0; --l) {
+    const CoarseLev L = levs[l];
+    double*& x = xs[l];
+    double*& x2 = x2s[l];
+    const double* xc = xs[l + 1];
+    int post = nu;
+    if (L.tentative && post >= 1) {
+      cc_sweep<2>(L, gt, gn, w, alpha, x, xc, x2, 0);
+      cl.sync();
+      if (threadIdx.x == 0) { double* t = x; x = x2; x2 = t; }
+      __syncthreads();
+      --post;
+    } else {
+      for (int i = gt; i < L.n; i += gn) {
+        double s = 0.0;
+        for (int m = L.prp[i]; m < L.prp[i + 1]; ++m) s += L.pv[m] * __ldcg(xc + L.pci[m]);
+        x[i] = __ldcg(x + i) + alpha * s;
+      }
+      cl.sync();
+    }
+    for (int k = 0; k < post; ++k) {
+      cc_sweep<0>(L, gt, gn, w, 0.0, x, nullptr, x2, 0);
+      cl.sync();
+      if (threadIdx.x == 0) { double* t = x; x = x2; x2 = t; }
+      __syncthreads();
+    }
+  }
+  // the caller reads the result from levels[fuse_from].x
+  if (xs[0] != levs[0].x) {
+    for (int i = gt; i < levs[0].n; i += gn) levs[0].x[i] = __ldcg(xs[0] + i);
+  }
+}
+}  // namespace
+
+static void coarse_cycle_launch(const Amg& A, AmgBlock& B, cudaStream_t s) {
+  static int cluster = 0;
+  if (!cluster) {
+    cluster = 8;
+    if (cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(CC_THREADS);
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 16; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+      q.attrs = &at;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, k_coarse_cycle, &q) == cudaSuccess && n >= 1) cluster = 16;
+    }
+    cudaGetLastError();
+    if (const char* e = getenv("HC_AMG_FUSE_CLUSTER")) cluster = atoi(e) >= 16 ? 16 : std::max(1, atoi(e));
+  }
+  static const int threads = getenv("HC_AMG_FUSE_THREADS") ? atoi(getenv("HC_AMG_FUSE_THREADS")) : CC_THREADS;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  const int nlev = (int)B.levels.size() - B.fuse_from;
+  HC_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_cycle, (const CoarseLev*)B.clev.p, nlev,
+                             (const double*)B.dense_inv.p, A.omega, B.alpha, A.nu_c));
+  HC_COUNT();
 }
 
 static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s);
@@ -806,7 +1035,7 @@ static void csr_sweep(const Amg& A, const AmgLevel& L, double w, const double* b
   auto go = [&](auto vs_tag, auto* vals) {
     constexpr int VS = decltype(vs_tag)::value;
     using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
-    k_csr_jacobi_v<VS, VT><<<nblk((long long)VS * L.n), TPB, 0, s>>>(L.n, w, L.A.rp.p, L.A.ci.p, vals,
+    launch(k_csr_jacobi_v<VS, VT>, nblk((long long)VS * L.n), TPB, 0, s, L.n, w, L.A.rp.p, L.A.ci.p, vals,
                                                                       L.dinv.p, b, x, y, resid);
     HC_COUNT();
   };
@@ -832,7 +1061,7 @@ static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha,
   auto go = [&](auto vs_tag, auto* vals) {
     constexpr int VS = decltype(vs_tag)::value;
     using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
-    k_csr_x<VS, VT, XM><<<nblk((long long)VS * L.n), TPB, 0, s>>>(
+    launch(k_csr_x<VS, VT, XM>, nblk((long long)VS * L.n), TPB, 0, s, 
         L.n, w, alpha, L.A.rp.p, L.A.ci.p, vals, L.dinv.p, b, x, parent, xc, y, resid);
     HC_COUNT();
   };
@@ -858,10 +1087,10 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
     }
     csr_sweep_x<0>(A, L, 0.0, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.res.p, 1, s);
   } else {
-    k_csr_smooth0<<<nblk(L.n), TPB, 0, s>>>(L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
+    launch(k_csr_smooth0, nblk(L.n), TPB, 0, s, L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
     csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.res.p, 1, s);
   }
-  k_restrict_v<<<nblk(8LL * U.n), TPB, 0, s>>>(U.n, L.pt_ptr.p, L.pt_row.p, L.ptv.p, L.res.p,
+  launch(k_restrict_v, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, L.ptv.p, L.res.p,
                                                U.b.p); HC_COUNT();
   solve_level(A, B, l + 1, s);
   const bool tentative = L.P.nnz == (long long)L.n;  // one prolongator entry per row
@@ -872,7 +1101,7 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
     std::swap(L.x.p, L.x2.p);
     --post;
   } else {
-    k_csr_prolong<<<nblk(L.n), TPB, 0, s>>>(L.n, B.alpha, L.P.rp.p, L.P.ci.p, L.P.v.p, U.x.p,
+    launch(k_csr_prolong, nblk(L.n), TPB, 0, s, L.n, B.alpha, L.P.rp.p, L.P.ci.p, L.P.v.p, U.x.p,
                                             L.x.p); HC_COUNT();
   }
   for (int k = 0; k < post; ++k) {
@@ -884,9 +1113,13 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
 // approximate solve at level l >= 1 (rhs L.b -> L.x): gamma cycles on the first
 // wdepth levels, one below, dense LU at the coarsest level
 static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
+  if (B.fuse_from >= 1 && (int)l == B.fuse_from) {
+    coarse_cycle_launch(A, B, s);
+    return;
+  }
   AmgLevel& L = B.levels[l];
   if (l + 1 == B.levels.size()) {
-    k_dense_matvec<<<nblk(L.n, 8), 256, 0, s>>>(L.n, B.dense_inv.p, L.b.p, L.x.p); HC_COUNT();
+    launch(k_dense_matvec, nblk(L.n, 8), 256, 0, s, L.n, B.dense_inv.p, L.b.p, L.x.p); HC_COUNT();
     return;
   }
   cycle_once(A, B, l, s);
@@ -897,19 +1130,21 @@ static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
     std::swap(L.b.p, L.res.p);
     cycle_once(A, B, l, s);
     std::swap(L.b.p, L.res.p);
-    k_vec_add<<<nblk(L.n), TPB, 0, s>>>(L.n, L.acc.p, L.x.p); HC_COUNT();
+    launch(k_vec_add, nblk(L.n), TPB, 0, s, L.n, L.acc.p, L.x.p); HC_COUNT();
   }
 }
 
 namespace {
 __global__ void k_smooth0_s(long long n, double w, const double* __restrict__ dinv,
                             const double* __restrict__ r, double* __restrict__ e) {
+  pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v < n) e[v] = w * dinv[v] * r[v];
 }
 __global__ void k_prolong0_s(long long n, double alpha, const int32_t* __restrict__ prp,
                              const int32_t* __restrict__ pci, const double* __restrict__ pv,
                              const double* __restrict__ x1, double* __restrict__ e) {
+  pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= n) return;
   int p0 = prp[v], p1 = prp[v + 1];
@@ -921,6 +1156,7 @@ __global__ void k_prolong0_s(long long n, double alpha, const int32_t* __restric
 // T r split into scalar field right-hand sides
 __global__ void k_split_T(DevParams P, const uint8_t* __restrict__ lab, const double2* __restrict__ r,
                           double* __restrict__ rc, double* __restrict__ rp) {
+  pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= P.nvox) return;
   double2 a = r[v];
@@ -929,6 +1165,7 @@ __global__ void k_split_T(DevParams P, const uint8_t* __restrict__ lab, const do
 }
 __global__ void k_merge_s(long long n, const double* __restrict__ ec, const double* __restrict__ ep,
                           double2* __restrict__ z) {
+  pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v < n) z[v] = make_double2(ec ? ec[v] : 0.0, ep[v]);
 }
@@ -961,7 +1198,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
     HC_COUNT();
   };
   if (B.levels.size() == 1) {
-    k_smooth0_s<<<nb, TPB, 0, s>>>(nv, w, L0.dinv.p, r, e); HC_COUNT();
+    launch(k_smooth0_s, nb, TPB, 0, s, nv, w, L0.dinv.p, r, e); HC_COUNT();
     return e;
   }
   AmgLevel& L1 = B.levels[1];
@@ -972,17 +1209,17 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
       std::swap(e, e2);
     }
   } else {
-    k_smooth0_s<<<nb, TPB, 0, s>>>(nv, w, L0.dinv.p, r, e); HC_COUNT();
+    launch(k_smooth0_s, nb, TPB, 0, s, nv, w, L0.dinv.p, r, e); HC_COUNT();
     for (int k = 1; k < A.nu; ++k) {
       sweep(EP_SMOOTH, e, e2);
       std::swap(e, e2);
     }
   }
   sweep(EP_RESID, e, A.res.p);
-  k_restrict_v<<<nblk(8LL * L1.n), TPB, 0, s>>>(L1.n, L0.pt_ptr.p, L0.pt_row.p, L0.ptv.p, A.res.p,
+  launch(k_restrict_v, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, L0.ptv.p, A.res.p,
                                                 L1.b.p); HC_COUNT();
   solve_level(A, B, 1, s);
-  k_prolong0_s<<<nb, TPB, 0, s>>>(nv, B.alpha, L0.P.rp.p, L0.P.ci.p, L0.P.v.p, L1.x.p, e); HC_COUNT();
+  launch(k_prolong0_s, nb, TPB, 0, s, nv, B.alpha, L0.P.rp.p, L0.P.ci.p, L0.P.v.p, L1.x.p, e); HC_COUNT();
   for (int k = 0; k < A.nu; ++k) {
     sweep(EP_SMOOTH, e, e2);
     std::swap(e, e2);
@@ -997,10 +1234,10 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
   Amg& A = *op.amg;
   const long long nv = op.P.nvox;
   const int nb = nblk(nv);
-  k_split_T<<<nb, TPB, 0, s>>>(op.P, op.labels.p, r, A.rs[0].p, A.rs[1].p); HC_COUNT();
+  launch(k_split_T, nb, TPB, 0, s, op.P, op.labels.p, r, A.rs[0].p, A.rs[1].p); HC_COUNT();
   double* ep = vcycle_fine(op, 1, A.rs[1].p, inv_dt, s);
   if (mode == 1) {
-    k_merge_s<<<nb, TPB, 0, s>>>(nv, nullptr, ep, z); HC_COUNT();
+    launch(k_merge_s, nb, TPB, 0, s, nv, nullptr, ep, z); HC_COUNT();
     return;
   }
   // c-block right-hand side: T r_c - (T J)_cp e_phi
@@ -1010,7 +1247,7 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
                                   nullptr, A.rc2.p, s);
   HC_COUNT();
   double* ec = vcycle_fine(op, 0, A.rc2.p, inv_dt, s);
-  k_merge_s<<<nb, TPB, 0, s>>>(nv, ec, ep, z); HC_COUNT();
+  launch(k_merge_s, nb, TPB, 0, s, nv, ec, ep, z); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 

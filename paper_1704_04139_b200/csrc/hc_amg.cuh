@@ -27,11 +27,29 @@ struct AmgLevel {
   DBuf<double> x, x2, b, res, acc;       // cycle vectors (levels >= 1)
 };
 
+// device view of one CSR level for the cluster-fused coarse cycle (hc_amg.cu)
+struct CoarseLev {
+  int n;
+  const int32_t *rp, *ci;
+  const float* vf;              // fp32 values (or null: vd)
+  const double* vd;
+  const double* dinv;
+  double *b, *x, *x2, *res;
+  int tentative;                // prolongator is the tentative one (one entry of 1 per row)
+  const int32_t* parent;
+  const int32_t *prp, *pci;
+  const double* pv;
+  const int32_t *pt_ptr, *pt_row;
+  const double* ptv;
+};
+
 struct AmgBlock {
   int field = 0;                  // 0: c block of T J, 1: phi block of J
   double alpha = 1.0;             // coarse-correction scaling
   std::vector<AmgLevel> levels;   // levels[0] is the fine grid
   DBuf<double> dense, dense_inv;  // coarsest matrix and its inverse
+  int fuse_from = -1;             // levels >= fuse_from run as one cluster kernel (-1: none)
+  DBuf<CoarseLev> clev;           // their device views
 };
 
 struct AmgGraph {
@@ -49,7 +67,7 @@ struct Amg {
   std::vector<AmgGraph> graphs;
   AmgBlock blk[2];
   int coarse_max = 128;       // <= HC_COARSE_MAX (the coarsest inverse lives in shared memory)
-  int nu = 2;
+  int nu = 1;                // smoothing sweeps on the fine level (measured: 1 beats 2 on the medium cell)
   int nu_c = 2;              // smoothing sweeps on the CSR levels
   int sa_levels_c = 0;       // smoothed transfers of the c block (plain aggregation suffices)
   double omega = 0.9;        // Jacobi smoothing weight
@@ -59,6 +77,8 @@ struct Amg {
   int gamma = 1;             // cycles per coarse-level solve (2 = W-cycle)
   int wdepth = 3;
   int wmin = 1;
+  int fuse_rows = 0;          // levels with at most this many rows ... (0: off, measured slower)
+  long long fuse_nnz = 400000; // ... and nonzeros run as one cluster kernel (0 rows: off)
   int coarsen = 2;           // block growth factor of the transfers above level 1              // gamma cycles on CSR levels wmin..wdepth
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int refresh = 0;          // numeric setup every Newton iteration (1) or once per solve (0)

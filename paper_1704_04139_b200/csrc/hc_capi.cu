@@ -14,6 +14,13 @@
 
 namespace hc {
 std::atomic<unsigned long long> g_launch_count{0};
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HC_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
 thread_local unsigned long long t_launch_count = 0;
 Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
                           const hc_params& hp);

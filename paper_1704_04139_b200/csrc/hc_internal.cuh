@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/halfcell_b200.h"
@@ -293,4 +294,37 @@ double norm2_grid(Operator& op, const double2* v, int field_mask, cudaStream_t s
 Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
                           const hc_params& hp);
 
+}  // namespace hc
+
+namespace hc {
+// ---- programmatic dependent launch (PDL) --------------------------------------------
+// Kernels of the Krylov / multigrid loop are launched with programmatic stream
+// serialization, so a kernel's launch and prologue overlap its predecessor's tail.
+// Every such kernel calls pdl_wait() as its first statement (before any early exit):
+// it blocks until the predecessor grid has completed and its writes are visible, which
+// also keeps the ordering transitive along the stream.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the successor grid launch now (its CTAs then wait in pdl_wait) when this grid is
+// at most about one wave, so an early launch cannot steal slots from our own later waves.
+__device__ __forceinline__ void pdl_trigger_small() {
+  if (gridDim.x * gridDim.y * gridDim.z <= 592u) asm volatile("griddepcontrol.launch_dependents;");
+}
+
+bool pdl_enabled();   // HC_PDL (default 1)
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  HC_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 }  // namespace hc

@@ -65,6 +65,7 @@ __device__ __forceinline__ double fin_sum_block(const double* part, int nb) {
 __global__ void k_dev_dot2(long long n, const double* __restrict__ ks, const double2* __restrict__ a,
                            const double2* __restrict__ b, const double2* __restrict__ c,
                            const double2* __restrict__ d, double* __restrict__ part) {
+  pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   double s1 = 0.0, s2 = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -81,6 +82,7 @@ __global__ void k_dev_dot2(long long n, const double* __restrict__ ks, const dou
 
 // 0: beta  1: alpha  2: s-norm  3: omega  4: r-norm / next rho   (one block of 256)
 __global__ void k_dev_scalar(int what, int nb, const double* __restrict__ part, double* ks) {
+  pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   double s1 = 0.0, s2 = 0.0;
   if (what >= 1) s1 = fin_sum_block(part, nb);
@@ -115,6 +117,7 @@ __global__ void k_dev_scalar(int what, int nb, const double* __restrict__ part, 
 
 __global__ void k_dev_p(long long n, const double* __restrict__ ks, const double2* __restrict__ r,
                         const double2* __restrict__ v, double2* __restrict__ p) {
+  pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   const double beta = ks[S_BETA], omega = ks[S_OMEGA];
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -127,6 +130,7 @@ __global__ void k_dev_p(long long n, const double* __restrict__ ks, const double
 __global__ void k_dev_s(long long n, const double* __restrict__ ks, const double2* __restrict__ r,
                         const double2* __restrict__ v, double2* __restrict__ s,
                         double* __restrict__ part) {
+  pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   const double alpha = ks[S_ALPHA];
   double acc = 0.0;
@@ -145,6 +149,7 @@ __global__ void k_dev_xr(long long n, const double* __restrict__ ks, const doubl
                          const double2* __restrict__ sh, const double2* __restrict__ s,
                          const double2* __restrict__ t, const double2* __restrict__ rhat,
                          double2* __restrict__ x, double2* __restrict__ r, double* __restrict__ part) {
+  pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   const double alpha = ks[S_ALPHA], omega = ks[S_OMEGA];
   double a1 = 0.0, a2 = 0.0;
@@ -161,6 +166,7 @@ __global__ void k_dev_xr(long long n, const double* __restrict__ ks, const doubl
 }
 
 __global__ void k_dev_init(int nb, const double* __restrict__ part, double* ks, double tol2) {
+  pdl_wait();
   double b2 = fin_sum_block(part, nb);
   if (threadIdx.x != 0) return;
   for (int i = 0; i < S_NSLOT; ++i) ks[i] = 0.0;
@@ -210,8 +216,8 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   HC_CUDA(cudaMemsetAsync(W.kp.p, 0, n * sizeof(double2), s));
   HC_CUDA(cudaMemsetAsync(W.kv.p, 0, n * sizeof(double2), s));
   HC_CUDA(cudaMemsetAsync(G.ks.p, 0, S_NSLOT * sizeof(double), s));
-  k_dev_dot2<<<nb, TPB, 0, s>>>(n, G.ks.p, b, b, nullptr, nullptr, G.part.p); HC_COUNT();
-  k_dev_init<<<1, 256, 0, s>>>(nb, G.part.p, G.ks.p, rtol * rtol); HC_COUNT();
+  launch(k_dev_dot2, nb, TPB, 0, s, n, G.ks.p, b, b, nullptr, nullptr, G.part.p); HC_COUNT();
+  launch(k_dev_init, 1, 256, 0, s, nb, G.part.p, G.ks.p, rtol * rtol); HC_COUNT();
   // (re)capture the iteration graph for this mode / dt
   if (!G.exec[mode] || G.inv_dt[mode] != inv_dt) {
     if (G.exec[mode]) cudaGraphExecDestroy(G.exec[mode]);
@@ -221,21 +227,21 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
     HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     double* ks = G.ks.p;
     double* part = G.part.p;
-    k_dev_scalar<<<1, 256, 0, s>>>(0, nb, part, ks); HC_COUNT();
-    k_dev_p<<<(int)((n + TPB - 1) / TPB), TPB, 0, s>>>(n, ks, W.kr.p, W.kv.p, W.kp.p); HC_COUNT();
+    launch(k_dev_scalar, 1, 256, 0, s, 0, nb, part, ks); HC_COUNT();
+    launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p); HC_COUNT();
     amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s);
     apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
-    k_dev_dot2<<<nb, TPB, 0, s>>>(n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part); HC_COUNT();
-    k_dev_scalar<<<1, 256, 0, s>>>(1, nb, part, ks); HC_COUNT();
-    k_dev_s<<<nb, TPB, 0, s>>>(n, ks, W.kr.p, W.kv.p, W.ks.p, part); HC_COUNT();
-    k_dev_scalar<<<1, 256, 0, s>>>(2, nb, part, ks); HC_COUNT();
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part); HC_COUNT();
+    launch(k_dev_scalar, 1, 256, 0, s, 1, nb, part, ks); HC_COUNT();
+    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part); HC_COUNT();
+    launch(k_dev_scalar, 1, 256, 0, s, 2, nb, part, ks); HC_COUNT();
     amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s);
     apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
-    k_dev_dot2<<<nb, TPB, 0, s>>>(n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part); HC_COUNT();
-    k_dev_scalar<<<1, 256, 0, s>>>(3, nb, part, ks); HC_COUNT();
-    k_dev_xr<<<nb, TPB, 0, s>>>(n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part); HC_COUNT();
+    launch(k_dev_scalar, 1, 256, 0, s, 3, nb, part, ks); HC_COUNT();
+    launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
                                 part); HC_COUNT();
-    k_dev_scalar<<<1, 256, 0, s>>>(4, nb, part, ks); HC_COUNT();
+    launch(k_dev_scalar, 1, 256, 0, s, 4, nb, part, ks); HC_COUNT();
     HC_CUDA(cudaStreamEndCapture(s, &graph));
     op.capturing = false;
     G.n_kernels[mode] = t_launch_count - c0;

@@ -88,6 +88,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
          const double* __restrict__ e, const double* __restrict__ r, const double* __restrict__ dinv,
          double omega, double inv_dt, int flags, double2* __restrict__ out2, double* __restrict__ out,
          int zc) {
+  pdl_wait();
   constexpr bool FULLM = MODE == SM_FULL;
   constexpr bool X0 = EPI == EP_SMOOTH0;   // input e0 = w D^-1 r materialised from staged r, dinv
   constexpr int S = 4;
@@ -360,8 +361,8 @@ inline void fine_launch_p(const DevParams& P, const FineArgs& F, const int32_t* 
   const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
   const int bz = pick_bz(bx, by, P.nz, per_sm, n_sm);
   const int zc = (P.nz + bz - 1) / bz;
-  k_fine_p<MODE, EPI><<<dim3(bx, by, bz), dim3(VX, VY, 1), smem, s>>>(
-      P, F, lab4, V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
+  launch(k_fine_p<MODE, EPI>, dim3(bx, by, bz), dim3(VX, VY, 1), smem, s, P, F, lab4, V, e, r, dinv, omega,
+         inv_dt, flags, out2, out, zc);
 }
 
 }  // namespace hc

@@ -126,6 +126,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
            const double2* __restrict__ V, const double* __restrict__ e, const double* __restrict__ r,
            const double* __restrict__ dinv, double omega, double inv_dt, int flags,
            double2* __restrict__ out2, double* __restrict__ out, int zc) {
+  pdl_wait();
   using L = TmaLayout<MODE, EPI>;
   constexpr bool FULLM = L::FULLM, X0 = L::X0;
   constexpr bool RES = MODE == SM_RES;
@@ -492,8 +493,8 @@ inline bool fine_launch_tma(TmaCache& cache, const DevParams& P, const FineArgs&
     }
     const int bz = pick_bz(bx, by, P.nz, per_sm, n_sm);
     const int zc = (P.nz + bz - 1) / bz;
-    kern<<<dim3(bx, by, (P.nz + zc - 1) / zc), dim3(VX, L::THREADS / VX, 1), smem, s>>>(
-        P, M, F, labt, V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
+    launch(kern, dim3(bx, by, (P.nz + zc - 1) / zc), dim3(VX, L::THREADS / VX, 1), smem, s, P, M, F, labt,
+           V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
   };
   if (MODE == SM_FULL && (flags & 4)) go(k_fine_tma<MODE, EPI, true>);
   else go(k_fine_tma<MODE, EPI, false>);

@@ -1,6 +1,5 @@
-for zc in 0 3 6 12 24; do
-  echo "medium zc=$zc: $(HC_ZC_TARGET=$zc timeout 120 python tools/stencil_ab.py medium 3 2>&1 | grep kind)"
-done
-for zc in 0 6 18; do
-  echo "large zc=$zc: $(HC_ZC_TARGET=$zc timeout 120 python tools/stencil_ab.py large 3 2>&1 | grep kind)"
-done
+for cfg in medium large; do
+for cfgs in "2 2" "1 2" "1 1"; do
+  set -- $cfgs
+  echo "$cfg nu=$1 nu_c=$2: $(HC_AMG_NU=$1 HC_AMG_NU_C=$2 timeout 200 python bench.py --config $cfg --steps 6 --no-cpu-baseline --no-at-scale 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2), d["krylov_iters_per_step"], d["newton_iters_per_step"])')"
+done; done
