@@ -1,5 +1,7 @@
-for cfg in medium large; do
-for cfgs in "2 2" "1 2" "1 1"; do
-  set -- $cfgs
-  echo "$cfg nu=$1 nu_c=$2: $(HC_AMG_NU=$1 HC_AMG_NU_C=$2 timeout 200 python bench.py --config $cfg --steps 6 --no-cpu-baseline --no-at-scale 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2), d["krylov_iters_per_step"], d["newton_iters_per_step"])')"
-done; done
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for r in 8 16; do
+  echo "refresh_solves=$r: $(HC_AMG_REFRESH_SOLVES=$r timeout 150 python bench.py --steps 10 --no-cpu-baseline --no-at-scale 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2), d["krylov_iters_per_step"], d["gpu_launches"])')"
+done
+for r in 8 16; do
+  echo "large refresh_solves=$r: $(HC_AMG_REFRESH_SOLVES=$r timeout 250 python bench.py --config large --steps 6 --no-cpu-baseline --no-at-scale 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2), d["krylov_iters_per_step"], d["gpu_launches"])')"
+done
