@@ -165,6 +165,13 @@ __global__ void k_dev_xr(long long n, const double* __restrict__ ks, const doubl
   block_part2(a1, a2, part);
 }
 
+// WHILE-node condition of the device-resident loop: continue while not converged / broken
+// down and under the iteration budget
+__global__ void k_dev_cond(const double* __restrict__ ks, cudaGraphConditionalHandle h, int maxit) {
+  pdl_wait();
+  cudaGraphSetConditional(h, (ks[S_DONE] == 0.0 && ks[S_ITERS] < (double)maxit) ? 1u : 0u);
+}
+
 __global__ void k_dev_init(int nb, const double* __restrict__ part, double* ks, double tol2) {
   pdl_wait();
   double b2 = fin_sum_block(part, nb);
@@ -178,7 +185,9 @@ __global__ void k_dev_init(int nb, const double* __restrict__ part, double* ks, 
 }  // namespace
 
 struct KrylovGraphs {
-  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // per mode
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // per mode: one iteration
+  cudaGraphExec_t loop[2] = {nullptr, nullptr};  // per mode: WHILE node around the iteration
+  int loop_maxit[2] = {-1, -1};
   double inv_dt[2] = {-1.0, -1.0};
   unsigned long long n_kernels[2] = {0, 0};
   double2* x_ptr[2] = {nullptr, nullptr};
@@ -186,6 +195,7 @@ struct KrylovGraphs {
   double* ks_host = nullptr;
   ~KrylovGraphs() {
     for (auto e : exec) if (e) cudaGraphExecDestroy(e);
+    for (auto e : loop) if (e) cudaGraphExecDestroy(e);
     if (ks_host) cudaFreeHost(ks_host);
   }
 };
@@ -218,13 +228,8 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   HC_CUDA(cudaMemsetAsync(G.ks.p, 0, S_NSLOT * sizeof(double), s));
   launch(k_dev_dot2, nb, TPB, 0, s, n, G.ks.p, b, b, nullptr, nullptr, G.part.p); HC_COUNT();
   launch(k_dev_init, 1, 256, 0, s, nb, G.part.p, G.ks.p, rtol * rtol); HC_COUNT();
-  // (re)capture the iteration graph for this mode / dt
-  if (!G.exec[mode] || G.inv_dt[mode] != inv_dt) {
-    if (G.exec[mode]) cudaGraphExecDestroy(G.exec[mode]);
-    unsigned long long c0 = t_launch_count;
-    cudaGraph_t graph;
-    op.capturing = true;
-    HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  // the body of one BiCGStab iteration (captured, never run eagerly)
+  auto iteration = [&]() {
     double* ks = G.ks.p;
     double* part = G.part.p;
     launch(k_dev_scalar, 1, 256, 0, s, 0, nb, part, ks); HC_COUNT();
@@ -240,8 +245,19 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
     launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part); HC_COUNT();
     launch(k_dev_scalar, 1, 256, 0, s, 3, nb, part, ks); HC_COUNT();
     launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
-                                part); HC_COUNT();
+           part); HC_COUNT();
     launch(k_dev_scalar, 1, 256, 0, s, 4, nb, part, ks); HC_COUNT();
+  };
+  const bool rebuild = !G.exec[mode] || G.inv_dt[mode] != inv_dt;
+  if (rebuild) {
+    if (G.exec[mode]) cudaGraphExecDestroy(G.exec[mode]);
+    if (G.loop[mode]) cudaGraphExecDestroy(G.loop[mode]);
+    G.exec[mode] = G.loop[mode] = nullptr;
+    unsigned long long c0 = t_launch_count;
+    cudaGraph_t graph;
+    op.capturing = true;
+    HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    iteration();
     HC_CUDA(cudaStreamEndCapture(s, &graph));
     op.capturing = false;
     G.n_kernels[mode] = t_launch_count - c0;
@@ -251,18 +267,66 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
     G.inv_dt[mode] = inv_dt;
     G.x_ptr[mode] = x;
   }
+  if (op.krylov_while && (rebuild || G.loop_maxit[mode] != maxit)) {
+    // the whole solve as ONE graph: a WHILE conditional node whose body is one iteration
+    // and whose condition a device kernel sets from the convergence flag — no host
+    // round trip until the solve is finished
+    if (G.loop[mode]) cudaGraphExecDestroy(G.loop[mode]);
+    G.loop[mode] = nullptr;
+    cudaGraph_t outer = nullptr;
+    bool ok = cudaGraphCreate(&outer, 0) == cudaSuccess;
+    cudaGraphConditionalHandle h = 0;
+    ok = ok && cudaGraphConditionalHandleCreate(&h, outer, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    ok = ok && cudaGraphAddNode(&node, outer, nullptr, 0, &np) == cudaSuccess;
+    if (ok) {
+      cudaGraph_t body = np.conditional.phGraph_out[0];
+      unsigned long long c0 = t_launch_count;
+      op.capturing = true;
+      ok = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+           cudaSuccess;
+      if (ok) {
+        iteration();
+        k_dev_cond<<<1, 32, 0, s>>>(G.ks.p, h, maxit);
+        cudaGraph_t got;
+        ok = cudaStreamEndCapture(s, &got) == cudaSuccess;
+      }
+      op.capturing = false;
+      uncount(t_launch_count - c0);
+      ok = ok && cudaGraphInstantiate(&G.loop[mode], outer, 0) == cudaSuccess;
+    }
+    if (outer) cudaGraphDestroy(outer);
+    cudaGetLastError();
+    if (!ok) {
+      G.loop[mode] = nullptr;
+      op.krylov_while = false;   // fall back to batched iteration graphs
+      if (op.krylov_log) fprintf(stderr, "krylov: conditional WHILE graph unavailable, using batches\n");
+    }
+    G.loop_maxit[mode] = maxit;
+  }
   if (G.x_ptr[mode] != x) throw Error(HC_ERR_ARGUMENT, "bicgstab_dev: solution buffer changed");
   int done_iters = 0;
   const int batch = op.krylov_batch;
+  const bool dev_loop = op.krylov_while && G.loop[mode];
   while (true) {
-    for (int k = 0; k < batch; ++k) {
-      HC_CUDA(cudaGraphLaunch(G.exec[mode], s));
-      count_graph_launch(G.n_kernels[mode]);
+    if (dev_loop) {
+      HC_CUDA(cudaGraphLaunch(G.loop[mode], s));
+    } else {
+      for (int k = 0; k < batch; ++k) {
+        HC_CUDA(cudaGraphLaunch(G.exec[mode], s));
+        count_graph_launch(G.n_kernels[mode]);
+      }
     }
     HC_CUDA(cudaMemcpyAsync(G.ks_host, G.ks.p, S_NSLOT * sizeof(double), cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
     const double* h = G.ks_host;
     done_iters = (int)h[S_ITERS];
+    if (dev_loop) count_graph_launch((G.n_kernels[mode] + 1) * (unsigned long long)std::max(done_iters, 1));
     if (h[S_ERR] != 0.0) {
       char msg[128];
       snprintf(msg, sizeof msg, "iterative linear solver stalled (breakdown %d at iteration %d)",
