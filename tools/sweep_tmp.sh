@@ -1,5 +1,4 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for w in 1 0; do
-  echo "while=$w: $(HC_KRYLOV_WHILE=$w HC_KRYLOV_LOG=1 timeout 150 python bench.py --steps 10 --no-cpu-baseline --no-at-scale 2>/tmp/err_$w | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2), d["krylov_iters_per_step"], d["gpu_launches"], d["e2e"]["value"])')"; grep -i "krylov:" /tmp/err_$w | head -2
-done
-echo "large: $(timeout 250 python bench.py --config large --steps 6 --no-cpu-baseline --no-at-scale 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2), d["krylov_iters_per_step"], d["gpu_launches"])')"
+timeout 300 python bench.py --config pod --steps 5 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print("pod", d["ms_per_step"], d["value"])'
+for k in 60 80; do for m in 300 400; do
+echo "rom k=$k m=$m: $(timeout 300 python bench.py --config rom --rom-rank $k --rom-ei $m 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"]), d["newton_iters_per_step"], d["qoi_max_rel_dev_vs_fom_training_window"])')"
+done; done
