@@ -433,7 +433,9 @@ def run_pod(args, ws, rank, local):
     torch.cuda.set_device(local)
     n_dof, n_snap = 2_100_000, 400
     g = torch.Generator(device="cuda").manual_seed(7)
-    S = torch.randn(n_snap, n_dof, device="cuda", dtype=torch.float64, generator=g).t()  # column-major
+    # row-major (n_dof, n_snap): the snapshots of one DOF contiguous, as the ROM's snapshot
+    # matrix is stored; hc_pod_gram_rows reads it in place
+    S = torch.randn(n_dof, n_snap, device="cuda", dtype=torch.float64, generator=g)
     w = torch.rand(n_dof, device="cuda", dtype=torch.float64, generator=g) + 0.5
     for _ in range(args.warmup):
         pod.pod_gram(S, w)

@@ -149,6 +149,12 @@ int hc_step_batch(hc_operator* const* ops, int32_t n, double* const* x, double* 
 int hc_pod_gram(const double* S, const double* w, int64_t n_dof, int64_t n_snap, double* G,
                 void* stream);
 
+/* The same Gram for S stored row-major (n_dof x n_snap, the snapshots of one DOF
+ * contiguous — the layout a snapshot matrix filled column by column in a row-major
+ * tensor has); no transpose copy. */
+int hc_pod_gram_rows(const double* S, const double* w, int64_t n_dof, int64_t n_snap, double* G,
+                     void* stream);
+
 /* Reduced-order model for the online stage (SPEC mor.build_rom / solve_rom; no
  * counterpart in the reference tree, whose mor package is not shipped).  All arrays are
  * device memory.  x = B x~ with B = blockdiag(V_c, V_phi); the first k_c reduced

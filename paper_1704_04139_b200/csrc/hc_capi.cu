@@ -25,7 +25,7 @@ thread_local unsigned long long t_launch_count = 0;
 Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
                           const hc_params& hp);
 void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
-              cudaStream_t s);
+              cudaStream_t s, bool rows);
 void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, double mu, double dt,
              int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
              double* qoi, int32_t* iters, int32_t* status_host, cudaStream_t s);
@@ -589,7 +589,15 @@ int hc_pod_gram(const double* Sm, const double* w, int64_t n_dof, int64_t n_snap
                 void* stream) {
   return guarded([&] {
     if (n_dof < 0 || n_snap < 0) throw Error(HC_ERR_ARGUMENT, "negative size");
-    pod_gram(Sm, w, n_dof, n_snap, G, S(stream));
+    pod_gram(Sm, w, n_dof, n_snap, G, S(stream), false);
+  });
+}
+
+int hc_pod_gram_rows(const double* Sm, const double* w, int64_t n_dof, int64_t n_snap, double* G,
+                     void* stream) {
+  return guarded([&] {
+    if (n_dof < 0 || n_snap < 0) throw Error(HC_ERR_ARGUMENT, "negative size");
+    pod_gram(Sm, w, n_dof, n_snap, G, S(stream), true);
   });
 }
 

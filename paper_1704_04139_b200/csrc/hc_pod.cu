@@ -1,5 +1,7 @@
 // POD snapshot Gram matrix G = S^T diag(w) S (method of snapshots, SPEC mor.pod),
-// the only dense contraction of the path.  S is n_dof x n_snap column-major fp64.
+// the only dense contraction of the path.  S is n_dof x n_snap fp64, column-major or
+// row-major (snapshots contiguous per DOF: a DOF chunk of every snapshot is one block,
+// so concurrent CTAs share pages and L2 lines; no transpose copy is needed).
 //
 // FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).  Each CTA owns one 64x64 tile of
 // the upper triangle of G (G is symmetric: 28 of 49 tiles for 400 snapshots) and
@@ -37,6 +39,7 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // part[z][j * n + i] = sum_{k in slice z} S[k][i] w[k] S[k][j]   for the tile pair (ti <= tj)
+template <bool ROWS>
 __global__ void __launch_bounds__(NT) k_gram(const double* __restrict__ S, const double* __restrict__ w,
                                              long long n_dof, int n, int tiles, long long k_per,
                                              double* __restrict__ part) {
@@ -58,14 +61,18 @@ __global__ void __launch_bounds__(NT) k_gram(const double* __restrict__ S, const
   auto stage = [&](long long k0, int s) {
     // 64 columns x 32 DOFs per panel: 2048 elements per panel, 16 per thread
     for (int e = tid; e < BT * KC; e += NT) {
-      const int col = e / KC, kk = e - col * KC;
+      // column-major S: consecutive threads walk k (a column's 256 B); row-major S
+      // (snapshots contiguous per DOF): consecutive threads walk the 64 snapshots of one
+      // DOF row, and a whole 32-DOF chunk of all snapshots is one contiguous block
+      const int col = ROWS ? e % BT : e / KC, kk = ROWS ? e / BT : e - col * KC;
       const long long k = k0 + kk;
       const int gi = i0 + col, gj = j0 + col;
       const bool kin = k < k_end;
-      cp8(As + (s * BT + col) * LD + kk, S + (long long)min(gi, n - 1) * n_dof + (kin ? k : 0),
-          (kin && gi < n) ? 8 : 0);
-      cp8(Bs + (s * BT + col) * LD + kk, S + (long long)min(gj, n - 1) * n_dof + (kin ? k : 0),
-          (kin && gj < n) ? 8 : 0);
+      const long long kk0 = kin ? k : 0;
+      const double* ai = ROWS ? S + kk0 * n + min(gi, n - 1) : S + (long long)min(gi, n - 1) * n_dof + kk0;
+      const double* bj = ROWS ? S + kk0 * n + min(gj, n - 1) : S + (long long)min(gj, n - 1) * n_dof + kk0;
+      cp8(As + (s * BT + col) * LD + kk, ai, (kin && gi < n) ? 8 : 0);
+      cp8(Bs + (s * BT + col) * LD + kk, bj, (kin && gj < n) ? 8 : 0);
     }
     if (tid < KC) {
       const long long k = k0 + tid;
@@ -141,7 +148,7 @@ __global__ void k_reduce_sym(int n, int nz, int tiles, const double* __restrict_
 }  // namespace
 
 void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
-              cudaStream_t s) {
+              cudaStream_t s, bool rows) {
   if (n_snap == 0) return;
   const int n = (int)n_snap;
   const int tiles = (n + BT - 1) / BT;
@@ -152,18 +159,21 @@ void pod_gram(const double* S, const double* w, long long n_dof, long long n_sna
   const size_t smem = (size_t)(2 * ST * BT * LD + ST * KC) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    HC_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HC_CUDA(cudaFuncSetAttribute(k_gram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HC_CUDA(cudaFuncSetAttribute(k_gram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   int per_sm = 1;
-  HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram, NT, smem));
+  HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram<false>, NT, smem));
   const long long want = std::max<long long>(1, ((long long)std::max(per_sm, 1) * sms + pairs - 1) / pairs);
   long long k_per = (n_dof + want - 1) / want;
   k_per = std::max<long long>(KC, ((k_per + KC - 1) / KC) * KC);
   const int nz = (int)std::max<long long>(1, (n_dof + k_per - 1) / k_per);
   DBuf<double> part((size_t)nz * n * n);
   HC_CUDA(cudaMemsetAsync(part.p, 0, part.n * sizeof(double), s));
-  k_gram<<<dim3(pairs, nz), NT, smem, s>>>(S, w, n_dof, n, tiles, k_per, part.p); HC_COUNT();
+  if (rows) k_gram<true><<<dim3(pairs, nz), NT, smem, s>>>(S, w, n_dof, n, tiles, k_per, part.p);
+  else k_gram<false><<<dim3(pairs, nz), NT, smem, s>>>(S, w, n_dof, n, tiles, k_per, part.p);
+  HC_COUNT();
   HC_CHECK_LAUNCH();
   const long long nn = (long long)n * n;
   k_reduce_sym<<<(int)((nn + 255) / 256), 256, 0, s>>>(n, nz, tiles, part.p, G); HC_COUNT();

@@ -14,21 +14,24 @@ from .errors import ReductionError
 
 
 def pod_gram(S, w=None):
-    """``S^T diag(w) S`` for an (n_dof, n_snap) fp64 snapshot matrix."""
+    """``S^T diag(w) S`` for an (n_dof, n_snap) fp64 snapshot matrix (row- or column-major
+    CUDA tensors are used in place; anything else is copied to the device)."""
     t = _dev.torch()
+    rows = False
     if _dev.is_tensor(S) and S.is_cuda and S.dtype == t.float64 and S.dim() == 2 \
             and S.t().is_contiguous():
-        Sc = S.t()                      # already column-major: no copy
+        Sc = S.t()                      # column-major storage of S: no copy
     else:
-        Sd = _dev.to_dev(S)
-        if Sd.dim() != 2:
+        Sc = _dev.to_dev(S)             # row-major storage (snapshots contiguous per DOF)
+        if Sc.dim() != 2:
             raise ValueError("snapshot matrix must be 2-D (n_dof, n_snap)")
-        Sc = Sd.t().contiguous()        # column-major storage of S
-    n_snap, n_dof = Sc.shape
+        rows = True
+    n_dof, n_snap = (Sc.shape[1], Sc.shape[0]) if not rows else (Sc.shape[0], Sc.shape[1])
     wd = _dev.to_dev(w) if w is not None else None
     G = t.empty((n_snap, n_snap), dtype=t.float64, device="cuda")
-    _native.check(_native.lib().hc_pod_gram(_dev.ptr(Sc), _dev.ptr(wd) if wd is not None else None,
-                                            int(n_dof), int(n_snap), _dev.ptr(G), _dev.stream()))
+    fn = _native.lib().hc_pod_gram_rows if rows else _native.lib().hc_pod_gram
+    _native.check(fn(_dev.ptr(Sc), _dev.ptr(wd) if wd is not None else None, int(n_dof), int(n_snap),
+                     _dev.ptr(G), _dev.stream()))
     G = G.t()  # column-major result -> row-major view
     return _dev.like_input(G.contiguous(), S)
 
