@@ -1225,7 +1225,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   const double w = A.omega;
   const int nb = nblk(nv);
   FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
-             op.if_cslot.p, op.elz.p};
+             op.if_cslot.p, op.elz.p, nullptr, op.tp_off.p};
   const dim3 vg = vox_grid(op.P), vb = vox_block();
   double* e = A.ea[f].p;
   double* e2 = A.eb[f].p;
@@ -1286,7 +1286,7 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
   }
   // c-block right-hand side: T r_c - (T J)_cp e_phi
   FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
-             op.if_cslot.p, op.elz.p};
+             op.if_cslot.p, op.elz.p, nullptr, op.tp_off.p};
   fine_launch_op<SM_CP, EP_RESID>(op, F, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0,
                                   nullptr, A.rc2.p, s);
   HC_COUNT();

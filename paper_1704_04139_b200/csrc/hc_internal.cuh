@@ -255,6 +255,7 @@ struct Operator {
   DBuf<double> if_cslot;       // TMA stencil: (alpha, beta, gamma) per interface face slot
   DBuf<int2> elz;              // TMA stencil: electrolyte z range per 32 x 8 tile column
   DBuf<double> if_islot;       // TMA residual: interface current per face slot
+  DBuf<int32_t> tp_off;        // TMA stencil: first slot per (tile, plane), slots tile-plane ordered
   DBuf<double> inv_c;          // gX / c per electrolyte voxel (linearized)
   DBuf<double> red;            // reduction scratch
   DBuf<double> host_x, host_npl;  // staging for the host-buffer entry point

@@ -439,8 +439,9 @@ __global__ void k_lin_scatter(DevParams P, long long n_if, const int32_t* __rest
   ifv[ie] = -cb; ifv[nslot + ie] = -ca; ifv[2 * nslot + ie] = cg;
 }
 
-// the same, into the compact per-face slots of the TMA stencil (AoS triples; a
-// voxel's slots are consecutive in direction order, first slot in its label word)
+// the same, into the compact per-face slots of the TMA stencil (AoS, 32 B per slot: the
+// triple + pad; a voxel's slots are consecutive in direction order, first slot in its
+// label word)
 __global__ void k_lin_scatter_c(DevParams P, long long n_if, const int32_t* __restrict__ so,
                                 const int32_t* __restrict__ el, const int32_t* __restrict__ labt,
                                 const double* __restrict__ coef, double* __restrict__ cs) {
@@ -452,7 +453,7 @@ __global__ void k_lin_scatter_c(DevParams P, long long n_if, const int32_t* __re
     const unsigned w = (unsigned)labt[v];
     return (long long)(w >> 9) + __popc(((w >> 3) & 63u) & ((1u << d) - 1u));
   };
-  const long long is = 3 * slot(s, dir_to(P, s, e)), ie = 3 * slot(e, dir_to(P, e, s));
+  const long long is = 4 * slot(s, dir_to(P, s, e)), ie = 4 * slot(e, dir_to(P, e, s));
   cs[is] = ca; cs[is + 1] = cb; cs[is + 2] = cg;
   cs[ie] = -cb; cs[ie + 1] = -ca; cs[ie + 2] = cg;
 }
@@ -681,7 +682,7 @@ void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2
               cudaStream_t s, int which) {
   if (which & 1) {
     FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
-               op.if_cslot.p, op.elz.p};
+               op.if_cslot.p, op.elz.p, nullptr, op.tp_off.p};
     fine_launch_op<SM_FULL, EP_STORE>(op, F, vg, nullptr, nullptr, nullptr, 0.0, inv_dt, flags, out,
                                       nullptr, s);
     HC_COUNT();
@@ -969,21 +970,36 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
       // interface faces are consecutive in the compact coefficient array
       std::vector<int32_t> dirs(op->if_dir.n);
       HC_CUDA(cudaMemcpy(dirs.data(), op->if_dir.p, dirs.size() * 4, cudaMemcpyDeviceToHost));
+      // slots numbered tile-plane by tile-plane (32 x 8 tile, plane z), so the slots a
+      // TMA stencil CTA needs for one plane are one contiguous block (bulk-copied by its
+      // producer warp); tp_off[tile-plane] = first slot of that block
+      const int tbx0 = (nx + VX - 1) / VX, tby0 = (ny + VY - 1) / VY;
+      std::vector<int32_t> tp_off((size_t)tbx0 * tby0 * nz + 1, 0);
       long long slot = 0;
       bool fits = true;
-      for (long long v = 0; v < nvox; ++v) {
-        int mask = 0;
-        if (rank[v] >= 0)
-          for (int d = 0; d < 6; ++d) mask |= (dirs[6LL * rank[v] + d] >= 0) << d;
-        if (slot >= (1LL << 23)) fits = false;
-        l4[v] = ((int32_t)labels_host[v] + 1) | (mask << 3) | (int32_t)((slot & ((1 << 23) - 1)) << 9);
-        slot += __builtin_popcount(mask);
-      }
+      for (int z = 0; z < nz; ++z)
+        for (int ty = 0; ty < tby0; ++ty)
+          for (int tx = 0; tx < tbx0; ++tx) {
+            tp_off[((size_t)z * tby0 + ty) * tbx0 + tx] = (int32_t)slot;
+            for (int y = ty * VY; y < std::min(ny, ty * VY + VY); ++y)
+              for (int x = tx * VX; x < std::min(nx, tx * VX + VX); ++x) {
+                const long long v = ((long long)z * ny + y) * nx + x;
+                int mask = 0;
+                if (rank[v] >= 0)
+                  for (int d = 0; d < 6; ++d) mask |= (dirs[6LL * rank[v] + d] >= 0) << d;
+                if (slot >= (1LL << 23)) fits = false;
+                l4[v] = ((int32_t)labels_host[v] + 1) | (mask << 3) | (int32_t)((slot & ((1 << 23) - 1)) << 9);
+                slot += __builtin_popcount(mask);
+              }
+          }
+      tp_off.back() = (int32_t)slot;
       if (fits) {
         op->labt.alloc(nvox);
         HC_CUDA(cudaMemcpy(op->labt.p, l4.data(), nvox * 4, cudaMemcpyHostToDevice));
-        op->if_cslot.alloc(std::max<long long>(3 * slot, 1));
+        op->if_cslot.alloc(std::max<long long>(4 * slot, 2));
         HC_CUDA(cudaMemset(op->if_cslot.p, 0, op->if_cslot.n * sizeof(double)));
+        op->tp_off.alloc(tp_off.size());
+        HC_CUDA(cudaMemcpy(op->tp_off.p, tp_off.data(), tp_off.size() * 4, cudaMemcpyHostToDevice));
         op->if_islot.alloc(std::max<long long>(slot, 1));
         HC_CUDA(cudaMemset(op->if_islot.p, 0, op->if_islot.n * sizeof(double)));
         const int tbx = (nx + VX - 1) / VX, tby = (ny + VY - 1) / VY;

@@ -36,6 +36,7 @@ struct FineArgs {
   const double* cslot;    // TMA stencil: compact row-oriented (alpha, beta, gamma) per interface face slot
   const int2* elz;        // TMA stencil: per 32 x 8 tile column, z range holding electrolyte (lo, hi)
   const double* islot;    // TMA residual: interface current per face slot, oriented from the row
+  const int32_t* tp_off;  // TMA stencil: first face slot of every (32 x 8 tile, plane), + total
 };
 
 }  // namespace hc

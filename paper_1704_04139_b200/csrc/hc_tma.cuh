@@ -60,6 +60,12 @@ __device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, 
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 // tensor maps of one launch (passed by value; __grid_constant__ keeps them in param space)
 struct TmaMaps {
   CUtensorMap lab;   // int32 [nz][ny][nx], box 40 x 10 x 1
@@ -92,6 +98,9 @@ constexpr int T_LW = VX + 8, T_LOFF = 4;    // labels
 constexpr int T_DW = VX + 4, T_DOFF = 2;    // double (scalar values, gX/c, r, dinv)
 constexpr int T_QW = VX + 2, T_QOFF = 1;    // double2 values
 constexpr int T_LN = T_LW * T_TH, T_DN = T_DW * T_TH, T_QN = T_QW * T_TH;
+// interface face slots staged per (tile, plane): up to T_SLOTCAP 32-byte slots (the rest,
+// on very interface-dense tile-planes, is read from global memory)
+constexpr int T_SLOTCAP = 256;
 
 template <int MODE, int EPI>
 struct TmaLayout {
@@ -105,7 +114,9 @@ struct TmaLayout {
   static constexpr bool HAS_AUX = FULLM || X0;
   static constexpr int AUX2 = AUX + (HAS_AUX ? ((T_DN * 8 + 127) / 128) * 128 : 0);
   static constexpr int LOG = AUX2 + (X0 ? ((T_DN * 8 + 127) / 128) * 128 : 0);   // log c (residual)
-  static constexpr int SLOT = LOG + (MODE == 4 ? ((T_QN * 8 + 127) / 128) * 128 : 0);
+  static constexpr int SLT = LOG + (MODE == 4 ? ((T_QN * 8 + 127) / 128) * 128 : 0);  // face slots
+  static constexpr bool HAS_SLT = MODE != 4;
+  static constexpr int SLOT = SLT + (HAS_SLT ? T_SLOTCAP * 32 : 0);
   static constexpr int THREADS = VX * (VY + 1);   // + producer warp
 };
 
@@ -137,6 +148,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
   unsigned char* ring = smem_dyn + ((128 - ((unsigned)__cvta_generic_to_shared(smem_dyn) & 127)) & 127);
   __shared__ __align__(16) double2 sPC[64];   // (P, C) per (a << 3 | b)
   __shared__ __align__(8) unsigned long long full[T_S], empty[T_S], ready[T_S];
+  __shared__ int tp_start[T_S];   // first global face slot of the tile-plane staged in each ring slot
   const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
   const int x0 = blockIdx.x * VX, y0 = blockIdx.y * VY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);   // planes z0 .. z1 are staged
@@ -160,23 +172,40 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
     const int i = (a - 1) * 6 + (b - 1);
     sPC[tid] = ok ? make_double2(P.gP[i], P.gC[i]) : make_double2(0.0, 0.0);
   }
+  // producer warp: face-slot block of plane j = lane + 32 r of this tile column (loaded
+  // lane-parallel; the first batch before the barrier so its latency overlaps the setup)
+  int st_l = 0, cnt_l = 0;
+  auto load_tp = [&](int jb) {
+    st_l = cnt_l = 0;
+    const int zz = z0 + jb + (int)threadIdx.x;
+    if (L::HAS_SLT && jb + (int)threadIdx.x <= nplane && zz < nz) {
+      const long long tpi = ((long long)zz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      st_l = F.tp_off[tpi];
+      cnt_l = min(F.tp_off[tpi + 1] - st_l, T_SLOTCAP);
+    }
+  };
+  if (threadIdx.y == T_WARPS) load_tp(0);
   __syncthreads();   // barriers initialised, tables built (the only CTA-wide barrier)
 
   if (threadIdx.y == T_WARPS) {   // ---------------- producer warp
-    if (threadIdx.x == 0) {
-      const unsigned sbase = (unsigned)__cvta_generic_to_shared(ring);
-      constexpr unsigned tx = T_LN * 4 + (X0 ? 2 * T_DN * 8 : L::VBYTES);
-      // gX/c tiles only on planes next to electrolyte in this tile column (it is zero
-      // elsewhere and only electrolyte rows read it)
-      int2 elz = make_int2(0, -1);
-      if constexpr (OC) elz = F.elz[blockIdx.y * gridDim.x + blockIdx.x];
-      for (int j = 0; j <= nplane; ++j) {
+    const int lane = threadIdx.x;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(ring);
+    constexpr unsigned tx = T_LN * 4 + (X0 ? 2 * T_DN * 8 : L::VBYTES);
+    // gX/c tiles only on planes next to electrolyte in this tile column (it is zero
+    // elsewhere and only electrolyte rows read it)
+    int2 elz = make_int2(0, -1);
+    if constexpr (OC) elz = F.elz[blockIdx.y * gridDim.x + blockIdx.x];
+    for (int j = 0; j <= nplane; ++j) {
+      if (j && (j & 31) == 0) load_tp(j);
+      const int st = __shfl_sync(0xffffffffu, st_l, j & 31), cnt = __shfl_sync(0xffffffffu, cnt_l, j & 31);
+      if (lane == 0) {
         const int slot = j % T_S;
         if (j >= T_S) mbar_wait(empty0 + 8 * slot, ((j / T_S) - 1) & 1);
         const unsigned b = full0 + 8 * slot, s = sbase + slot * L::SLOT;
         const int zz = z0 + j;
         const bool wtile = OC && zz >= elz.x - 1 && zz <= elz.y + 1;
-        mbar_expect_tx(b, tx + (wtile ? T_DN * 8 : 0));
+        tp_start[slot] = st;
+        mbar_expect_tx(b, tx + (wtile ? T_DN * 8 : 0) + 32u * cnt);
         tma_load3(s + L::LAB, &M.lab, x0 - T_LOFF, y0 - 1, zz, b);
         if constexpr (X0) {
           tma_load3(s + L::AUX, &M.aux, x0 - T_DOFF, y0 - 1, zz, b);
@@ -187,7 +216,9 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         } else {
           tma_load3(s + L::VAL, &M.val, x0 - T_DOFF, y0 - 1, zz, b);
         }
+        if (L::HAS_SLT && cnt) bulk_load(s + L::SLT, F.cslot + 4LL * st, 32u * cnt, b);
       }
+      __syncwarp();
     }
     return;
   }
@@ -260,14 +291,6 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
     if constexpr (RES) logs_for(j + 2);
     mbar_wait((RES ? ready0 : full0) + 8 * K, ph0);
     mbar_wait((RES ? ready0 : full0) + 8 * K1, ph1);
-    if (!RES && active) {   // pull the next plane's interface coefficients towards L1
-      const unsigned w1 = *reinterpret_cast<const unsigned*>(S1 + lofs);
-      if (w1 & (63u << 3)) {
-        const double* c = F.cslot + 3LL * (w1 >> 9);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(c));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(c + 5));
-      }
-    }
     auto lab_at = [&](const unsigned char* Sx, int o) -> int {
       return *reinterpret_cast<const int*>(Sx + lofs + 4 * o);
     };
@@ -379,15 +402,21 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
             for (int k = 0; k < n; ++k) si += c[k];
           }
         } else if (mask) {
-          const double* c = F.cslot + 3LL * ((unsigned)aw >> 9);
+          // the tile-plane's slots were bulk-copied with the plane (global if over capacity)
+          const int gs = (int)((unsigned)aw >> 9), loc = gs - tp_start[K];
+          const double* c = loc + __popc(mask) <= T_SLOTCAP
+                                 ? reinterpret_cast<const double*>(S0 + L::SLT) + 4 * loc
+                                 : F.cslot + 4LL * gs;
 #pragma unroll
           for (int d = 0; d < 6; ++d) {
             if (mask & (1u << d)) {
               const VT vb = nb_val(d);
-              if constexpr (FULLM) si += c[0] * va.x + c[1] * vb.x + c[2] * (va.y - vb.y);
-              else if (MODE == SM_CONC) si += c[0] * va + c[1] * vb;
-              else si += c[2] * (va - vb);
-              c += 3;
+              const double2 ab = *reinterpret_cast<const double2*>(c);
+              const double g = c[2];
+              if constexpr (FULLM) si += ab.x * va.x + ab.y * vb.x + g * (va.y - vb.y);
+              else if (MODE == SM_CONC) si += ab.x * va + ab.y * vb;
+              else si += g * (va - vb);
+              c += 4;
             }
           }
         }
@@ -483,8 +512,10 @@ inline bool fine_launch_tma(TmaCache& cache, const DevParams& P, const FineArgs&
   }
   const size_t smem = (size_t)T_S * L::SLOT + 128;
   const int bx = (P.nx + VX - 1) / VX, by = (P.ny + VY - 1) / VY;
-  auto go = [&](auto kern) {
-    static int per_sm = 0;   // one cache per instantiation (kern is a distinct type per lambda call site)
+  auto go = [&](auto onec) {
+    constexpr bool OC = decltype(onec)::value;
+    auto kern = k_fine_tma<MODE, EPI, OC>;
+    static int per_sm = 0;   // one per (MODE, EPI, OC) instantiation
     if (!per_sm) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -496,8 +527,8 @@ inline bool fine_launch_tma(TmaCache& cache, const DevParams& P, const FineArgs&
     launch(kern, dim3(bx, by, (P.nz + zc - 1) / zc), dim3(VX, L::THREADS / VX, 1), smem, s, P, M, F, labt,
            V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
   };
-  if (MODE == SM_FULL && (flags & 4)) go(k_fine_tma<MODE, EPI, true>);
-  else go(k_fine_tma<MODE, EPI, false>);
+  if (MODE == SM_FULL && (flags & 4)) go(std::true_type{});
+  else go(std::false_type{});
   return true;
 }
 
@@ -507,7 +538,7 @@ inline bool res_launch_tma(Operator& op, const double2* X, double mu, int parts,
                            double inv_dt, double2* out, cudaStream_t s) {
   if (op.stencil_kind != 3 || !op.tma) return false;
   FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
-             op.if_cslot.p, op.elz.p, op.if_islot.p};
+             op.if_cslot.p, op.elz.p, op.if_islot.p, op.tp_off.p};
   return fine_launch_tma<SM_RES, EP_STORE>(*op.tma, op.P, F, op.labt.p, X, nullptr, cprev, nullptr, mu,
                                            inv_dt, parts, out, nullptr, op.n_sm, s);
 }

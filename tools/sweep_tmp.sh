@@ -1,4 +1,4 @@
-timeout 300 python bench.py --config pod --steps 5 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print("pod", d["ms_per_step"], d["value"])'
-for k in 60 80; do for m in 300 400; do
-echo "rom k=$k m=$m: $(timeout 300 python bench.py --config rom --rom-rank $k --rom-ei $m 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"]), d["newton_iters_per_step"], d["qoi_max_rel_dev_vs_fom_training_window"])')"
-done; done
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_solver_variants.py -x -q 2>&1 | tail -1
+timeout 300 python tools/stencil_ab.py large 3 2>&1 | grep kind
+timeout 300 python tools/stencil_ab.py medium 3 2>&1 | grep kind
+echo "medium: $(timeout 150 python bench.py --steps 10 --no-cpu-baseline --no-at-scale 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2), d["krylov_iters_per_step"], d["roofline"]["frac"])')"
