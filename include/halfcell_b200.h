@@ -190,12 +190,13 @@ typedef struct hc_rom {
  * Jacobian refreshed at the first iteration of every jac_steps-th step (and of a step
  * following one that needed more than `refresh` iterations) and every `refresh`
  * iterations inside a step, converged when each block's update is <= rtol relative.  qoi[2 n_steps] receives (cell voltage, mean
- * solid concentration) per step, iters[n_steps] the Newton iterations (device).  One
+ * solid concentration) per step, iters[n_steps] the Newton iterations, xt_steps
+ * [n_steps][k] (optional, may be NULL) the reduced state after every step (device).  One
  * kernel launch (one thread-block cluster) runs the whole loop.  HC_ERR_NONCONVERGENCE carries the failing step
  * in *failed_step. */
 int hc_rom_run(hc_operator* op, const hc_rom* rom, double* xt, double* n_pl, double mu, double dt,
                int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
-               double* qoi, int32_t* iters, int32_t* failed_step, void* stream);
+               double* qoi, int32_t* iters, double* xt_steps, int32_t* failed_step, void* stream);
 
 /* Evict L2 by streaming a `bytes`-sized buffer through it (reads only, so no dirty
  * lines are left behind); used between timed iterations. */

@@ -106,8 +106,8 @@ _SIGS = {
     "hc_rom_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HcRom), ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                                   ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
-                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32),
-                                  ctypes.c_void_p]),
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

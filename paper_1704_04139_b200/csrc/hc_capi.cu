@@ -28,7 +28,7 @@ void pod_gram(const double* S, const double* w, long long n_dof, long long n_sna
               cudaStream_t s, bool rows);
 void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, double mu, double dt,
              int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
-             double* qoi, int32_t* iters, int32_t* status_host, cudaStream_t s);
+             double* qoi, int32_t* iters, double* xt_steps, int32_t* status_host, cudaStream_t s);
 
 Operator::~Operator() {
   destroy_krylov_graphs(kg);
@@ -603,13 +603,13 @@ int hc_pod_gram_rows(const double* Sm, const double* w, int64_t n_dof, int64_t n
 
 int hc_rom_run(hc_operator* opq, const hc_rom* rom, double* xt, double* n_pl, double mu, double dt,
                int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
-               double* qoi, int32_t* iters, int32_t* failed_step, void* stream) {
+               double* qoi, int32_t* iters, double* xt_steps, int32_t* failed_step, void* stream) {
   return guarded([&] {
     if (!opq || !rom || !xt) throw Error(HC_ERR_ARGUMENT, "null argument");
     if (!(dt > 0.0) || n_steps < 0 || max_iter < 1) throw Error(HC_ERR_ARGUMENT, "bad step settings");
     int32_t st[2] = {0, 0};
     rom_run(*(Operator*)opq, rom, xt, n_pl, mu, dt, n_steps, rtol, max_iter, refresh, std::max(1, jac_steps),
-            qoi, iters, st, S(stream));
+            qoi, iters, xt_steps, st, S(stream));
     if (failed_step) *failed_step = st[0] ? st[1] : -1;
     if (st[0] == 1) throw Error(HC_ERR_NONCONVERGENCE, "reduced Newton did not converge");
     if (st[0] == 2) throw Error(HC_ERR_NUMERICS, "reduced Newton produced a non-finite update");

@@ -81,7 +81,7 @@ __device__ void rom_face(const DevParams& P, int kind, const double* xs, const i
 }
 
 struct RomWork {
-  double *x, *xs, *fq, *fdq, *nn, *rr, *G, *J, *npl, *qoi;
+  double *x, *xs, *fq, *fdq, *nn, *rr, *G, *J, *npl, *qoi, *xt_steps;
   int32_t *iters, *status;
 };
 
@@ -333,6 +333,8 @@ k_rom_run(DevParams P, RomDev R, RomWork W, double mu, double dt, double face_ar
         W.qoi[2 * step + 1] = c;
         W.iters[step] = it;
       }
+      if (W.xt_steps)
+        for (int j = tid; j < k; j += 32) W.xt_steps[(long long)step * k + j] = sx[j];
     }
     cl.sync();
   }
@@ -341,7 +343,7 @@ k_rom_run(DevParams P, RomDev R, RomWork W, double mu, double dt, double face_ar
 
 void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, double mu, double dt,
              int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
-             double* qoi, int32_t* iters, int32_t* status_host, cudaStream_t s) {
+             double* qoi, int32_t* iters, double* xt_steps, int32_t* status_host, cudaStream_t s) {
   RomDev R{rom->k, rom->k_c, rom->m, rom->n_s, rom->n_f, rom->n_pl, rom->A, rom->Mr, rom->bnd,
            rom->E, rom->BS, rom->row_coef, rom->q_v, rom->q_ac, rom->f_kind, rom->f_dof, rom->f_slot,
            rom->row_ptr, rom->row_face, rom->pl_ptr, rom->pl_face};
@@ -351,7 +353,7 @@ void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, dou
       nn(std::max(R.m, 1)), rr(R.k), G((long long)std::max(R.m, 1) * R.k), J((long long)R.k * R.k);
   DBuf<int32_t> st(4);
   HC_CUDA(cudaMemsetAsync(st.p, 0, 4 * sizeof(int32_t), s));
-  RomWork W{xt, xs.p, fq.p, fdq.p, nn.p, rr.p, G.p, J.p, npl, qoi, iters, st.p};
+  RomWork W{xt, xs.p, fq.p, fdq.p, nn.p, rr.p, G.p, J.p, npl, qoi, xt_steps, iters, st.p};
   const size_t smem = ((size_t)R.k * R.k + 3 * R.k + 64 + (size_t)TK * R.k) * sizeof(double) +
                       (R.k + 4) * sizeof(int);
   HC_CUDA(cudaFuncSetAttribute(k_rom_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

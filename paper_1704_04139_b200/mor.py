@@ -207,16 +207,40 @@ def _face_tables(op):
 
 def build_rom(op, snaps: Snapshots, k_c: int, k_p: int, m: int) -> ReducedModel:
     """Offline stage: POD bases, EI data, projected blocks, restricted stencil."""
+    nc = op.dof.n_c
+    Vc, _ = pod_rank(snaps.X[:nc], k_c)
+    Vp, _ = pod_rank(snaps.X[nc:], k_p)
+    W, _ = pod_rank(snaps.N, m)
+    return assemble_rom(op, Vc, Vp, W)
+
+
+def build_rom_twin(op, snaps: Snapshots, k_c: int, k_p: int, m: int, keep_fraction: float = 0.97):
+    """The reduced model and its validation twin (SPEC mor.build_rom, §3.2): the twin uses
+    all k_c + k_p POD vectors and M^ = M + max(3, 3% of M) EI vectors, the model the first
+    ceil(keep_fraction k) of each basis and the first M EI vectors — nested spaces, so
+    their distance is measured in reduced coordinates."""
+    import math
+    nc = op.dof.n_c
+    Vc, _ = pod_rank(snaps.X[:nc], k_c)
+    Vp, _ = pod_rank(snaps.X[nc:], k_p)
+    m_hat = m + max(3, int(math.ceil(0.03 * m)))
+    W, _ = pod_rank(snaps.N, m_hat)
+    twin = assemble_rom(op, Vc, Vp, W)
+    kc = max(1, int(math.ceil(keep_fraction * Vc.shape[1])))
+    kp = max(1, int(math.ceil(keep_fraction * Vp.shape[1])))
+    rom = assemble_rom(op, Vc[:, :kc].contiguous(), Vp[:, :kp].contiguous(), W[:, :min(m, W.shape[1])].contiguous())
+    return rom, twin
+
+
+def assemble_rom(op, Vc, Vp, W) -> ReducedModel:
+    """Projected blocks, EI rows / projection and the restricted stencil for given bases."""
     t = _dev.torch()
     dof = op.dof
     nc, n = dof.n_c, dof.n_total
-    Vc, _ = pod_rank(snaps.X[:nc], k_c)
-    Vp, _ = pod_rank(snaps.X[nc:], k_p)
     k_c, k_p = Vc.shape[1], Vp.shape[1]
     k = k_c + k_p
     if k > 160:
         raise ReductionError("reduced dimension exceeds HC_ROM_MAX_K (160)")
-    W, _ = pod_rank(snaps.N, m)
     m = W.shape[1]
     pi = deim(W)
     # ---- affine blocks: A~ = B^T A_lin B, M~ = B^T diag(c rows) B, b~ = B^T b_bnd
@@ -298,11 +322,12 @@ class RomTrajectory:
     voltage: np.ndarray        # per step
     mean_solid_c: np.ndarray   # per step
     newton_iters: np.ndarray
+    states: object = None      # (n_steps, k) reduced states per step (device), if requested
 
 
 def solve_rom(op, rom: ReducedModel, xt0, n_pl0, mu: float, dt: float, n_steps: int,
               rtol: float = 1e-10, max_iter: int = 40, refresh: int = 6,
-              jac_steps: int = 8) -> RomTrajectory:
+              jac_steps: int = 8, keep_states: bool = False) -> RomTrajectory:
     """Reduced implicit-Euler trajectory, one kernel launch (hc_rom_run); the reduced
     Jacobian is refreshed every ``jac_steps`` steps (chord Newton in between)."""
     t = _dev.torch()
@@ -310,11 +335,12 @@ def solve_rom(op, rom: ReducedModel, xt0, n_pl0, mu: float, dt: float, n_steps: 
     npl = _dev.to_dev(n_pl0 if np.size(n_pl0) else np.zeros(1)).clone()
     qoi = t.empty(2 * max(n_steps, 1), dtype=t.float64, device="cuda")
     its = t.empty(max(n_steps, 1), dtype=t.int32, device="cuda")
+    states = t.empty((max(n_steps, 1), rom.k), dtype=t.float64, device="cuda") if keep_states else None
     failed = ctypes.c_int32(-1)
     code = _native.lib().hc_rom_run(op.native.handle, ctypes.byref(rom.struct), _dev.ptr(xt),
                                     _dev.ptr(npl), float(mu), float(dt), int(n_steps), float(rtol),
                                     int(max_iter), int(refresh), int(jac_steps), _dev.ptr(qoi),
-                                    _dev.ptr(its),
+                                    _dev.ptr(its), _dev.ptr(states) if keep_states else None,
                                     ctypes.byref(failed), _dev.stream())
     if code:
         try:
@@ -322,4 +348,28 @@ def solve_rom(op, rom: ReducedModel, xt0, n_pl0, mu: float, dt: float, n_steps: 
         except Exception as e:  # noqa: BLE001
             raise ReductionError(f"reduced Newton failed at step {failed.value}: {e}") from e
     q = qoi.cpu().numpy()[: 2 * n_steps].reshape(-1, 2) if n_steps else np.zeros((0, 2))
-    return RomTrajectory(xt, npl, q[:, 0], q[:, 1], its.cpu().numpy()[:n_steps])
+    return RomTrajectory(xt, npl, q[:, 0], q[:, 1], its.cpu().numpy()[:n_steps],
+                         states[:n_steps] if keep_states else None)
+
+
+def estimate_error(op, rom: ReducedModel, twin: ReducedModel, x0, n_pl0, mu: float, dt: float,
+                   n_steps: int, theta: float = 0.0, **kw):
+    """Hierarchical error estimate (SPEC mor.estimate_error; arXiv 1704.04139 Eqs. 21-22):
+    run the model and its (nested, larger) validation twin and return, per field,
+    1/(1-theta) max_n ||x~_n - x^_n|| / ||x^_n||  (L-infinity in time of relative L2 in
+    space), evaluated in the twin's reduced coordinates — exact because the bases are
+    nested and orthonormal."""
+    if not 0.0 <= theta < 1.0:
+        raise ValueError("theta must be in [0, 1)")
+    t = _dev.torch()
+    a = solve_rom(op, rom, rom.project(x0), n_pl0, mu, dt, n_steps, keep_states=True, **kw)
+    b = solve_rom(op, twin, twin.project(x0), n_pl0, mu, dt, n_steps, keep_states=True, **kw)
+    sa, sb = a.states, b.states
+    kc, kc2 = rom.k_c, twin.k_c
+    dc = sb[:, :kc2].clone()
+    dc[:, :kc] -= sa[:, :kc]
+    dp = sb[:, kc2:].clone()
+    dp[:, : rom.k_p] -= sa[:, kc:]
+    rel = lambda d, ref: float(t.max(t.linalg.vector_norm(d, dim=1) / t.linalg.vector_norm(ref, dim=1)))  # noqa: E731
+    f = 1.0 / (1.0 - theta)
+    return f * rel(dc, sb[:, :kc2]), f * rel(dp, sb[:, kc2:])

@@ -99,3 +99,23 @@ def test_rom_reproduces_training_trajectory(cell):
     fom_v, fom_ac = v_cp @ X[:, 1:], v_ac @ X[:, 1:]
     assert np.max(np.abs(tr.voltage - fom_v)) <= 1e-3 * np.max(np.abs(fom_v))
     assert np.max(np.abs(tr.mean_solid_c - fom_ac) / np.abs(fom_ac)) <= 1e-3
+
+
+def test_error_estimator_twin_and_true_error(cell):
+    """SPEC mor.estimate_error: twin = same model -> 0; otherwise the estimate tracks the
+    true ROM error (vs the full-order trajectory) within a factor 10."""
+    import torch
+    from paper_1704_04139_b200 import mor
+    op, snaps, st = cell["op"], cell["snaps"], cell["st"]
+    rom, twin = mor.build_rom_twin(op, snaps, 8, 8, 16, keep_fraction=0.75)
+    ec, ep = mor.estimate_error(op, twin, twin, st.x, st.n_pl, cell["mu"], cell["dt"], N_TRAIN)
+    assert ec == 0.0 and ep == 0.0
+    ec, ep = mor.estimate_error(op, rom, twin, st.x, st.n_pl, cell["mu"], cell["dt"], N_TRAIN)
+    assert ec > 0.0 and ep > 0.0
+    tr = mor.solve_rom(op, rom, rom.project(st.x), st.n_pl, cell["mu"], cell["dt"], N_TRAIN, keep_states=True)
+    nc = op.dof.n_c
+    X = snaps.X[:, 1:].t()                         # (steps, n)
+    L = torch.stack([rom.lift(tr.states[i]) for i in range(N_TRAIN)])
+    true_c = float(torch.max(torch.linalg.vector_norm(L[:, :nc] - X[:, :nc], dim=1)
+                             / torch.linalg.vector_norm(X[:, :nc], dim=1)))
+    assert 0.1 <= ec / true_c <= 10.0
