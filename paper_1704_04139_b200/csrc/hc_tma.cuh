@@ -115,8 +115,9 @@ struct TmaLayout {
   static constexpr int AUX2 = AUX + (HAS_AUX ? ((T_DN * 8 + 127) / 128) * 128 : 0);
   static constexpr int LOG = AUX2 + (X0 ? ((T_DN * 8 + 127) / 128) * 128 : 0);   // log c (residual)
   static constexpr int SLT = LOG + (MODE == 4 ? ((T_QN * 8 + 127) / 128) * 128 : 0);  // face slots
-  static constexpr bool HAS_SLT = MODE != 4;
-  static constexpr int SLOT = SLT + (HAS_SLT ? T_SLOTCAP * 32 : 0);
+  static constexpr bool HAS_SLT = true;
+  static constexpr int SB = MODE == 4 ? 8 : 32;   // bytes per staged slot: current | (alpha, beta, gamma, pad)
+  static constexpr int SLOT = SLT + ((T_SLOTCAP + 2) * SB + 127) / 128 * 128;
   static constexpr int THREADS = VX * (VY + 1);   // + producer warp
 };
 
@@ -204,8 +205,11 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         const unsigned b = full0 + 8 * slot, s = sbase + slot * L::SLOT;
         const int zz = z0 + j;
         const bool wtile = OC && zz >= elz.x - 1 && zz <= elz.y + 1;
-        tp_start[slot] = st;
-        mbar_expect_tx(b, tx + (wtile ? T_DN * 8 : 0) + 32u * cnt);
+        // residual slots are 8 B: start the bulk copy at the 16-byte aligned slot below
+        const int sta = RES ? (st & ~1) : st;
+        const unsigned sbytes = RES ? (unsigned)(((cnt + (st - sta)) * 8 + 15) & ~15) : 32u * cnt;
+        tp_start[slot] = sta;
+        mbar_expect_tx(b, tx + (wtile ? T_DN * 8 : 0) + (cnt ? sbytes : 0u));
         tma_load3(s + L::LAB, &M.lab, x0 - T_LOFF, y0 - 1, zz, b);
         if constexpr (X0) {
           tma_load3(s + L::AUX, &M.aux, x0 - T_DOFF, y0 - 1, zz, b);
@@ -216,7 +220,10 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         } else {
           tma_load3(s + L::VAL, &M.val, x0 - T_DOFF, y0 - 1, zz, b);
         }
-        if (L::HAS_SLT && cnt) bulk_load(s + L::SLT, F.cslot + 4LL * st, 32u * cnt, b);
+        if (cnt) {
+          if constexpr (RES) bulk_load(s + L::SLT, F.islot + sta, sbytes, b);
+          else bulk_load(s + L::SLT, F.cslot + 4LL * st, sbytes, b);
+        }
       }
       __syncwarp();
     }
@@ -397,8 +404,10 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         if constexpr (RES) {
           // interface currents, one per face slot, oriented from this row (k_residual_islot)
           if (mask && (flags & PART_BV)) {
-            const double* c = F.islot + ((unsigned)aw >> 9);
+            const int gs = (int)((unsigned)aw >> 9), loc = gs - tp_start[K];
             const int n = __popc(mask);
+            const double* c = loc + n <= T_SLOTCAP ? reinterpret_cast<const double*>(S0 + L::SLT) + loc
+                                                   : F.islot + gs;
             for (int k = 0; k < n; ++k) si += c[k];
           }
         } else if (mask) {
