@@ -159,43 +159,6 @@ __global__ void k_smooth_P(int n, int smooth, double w, const int32_t* __restric
     pv[find_col(pci, p0, p1, parent[aci[k]])] += s * av[k];
 }
 
-// AP = A P (row-wise), then A_next = P^T (AP): two per-row passes, no atomics
-__global__ void k_ap(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
-                     const double* __restrict__ av, const int32_t* __restrict__ prp,
-                     const int32_t* __restrict__ pci, const double* __restrict__ pv,
-                     const int32_t* __restrict__ qrp, const int32_t* __restrict__ qci,
-                     double* __restrict__ qv) {
-  pdl_wait();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int r0 = qrp[i], r1 = qrp[i + 1];
-  if (r0 == r1) return;
-  for (int k = r0; k < r1; ++k) qv[k] = 0.0;
-  for (int k = arp[i]; k < arp[i + 1]; ++k) {
-    int j = aci[k];
-    double a = av[k];
-    for (int m = prp[j]; m < prp[j + 1]; ++m) qv[find_col(qci, r0, r1, pci[m])] += a * pv[m];
-  }
-}
-
-__global__ void k_ptap(int n_next, const int32_t* __restrict__ pt_ptr,
-                       const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
-                       const double* __restrict__ pv, const int32_t* __restrict__ qrp,
-                       const int32_t* __restrict__ qci, const double* __restrict__ qv,
-                       const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
-                       double* __restrict__ nv) {
-  pdl_wait();
-  int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= n_next) return;
-  int r0 = nrp[I], r1 = nrp[I + 1];
-  for (int k = r0; k < r1; ++k) nv[k] = 0.0;
-  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) {
-    int i = pt_row[q];
-    double p = pv[pt_idx[q]];
-    for (int m = qrp[i]; m < qrp[i + 1]; ++m) nv[find_col(nci, r0, r1, qci[m])] += p * qv[m];
-  }
-}
-
 // Warp-per-row variants of the two Galerkin passes.  Within one (fine row, P row) pair
 // the lanes take distinct output columns (a CSR row has unique columns), so the updates
 // need no atomics, and the pairs are visited in the serial kernels' order: every output
@@ -320,56 +283,6 @@ __global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const dou
 }
 
 // ---- cycle kernels ------------------------------------------------------------
-__device__ __forceinline__ double fld(const double2& a, int f) { return f ? a.y : a.x; }
-
-__global__ void k_fine_smooth0(long long n, int f, double w, const double* __restrict__ dinv,
-                               const double2* __restrict__ r, double2* __restrict__ e) {
-  pdl_wait();
-  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= n) return;
-  double val = w * dinv[v] * fld(r[v], f);
-  e[v] = f ? make_double2(0.0, val) : make_double2(val, 0.0);
-}
-
-__global__ void k_fine_smooth(long long n, int f, double w, const double* __restrict__ dinv,
-                              const double2* __restrict__ r, const double2* __restrict__ t,
-                              double2* __restrict__ e) {
-  pdl_wait();
-  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= n) return;
-  double d = w * dinv[v] * (fld(r[v], f) - fld(t[v], f));
-  if (f) e[v].y += d; else e[v].x += d;
-}
-
-// b1 = P0^T (r - t) on field f
-__global__ void k_fine_restrict(int n1, int f, const int32_t* __restrict__ pt_ptr,
-                                const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
-                                const double* __restrict__ pv, const double2* __restrict__ r,
-                                const double2* __restrict__ t, double* __restrict__ b1) {
-  pdl_wait();
-  int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= n1) return;
-  double s = 0.0;
-  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) {
-    int v = pt_row[q];
-    s += pv[pt_idx[q]] * (fld(r[v], f) - fld(t[v], f));
-  }
-  b1[I] = s;
-}
-
-// e += alpha P0 x1 on field f
-__global__ void k_fine_prolong(long long n, int f, double alpha, const int32_t* __restrict__ prp,
-                               const int32_t* __restrict__ pci, const double* __restrict__ pv,
-                               const double* __restrict__ x1, double2* __restrict__ e) {
-  pdl_wait();
-  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= n) return;
-  int p0 = prp[v], p1 = prp[v + 1];
-  if (p0 == p1) return;
-  double s = 0.0;
-  for (int m = p0; m < p1; ++m) s += pv[m] * x1[pci[m]];
-  if (f) e[v].y += alpha * s; else e[v].x += alpha * s;
-}
 
 __global__ void k_csr_smooth0(int n, double w, const double* __restrict__ dinv,
                               const double* __restrict__ b, double* __restrict__ x) {
@@ -440,41 +353,6 @@ __global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict
     const double xi = xin(i);
     y[i] = resid ? b[i] - s : xi + w * dinv[i] * (b[i] - s);
   }
-}
-
-__global__ void k_csr_jacobi(int n, double w, const int32_t* __restrict__ rp,
-                             const int32_t* __restrict__ cl, const double* __restrict__ v,
-                             const double* __restrict__ dinv, const double* __restrict__ b,
-                             const double* __restrict__ x, double* __restrict__ y) {
-  pdl_wait();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double s = b[i];
-  for (int k = rp[i]; k < rp[i + 1]; ++k) s -= v[k] * x[cl[k]];
-  y[i] = x[i] + w * dinv[i] * s;
-}
-
-__global__ void k_csr_resid(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ cl,
-                            const double* __restrict__ v, const double* __restrict__ b,
-                            const double* __restrict__ x, double* __restrict__ res) {
-  pdl_wait();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double s = b[i];
-  for (int k = rp[i]; k < rp[i + 1]; ++k) s -= v[k] * x[cl[k]];
-  res[i] = s;
-}
-
-__global__ void k_csr_restrict(int n_next, const int32_t* __restrict__ pt_ptr,
-                               const int32_t* __restrict__ pt_row, const int32_t* __restrict__ pt_idx,
-                               const double* __restrict__ pv, const double* __restrict__ res,
-                               double* __restrict__ b_next) {
-  pdl_wait();
-  int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= n_next) return;
-  double s = 0.0;
-  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) s += pv[pt_idx[q]] * res[pt_row[q]];
-  b_next[I] = s;
 }
 
 __global__ void k_csr_prolong(int n, double alpha, const int32_t* __restrict__ prp,

@@ -262,7 +262,7 @@ struct Operator {
   Amg* amg = nullptr;
   Work* work = nullptr;
   int krylov_log = 0;
-  int stencil_kind = 3;            // 1: register-prefetch tiles, 2: cp.async ring, 3: TMA ring (nx % 4 == 0, else 2)
+  int stencil_kind = 3;            // 2: cp.async ring, 3: TMA ring (nx % 4 == 0, else 2)
   bool dev_krylov = true;          // device-resident BiCGStab (hc_krylov.cu)
   int krylov_batch = 4;            // iteration graphs launched per status check (fallback)
   bool krylov_while = true;        // whole solve as one graph with a device-side WHILE node

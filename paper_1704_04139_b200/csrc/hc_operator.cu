@@ -36,11 +36,6 @@ __device__ __forceinline__ bool grounded(const DevParams& P, uint8_t lab, int z)
   return z == P.nz - 1 && lab == CC;
 }
 
-__device__ __forceinline__ double harm(const DevParams& P, uint8_t a, uint8_t b) {
-  double sa = P.sig[a], sb = P.sig[b];
-  return 2.0 * sa * sb / (sa + sb) * P.gF2;
-}
-
 // face f in reference enumeration order -> (lo, hi) voxel (operator.py:132-138)
 __device__ __forceinline__ void face_voxels(const DevParams& P, long long f, long long& lo,
                                             long long& hi) {
@@ -269,70 +264,6 @@ __global__ void k_gather(int n_c, int n_p, const int32_t* __restrict__ c_vox,
   if (i < n_p) x[n_c + i] = xg[p_vox[i]].y;
 }
 
-// ------------------------------------------------------------- residual kernels
-// Linear two-point fluxes, grounded closures, chemical-potential (1/c) faces,
-// boundary drive and the implicit-Euler time term, one thread per voxel.
-__global__ void __launch_bounds__(TPB) k_residual_stencil(
-    DevParams P, const uint8_t* __restrict__ lab, const double2* __restrict__ X, double mu,
-    int parts, const double* __restrict__ cprev, double inv_dt, double2* __restrict__ out) {
-  int x, y, z, v;
-  if (!vox_index(P, x, y, z, v)) return;
-  uint8_t a = lab[v];
-  if (grounded(P, a, z)) {
-    out[v] = make_double2(0.0, 0.0);
-    return;
-  }
-  double2 xa = X[v];
-  double rc = 0.0, rp = 0.0;
-  const bool lin = parts & PART_LIN;
-  const bool one_c = (parts & PART_1C) && a == EL;
-  const double logca = one_c ? log(xa.x) : 0.0;
-  const double gM = P.t_plus * P.kappa * P.gF2;
-  const double gel = P.d_el * P.inv_h2, ggr = P.d_gr * P.inv_h2;
-#pragma unroll
-  for (int d = 0; d < 6; ++d) {
-    long long nb;
-    int zb = z;
-    if (d == 0) { if (x == 0) continue; nb = v - 1; }
-    else if (d == 1) { if (x + 1 >= P.nx) continue; nb = v + 1; }
-    else if (d == 2) { if (y == 0) continue; nb = v - P.nx; }
-    else if (d == 3) { if (y + 1 >= P.ny) continue; nb = v + P.nx; }
-    else if (d == 4) { if (z == 0) continue; nb = v - P.nxy; zb = z - 1; }
-    else { if (z + 1 >= P.nz) continue; nb = v + P.nxy; zb = z + 1; }
-    uint8_t b = lab[nb];
-    uint8_t k = kind_of(a, b);
-    if (grounded(P, b, zb)) {
-      if (lin && (k == K_CONT || k == K_CONTACT)) rp += harm(P, a, b) * xa.y;
-      continue;
-    }
-    if (k == K_CONT) {
-      double2 xb = X[nb];
-      if (lin) {
-        if (a == GR) {
-          rc += ggr * (xa.x - xb.x);
-          rp += P.sigma_gr * P.gF2 * (xa.y - xb.y);
-        } else if (a == EL) {
-          rc += gel * (xa.x - xb.x) + gM * (xa.y - xb.y);
-          rp += P.kappa * P.gF2 * (xa.y - xb.y);
-        } else {
-          rp += P.sig[a] * P.gF2 * (xa.y - xb.y);
-        }
-      }
-      if (one_c) {
-        double q = P.gX * (logca - log(xb.x));
-        rp += q;
-        rc += P.t_plus * q;
-      }
-    } else if (k == K_CONTACT && lin) {
-      double2 xb = X[nb];
-      rp += harm(P, a, b) * (xa.y - xb.y);
-    }
-  }
-  if ((parts & PART_BND) && a == CW && z == 0) rp += mu * P.drive;
-  if ((parts & PART_TIME) && (a == GR || a == EL)) rc += (xa.x - cprev[v]) * inv_dt;
-  out[v] = make_double2(rc, rp);
-}
-
 // Interface currents over the compacted face list (operator.py:331-357).
 __global__ void __launch_bounds__(TPB) k_residual_iface(
     DevParams P, long long n_if, const int32_t* __restrict__ so, const int32_t* __restrict__ el,
@@ -465,94 +396,6 @@ __global__ void k_lin_invc(DevParams P, const uint8_t* __restrict__ lab,
   w[v] = lab[v] == EL ? P.gX / X[v].x : 0.0;
 }
 
-// ------------------------------------------------------------------------ J v
-// flags: 1 = add mass (inv_dt on c rows), 2 = apply the row transform T
-// (c_el row -= t+ * phi_el row), 4 = include 1/c terms
-__global__ void __launch_bounds__(TPB) k_jvp_stencil(DevParams P, const uint8_t* __restrict__ lab,
-                                                     const double* __restrict__ w,
-                                                     const double2* __restrict__ V,
-                                                     double inv_dt, int flags,
-                                                     double2* __restrict__ out) {
-  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (v >= P.nvox) return;
-  int x, y, z;
-  coords(P, v, x, y, z);
-  uint8_t a = lab[v];
-  if (grounded(P, a, z)) {
-    out[v] = make_double2(0.0, 0.0);
-    return;
-  }
-  double2 va = V[v];
-  double rc = 0.0, rp = 0.0;
-  const bool one_c = (flags & 4) && a == EL;
-  const double ua = one_c ? w[v] * va.x : 0.0;
-  const double gM = P.t_plus * P.kappa * P.gF2;
-  const double gel = P.d_el * P.inv_h2, ggr = P.d_gr * P.inv_h2;
-#pragma unroll
-  for (int d = 0; d < 6; ++d) {
-    long long nb;
-    int zb = z;
-    if (d == 0) { if (x == 0) continue; nb = v - 1; }
-    else if (d == 1) { if (x + 1 >= P.nx) continue; nb = v + 1; }
-    else if (d == 2) { if (y == 0) continue; nb = v - P.nx; }
-    else if (d == 3) { if (y + 1 >= P.ny) continue; nb = v + P.nx; }
-    else if (d == 4) { if (z == 0) continue; nb = v - P.nxy; zb = z - 1; }
-    else { if (z + 1 >= P.nz) continue; nb = v + P.nxy; zb = z + 1; }
-    uint8_t b = lab[nb];
-    uint8_t k = kind_of(a, b);
-    if (grounded(P, b, zb)) {
-      if (k == K_CONT || k == K_CONTACT) rp += harm(P, a, b) * va.y;
-      continue;
-    }
-    if (k == K_CONT) {
-      double2 vb = V[nb];
-      if (a == GR) {
-        rc += ggr * (va.x - vb.x);
-        rp += P.sigma_gr * P.gF2 * (va.y - vb.y);
-      } else if (a == EL) {
-        rc += gel * (va.x - vb.x) + gM * (va.y - vb.y);
-        rp += P.kappa * P.gF2 * (va.y - vb.y);
-        if (one_c) {
-          double dq = ua - w[nb] * vb.x;
-          rp += dq;
-          rc += P.t_plus * dq;
-        }
-      } else {
-        rp += P.sig[a] * P.gF2 * (va.y - vb.y);
-      }
-    } else if (k == K_CONTACT) {
-      double2 vb = V[nb];
-      rp += harm(P, a, b) * (va.y - vb.y);
-    }
-  }
-  if ((flags & 1) && (a == GR || a == EL)) rc += va.x * inv_dt;
-  if ((flags & 2) && a == EL) rc -= P.t_plus * rp;
-  if (flags & 8) rc = 0.0;
-  out[v] = make_double2(rc, rp);
-}
-
-__global__ void __launch_bounds__(TPB) k_jvp_iface(DevParams P, long long n_if,
-                                                   const int32_t* __restrict__ so,
-                                                   const int32_t* __restrict__ el,
-                                                   const int8_t* __restrict__ kind,
-                                                   const double* __restrict__ coef,
-                                                   const double2* __restrict__ V, int flags,
-                                                   double2* __restrict__ out) {
-  long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (f >= n_if) return;
-  int32_t s = so[f], e = el[f];
-  double2 vs = V[s], ve = V[e];
-  int8_t k = kind[f];
-  double dv = coef[f] * (k == IF_BV ? vs.x : 0.0) + coef[n_if + f] * ve.x +
-              coef[2 * n_if + f] * (vs.y - ve.y);
-  double ec = (flags & 2) ? -(1.0 - P.t_plus) * dv : -dv;
-  const bool c_rows = !(flags & 8);
-  if (k == IF_BV && c_rows) atomicAdd(&out[s].x, dv);
-  atomicAdd(&out[s].y, dv);
-  if (c_rows) atomicAdd(&out[e].x, ec);
-  atomicAdd(&out[e].y, -dv);
-}
-
 // ------------------------------------------------------------------ reductions
 // per-block partial sums of squares of the selected fields; field_mask 1 = c, 2 = phi
 __global__ void k_sumsq(long long n, const double2* __restrict__ v, int field_mask,
@@ -614,11 +457,7 @@ void residual_grid(Operator& op, const double2* xg, const double* npl, double mu
     return;
   }
   if (which & 1) {
-    if (op.stencil_kind >= 2)
-      res_launch_p(op.P, op.lab4.p, xg, mu, parts, cprev, inv_dt, out, op.n_sm, s);
-    else
-      k_residual_stencil<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, op.labels.p, xg, mu, parts,
-                                                               cprev, inv_dt, out);
+    res_launch_p(op.P, op.lab4.p, xg, mu, parts, cprev, inv_dt, out, op.n_sm, s);
     HC_COUNT();
   }
   if ((which & 2) && (parts & PART_BV) && op.n_if)
@@ -687,9 +526,6 @@ void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2
                                       nullptr, s);
     HC_COUNT();
   }
-  if (false)
-    k_jvp_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
-                                                    op.if_kind.p, op.if_coef.p, vg, flags, out); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 
