@@ -100,7 +100,10 @@ constexpr int T_QW = VX + 2, T_QOFF = 1;    // double2 values
 constexpr int T_LN = T_LW * T_TH, T_DN = T_DW * T_TH, T_QN = T_QW * T_TH;
 // interface face slots staged per (tile, plane): up to T_SLOTCAP 32-byte slots (the rest,
 // on very interface-dense tile-planes, is read from global memory)
-constexpr int T_SLOTCAP = 256;
+#ifndef HC_TMA_SLOTCAP
+#define HC_TMA_SLOTCAP 256
+#endif
+constexpr int T_SLOTCAP = HC_TMA_SLOTCAP;
 
 template <int MODE, int EPI>
 struct TmaLayout {
