@@ -38,7 +38,7 @@ sys.path.insert(0, REPO)
 METRIC = "implicit time steps/s and residual+J*v GDOF/s; % of B200 HBM roofline"
 FALLBACK_HBM_GBS = 6650.0
 L2_FLUSH_BYTES = 256 << 20
-LINEAR_SAFETY = 0.1
+LINEAR_SAFETY = float(os.environ.get("HC_BENCH_LINEAR_SAFETY", "0.3"))
 
 
 def dist_env():
@@ -364,7 +364,7 @@ def run_ours(args, ws, rank, local):
                        "every timed step and every timed kernel launch",
                        "parallelism": f"replicas x{ws}",
                        "newton": "tol = max(1e-10, 1e-9 |F0|, floor) as the reference; Krylov "
-                                 "rtol_k = max(1e-10, 0.1 tol / |F_k|)"},
+                                 f"rtol_k = max(1e-10, {LINEAR_SAFETY} tol / |F_k|)"},
             "newton_iters_per_step": float(np.mean(newton)),
             "krylov_iters_per_step": float(np.mean(krylov)),
             "gdof_per_s": {"residual": ndof / (kt["res_ms"] * 1e-3) / 1e9,

@@ -100,7 +100,7 @@ def test_newton_solve(case):
     assert np.max(np.abs(res.x[nc:] - ref[nc:])) < 1e-8
 
 
-@pytest.mark.parametrize("linear_safety", [0.0, 0.1])
+@pytest.mark.parametrize("linear_safety", [0.0, 0.1, 0.3])
 def test_transient_curves(case, linear_safety):
     """Curves vs the reference; also with the inexact-Newton Krylov tolerance the bench
     uses (linear_safety=0.1: never solve beyond what the Newton tolerance can use)."""

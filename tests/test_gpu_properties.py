@@ -76,14 +76,16 @@ def test_setup_is_reproducible():
         assert np.array_equal(getattr(op, a), getattr(op2, a))
 
 
-def test_inexact_newton_curves_match_exact_on_tiny_config():
+@pytest.mark.parametrize("safety", [0.1, 0.3])
+def test_inexact_newton_curves_match_exact_on_tiny_config(safety):
     """BASELINE config 0 (tiny cell, 1C, dt = 1 s, 10 steps): the voltage, mean solid
-    concentration and plated-inventory curves with the bench's inexact-Newton Krylov
-    tolerance (linear_safety = 0.1) agree with the exact-tolerance path within 1e-6."""
+    concentration and plated-inventory curves with an inexact-Newton Krylov tolerance
+    (linear_safety: Krylov stops at safety x the Newton tolerance) agree with the
+    exact-tolerance path within 1e-6."""
     P, rs, grid, params, op, mu = _cell("tiny")
     v_cp, v_ac = P.qoi_vectors(op.dof)
     curves = {}
-    for ls in (0.0, 0.1):
+    for ls in (0.0, safety):
         cfg = P.SolverConfig(dt_init=min(0.05, rs.dt), dt_max=rs.dt, linear_safety=ls)
         st = P.prepare_initial_state(op, params, mu, cfg)
         vs, cs, ns = [], [], []
@@ -93,7 +95,7 @@ def test_inexact_newton_curves_match_exact_on_tiny_config():
             cs.append(v_ac @ st.x)
             ns.append(st.n_pl.sum())
         curves[ls] = (np.array(vs), np.array(cs), np.array(ns))
-    (v0, c0, n0), (v1, c1, n1) = curves[0.0], curves[0.1]
+    (v0, c0, n0), (v1, c1, n1) = curves[0.0], curves[safety]
     assert np.max(np.abs(v1 - v0) / np.abs(v0)) < 1e-6
     assert np.max(np.abs(c1 - c0) / np.abs(c0)) < 1e-6
     assert np.allclose(n1, n0, rtol=1e-6, atol=0.0)

@@ -1,3 +1,3 @@
-for lib in paper_1704_04139_b200/libhalfcell_b200.so paper_1704_04139_b200/libhc_s5_c128.so paper_1704_04139_b200/libhc_s6_c128.so paper_1704_04139_b200/libhc_s8_c64.so paper_1704_04139_b200/libhc_s4_c128.so; do
-  echo "$lib: $(HC_LIB=$lib timeout 120 python tools/stencil_ab.py large 3 2>&1 | grep kind) | $(HC_LIB=$lib timeout 120 python tools/stencil_ab.py medium 3 2>&1 | grep kind | cut -c1-60)"
+for ls in 0.1 0.3 1.0; do
+  echo "ls=$ls: $(HC_BENCH_LINEAR_SAFETY=$ls timeout 150 python bench.py --steps 10 --no-cpu-baseline --no-at-scale 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2), d["krylov_iters_per_step"], d["newton_iters_per_step"])')"
 done
