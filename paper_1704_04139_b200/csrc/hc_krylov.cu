@@ -1,9 +1,9 @@
 // Device-resident BiCGStab: scalars live in device memory, dot products are fused
-// into the vector-update kernels as per-block partials finalized by one-thread
-// kernels, and one iteration is a single CUDA graph.  The host launches the
-// iteration graph in batches and reads one status word per batch; kernels become
-// no-ops once the device has declared convergence, so the result is identical to
-// stopping exactly at the converged iteration.
+// into the vector-update kernels as per-block partials that the kernel's last block
+// finalizes (ticket pattern, fixed summation order), and one iteration is a single
+// CUDA graph; the whole solve is one graph with a WHILE conditional node (fallback:
+// batches of iteration graphs with one status read per batch).  Kernels become no-ops
+// once the device has declared convergence.
 //
 // Algorithm and breakdown/stall semantics: right-preconditioned BiCGStab as in
 // bicgstab() (hc_solver.cu), which replaces the reference's direct / ILU-LGMRES
@@ -48,7 +48,7 @@ __device__ __forceinline__ void block_part2(double s1, double s2, double* part) 
 __device__ __forceinline__ double fin_sum_block(const double* part, int nb) {
   __shared__ double sh[32];
   double s = 0.0;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) s += part[i];
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) s += __ldcg(part + i);   // other blocks' partials
   s = warp_sum(s);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
@@ -62,9 +62,12 @@ __device__ __forceinline__ double fin_sum_block(const double* part, int nb) {
   return t;
 }
 
-__global__ void k_dev_dot2(long long n, const double* __restrict__ ks, const double2* __restrict__ a,
+__device__ void finish_in_last_block(int what, const double* part, double* ks, unsigned* ticket);
+
+__global__ void k_dev_dot2(long long n, double* ks, const double2* __restrict__ a,
                            const double2* __restrict__ b, const double2* __restrict__ c,
-                           const double2* __restrict__ d, double* __restrict__ part) {
+                           const double2* __restrict__ d, double* __restrict__ part, int what,
+                           unsigned* ticket) {
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   double s1 = 0.0, s2 = 0.0;
@@ -78,12 +81,11 @@ __global__ void k_dev_dot2(long long n, const double* __restrict__ ks, const dou
     }
   }
   block_part2(s1, s2, part);
+  if (what >= 0) finish_in_last_block(what, part, ks, ticket);
 }
 
 // 0: beta  1: alpha  2: s-norm  3: omega  4: r-norm / next rho   (one block of 256)
-__global__ void k_dev_scalar(int what, int nb, const double* __restrict__ part, double* ks) {
-  pdl_wait();
-  if (ks[S_DONE] != 0.0) return;
+__device__ void scalar_step(int what, int nb, const double* part, double* ks) {
   double s1 = 0.0, s2 = 0.0;
   if (what >= 1) s1 = fin_sum_block(part, nb);
   if (what >= 3) s2 = fin_sum_block(part + nb, nb);
@@ -115,21 +117,47 @@ __global__ void k_dev_scalar(int what, int nb, const double* __restrict__ part, 
   }
 }
 
-__global__ void k_dev_p(long long n, const double* __restrict__ ks, const double2* __restrict__ r,
+__global__ void k_dev_scalar(int what, int nb, const double* __restrict__ part, double* ks) {
+  pdl_wait();
+  if (ks[S_DONE] != 0.0) return;
+  scalar_step(what, nb, part, ks);
+}
+
+// The last block of a partial-producing kernel finalizes the scalar step itself
+// (threadfence + ticket): one launch per reduction instead of two.  The partials are
+// still summed in a fixed order, so the result is unchanged.
+__device__ void finish_in_last_block(int what, const double* part, double* ks, unsigned* ticket) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  scalar_step(what, gridDim.x, part, ks);
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+__global__ void k_dev_p(long long n, double* ks, const double2* __restrict__ r,
                         const double2* __restrict__ v, double2* __restrict__ p) {
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
-  const double beta = ks[S_BETA], omega = ks[S_OMEGA];
+  // beta = (rho1 / rho) (alpha / omega), formerly k_dev_scalar(0): every thread derives it
+  const double rho1 = ks[S_RHO1];
+  const double beta = (rho1 / ks[S_RHO]) * (ks[S_ALPHA] / ks[S_OMEGA]), omega = ks[S_OMEGA];
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i == 0 && (rho1 == 0.0 || !isfinite(rho1))) { ks[S_ERR] = 1; ks[S_DONE] = 1; }
   if (i >= n) return;
   double2 pi = p[i], ri = r[i], vi = v[i];
   p[i] = make_double2(ri.x + beta * (pi.x - omega * vi.x), ri.y + beta * (pi.y - omega * vi.y));
 }
 
 // s = r - alpha v, partial ||s||^2
-__global__ void k_dev_s(long long n, const double* __restrict__ ks, const double2* __restrict__ r,
+__global__ void k_dev_s(long long n, double* ks, const double2* __restrict__ r,
                         const double2* __restrict__ v, double2* __restrict__ s,
-                        double* __restrict__ part) {
+                        double* __restrict__ part, unsigned* ticket) {
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   const double alpha = ks[S_ALPHA];
@@ -142,13 +170,15 @@ __global__ void k_dev_s(long long n, const double* __restrict__ ks, const double
     acc += si.x * si.x + si.y * si.y;
   }
   block_part2(acc, 0.0, part);
+  finish_in_last_block(2, part, ks, ticket);
 }
 
 // x += alpha phat + omega shat; r = s - omega t; partials ||r||^2 and <rhat, r>
-__global__ void k_dev_xr(long long n, const double* __restrict__ ks, const double2* __restrict__ ph,
+__global__ void k_dev_xr(long long n, double* ks, const double2* __restrict__ ph,
                          const double2* __restrict__ sh, const double2* __restrict__ s,
                          const double2* __restrict__ t, const double2* __restrict__ rhat,
-                         double2* __restrict__ x, double2* __restrict__ r, double* __restrict__ part) {
+                         double2* __restrict__ x, double2* __restrict__ r, double* __restrict__ part,
+                         unsigned* ticket) {
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   const double alpha = ks[S_ALPHA], omega = ks[S_OMEGA];
@@ -163,6 +193,7 @@ __global__ void k_dev_xr(long long n, const double* __restrict__ ks, const doubl
     a2 += h.x * ri.x + h.y * ri.y;
   }
   block_part2(a1, a2, part);
+  finish_in_last_block(4, part, ks, ticket);
 }
 
 // WHILE-node condition of the device-resident loop: continue while not converged / broken
@@ -192,6 +223,7 @@ struct KrylovGraphs {
   unsigned long long n_kernels[2] = {0, 0};
   double2* x_ptr[2] = {nullptr, nullptr};
   DBuf<double> ks, part;
+  DBuf<unsigned> ticket;   // last-block ticket of the fused reductions (self-resetting)
   double* ks_host = nullptr;
   ~KrylovGraphs() {
     for (auto e : exec) if (e) cudaGraphExecDestroy(e);
@@ -217,6 +249,8 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   if (!G.ks.p) {
     G.ks.alloc(S_NSLOT);
     G.part.alloc(4 * nb + 8);
+    G.ticket.alloc(1);
+    HC_CUDA(cudaMemset(G.ticket.p, 0, sizeof(unsigned)));
     HC_CUDA(cudaMallocHost(&G.ks_host, S_NSLOT * sizeof(double)));
   }
   // init: x = 0, r = rhat = b, p = v = 0
@@ -226,27 +260,23 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   HC_CUDA(cudaMemsetAsync(W.kp.p, 0, n * sizeof(double2), s));
   HC_CUDA(cudaMemsetAsync(W.kv.p, 0, n * sizeof(double2), s));
   HC_CUDA(cudaMemsetAsync(G.ks.p, 0, S_NSLOT * sizeof(double), s));
-  launch(k_dev_dot2, nb, TPB, 0, s, n, G.ks.p, b, b, nullptr, nullptr, G.part.p); HC_COUNT();
+  launch(k_dev_dot2, nb, TPB, 0, s, n, G.ks.p, b, b, nullptr, nullptr, G.part.p, -1, G.ticket.p); HC_COUNT();
   launch(k_dev_init, 1, 256, 0, s, nb, G.part.p, G.ks.p, rtol * rtol); HC_COUNT();
   // the body of one BiCGStab iteration (captured, never run eagerly)
   auto iteration = [&]() {
     double* ks = G.ks.p;
     double* part = G.part.p;
-    launch(k_dev_scalar, 1, 256, 0, s, 0, nb, part, ks); HC_COUNT();
+    unsigned* tk = G.ticket.p;
     launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p); HC_COUNT();
     amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s);
     apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
-    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part); HC_COUNT();
-    launch(k_dev_scalar, 1, 256, 0, s, 1, nb, part, ks); HC_COUNT();
-    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part); HC_COUNT();
-    launch(k_dev_scalar, 1, 256, 0, s, 2, nb, part, ks); HC_COUNT();
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part, 1, tk); HC_COUNT();
+    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk); HC_COUNT();
     amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s);
     apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
-    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part); HC_COUNT();
-    launch(k_dev_scalar, 1, 256, 0, s, 3, nb, part, ks); HC_COUNT();
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part, 3, tk); HC_COUNT();
     launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
-           part); HC_COUNT();
-    launch(k_dev_scalar, 1, 256, 0, s, 4, nb, part, ks); HC_COUNT();
+           part, tk); HC_COUNT();
   };
   const bool rebuild = !G.exec[mode] || G.inv_dt[mode] != inv_dt;
   if (rebuild) {
