@@ -72,9 +72,12 @@ def make_batch(n_cells: int = 128, first_seed: int = 100, spec: CellSpec = BATCH
     return cells
 
 
-def step_batch(cells: list[BatchCell], dt: float, cfg: SolverConfig, n_threads: int = 16):
+def step_batch(cells: list[BatchCell], dt: float, cfg: SolverConfig, n_threads: int | None = None):
     """One accepted implicit step for every cell (concurrently on the device)."""
+    import os
     n = len(cells)
+    if n_threads is None:
+        n_threads = int(os.environ.get("HC_BATCH_THREADS", "16"))
     ops = (ctypes.c_void_p * n)(*[c.op.native.handle.value for c in cells])
     xs = (ctypes.c_void_p * n)(*[c.x.data_ptr() for c in cells])
     ns = (ctypes.c_void_p * n)(*[c.n_pl.data_ptr() for c in cells])

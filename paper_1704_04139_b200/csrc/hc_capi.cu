@@ -32,6 +32,7 @@ void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, dou
 
 Operator::~Operator() {
   destroy_krylov_graphs(kg);
+  destroy_newton_graph(ng);
   delete tma;
   delete amg;
   delete work;

@@ -220,6 +220,8 @@ struct Amg;   // hc_amg.cu
 struct Work;  // hc_solver.cu
 struct KrylovGraphs;  // hc_krylov.cu
 struct TmaCache;      // hc_tma.cuh
+struct NewtonGraph;   // hc_solver.cu
+void destroy_newton_graph(NewtonGraph* g);
 void destroy_krylov_graphs(KrylovGraphs* g);
 
 // The device-resident operator: geometry, DOF numbering, compacted face lists
@@ -266,6 +268,8 @@ struct Operator {
   bool dev_krylov = true;          // device-resident BiCGStab (hc_krylov.cu)
   int krylov_batch = 4;            // iteration graphs launched per status check (fallback)
   bool krylov_while = true;        // whole solve as one graph with a device-side WHILE node
+  bool newton_dev = false;         // whole Newton solve as one graph (conditional nodes); HC_NEWTON_DEV=1
+  NewtonGraph* ng = nullptr;
   bool capturing = false;          // inside a stream capture (no nested capture)
   KrylovGraphs* kg = nullptr;
   cudaStream_t stream = nullptr;   // private non-blocking stream (graph capture needs one)

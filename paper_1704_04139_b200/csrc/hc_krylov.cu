@@ -203,6 +203,30 @@ __global__ void k_dev_cond(const double* __restrict__ ks, cudaGraphConditionalHa
   cudaGraphSetConditional(h, (ks[S_DONE] == 0.0 && ks[S_ITERS] < (double)maxit) ? 1u : 0u);
 }
 
+// k_dev_init with the relative tolerance read from device memory (device Newton)
+__global__ void k_dev_init_dev(int nb, const double* __restrict__ part, double* ks,
+                               const double* __restrict__ rtol) {
+  pdl_wait();
+  double b2 = fin_sum_block(part, nb);
+  if (threadIdx.x != 0) return;
+  const double t = *rtol;
+  for (int i = 0; i < S_NSLOT; ++i) ks[i] = 0.0;
+  ks[S_RHO] = ks[S_ALPHA] = ks[S_OMEGA] = 1.0;
+  ks[S_RHO1] = b2;
+  ks[S_TOL2] = t * t * b2;
+  if (b2 == 0.0) ks[S_DONE] = 1;
+}
+
+// after a device-resident solve: breakdown or budget exhaustion fails the Newton step
+__global__ void k_dev_check(const double* __restrict__ ks, int maxit, double* ns) {
+  pdl_wait();
+  ns[NS_KITERS] += ks[S_ITERS];
+  if (ks[S_ERR] != 0.0 || ks[S_DONE] == 0.0) {
+    ns[NS_STATUS] = 2.0;
+    ns[NS_WHY] = ks[S_ERR] != 0.0 ? 10.0 + ks[S_ERR] : 9.0;
+  }
+}
+
 __global__ void k_dev_init(int nb, const double* __restrict__ part, double* ks, double tol2) {
   pdl_wait();
   double b2 = fin_sum_block(part, nb);
@@ -372,6 +396,56 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
     }
   }
   return done_iters;
+}
+
+
+void krylov_append(Operator& op, GraphBuilder& gb, const double2* b, double2* x, double inv_dt, int mode,
+                   const double* rtol_dev, int maxit, double* ns) {
+  Work& W = work(op);
+  if (!op.kg) op.kg = new KrylovGraphs();
+  KrylovGraphs& G = *op.kg;
+  const long long n = op.P.nvox;
+  const int nb = (int)std::min<long long>((n + TPB - 1) / TPB, 2LL * op.n_sm);
+  if (!G.ks.p) {
+    G.ks.alloc(S_NSLOT);
+    G.part.alloc(4 * nb + 8);
+    G.ticket.alloc(1);
+    HC_CUDA(cudaMemset(G.ticket.p, 0, sizeof(unsigned)));
+    HC_CUDA(cudaMallocHost(&G.ks_host, S_NSLOT * sizeof(double)));
+  }
+  cudaStream_t s = gb.s;
+  double* ks = G.ks.p;
+  double* part = G.part.p;
+  unsigned* tk = G.ticket.p;
+  // the WHILE handle is set explicitly before the node: a nested loop is re-entered in
+  // every Newton iteration, while the handle default is applied once per graph launch
+  cudaGraphConditionalHandle h = gb.handle(0);
+  gb.capture([&] {
+    HC_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double2), s));
+    HC_CUDA(cudaMemcpyAsync(W.kr.p, b, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    HC_CUDA(cudaMemcpyAsync(W.khat.p, b, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    HC_CUDA(cudaMemsetAsync(W.kp.p, 0, n * sizeof(double2), s));
+    HC_CUDA(cudaMemsetAsync(W.kv.p, 0, n * sizeof(double2), s));
+    HC_CUDA(cudaMemsetAsync(ks, 0, S_NSLOT * sizeof(double), s));   // clears DONE of the last solve
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, b, b, nullptr, nullptr, part, -1, tk); HC_COUNT();
+    launch(k_dev_init_dev, 1, 256, 0, s, nb, (const double*)part, ks, rtol_dev); HC_COUNT();
+    k_dev_cond<<<1, 32, 0, s>>>(ks, h, maxit);
+  });
+  GraphBuilder body{s, gb.cond(h, cudaGraphCondTypeWhile), {}};
+  body.capture([&] {
+    launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p); HC_COUNT();
+    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s);
+    apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part, 1, tk); HC_COUNT();
+    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk); HC_COUNT();
+    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s);
+    apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part, 3, tk); HC_COUNT();
+    launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
+           part, tk); HC_COUNT();
+    k_dev_cond<<<1, 32, 0, s>>>(ks, h, maxit);
+  });
+  gb.capture([&] { launch(k_dev_check, 1, 1, 0, s, (const double*)ks, maxit, ns); HC_COUNT(); });
 }
 
 }  // namespace hc

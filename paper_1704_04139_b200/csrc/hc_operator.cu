@@ -675,6 +675,7 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
   if (const char* e = getenv("HC_STENCIL")) op->stencil_kind = atoi(e);
   if (const char* e = getenv("HC_KRYLOV_BATCH")) op->krylov_batch = std::max(1, atoi(e));
   if (const char* e = getenv("HC_KRYLOV_WHILE")) op->krylov_while = atoi(e) != 0;
+  if (const char* e = getenv("HC_NEWTON_DEV")) op->newton_dev = atoi(e) != 0;
   HC_CUDA(cudaEventCreateWithFlags(&op->ev_in, cudaEventDisableTiming));
   HC_CUDA(cudaEventCreateWithFlags(&op->ev_out, cudaEventDisableTiming));
   op->labels.alloc(nvox);

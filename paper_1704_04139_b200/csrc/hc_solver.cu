@@ -3,6 +3,7 @@
 // adaptive implicit-Euler step with the explicit plated-inventory update.
 //
 // Reference: fvm/newton.py:62-206, fvm/timestepping.py:260-312.
+#include <chrono>
 #include <cmath>
 #include <algorithm>
 #include <initializer_list>
@@ -223,6 +224,104 @@ __global__ void k_sum(long long n, const double* __restrict__ a, double* __restr
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+
+// ---- device-resident Newton: scalar control kernels (state in ns[NS_*]) -------------
+// block-wide fixed-order reduction (sum or min) of nb partials; valid in thread 0
+template <bool MIN>
+__device__ double ns_reduce(const double* part, int nb) {
+  __shared__ double sh[32];
+  double v = MIN ? INFINITY : 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) v = MIN ? fmin(v, part[i]) : v + part[i];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double u = __shfl_down_sync(0xffffffffu, v, o);
+    v = MIN ? fmin(v, u) : v + u;
+  }
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : (MIN ? INFINITY : 0.0);
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_down_sync(0xffffffffu, v, o);
+      v = MIN ? fmin(v, u) : v + u;
+    }
+  }
+  __syncthreads();
+  return v;
+}
+
+// norm of k_sumsq2 partials (fields separately, then masked; +inf if any is non-finite)
+__global__ void k_ns_norm(int nb, const double* __restrict__ part, int mask, double scale, double* ns,
+                          int slot) {
+  const double c = ns_reduce<false>(part, nb);
+  const double p = ns_reduce<false>(part + nb, nb);
+  if (threadIdx.x != 0) return;
+  double v;
+  if (!isfinite(c) || !isfinite(p)) v = INFINITY;
+  else v = sqrt((mask & 1 ? c : 0.0) + (mask & 2 ? p : 0.0));
+  ns[slot] = scale * v;
+}
+// tolerance rule of newton.py: max(atol, rtol |F0|, floor); floor arrives in ns[NS_TOL]
+__global__ void k_ns_init(double* ns, double atol, double rtol) {
+  const double n0 = ns[NS_NORM0];
+  ns[NS_IT] = 0.0;
+  ns[NS_KITERS] = 0.0;
+  ns[NS_NORM] = n0;
+  ns[NS_WHY] = 0.0;
+  if (!isfinite(n0)) { ns[NS_STATUS] = 2.0; ns[NS_WHY] = 1.0; return; }
+  const double tol = fmax(fmax(atol, rtol * n0), ns[NS_TOL]);
+  ns[NS_TOL] = tol;
+  ns[NS_STATUS] = n0 <= tol ? 1.0 : 0.0;
+}
+__global__ void k_ns_newton_cond(const double* ns, cudaGraphConditionalHandle h, int max_iter) {
+  cudaGraphSetConditional(h, (ns[NS_STATUS] == 0.0 && ns[NS_IT] < (double)max_iter) ? 1u : 0u);
+}
+__global__ void k_ns_rebuild_cond(const double* ns, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, (ns[NS_IT] == 0.0 && ns[NS_REBUILD] != 0.0 && ns[NS_STATUS] == 0.0) ? 1u : 0u);
+}
+__global__ void k_ns_lintol(double* ns, double linear_rtol, double safety) {
+  ns[NS_LINTOL] = fmin(0.1, fmax(linear_rtol, safety * ns[NS_TOL] / ns[NS_NORM]));
+}
+// positivity guard: alpha = min(1, 0.99 min_i c_i / -d_i) over the block minima
+__global__ void k_ns_guard(int rb, const double* __restrict__ part, double* ns, cudaGraphConditionalHandle h) {
+  const double lim = ns_reduce<true>(part, rb);
+  if (threadIdx.x != 0) return;
+  double alpha = 1.0;
+  if (isfinite(lim)) alpha = fmin(alpha, 0.99 * lim);
+  if (alpha <= 0.0 && ns[NS_STATUS] == 0.0) { ns[NS_STATUS] = 2.0; ns[NS_WHY] = 2.0; }
+  ns[NS_ALPHA] = alpha;
+  ns[NS_ACC] = 0.0;
+  ns[NS_H] = 0.0;
+  ns[NS_NTRY] = INFINITY;
+  cudaGraphSetConditional(h, ns[NS_STATUS] == 0.0 ? 1u : 0u);
+}
+__global__ void k_ns_axpy(long long n, const double2* __restrict__ a, const double* __restrict__ ns,
+                          const double2* __restrict__ b, double2* __restrict__ y) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double alpha = ns[NS_ALPHA];
+  double2 u = a[i], w = b[i];
+  y[i] = make_double2(u.x + alpha * w.x, u.y + alpha * w.y);
+}
+// backtracking (8 halvings): accept if finite and no worse than the current residual or
+// already within tolerance; otherwise halve alpha and try again
+__global__ void k_ns_ls(double* ns, cudaGraphConditionalHandle h) {
+  const double nt = ns[NS_NTRY];
+  if (isfinite(nt) && (nt <= ns[NS_NORM] || nt <= ns[NS_TOL])) ns[NS_ACC] = 1.0;
+  else { ns[NS_ALPHA] *= 0.5; ns[NS_H] += 1.0; }
+  cudaGraphSetConditional(h, (ns[NS_STATUS] == 0.0 && ns[NS_ACC] == 0.0 && ns[NS_H] <= 8.0) ? 1u : 0u);
+}
+__global__ void k_ns_lsfinal_cond(const double* ns, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, (ns[NS_STATUS] == 0.0 && ns[NS_ACC] == 0.0) ? 1u : 0u);
+}
+__global__ void k_ns_lsfinal_check(double* ns) {
+  if (!isfinite(ns[NS_NTRY])) { ns[NS_STATUS] = 2.0; ns[NS_WHY] = 3.0; }
+}
+__global__ void k_ns_accept(double* ns) {
+  if (ns[NS_STATUS] != 0.0) return;
+  ns[NS_NORM] = ns[NS_NTRY];
+  ns[NS_IT] += 1.0;
+  if (ns[NS_NORM] <= ns[NS_TOL]) ns[NS_STATUS] = 1.0;
+}
 }  // namespace
 
 // ------------------------------------------------------------------ workspace
@@ -361,12 +460,203 @@ static void ensure_amg(Operator& op) {
   if (!op.amg) op.amg = build_amg(op);
 }
 
+// ---- device-resident Newton solve -----------------------------------------------------
+// The whole newton_solve of one implicit step (newton.py:86-168) as ONE CUDA graph: a
+// WHILE node over Newton iterations whose body linearizes, rebuilds the multigrid values
+// under an IF node, runs the BiCGStab WHILE loop, applies the positivity guard and the
+// backtracking line search (another WHILE node) — every decision taken by one-thread
+// kernels on device scalars.  The host launches the graph and reads the scalars once.
+struct NewtonGraph {
+  cudaGraphExec_t exec = nullptr;
+  double dt = -1.0, mu = 0.0;
+  const double* npl = nullptr;
+  hc_solver_config cfg{};
+  DBuf<double> ns;
+  double* ns_host = nullptr;
+  unsigned long long per_iter_kernels = 0;
+  ~NewtonGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (ns_host) cudaFreeHost(ns_host);
+  }
+};
+void destroy_newton_graph(NewtonGraph* g) { delete g; }
+
+static bool same_cfg(const hc_solver_config& a, const hc_solver_config& b) {
+  return a.newton_rtol == b.newton_rtol && a.newton_atol == b.newton_atol &&
+         a.newton_max_iter == b.newton_max_iter && a.krylov_max_iter == b.krylov_max_iter &&
+         a.linear_rtol == b.linear_rtol && a.implicit_plated == b.implicit_plated &&
+         a.linear_safety == b.linear_safety;
+}
+
+static void build_newton_graph(Operator& op, NewtonGraph& NG, const double* npl, double dt, double mu,
+                               const hc_solver_config& cfg, cudaStream_t s) {
+  Work& W = work(op);
+  const long long n = op.P.nvox;
+  const int nb = nblk(n);
+  const int rb = red_blocks(op);
+  const double inv_dt = 1.0 / dt;
+  const double beta = cfg.implicit_plated ? dt * op.info.face_area / op.host_params.faraday : 0.0;
+  const int parts = PART_LIN | PART_BV | PART_1C | PART_BND | PART_TIME;
+  double* ns = NG.ns.p;
+  cudaGraph_t outer;
+  HC_CUDA(cudaGraphCreate(&outer, 0));
+  const unsigned long long c0 = t_launch_count;
+  op.capturing = true;
+  try {
+    GraphBuilder gb{s, outer, {}};
+    auto norm_into = [&](const double2* v, int slot, double scale) {
+      k_sumsq2<<<rb, TPB, 0, s>>>(n, v, W.part.p); HC_COUNT();
+      k_ns_norm<<<1, 256, 0, s>>>(rb, W.part.p, 3, scale, ns, slot); HC_COUNT();
+    };
+    cudaGraphConditionalHandle hn = gb.handle(0);
+    gb.capture([&] {
+      residual_grid(op, W.x.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.r.p, s);
+      norm_into(W.r.p, NS_NORM0, 1.0);
+      k_abs_lin<<<vox_grid(op.P), vox_block(), 0, s>>>(op.P, op.labels.p, W.x.p, inv_dt, W.rt.p); HC_COUNT();
+      norm_into(W.rt.p, NS_TOL, 1e-13);
+      k_ns_init<<<1, 1, 0, s>>>(ns, cfg.newton_atol, cfg.newton_rtol); HC_COUNT();
+      k_ns_newton_cond<<<1, 1, 0, s>>>(ns, hn, cfg.newton_max_iter); HC_COUNT();
+    });
+    GraphBuilder body{s, gb.cond(hn, cudaGraphCondTypeWhile), {}};
+    cudaGraphConditionalHandle hr = body.handle(0);
+    body.capture([&] {
+      linearize(op, W.x.p, npl, beta, s);
+      k_ns_rebuild_cond<<<1, 1, 0, s>>>(ns, hr); HC_COUNT();
+    });
+    {
+      GraphBuilder rbld{s, body.cond(hr, cudaGraphCondTypeIf), {}};
+      rbld.capture([&] { amg_update(op, inv_dt, 3, s); });
+    }
+    body.capture([&] {
+      k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
+      k_ns_lintol<<<1, 1, 0, s>>>(ns, cfg.linear_rtol, cfg.linear_safety); HC_COUNT();
+    });
+    krylov_append(op, body, W.b.p, W.d.p, inv_dt, 0, ns + NS_LINTOL, cfg.krylov_max_iter, ns);
+    cudaGraphConditionalHandle hl = body.handle(0);
+    body.capture([&] {
+      k_pos_min<<<rb, TPB, 0, s>>>(op.P, op.labels.p, W.x.p, W.d.p, W.part.p); HC_COUNT();
+      k_ns_guard<<<1, 256, 0, s>>>(rb, W.part.p, ns, hl); HC_COUNT();
+    });
+    auto trial = [&](GraphBuilder& b) {
+      b.capture([&] {
+        k_ns_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, ns, W.d.p, W.xt.p); HC_COUNT();
+        residual_grid(op, W.xt.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.rt.p, s);
+        norm_into(W.rt.p, NS_NTRY, 1.0);
+      });
+    };
+    {
+      GraphBuilder ls{s, body.cond(hl, cudaGraphCondTypeWhile), {}};
+      trial(ls);
+      ls.capture([&] { k_ns_ls<<<1, 1, 0, s>>>(ns, hl); HC_COUNT(); });
+    }
+    cudaGraphConditionalHandle hf = body.handle(0);
+    body.capture([&] { k_ns_lsfinal_cond<<<1, 1, 0, s>>>(ns, hf); HC_COUNT(); });
+    {
+      GraphBuilder fin{s, body.cond(hf, cudaGraphCondTypeIf), {}};
+      trial(fin);
+      fin.capture([&] { k_ns_lsfinal_check<<<1, 1, 0, s>>>(ns); HC_COUNT(); });
+    }
+    body.capture([&] {
+      HC_CUDA(cudaMemcpyAsync(W.x.p, W.xt.p, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      HC_CUDA(cudaMemcpyAsync(W.r.p, W.rt.p, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      k_ns_accept<<<1, 1, 0, s>>>(ns); HC_COUNT();
+      k_ns_newton_cond<<<1, 1, 0, s>>>(ns, hn, cfg.newton_max_iter); HC_COUNT();
+    });
+    op.capturing = false;
+    NG.per_iter_kernels = t_launch_count - c0;
+    uncount(t_launch_count - c0);
+    if (NG.exec) cudaGraphExecDestroy(NG.exec);
+    NG.exec = nullptr;
+    HC_CUDA(cudaGraphInstantiate(&NG.exec, outer, 0));
+    HC_CUDA(cudaGraphUpload(NG.exec, s));
+  } catch (...) {
+    op.capturing = false;
+    uncount(t_launch_count - c0);
+    cudaGraphDestroy(outer);
+    cudaGetLastError();
+    throw;
+  }
+  cudaGraphDestroy(outer);
+  NG.dt = dt;
+  NG.mu = mu;
+  NG.npl = npl;
+  NG.cfg = cfg;
+}
+
+// returns false if the device path is unavailable (the caller runs the host loop)
+static bool newton_grid_dev(Operator& op, const double* npl, double dt, double mu,
+                            const hc_solver_config& cfg, hc_newton_stats& st, cudaStream_t s) {
+  Amg& A = *op.amg;
+  if (!op.newton_dev || A.refresh || op.iterate_hook || !op.dev_krylov || !op.krylov_while) return false;
+  if (!op.ng) {
+    op.ng = new NewtonGraph();
+    op.ng->ns.alloc(NS_N);
+    HC_CUDA(cudaMallocHost(&op.ng->ns_host, NS_N * sizeof(double)));
+  }
+  NewtonGraph& NG = *op.ng;
+  const double inv_dt = 1.0 / dt;
+  if (!NG.exec || NG.dt != dt || NG.mu != mu || NG.npl != npl || !same_cfg(NG.cfg, cfg)) {
+    try {
+      auto t0 = std::chrono::steady_clock::now();
+      build_newton_graph(op, NG, npl, dt, mu, cfg, s);
+      if (op.krylov_log)
+        fprintf(stderr, "newton(dev): graph built in %.1f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    } catch (const Error& e) {
+      if (op.krylov_log) fprintf(stderr, "newton: device graph unavailable (%s), host loop\n", e.what());
+      op.newton_dev = false;
+      return false;
+    }
+  }
+  ++A.solves;
+  const bool rebuild = A.solves % A.refresh_solves == 1 || A.refresh_solves == 1 || A.last_inv_dt != inv_dt;
+  NG.ns_host[NS_REBUILD] = rebuild ? 1.0 : 0.0;
+  HC_CUDA(cudaMemcpyAsync(NG.ns.p + NS_REBUILD, NG.ns_host + NS_REBUILD, sizeof(double),
+                          cudaMemcpyHostToDevice, s));
+  auto tl = std::chrono::steady_clock::now();
+  HC_CUDA(cudaGraphLaunch(NG.exec, s));
+  const double launch_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
+  HC_CUDA(cudaMemcpyAsync(NG.ns_host, NG.ns.p, NS_N * sizeof(double), cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaStreamSynchronize(s));
+  if (op.krylov_log)
+    fprintf(stderr, "newton(dev): launch %.3f ms, launch+sync %.2f ms\n", launch_ms,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count());
+  const double* h = NG.ns_host;
+  if (op.krylov_log)
+    fprintf(stderr, "newton(dev): dt=%g status=%g it=%g kiters=%g norm0=%.3e tol=%.3e norm=%.3e lintol=%.3e rebuild=%d why=%g\n",
+            dt, h[NS_STATUS], h[NS_IT], h[NS_KITERS], h[NS_NORM0], h[NS_TOL], h[NS_NORM], h[NS_LINTOL],
+            (int)rebuild, h[NS_WHY]);
+  if (rebuild && h[NS_IT] + (h[NS_STATUS] == 1.0 ? 0.0 : 1.0) > 0.0) A.last_inv_dt = inv_dt;
+  count_graph_launch(NG.per_iter_kernels * (unsigned long long)std::max(1.0, h[NS_IT]));
+  st.norm0 = h[NS_NORM0];
+  st.tol = h[NS_TOL];
+  st.n_iter = (int)h[NS_IT];
+  st.norm_final = h[NS_NORM];
+  st.krylov_iters += (int)h[NS_KITERS];
+  if (h[NS_STATUS] == 1.0) return true;
+  const int why = (int)h[NS_WHY];
+  char msg[200];
+  if (why == 1)
+    snprintf(msg, sizeof msg, "initial residual not evaluable: operator produced a non-finite value");
+  else if (why == 2)
+    snprintf(msg, sizeof msg, "positivity guard blocked the Newton step");
+  else if (why == 3)
+    snprintf(msg, sizeof msg, "residual not evaluable under damping");
+  else if (why >= 9)
+    snprintf(msg, sizeof msg, "iterative linear solver stalled (%s)", why == 9 ? "iteration budget" : "breakdown");
+  else
+    snprintf(msg, sizeof msg, "Newton did not reach tolerance %.3e in %d iterations (last residual %.3e)",
+             h[NS_TOL], cfg.newton_max_iter, h[NS_NORM]);
+  throw Error(HC_ERR_NONCONVERGENCE, msg);
+}
+
 // newton_solve (newton.py:86-168) on the grid layout.  W.x holds the guess on
 // entry and the solution on exit; W.cprev holds c_prev per voxel.
 void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc_solver_config& cfg,
                  hc_newton_stats& st, cudaStream_t s) {
   if (!(dt > 0)) throw Error(HC_ERR_ARGUMENT, "dt must be positive");
   ensure_amg(op);
+  if (newton_grid_dev(op, npl, dt, mu, cfg, st, s)) return;
   Work& W = work(op);
   const long long n = op.P.nvox;
   const int nb = nblk(n);

@@ -1,6 +1,7 @@
 """GPU: the solver's execution variants reach the same implicit step.
 
-The device-side WHILE-node Krylov loop vs batched iteration graphs, the optional
+The device-resident Newton graph (Newton / line search / Krylov loops as conditional
+nodes), the device-side WHILE-node Krylov loop vs batched iteration graphs, the optional
 cluster-fused coarse multigrid cycle and the cp.async stencil path are
 execution strategies, not different algorithms: the Newton solution of one implicit
 step must agree to the Newton tolerance.  Each variant is selected by its environment
@@ -37,6 +38,7 @@ def _step_with(env):
 
 
 @pytest.mark.parametrize("env", [
+    {"HC_NEWTON_DEV": "1"},
     {"HC_KRYLOV_WHILE": "0"},
     {"HC_AMG_FUSE_ROWS": "4096"},
     {"HC_STENCIL": "2"},
