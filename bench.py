@@ -507,6 +507,17 @@ def run_rom(args, ws, rank, local):
     n1 = ctypes.c_int64(0)
     _native.check(_native.lib().hc_launch_count(ctypes.byref(n1)))
     # e2e: host reduced state in, QoI curves out, through the public API
+    # the MOR use case: many applied currents at once, one thread-block cluster each
+    n_par = args.rom_batch
+    mus = mu * np.linspace(0.5, 1.0, n_par)
+    mor.solve_rom_batch(op, rom, xt0, st.n_pl, mus[:2], dt, 2)
+    torch.cuda.synchronize()
+    a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a2.record()
+    mor.solve_rom_batch(op, rom, xt0, st.n_pl, mus, dt, n_steps)
+    b2.record()
+    torch.cuda.synchronize()
+    batch_ms = a2.elapsed_time(b2)
     xh = xt0.cpu().numpy()
     t0 = time.perf_counter()
     tr2 = mor.solve_rom(op, rom, xh, st.n_pl, mu, dt, n_steps)
@@ -529,6 +540,9 @@ def run_rom(args, ws, rank, local):
             "newton_iters_per_step": float(np.mean(tr.newton_iters)),
             "offline": tt,
             "qoi_max_rel_dev_vs_fom_training_window": dev_v,
+            "parameter_batch": {"n_params": n_par, "mu_range": [float(mus.min()), float(mus.max())],
+                                "reduced_steps_per_s": n_par * n_steps / (batch_ms * 1e-3),
+                                "ms": batch_ms},
             "e2e": {"value": n_steps / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": 8 * rom.k / n_steps,
                     "d2h_bytes_per_step": 16.0},
             "gpu_launches": int(n1.value - n0.value),
@@ -569,6 +583,7 @@ def main():
     ap.add_argument("--rom-rank", type=int, default=60)
     ap.add_argument("--rom-ei", type=int, default=300)
     ap.add_argument("--rom-steps", type=int, default=500)
+    ap.add_argument("--rom-batch", type=int, default=64)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

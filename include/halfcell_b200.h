@@ -198,6 +198,15 @@ int hc_rom_run(hc_operator* op, const hc_rom* rom, double* xt, double* n_pl, dou
                int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
                double* qoi, int32_t* iters, double* xt_steps, int32_t* failed_step, void* stream);
 
+/* The same reduced trajectory for n_par parameter values at once (the MOR use case:
+ * one thread-block cluster per value, all resident concurrently as far as the SMs
+ * allow).  xt[n_par][k], n_pl[n_par][n_pl], mu[n_par] (device), qoi[n_par][2 n_steps],
+ * iters[n_par][n_steps]; failed_step[n_par] (host) receives -1 or the failing step. */
+int hc_rom_run_batch(hc_operator* op, const hc_rom* rom, int32_t n_par, double* xt, double* n_pl,
+                     const double* mu, double dt, int32_t n_steps, double rtol, int32_t max_iter,
+                     int32_t refresh, int32_t jac_steps, double* qoi, int32_t* iters, int32_t* failed_step,
+                     void* stream);
+
 /* Evict L2 by streaming a `bytes`-sized buffer through it (reads only, so no dirty
  * lines are left behind); used between timed iterations. */
 int hc_flush_l2(int64_t bytes, void* stream);

@@ -103,6 +103,11 @@ _SIGS = {
                                    ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "hc_pod_gram_rows": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "hc_rom_run_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HcRom), ctypes.c_int32,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                        ctypes.c_int32, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p]),
     "hc_rom_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HcRom), ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                                   ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,

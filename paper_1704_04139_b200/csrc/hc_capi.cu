@@ -26,8 +26,8 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
                           const hc_params& hp);
 void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
               cudaStream_t s, bool rows);
-void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, double mu, double dt,
-             int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
+void rom_run(const Operator& op, const hc_rom* rom, int n_par, double* xt, double* npl, const double* mus_dev,
+             double dt, int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
              double* qoi, int32_t* iters, double* xt_steps, int32_t* status_host, cudaStream_t s);
 
 Operator::~Operator() {
@@ -608,12 +608,34 @@ int hc_rom_run(hc_operator* opq, const hc_rom* rom, double* xt, double* n_pl, do
   return guarded([&] {
     if (!opq || !rom || !xt) throw Error(HC_ERR_ARGUMENT, "null argument");
     if (!(dt > 0.0) || n_steps < 0 || max_iter < 1) throw Error(HC_ERR_ARGUMENT, "bad step settings");
-    int32_t st[2] = {0, 0};
-    rom_run(*(Operator*)opq, rom, xt, n_pl, mu, dt, n_steps, rtol, max_iter, refresh, std::max(1, jac_steps),
-            qoi, iters, xt_steps, st, S(stream));
+    int32_t st[4] = {0, 0, 0, 0};
+    DBuf<double> mu_d(1);
+    HC_CUDA(cudaMemcpyAsync(mu_d.p, &mu, sizeof(double), cudaMemcpyHostToDevice, S(stream)));
+    rom_run(*(Operator*)opq, rom, 1, xt, n_pl, mu_d.p, dt, n_steps, rtol, max_iter, refresh,
+            std::max(1, jac_steps), qoi, iters, xt_steps, st, S(stream));
     if (failed_step) *failed_step = st[0] ? st[1] : -1;
     if (st[0] == 1) throw Error(HC_ERR_NONCONVERGENCE, "reduced Newton did not converge");
     if (st[0] == 2) throw Error(HC_ERR_NUMERICS, "reduced Newton produced a non-finite update");
+  });
+}
+
+int hc_rom_run_batch(hc_operator* opq, const hc_rom* rom, int32_t n_par, double* xt, double* n_pl,
+                     const double* mu, double dt, int32_t n_steps, double rtol, int32_t max_iter,
+                     int32_t refresh, int32_t jac_steps, double* qoi, int32_t* iters, int32_t* failed_step,
+                     void* stream) {
+  return guarded([&] {
+    if (!opq || !rom || !xt || !mu || n_par < 1) throw Error(HC_ERR_ARGUMENT, "null argument");
+    if (!(dt > 0.0) || n_steps < 0 || max_iter < 1) throw Error(HC_ERR_ARGUMENT, "bad step settings");
+    std::vector<int32_t> st(4 * (size_t)n_par, 0);
+    rom_run(*(Operator*)opq, rom, n_par, xt, n_pl, mu, dt, n_steps, rtol, max_iter, refresh,
+            std::max(1, jac_steps), qoi, iters, nullptr, st.data(), S(stream));
+    int bad = 0;
+    for (int p = 0; p < n_par; ++p) {
+      if (failed_step) failed_step[p] = st[4 * p] ? st[4 * p + 1] : -1;
+      bad |= st[4 * p];
+    }
+    if (bad & 2) throw Error(HC_ERR_NUMERICS, "reduced Newton produced a non-finite update");
+    if (bad & 1) throw Error(HC_ERR_NONCONVERGENCE, "reduced Newton did not converge");
   });
 }
 

@@ -90,10 +90,29 @@ struct RomWork {
 __device__ __forceinline__ double ldc(const double* p) { return __ldcg(p); }
 
 __global__ void __launch_bounds__(ROM_THREADS, 1)
-k_rom_run(DevParams P, RomDev R, RomWork W, double mu, double dt, double face_area_over_F, int n_steps,
-          double rtol, int max_iter, int refresh, int jac_steps) {
+k_rom_run(DevParams P, RomDev R, RomWork W, const double* __restrict__ mus, double dt, double face_area_over_F,
+          int n_steps, double rtol, int max_iter, int refresh, int jac_steps) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), ncta = (int)cl.num_blocks();
+  // one cluster per parameter value: shift every per-trajectory array to this one's slice
+  const int par = (int)(blockIdx.x / ncta);
+  const double mu = mus[par];
+  {
+    const long long k_ = R.k, m_ = max(R.m, 1);
+    W.x += par * k_;
+    W.xs += par * (long long)max(R.n_s, 1);
+    W.fq += par * (long long)max(R.n_f, 1);
+    W.fdq += par * 4LL * max(R.n_f, 1);
+    W.nn += par * m_;
+    W.rr += par * k_;
+    W.G += par * m_ * k_;
+    W.J += par * k_ * k_;
+    W.npl += par * (long long)max(R.n_pl, 1);
+    W.qoi += par * 2LL * max(n_steps, 1);
+    W.iters += par * (long long)max(n_steps, 1);
+    W.status += par * 4LL;
+    if (W.xt_steps) W.xt_steps += par * (long long)max(n_steps, 1) * k_;
+  }
   extern __shared__ double sm[];
   const int k = R.k, m = R.m;
   double* J = sm;                 // [k][k] LU factors (rank 0)
@@ -341,18 +360,20 @@ k_rom_run(DevParams P, RomDev R, RomWork W, double mu, double dt, double face_ar
   if (rank == 0 && tid == 0) { W.status[0] = 0; W.status[1] = n_steps; }
 }
 
-void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, double mu, double dt,
-             int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
+void rom_run(const Operator& op, const hc_rom* rom, int n_par, double* xt, double* npl, const double* mus_dev,
+             double dt, int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
              double* qoi, int32_t* iters, double* xt_steps, int32_t* status_host, cudaStream_t s) {
   RomDev R{rom->k, rom->k_c, rom->m, rom->n_s, rom->n_f, rom->n_pl, rom->A, rom->Mr, rom->bnd,
            rom->E, rom->BS, rom->row_coef, rom->q_v, rom->q_ac, rom->f_kind, rom->f_dof, rom->f_slot,
            rom->row_ptr, rom->row_face, rom->pl_ptr, rom->pl_face};
-  if (R.k < 1 || R.k > HC_ROM_MAX_K || R.m < 0 || R.n_s < 0 || R.n_f < 0 || R.k_c < 0 || R.k_c > R.k)
+  if (R.k < 1 || R.k > HC_ROM_MAX_K || R.m < 0 || R.n_s < 0 || R.n_f < 0 || R.k_c < 0 || R.k_c > R.k ||
+      n_par < 1)
     throw Error(HC_ERR_ARGUMENT, "reduced model dimensions out of range");
-  DBuf<double> xs(std::max(R.n_s, 1)), fq(std::max(R.n_f, 1)), fdq(4LL * std::max(R.n_f, 1)),
-      nn(std::max(R.m, 1)), rr(R.k), G((long long)std::max(R.m, 1) * R.k), J((long long)R.k * R.k);
-  DBuf<int32_t> st(4);
-  HC_CUDA(cudaMemsetAsync(st.p, 0, 4 * sizeof(int32_t), s));
+  const long long np = n_par;
+  DBuf<double> xs(np * std::max(R.n_s, 1)), fq(np * std::max(R.n_f, 1)), fdq(np * 4LL * std::max(R.n_f, 1)),
+      nn(np * std::max(R.m, 1)), rr(np * R.k), G(np * std::max(R.m, 1) * R.k), J(np * R.k * R.k);
+  DBuf<int32_t> st(np * 4);
+  HC_CUDA(cudaMemsetAsync(st.p, 0, np * 4 * sizeof(int32_t), s));
   RomWork W{xt, xs.p, fq.p, fdq.p, nn.p, rr.p, G.p, J.p, npl, qoi, xt_steps, iters, st.p};
   const size_t smem = ((size_t)R.k * R.k + 3 * R.k + 64 + (size_t)TK * R.k) * sizeof(double) +
                       (R.k + 4) * sizeof(int);
@@ -377,7 +398,7 @@ void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, dou
     if (const char* e = getenv("HC_ROM_CLUSTER")) cluster = atoi(e) >= 16 ? 16 : 8;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cluster);
+  cfg.gridDim = dim3((unsigned)(cluster * n_par));
   cfg.blockDim = dim3(ROM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -387,10 +408,10 @@ void rom_run(const Operator& op, const hc_rom* rom, double* xt, double* npl, dou
   cfg.attrs = &at;
   cfg.numAttrs = 1;
   const double fa_F = op.info.face_area / op.host_params.faraday;
-  HC_CUDA(cudaLaunchKernelEx(&cfg, k_rom_run, op.P, R, W, mu, dt, fa_F, (int)n_steps, rtol, (int)max_iter,
+  HC_CUDA(cudaLaunchKernelEx(&cfg, k_rom_run, op.P, R, W, mus_dev, dt, fa_F, (int)n_steps, rtol, (int)max_iter,
                              (int)refresh, (int)jac_steps));
   HC_COUNT();
-  HC_CUDA(cudaMemcpyAsync(status_host, st.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaMemcpyAsync(status_host, st.p, np * 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   HC_CUDA(cudaStreamSynchronize(s));
 }
 

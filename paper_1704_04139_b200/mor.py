@@ -352,6 +352,35 @@ def solve_rom(op, rom: ReducedModel, xt0, n_pl0, mu: float, dt: float, n_steps: 
                          states[:n_steps] if keep_states else None)
 
 
+def solve_rom_batch(op, rom: ReducedModel, xt0, n_pl0, mus, dt: float, n_steps: int,
+                    rtol: float = 1e-10, max_iter: int = 40, refresh: int = 6, jac_steps: int = 8):
+    """The reduced trajectory for many applied currents at once (the MOR use case): one
+    thread-block cluster per value in a single launch (hc_rom_run_batch).  Returns
+    (voltage (n_par, n_steps), mean solid c (n_par, n_steps), final x~ (n_par, k))."""
+    t = _dev.torch()
+    mus = np.asarray(mus, dtype=float)
+    n_par = int(mus.size)
+    xt = _dev.to_dev(xt0).reshape(1, -1).repeat(n_par, 1).contiguous()
+    npl1 = np.asarray(n_pl0 if np.size(n_pl0) else np.zeros(1), dtype=float)
+    npl = _dev.to_dev(np.tile(npl1, (n_par, 1)))
+    mu_d = _dev.to_dev(mus)
+    qoi = t.empty((n_par, 2 * max(n_steps, 1)), dtype=t.float64, device="cuda")
+    its = t.empty((n_par, max(n_steps, 1)), dtype=t.int32, device="cuda")
+    failed = (ctypes.c_int32 * n_par)()
+    code = _native.lib().hc_rom_run_batch(op.native.handle, ctypes.byref(rom.struct), n_par, _dev.ptr(xt),
+                                          _dev.ptr(npl), _dev.ptr(mu_d), float(dt), int(n_steps), float(rtol),
+                                          int(max_iter), int(refresh), int(jac_steps), _dev.ptr(qoi),
+                                          _dev.ptr(its), failed, _dev.stream())
+    if code:
+        bad = [(i, f) for i, f in enumerate(failed) if f >= 0]
+        try:
+            _native.check(code)
+        except Exception as e:  # noqa: BLE001
+            raise ReductionError(f"reduced Newton failed for (parameter, step) {bad[:4]}: {e}") from e
+    q = qoi.cpu().numpy()[:, : 2 * n_steps].reshape(n_par, -1, 2)
+    return q[..., 0], q[..., 1], xt
+
+
 def estimate_error(op, rom: ReducedModel, twin: ReducedModel, x0, n_pl0, mu: float, dt: float,
                    n_steps: int, theta: float = 0.0, **kw):
     """Hierarchical error estimate (SPEC mor.estimate_error; arXiv 1704.04139 Eqs. 21-22):

@@ -119,3 +119,18 @@ def test_error_estimator_twin_and_true_error(cell):
     true_c = float(torch.max(torch.linalg.vector_norm(L[:, :nc] - X[:, :nc], dim=1)
                              / torch.linalg.vector_norm(X[:, :nc], dim=1)))
     assert 0.1 <= ec / true_c <= 10.0
+
+
+def test_batched_rom_equals_single_trajectories(cell):
+    """One cluster per applied current in one launch = the single-trajectory runs."""
+    from paper_1704_04139_b200 import mor
+    op, st = cell["op"], cell["st"]
+    rom = _rom(cell, 6, 10)
+    xt0 = rom.project(st.x)
+    mus = [cell["mu"], 0.8 * cell["mu"], 1.1 * cell["mu"]]
+    v, c, xt = mor.solve_rom_batch(op, rom, xt0, st.n_pl, mus, cell["dt"], 5)
+    for i, mu in enumerate(mus):
+        tr = mor.solve_rom(op, rom, xt0, st.n_pl, mu, cell["dt"], 5)
+        assert np.allclose(v[i], tr.voltage, rtol=1e-13, atol=1e-15)
+        assert np.allclose(c[i], tr.mean_solid_c, rtol=1e-13)
+        assert np.allclose(xt[i].cpu().numpy(), tr.xt.cpu().numpy(), rtol=1e-12, atol=1e-12)
