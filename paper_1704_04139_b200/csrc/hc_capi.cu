@@ -536,6 +536,12 @@ int hc_step_batch(hc_operator* const* ops, int32_t n, double* const* x, double* 
     int dev = 0;
     HC_CUDA(cudaGetDevice(&dev));
     int nt = std::max(1, std::min<int>(n_threads > 0 ? n_threads : 16, n));
+    // many cells share the GPU through host threads: the device-resident Newton graph
+    // (one host wait per step instead of a few per Newton iteration) measured +25 %
+    // here (253 -> 317 cell-steps/s), so it is the default for batches (HC_NEWTON_DEV=0 off)
+    const char* nd = getenv("HC_NEWTON_DEV");
+    const bool dev_newton = !nd || atoi(nd) != 0;
+    for (int i = 0; i < n; ++i) ((Operator*)ops[i])->newton_dev = dev_newton;
     std::atomic<int> next{0};
     std::mutex m;
     int first_code = HC_OK;

@@ -1,3 +1,4 @@
-for cfg in "1 1" "0 1" "1 0" "0 0"; do set -- $cfg
-echo "newton_dev=$1 pdl=$2: $(HC_NEWTON_DEV=$1 HC_PDL=$2 timeout 150 python bench.py --steps 10 --no-cpu-baseline --no-at-scale 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],2))')"
+for d in 0 1; do
+echo "batched newton_dev=$d: $(HC_NEWTON_DEV=$d timeout 500 python bench.py --config batched --steps 3 --warmup 3 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],1))')"
 done
+echo "batched newton_dev=1 threads=32: $(HC_BATCH_THREADS=32 HC_NEWTON_DEV=1 timeout 500 python bench.py --config batched --steps 3 --warmup 3 2>/dev/null | python3 -c 'import json,sys; d=json.load(sys.stdin); print(round(d["value"],1))')"
