@@ -355,14 +355,15 @@ __global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict
   }
 }
 
+template <class TV>
 __global__ void k_csr_prolong(int n, double alpha, const int32_t* __restrict__ prp,
-                              const int32_t* __restrict__ pci, const double* __restrict__ pv,
+                              const int32_t* __restrict__ pci, const TV* __restrict__ pv,
                               const double* __restrict__ xn, double* __restrict__ x) {
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
-  for (int m = prp[i]; m < prp[i + 1]; ++m) s += pv[m] * xn[pci[m]];
+  for (int m = prp[i]; m < prp[i + 1]; ++m) s += (double)pv[m] * xn[pci[m]];
   x[i] += alpha * s;
 }
 
@@ -373,15 +374,16 @@ __global__ void k_vec_add(int n, const double* __restrict__ a, double* __restric
 }
 
 // b[I] = sum_q ptv[q] res[pt_row[q]] (P^T res), 8 lanes per coarse row
+template <class TV>
 __global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
-                             const int32_t* __restrict__ pt_row, const double* __restrict__ ptv,
+                             const int32_t* __restrict__ pt_row, const TV* __restrict__ ptv,
                              const double* __restrict__ res, double* __restrict__ b1) {
   pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int I = (int)(gt >> 3), lane = (int)(gt & 7);
   if (I >= n1) return;
   double s = 0.0;
-  for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += 8) s += ptv[q] * res[pt_row[q]];
+  for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += 8) s += (double)ptv[q] * res[pt_row[q]];
   s += __shfl_down_sync(0xffffffffu, s, 4, 8);
   s += __shfl_down_sync(0xffffffffu, s, 2, 8);
   s += __shfl_down_sync(0xffffffffu, s, 1, 8);
@@ -609,6 +611,8 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     upload(L.pt_row, trow);
     upload(L.pt_idx, tidx);
     L.ptv.alloc(std::max<size_t>(tidx.size(), 1));
+    L.ptvf.alloc(std::max<size_t>(tidx.size(), 1));
+    L.P.vf.alloc(std::max<long long>(L.P.nnz, 1));
     // AP = A P pattern, then next-level pattern P^T (AP)
     HPat AP;
     {
@@ -748,6 +752,10 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
                                            L.P.v.p); HC_COUNT();
       launch(k_gather_ptv, nblk((long long)L.P.nnz), TPB, 0, s, (long long)L.P.nnz, L.pt_idx.p, L.P.v.p,
                                                            L.ptv.p); HC_COUNT();
+      if (A.fp32_coarse && L.P.nnz) {   // fp32 transfer values for the cycle (restriction / prolongation)
+        launch(k_to_float, nblk(L.P.nnz), TPB, 0, s, (long long)L.P.nnz, (const double*)L.ptv.p, L.ptvf.p); HC_COUNT();
+        launch(k_to_float, nblk(L.P.nnz), TPB, 0, s, (long long)L.P.nnz, (const double*)L.P.v.p, L.P.vf.p); HC_COUNT();
+      }
       launch(k_ap_w, nblk(32LL * L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.P.rp.p, L.P.ci.p, L.P.v.p,
                                      L.AP.rp.p, L.AP.ci.p, L.AP.v.p); HC_COUNT();
       launch(k_ptap_w, nblk(32LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p, L.P.v.p,
@@ -1012,7 +1020,11 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
     launch(k_csr_smooth0, nblk(L.n), TPB, 0, s, L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
     csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.res.p, 1, s);
   }
-  launch(k_restrict_v, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, L.ptv.p, L.res.p,
+  if (A.fp32_coarse)
+    launch(k_restrict_v<float>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, (const float*)L.ptvf.p, L.res.p,
+           U.b.p);
+  else
+  launch(k_restrict_v<double>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, (const double*)L.ptv.p, L.res.p,
                                                U.b.p); HC_COUNT();
   solve_level(A, B, l + 1, s);
   const bool tentative = L.P.nnz == (long long)L.n;  // one prolongator entry per row
@@ -1023,7 +1035,11 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
     std::swap(L.x.p, L.x2.p);
     --post;
   } else {
-    launch(k_csr_prolong, nblk(L.n), TPB, 0, s, L.n, B.alpha, L.P.rp.p, L.P.ci.p, L.P.v.p, U.x.p,
+    if (A.fp32_coarse)
+      launch(k_csr_prolong<float>, nblk(L.n), TPB, 0, s, L.n, B.alpha, L.P.rp.p, L.P.ci.p, (const float*)L.P.vf.p, U.x.p,
+             L.x.p);
+    else
+    launch(k_csr_prolong<double>, nblk(L.n), TPB, 0, s, L.n, B.alpha, L.P.rp.p, L.P.ci.p, (const double*)L.P.v.p, U.x.p,
                                             L.x.p); HC_COUNT();
   }
   for (int k = 0; k < post; ++k) {
@@ -1063,8 +1079,9 @@ __global__ void k_smooth0_s(long long n, double w, const double* __restrict__ di
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v < n) e[v] = w * dinv[v] * r[v];
 }
+template <class TV>
 __global__ void k_prolong0_s(long long n, double alpha, const int32_t* __restrict__ prp,
-                             const int32_t* __restrict__ pci, const double* __restrict__ pv,
+                             const int32_t* __restrict__ pci, const TV* __restrict__ pv,
                              const double* __restrict__ x1, double* __restrict__ e) {
   pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -1072,7 +1089,7 @@ __global__ void k_prolong0_s(long long n, double alpha, const int32_t* __restric
   int p0 = prp[v], p1 = prp[v + 1];
   if (p0 == p1) return;
   double s = 0.0;
-  for (int m = p0; m < p1; ++m) s += pv[m] * x1[pci[m]];
+  for (int m = p0; m < p1; ++m) s += (double)pv[m] * x1[pci[m]];
   e[v] += alpha * s;
 }
 // T r split into scalar field right-hand sides
@@ -1138,10 +1155,18 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
     }
   }
   sweep(EP_RESID, e, A.res.p);
-  launch(k_restrict_v, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, L0.ptv.p, A.res.p,
+  if (A.fp32_coarse)
+    launch(k_restrict_v<float>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const float*)L0.ptvf.p,
+           A.res.p, L1.b.p);
+  else
+  launch(k_restrict_v<double>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const double*)L0.ptv.p, A.res.p,
                                                 L1.b.p); HC_COUNT();
   solve_level(A, B, 1, s);
-  launch(k_prolong0_s, nb, TPB, 0, s, nv, B.alpha, L0.P.rp.p, L0.P.ci.p, L0.P.v.p, L1.x.p, e); HC_COUNT();
+  if (A.fp32_coarse)
+    launch(k_prolong0_s<float>, nb, TPB, 0, s, nv, B.alpha, L0.P.rp.p, L0.P.ci.p, (const float*)L0.P.vf.p, L1.x.p, e);
+  else
+    launch(k_prolong0_s<double>, nb, TPB, 0, s, nv, B.alpha, L0.P.rp.p, L0.P.ci.p, (const double*)L0.P.v.p, L1.x.p, e);
+  HC_COUNT();
   for (int k = 0; k < A.nu; ++k) {
     sweep(EP_SMOOTH, e, e2);
     std::swap(e, e2);

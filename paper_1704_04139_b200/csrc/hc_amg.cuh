@@ -24,6 +24,7 @@ struct AmgLevel {
   Csr AP;                                // A P (Galerkin intermediate)
   DBuf<int32_t> pt_ptr, pt_row, pt_idx;  // P^T: for each coarse unknown, (row, value index) pairs
   DBuf<double> ptv;                      // P^T values (gathered after every setup)
+  DBuf<float> ptvf;                      // fp32 copy used by the cycle's restriction
   DBuf<double> x, x2, b, res, acc;       // cycle vectors (levels >= 1)
 };
 
