@@ -1148,13 +1148,15 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
       std::swap(e, e2);
     }
   } else {
-    launch(k_smooth0_s, nb, TPB, 0, s, nv, w, L0.dinv.p, r, e); HC_COUNT();
-    for (int k = 1; k < A.nu; ++k) {
-      sweep(EP_SMOOTH, e, e2);
-      std::swap(e, e2);
-    }
+    // nu = 1: the zero-guess step e = w D^-1 r and the residual r - A e in one pass
+    double2* e_out = reinterpret_cast<double2*>(e);
+    if (f == 1)
+      fine_launch_op<SM_PHI, EP_RESID0>(op, F, nullptr, nullptr, r, L0.dinv.p, w, inv_dt, 0, e_out, A.res.p, s);
+    else
+      fine_launch_op<SM_CONC, EP_RESID0>(op, F, nullptr, nullptr, r, L0.dinv.p, w, inv_dt, 0, e_out, A.res.p, s);
+    HC_COUNT();
   }
-  sweep(EP_RESID, e, A.res.p);
+  if (A.nu >= 2) sweep(EP_RESID, e, A.res.p);
   if (A.fp32_coarse)
     launch(k_restrict_v<float>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const float*)L0.ptvf.p,
            A.res.p, L1.b.p);

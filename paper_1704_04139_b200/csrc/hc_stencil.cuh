@@ -25,7 +25,9 @@
 namespace hc {
 
 enum { SM_FULL = 0, SM_PHI = 1, SM_CONC = 2, SM_CP = 3 };
-enum { EP_STORE = 0, EP_SMOOTH = 1, EP_RESID = 2, EP_SMOOTH0 = 3 };  // SMOOTH0: first sweep from e0 = w D^-1 r
+enum { EP_STORE = 0, EP_SMOOTH = 1, EP_RESID = 2, EP_SMOOTH0 = 3, EP_RESID0 = 4 };
+// SMOOTH0: first sweep from e0 = w D^-1 r;  RESID0: r - A e0 with e0 = w D^-1 r, and e0 itself
+// written to the double* passed as out2 (the zero-guess smoothing step and the residual in one pass)
 
 struct FineArgs {
   const uint8_t* lab;
@@ -91,7 +93,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
          int zc) {
   pdl_wait();
   constexpr bool FULLM = MODE == SM_FULL;
-  constexpr bool X0 = EPI == EP_SMOOTH0;   // input e0 = w D^-1 r materialised from staged r, dinv
+  constexpr bool X0 = EPI == EP_SMOOTH0 || EPI == EP_RESID0;   // input e0 = w D^-1 r from staged r, dinv
   constexpr int S = 4;
   constexpr int TW = VX + 2, TH = VY + 2, TN = TW * TH;
   constexpr int VB = FULLM ? 16 : 8;       // bytes per staged value
@@ -304,10 +306,11 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
       } else {
         if (MODE == SM_CONC) rp += inv_dt * va;
         if (EPI == EP_STORE) out[v] = rp;
-        else if (EPI == EP_RESID) out[v] = rv - rp;
+        else if (EPI == EP_RESID || EPI == EP_RESID0) out[v] = rv - rp;
         else out[v] = va + omega * dv_ * (rv - rp);   // SMOOTH and SMOOTH0
       }
     }
+    if constexpr (EPI == EP_RESID0) reinterpret_cast<double*>(out2)[v] = va;
     lm = a;
     vm = va;
     if constexpr (FULLM) wm = wa;
@@ -351,7 +354,7 @@ inline void fine_launch_p(const DevParams& P, const FineArgs& F, const int32_t* 
                           int n_sm, cudaStream_t s) {
   constexpr bool FULLM = MODE == SM_FULL;
   constexpr int TN = (VX + 2) * (VY + 2);
-  const size_t smem = 4 * TN * ((FULLM ? 16 : 8) + (FULLM ? 8 : 0) + (EPI == EP_SMOOTH0 ? 8 : 0) + 4);
+  const size_t smem = 4 * TN * ((FULLM ? 16 : 8) + (FULLM ? 8 : 0) + (EPI == EP_SMOOTH0 || EPI == EP_RESID0 ? 8 : 0) + 4);
   static int per_sm = 0;
   if (!per_sm) {
     cudaFuncSetAttribute(k_fine_p<MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

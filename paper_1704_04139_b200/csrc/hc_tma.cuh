@@ -108,7 +108,7 @@ constexpr int T_SLOTCAP = HC_TMA_SLOTCAP;
 template <int MODE, int EPI>
 struct TmaLayout {
   static constexpr bool FULLM = MODE == SM_FULL || MODE == 4;   // double2 (c, phi) tiles
-  static constexpr bool X0 = EPI == EP_SMOOTH0;
+  static constexpr bool X0 = EPI == EP_SMOOTH0 || EPI == EP_RESID0;
   static constexpr int VW = FULLM ? T_QW : T_DW, VOFF = FULLM ? T_QOFF : T_DOFF;
   static constexpr int VBYTES = FULLM ? T_QN * 16 : T_DN * 8;
   static constexpr int LAB = 0;                                         // int32 [T_LN]
@@ -453,10 +453,11 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
           else rp = fma(elrow ? 1.0 - tp : 1.0, si, rp);   // (T J) on electrolyte c rows
           if (MODE == SM_CONC) rp = fma(inv_dt, va, rp);
           if (EPI == EP_STORE) out[v] = rp;
-          else if (EPI == EP_RESID) out[v] = rv - rp;
+          else if (EPI == EP_RESID || EPI == EP_RESID0) out[v] = rv - rp;
           else out[v] = va + omega * dv_ * (rv - rp);
         }
       }
+      if constexpr (EPI == EP_RESID0) reinterpret_cast<double*>(out2)[v] = va;
       lm = a;
       vm = va;
       if constexpr (OC || RES) wm = wa;
