@@ -141,7 +141,6 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
            const double2* __restrict__ V, const double* __restrict__ e, const double* __restrict__ r,
            const double* __restrict__ dinv, double omega, double inv_dt, int flags,
            double2* __restrict__ out2, double* __restrict__ out, int zc) {
-  pdl_wait();
   using L = TmaLayout<MODE, EPI>;
   constexpr bool FULLM = L::FULLM, X0 = L::X0;
   constexpr bool RES = MODE == SM_RES;
@@ -190,6 +189,9 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
   };
   if (threadIdx.y == T_WARPS) load_tp(0);
   __syncthreads();   // barriers initialised, tables built (the only CTA-wide barrier)
+  // programmatic dependent launch: everything above reads only static data (parameters,
+  // slot offsets), so it overlaps the predecessor kernel's tail; operands come after this
+  pdl_wait();
 
   if (threadIdx.y == T_WARPS) {   // ---------------- producer warp
     const int lane = threadIdx.x;
