@@ -105,14 +105,20 @@ __device__ __forceinline__ bool vox_index(const DevParams& P, int& x, int& y, in
   return true;
 }
 
-// np.interp on the OCP table (echem/kinetics.py:25-32), clamped at the ends.
+// np.interp on the OCP table (echem/kinetics.py:25-32), clamped at the ends.  The
+// segment is found by binary search (the last knot index j <= n-2 with soc[j] <= s),
+// the same segment the linear scan of the reference's np.interp picks.
 __device__ __host__ inline double ocp_dev(double c, const DevParams& P) {
   double s = c / P.c_gr_max;
   int n = P.n_ocp;
   if (!(s >= P.ocp_soc[0])) return (s != s) ? s : P.ocp_v[0];
   if (s >= P.ocp_soc[n - 1]) return P.ocp_v[n - 1];
-  int j = 0;
-  while (j + 1 < n - 1 && P.ocp_soc[j + 1] <= s) ++j;
+  int lo = 0, hi = n - 2;   // invariant: soc[lo] <= s
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.ocp_soc[mid] <= s) lo = mid; else hi = mid - 1;
+  }
+  const int j = lo;
   double slope = (P.ocp_v[j + 1] - P.ocp_v[j]) / (P.ocp_soc[j + 1] - P.ocp_soc[j]);
   return slope * (s - P.ocp_soc[j]) + P.ocp_v[j];
 }
@@ -123,9 +129,12 @@ __device__ __host__ inline double ocp_slope_dev(double c, const DevParams& P) {
   double s = c / P.c_gr_max;
   int n = P.n_ocp;
   if (s < P.ocp_soc[0] || s > P.ocp_soc[n - 1]) return 0.0;
-  int k = 0;  // number of knots <= s
-  while (k < n && P.ocp_soc[k] <= s) ++k;
-  int seg = k - 1;
+  int lo = 0, hi = n;   // k = number of knots <= s (searchsorted side=right)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (P.ocp_soc[mid] <= s) lo = mid + 1; else hi = mid;
+  }
+  int seg = lo - 1;
   if (seg < 0) seg = 0;
   if (seg > n - 2) seg = n - 2;
   return (P.ocp_v[seg + 1] - P.ocp_v[seg]) / (P.ocp_soc[seg + 1] - P.ocp_soc[seg]) / P.c_gr_max;

@@ -490,6 +490,9 @@ inline const CUtensorMap* tma_map(TmaCache& c, const void* ptr, int kind, int nx
   std::lock_guard<std::mutex> g(c.mu);
   auto it = c.maps.find(key);
   if (it != c.maps.end()) return &it->second;
+  // transient buffers (e.g. per-call tensors of the Python API) would grow the cache
+  // without bound; maps are cheap to re-encode, so start over past a few thousand
+  if (c.maps.size() >= 4096) c.maps.clear();
   CUtensorMap m;
   if (!tma_encode(&m, ptr, kind, nx, ny, nz)) return nullptr;
   return &c.maps.emplace(key, m).first->second;
