@@ -331,18 +331,27 @@ inline int ctas_per_sm_target() {
   static int t = -1;
   if (t < 0) {
     const char* e = getenv("HC_ZC_TARGET");
-    t = e ? atoi(e) : 12;
+    t = e ? atoi(e) : 6;
+  }
+  return t;
+}
+inline int min_planes_per_cta() {
+  static int t = -1;
+  if (t < 0) {
+    const char* e = getenv("HC_ZC_MIN");
+    t = std::max(1, e ? atoi(e) : 5);
   }
   return t;
 }
 
 // grid z-extent: about `target` CTAs per SM in total (HC_ZC_TARGET; 0 = exactly one
-// resident wave from the occupancy query), at least two planes per CTA
+// resident wave from the occupancy query), at least HC_ZC_MIN planes per CTA (every
+// CTA pays a pipeline fill and re-reads its first and last neighbour planes)
 inline int pick_bz(int bx, int by, int nz, int per_sm, int n_sm) {
   const int target = ctas_per_sm_target();
   const long long want = (long long)(target > 0 ? target : per_sm) * n_sm;
   int bz = (int)std::max<long long>(1, want / std::max(1, bx * by));
-  bz = std::min(bz, std::max(1, nz / 2));
+  bz = std::min(bz, std::max(1, nz / min_planes_per_cta()));
   const int zc = (nz + bz - 1) / bz;
   return (nz + zc - 1) / zc;
 }
