@@ -346,7 +346,21 @@ __global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict
     return x[j] + alpha * xc[parent[j]];
   };
   double s = 0.0;
-  for (int k = rp[i] + lane; k < rp[i + 1]; k += VS) s += (double)v[k] * xin(cl[k]);
+  // four nonzeros per trip with all index / value loads issued before the gathers (the
+  // rows are short, so a one-at-a-time loop is a chain of dependent L2 round trips);
+  // the summation order is the plain loop's
+  const int k1 = rp[i + 1];
+  int k = rp[i] + lane;
+  for (; k + 3 * VS < k1; k += 4 * VS) {
+    const int c0 = cl[k], c1 = cl[k + VS], c2 = cl[k + 2 * VS], c3 = cl[k + 3 * VS];
+    const double a0 = (double)v[k], a1 = (double)v[k + VS], a2 = (double)v[k + 2 * VS], a3 = (double)v[k + 3 * VS];
+    const double x0 = xin(c0), x1 = xin(c1), x2 = xin(c2), x3 = xin(c3);
+    s += a0 * x0;
+    s += a1 * x1;
+    s += a2 * x2;
+    s += a3 * x3;
+  }
+  for (; k < k1; k += VS) s += (double)v[k] * xin(cl[k]);
 #pragma unroll
   for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
   if (lane == 0) {
@@ -383,7 +397,16 @@ __global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
   int I = (int)(gt >> 3), lane = (int)(gt & 7);
   if (I >= n1) return;
   double s = 0.0;
-  for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += 8) s += (double)ptv[q] * res[pt_row[q]];
+  const int q1 = pt_ptr[I + 1];
+  int q = pt_ptr[I] + lane;
+  for (; q + 8 < q1; q += 16) {
+    const int r0 = pt_row[q], r1 = pt_row[q + 8];
+    const double a0 = (double)ptv[q], a1 = (double)ptv[q + 8];
+    const double x0 = res[r0], x1 = res[r1];
+    s += a0 * x0;
+    s += a1 * x1;
+  }
+  for (; q < q1; q += 8) s += (double)ptv[q] * res[pt_row[q]];
   s += __shfl_down_sync(0xffffffffu, s, 4, 8);
   s += __shfl_down_sync(0xffffffffu, s, 2, 8);
   s += __shfl_down_sync(0xffffffffu, s, 1, 8);
@@ -728,6 +751,13 @@ Amg* build_amg(const Operator& op) {
   }
   amg->res.alloc(nvox);
   amg->rc2.alloc(nvox);
+  if (const char* e = getenv("HC_AMG_BDIAG")) amg->bdiag = atoi(e) != 0;
+  if (amg->bdiag) {
+    amg->res_c.alloc(nvox);
+    HC_CUDA(cudaStreamCreateWithFlags(&amg->side, cudaStreamNonBlocking));
+    HC_CUDA(cudaEventCreateWithFlags(&amg->ev_fork, cudaEventDisableTiming));
+    HC_CUDA(cudaEventCreateWithFlags(&amg->ev_join, cudaEventDisableTiming));
+  }
   return amg.release();
 }
 
@@ -1124,6 +1154,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   const dim3 vg = vox_grid(op.P), vb = vox_block();
   double* e = A.ea[f].p;
   double* e2 = A.eb[f].p;
+  double* res = (f == 0 && A.bdiag) ? A.res_c.p : A.res.p;
   auto sweep = [&](int epi, const double* in, double* out) {
     if (f == 1) {
       if (epi == EP_SMOOTH0) fine_launch_op<SM_PHI, EP_SMOOTH0>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
@@ -1151,17 +1182,17 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
     // nu = 1: the zero-guess step e = w D^-1 r and the residual r - A e in one pass
     double2* e_out = reinterpret_cast<double2*>(e);
     if (f == 1)
-      fine_launch_op<SM_PHI, EP_RESID0>(op, F, nullptr, nullptr, r, L0.dinv.p, w, inv_dt, 0, e_out, A.res.p, s);
+      fine_launch_op<SM_PHI, EP_RESID0>(op, F, nullptr, nullptr, r, L0.dinv.p, w, inv_dt, 0, e_out, res, s);
     else
-      fine_launch_op<SM_CONC, EP_RESID0>(op, F, nullptr, nullptr, r, L0.dinv.p, w, inv_dt, 0, e_out, A.res.p, s);
+      fine_launch_op<SM_CONC, EP_RESID0>(op, F, nullptr, nullptr, r, L0.dinv.p, w, inv_dt, 0, e_out, res, s);
     HC_COUNT();
   }
-  if (A.nu >= 2) sweep(EP_RESID, e, A.res.p);
+  if (A.nu >= 2) sweep(EP_RESID, e, res);
   if (A.fp32_coarse)
     launch(k_restrict_v<float>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const float*)L0.ptvf.p,
-           A.res.p, L1.b.p);
+           res, L1.b.p);
   else
-  launch(k_restrict_v<double>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const double*)L0.ptv.p, A.res.p,
+  launch(k_restrict_v<double>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const double*)L0.ptv.p, res,
                                                 L1.b.p); HC_COUNT();
   solve_level(A, B, 1, s);
   if (A.fp32_coarse)
@@ -1184,6 +1215,18 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
   const long long nv = op.P.nvox;
   const int nb = nblk(nv);
   launch(k_split_T, nb, TPB, 0, s, op.P, op.labels.p, r, A.rs[0].p, A.rs[1].p); HC_COUNT();
+  if (mode == 0 && A.bdiag) {
+    // block Jacobi: fork the c-block V-cycle onto the side stream, join before the merge
+    HC_CUDA(cudaEventRecord(A.ev_fork, s));
+    HC_CUDA(cudaStreamWaitEvent(A.side, A.ev_fork, 0));
+    double* ec = vcycle_fine(op, 0, A.rs[0].p, inv_dt, A.side);
+    HC_CUDA(cudaEventRecord(A.ev_join, A.side));
+    double* ep = vcycle_fine(op, 1, A.rs[1].p, inv_dt, s);
+    HC_CUDA(cudaStreamWaitEvent(s, A.ev_join, 0));
+    launch(k_merge_s, nb, TPB, 0, s, nv, ec, ep, z); HC_COUNT();
+    HC_CHECK_LAUNCH();
+    return;
+  }
   double* ep = vcycle_fine(op, 1, A.rs[1].p, inv_dt, s);
   if (mode == 1) {
     launch(k_merge_s, nb, TPB, 0, s, nv, nullptr, ep, z); HC_COUNT();
@@ -1238,6 +1281,9 @@ void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mo
 
 Amg::~Amg() {
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (side) cudaStreamDestroy(side);
 }
 
 }  // namespace hc

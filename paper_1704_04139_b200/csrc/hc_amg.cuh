@@ -87,6 +87,13 @@ struct Amg {
   long long solves = 0;
   double last_inv_dt = -1.0;
   DBuf<double> rs[2], ea[2], eb[2], res, rc2;   // fine-level scalar vectors per block
+  DBuf<double> res_c;                           // the c block's fine residual (block Jacobi)
+  // block-Jacobi preconditioner (default): the two blocks' V-cycles are independent, so
+  // the c-block cycle runs on a side stream (a parallel branch of the captured graph);
+  // HC_AMG_BDIAG=0 restores block Gauss-Seidel (c right-hand side corrected by T J_cp e_phi)
+  bool bdiag = true;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 Amg* build_amg(const Operator& op);
