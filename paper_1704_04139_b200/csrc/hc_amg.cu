@@ -739,6 +739,12 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_FUSE_ROWS")) amg->fuse_rows = atoi(e);
   if (const char* e = getenv("HC_AMG_FUSE_NNZ")) amg->fuse_nnz = atoll(e);
   auto t0 = std::chrono::steady_clock::now();
+  for (int f = 0; f < 2; ++f) {
+    amg->blk[f].nu = amg->nu;
+    amg->blk[f].nu_c = amg->nu_c;
+  }
+  if (const char* e = getenv("HC_AMG_NU_C0")) amg->blk[0].nu = atoi(e);
+  if (const char* e = getenv("HC_AMG_NU_C_C0")) amg->blk[0].nu_c = atoi(e);
   build_block(op, lab, 0, *amg, amg->blk[0]);
   build_block(op, lab, 1, *amg, amg->blk[1]);
   if (getenv("HC_AMG_VERBOSE"))
@@ -981,7 +987,7 @@ static void coarse_cycle_launch(const Amg& A, AmgBlock& B, cudaStream_t s) {
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   const int nlev = (int)B.levels.size() - B.fuse_from;
   HC_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_cycle, (const CoarseLev*)B.clev.p, nlev,
-                             (const double*)B.dense_inv.p, A.omega, B.alpha, A.nu_c));
+                             (const double*)B.dense_inv.p, A.omega, B.alpha, B.nu_c));
   HC_COUNT();
 }
 
@@ -1038,7 +1044,7 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   AmgLevel& U = B.levels[l + 1];
   const double w = A.omega;
   // pre-smoothing from a zero guess: the first sweep materialises x0 = w D^-1 b itself
-  int pre = A.nu_c;
+  int pre = B.nu_c;
   if (pre >= 2) {
     csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.x.p, 0, s);
     for (int k = 2; k < pre; ++k) {
@@ -1058,7 +1064,7 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
                                                U.b.p); HC_COUNT();
   solve_level(A, B, l + 1, s);
   const bool tentative = L.P.nnz == (long long)L.n;  // one prolongator entry per row
-  int post = A.nu_c;
+  int post = B.nu_c;
   if (tentative && post >= 1) {
     // prolongation fused into the first post-sweep (P0 entries are all 1)
     csr_sweep_x<2>(A, L, w, B.alpha, L.b.p, L.x.p, L.parent.p, U.x.p, L.x2.p, 0, s);
@@ -1172,9 +1178,9 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
     return e;
   }
   AmgLevel& L1 = B.levels[1];
-  if (A.nu >= 2) {
+  if (B.nu >= 2) {
     sweep(EP_SMOOTH0, nullptr, e);          // e1 from the zero guess in one pass
-    for (int k = 2; k < A.nu; ++k) {
+    for (int k = 2; k < B.nu; ++k) {
       sweep(EP_SMOOTH, e, e2);
       std::swap(e, e2);
     }
@@ -1187,7 +1193,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
       fine_launch_op<SM_CONC, EP_RESID0>(op, F, nullptr, nullptr, r, L0.dinv.p, w, inv_dt, 0, e_out, res, s);
     HC_COUNT();
   }
-  if (A.nu >= 2) sweep(EP_RESID, e, res);
+  if (B.nu >= 2) sweep(EP_RESID, e, res);
   if (A.fp32_coarse)
     launch(k_restrict_v<float>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const float*)L0.ptvf.p,
            res, L1.b.p);
@@ -1200,7 +1206,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   else
     launch(k_prolong0_s<double>, nb, TPB, 0, s, nv, B.alpha, L0.P.rp.p, L0.P.ci.p, (const double*)L0.P.v.p, L1.x.p, e);
   HC_COUNT();
-  for (int k = 0; k < A.nu; ++k) {
+  for (int k = 0; k < B.nu; ++k) {
     sweep(EP_SMOOTH, e, e2);
     std::swap(e, e2);
   }
@@ -1210,11 +1216,13 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
 
 // z = M^{-1} r for the full (c, phi) system; mode 0 full, 1 phi block only
 static void amg_apply_impl(Operator& op, const double2* r, double2* z, double inv_dt, int mode,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool presplit) {
   Amg& A = *op.amg;
   const long long nv = op.P.nvox;
   const int nb = nblk(nv);
-  launch(k_split_T, nb, TPB, 0, s, op.P, op.labels.p, r, A.rs[0].p, A.rs[1].p); HC_COUNT();
+  if (!presplit) {
+    launch(k_split_T, nb, TPB, 0, s, op.P, op.labels.p, r, A.rs[0].p, A.rs[1].p); HC_COUNT();
+  }
   if (mode == 0 && A.bdiag) {
     // block Jacobi: fork the c-block V-cycle onto the side stream, join before the merge
     HC_CUDA(cudaEventRecord(A.ev_fork, s));
@@ -1247,24 +1255,24 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
 // captured once into a CUDA graph and replayed (the Galerkin values it reads
 // live in device memory, so re-linearization does not invalidate the graph).
 void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mode,
-               cudaStream_t s) {
+               cudaStream_t s, bool presplit) {
   Amg& A = *op.amg;
   if (!A.use_graphs || s == 0 || op.capturing) {
-    amg_apply_impl(op, r, z, inv_dt, mode, s);
+    amg_apply_impl(op, r, z, inv_dt, mode, s, presplit);
     return;
   }
   for (auto& g : A.graphs)
-    if (g.r == r && g.z == z && g.mode == mode && g.inv_dt == inv_dt) {
+    if (g.r == r && g.z == z && g.mode == mode && g.inv_dt == inv_dt && g.presplit == presplit) {
       HC_CUDA(cudaGraphLaunch(g.exec, s));
       count_graph_launch(g.n_kernels);
       return;
     }
   AmgGraph g;
-  g.r = r; g.z = z; g.mode = mode; g.inv_dt = inv_dt;
+  g.r = r; g.z = z; g.mode = mode; g.inv_dt = inv_dt; g.presplit = presplit;
   unsigned long long c0 = t_launch_count;
   cudaGraph_t graph;
   HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  amg_apply_impl(op, r, z, inv_dt, mode, s);
+  amg_apply_impl(op, r, z, inv_dt, mode, s, presplit);
   HC_CUDA(cudaStreamEndCapture(s, &graph));
   g.n_kernels = t_launch_count - c0;
   uncount(g.n_kernels);

@@ -45,6 +45,7 @@ struct CoarseLev {
 };
 
 struct AmgBlock {
+  int nu = 1, nu_c = 2;   // fine / CSR-level smoothing sweeps of this block (from Amg, HC_AMG_NU*_C0 override the c block)
   int field = 0;                  // 0: c block of T J, 1: phi block of J
   double alpha = 1.0;             // coarse-correction scaling
   std::vector<AmgLevel> levels;   // levels[0] is the fine grid
@@ -57,6 +58,7 @@ struct AmgGraph {
   const double2* r = nullptr;
   double2* z = nullptr;
   int mode = 0;
+  bool presplit = false;
   double inv_dt = 0.0;
   cudaGraphExec_t exec = nullptr;
   unsigned long long n_kernels = 0;
@@ -98,6 +100,9 @@ struct Amg {
 
 Amg* build_amg(const Operator& op);
 void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s);  // blocks: 1 c, 2 phi
-void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mode, cudaStream_t s);
+// presplit: the caller already wrote r's scalar right-hand sides (T r_c, r_phi) into
+// rs[0], rs[1] (the Krylov vector kernels do, saving the split pass)
+void amg_apply(Operator& op, const double2* r, double2* z, double inv_dt, int mode, cudaStream_t s,
+               bool presplit = false);
 
 }  // namespace hc

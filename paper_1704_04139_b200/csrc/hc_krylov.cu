@@ -140,8 +140,21 @@ __device__ void finish_in_last_block(int what, const double* part, double* ks, u
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// (rc, rp non-null: also the preconditioner's scalar right-hand sides T p_c, p_phi)
+struct SplitOut {
+  const uint8_t* lab;
+  double tp;
+  double* rc;
+  double* rp;
+  __device__ __forceinline__ void put(long long i, double2 a) const {
+    if (!rc) return;
+    rc[i] = lab[i] == EL ? a.x - tp * a.y : a.x;
+    rp[i] = a.y;
+  }
+};
+
 __global__ void k_dev_p(long long n, double* ks, const double2* __restrict__ r,
-                        const double2* __restrict__ v, double2* __restrict__ p) {
+                        const double2* __restrict__ v, double2* __restrict__ p, SplitOut so) {
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   // beta = (rho1 / rho) (alpha / omega), formerly k_dev_scalar(0): every thread derives it
@@ -151,13 +164,15 @@ __global__ void k_dev_p(long long n, double* ks, const double2* __restrict__ r,
   if (i == 0 && (rho1 == 0.0 || !isfinite(rho1))) { ks[S_ERR] = 1; ks[S_DONE] = 1; }
   if (i >= n) return;
   double2 pi = p[i], ri = r[i], vi = v[i];
-  p[i] = make_double2(ri.x + beta * (pi.x - omega * vi.x), ri.y + beta * (pi.y - omega * vi.y));
+  const double2 pn = make_double2(ri.x + beta * (pi.x - omega * vi.x), ri.y + beta * (pi.y - omega * vi.y));
+  p[i] = pn;
+  so.put(i, pn);
 }
 
 // s = r - alpha v, partial ||s||^2
 __global__ void k_dev_s(long long n, double* ks, const double2* __restrict__ r,
                         const double2* __restrict__ v, double2* __restrict__ s,
-                        double* __restrict__ part, unsigned* ticket) {
+                        double* __restrict__ part, unsigned* ticket, SplitOut so) {
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   const double alpha = ks[S_ALPHA];
@@ -167,6 +182,7 @@ __global__ void k_dev_s(long long n, double* ks, const double2* __restrict__ r,
     double2 ri = r[i], vi = v[i];
     double2 si = make_double2(ri.x - alpha * vi.x, ri.y - alpha * vi.y);
     s[i] = si;
+    so.put(i, si);
     acc += si.x * si.x + si.y * si.y;
   }
   block_part2(acc, 0.0, part);
@@ -287,16 +303,17 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   launch(k_dev_dot2, nb, TPB, 0, s, n, G.ks.p, b, b, nullptr, nullptr, G.part.p, -1, G.ticket.p); HC_COUNT();
   launch(k_dev_init, 1, 256, 0, s, nb, G.part.p, G.ks.p, rtol * rtol); HC_COUNT();
   // the body of one BiCGStab iteration (captured, never run eagerly)
+  const SplitOut so{op.labels.p, op.P.t_plus, op.amg->rs[0].p, op.amg->rs[1].p};
   auto iteration = [&]() {
     double* ks = G.ks.p;
     double* part = G.part.p;
     unsigned* tk = G.ticket.p;
-    launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p); HC_COUNT();
-    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s);
+    launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p, so); HC_COUNT();
+    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s, true);
     apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
     launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part, 1, tk); HC_COUNT();
-    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk); HC_COUNT();
-    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s);
+    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk, so); HC_COUNT();
+    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s, true);
     apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
     launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part, 3, tk); HC_COUNT();
     launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
@@ -431,14 +448,15 @@ void krylov_append(Operator& op, GraphBuilder& gb, const double2* b, double2* x,
     launch(k_dev_init_dev, 1, 256, 0, s, nb, (const double*)part, ks, rtol_dev); HC_COUNT();
     k_dev_cond<<<1, 32, 0, s>>>(ks, h, maxit);
   });
+  const SplitOut so{op.labels.p, op.P.t_plus, op.amg->rs[0].p, op.amg->rs[1].p};
   GraphBuilder body{s, gb.cond(h, cudaGraphCondTypeWhile), {}};
   body.capture([&] {
-    launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p); HC_COUNT();
-    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s);
+    launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p, so); HC_COUNT();
+    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s, true);
     apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
     launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part, 1, tk); HC_COUNT();
-    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk); HC_COUNT();
-    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s);
+    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk, so); HC_COUNT();
+    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s, true);
     apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
     launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part, 3, tk); HC_COUNT();
     launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
