@@ -335,7 +335,8 @@ __global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict
                         const int32_t* __restrict__ cl, const VT* __restrict__ v,
                         const double* __restrict__ dinv, const double* __restrict__ b,
                         const double* __restrict__ x, const int32_t* __restrict__ parent,
-                        const double* __restrict__ xc, double* __restrict__ y, int resid) {
+                        const double* __restrict__ xc, double* __restrict__ y, int resid,
+                        double* __restrict__ x0) {
   pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int i = (int)(gt / VS), lane = (int)(gt % VS);
@@ -366,6 +367,7 @@ __global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict
   if (lane == 0) {
     const double xi = xin(i);
     y[i] = resid ? b[i] - s : xi + w * dinv[i] * (b[i] - s);
+    if (x0) x0[i] = xi;   // residual of the zero-guess iterate: also store that iterate
   }
 }
 
@@ -741,10 +743,14 @@ Amg* build_amg(const Operator& op) {
   auto t0 = std::chrono::steady_clock::now();
   for (int f = 0; f < 2; ++f) {
     amg->blk[f].nu = amg->nu;
-    amg->blk[f].nu_c = amg->nu_c;
+    amg->blk[f].nu_c = amg->blk[f].pre_c = amg->blk[f].post_c = amg->nu_c;
   }
+  if (const char* e = getenv("HC_AMG_PRE_C"))
+    for (auto& b : amg->blk) b.pre_c = atoi(e);
+  if (const char* e = getenv("HC_AMG_POST_C"))
+    for (auto& b : amg->blk) b.post_c = atoi(e);
   if (const char* e = getenv("HC_AMG_NU_C0")) amg->blk[0].nu = atoi(e);
-  if (const char* e = getenv("HC_AMG_NU_C_C0")) amg->blk[0].nu_c = atoi(e);
+  if (const char* e = getenv("HC_AMG_NU_C_C0")) amg->blk[0].nu_c = amg->blk[0].pre_c = amg->blk[0].post_c = atoi(e);
   build_block(op, lab, 0, *amg, amg->blk[0]);
   build_block(op, lab, 1, *amg, amg->blk[1]);
   if (getenv("HC_AMG_VERBOSE"))
@@ -1021,14 +1027,14 @@ static void csr_sweep(const Amg& A, const AmgLevel& L, double w, const double* b
 template <int XM>
 static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha, const double* b,
                         const double* x, const int32_t* parent, const double* xc, double* y,
-                        int resid, cudaStream_t s) {
+                        int resid, cudaStream_t s, double* x0 = nullptr) {
   double avg = L.n ? (double)L.A.nnz / L.n : 0.0;
   const int VSsel = avg <= 12.0 ? 1 : (avg <= 48.0 ? 8 : 32);
   auto go = [&](auto vs_tag, auto* vals) {
     constexpr int VS = decltype(vs_tag)::value;
     using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
     launch(k_csr_x<VS, VT, XM>, nblk((long long)VS * L.n), TPB, 0, s, 
-        L.n, w, alpha, L.A.rp.p, L.A.ci.p, vals, L.dinv.p, b, x, parent, xc, y, resid);
+        L.n, w, alpha, L.A.rp.p, L.A.ci.p, vals, L.dinv.p, b, x, parent, xc, y, resid, x0);
     HC_COUNT();
   };
   const float* vf = L.A.vf.p;
@@ -1044,7 +1050,7 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   AmgLevel& U = B.levels[l + 1];
   const double w = A.omega;
   // pre-smoothing from a zero guess: the first sweep materialises x0 = w D^-1 b itself
-  int pre = B.nu_c;
+  int pre = B.pre_c;
   if (pre >= 2) {
     csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.x.p, 0, s);
     for (int k = 2; k < pre; ++k) {
@@ -1053,8 +1059,8 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
     }
     csr_sweep_x<0>(A, L, 0.0, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.res.p, 1, s);
   } else {
-    launch(k_csr_smooth0, nblk(L.n), TPB, 0, s, L.n, w, L.dinv.p, L.b.p, L.x.p); HC_COUNT();
-    csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.res.p, 1, s);
+    // x0 = w D^-1 b and b - A x0 in one pass
+    csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.res.p, 1, s, L.x.p);
   }
   if (A.fp32_coarse)
     launch(k_restrict_v<float>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, (const float*)L.ptvf.p, L.res.p,
@@ -1064,7 +1070,7 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
                                                U.b.p); HC_COUNT();
   solve_level(A, B, l + 1, s);
   const bool tentative = L.P.nnz == (long long)L.n;  // one prolongator entry per row
-  int post = B.nu_c;
+  int post = B.post_c;
   if (tentative && post >= 1) {
     // prolongation fused into the first post-sweep (P0 entries are all 1)
     csr_sweep_x<2>(A, L, w, B.alpha, L.b.p, L.x.p, L.parent.p, U.x.p, L.x2.p, 0, s);

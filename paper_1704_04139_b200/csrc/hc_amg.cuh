@@ -45,7 +45,7 @@ struct CoarseLev {
 };
 
 struct AmgBlock {
-  int nu = 1, nu_c = 2;   // fine / CSR-level smoothing sweeps of this block (from Amg, HC_AMG_NU*_C0 override the c block)
+  int nu = 1, nu_c = 2, pre_c = 2, post_c = 2;   // fine / CSR-level smoothing sweeps of this block (from Amg, HC_AMG_NU*_C0 override the c block)
   int field = 0;                  // 0: c block of T J, 1: phi block of J
   double alpha = 1.0;             // coarse-correction scaling
   std::vector<AmgLevel> levels;   // levels[0] is the fine grid
