@@ -484,7 +484,7 @@ def run_rom(args, ws, rank, local):
     tt = {}
     t0 = time.perf_counter()
     snaps = mor.collect_snapshots(op, st.x, st.n_pl, mu, dt, args.rom_snapshots,
-                                  P.SolverConfig(dt_init=dt, dt_max=dt, linear_safety=LINEAR_SAFETY))
+                                  P.SolverConfig(dt_init=dt, dt_max=dt, linear_safety=0.0))
     torch.cuda.synchronize()
     tt["snapshots_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
