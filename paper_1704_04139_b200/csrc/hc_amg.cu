@@ -203,6 +203,25 @@ __global__ void k_ptap_w(int n_next, const int32_t* __restrict__ pt_ptr,
   }
 }
 
+// R = P^T A for a tentative P: row I is the sum of its member rows (warp per coarse row,
+// members in order, the same fixed summation order as k_ptap_w)
+__global__ void k_pta_w(int n_next, const int32_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_row,
+                        const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                        const double* __restrict__ av, const int32_t* __restrict__ rrp,
+                        const int32_t* __restrict__ rci, double* __restrict__ rv) {
+  pdl_wait();
+  const int I = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (I >= n_next) return;
+  const int r0 = rrp[I], r1 = rrp[I + 1];
+  for (int k = r0 + lane; k < r1; k += 32) rv[k] = 0.0;
+  __syncwarp();
+  for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) {
+    const int i = pt_row[q];
+    for (int m = arp[i] + lane; m < arp[i + 1]; m += 32) rv[find_col(rci, r0, r1, aci[m])] += av[m];
+    __syncwarp();
+  }
+}
+
 // ---- coarsest level: dense LU with partial pivoting in one CTA --------------
 __global__ void k_dense_from_csr(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ cl,
                                  const double* __restrict__ v, double* __restrict__ A) {
@@ -414,6 +433,38 @@ __global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
   s += __shfl_down_sync(0xffffffffu, s, 1, 8);
   if (lane == 0) b1[I] = s;
 }
+// fused residual + restriction for a tentative prolongator: b1[I] = sum of b over the
+// aggregate's members - (R x)_I with R = P^T A (VS lanes per coarse row)
+template <int VS, class VT>
+__global__ void k_resid_restrict(int n1, const int32_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_row,
+                                 const int32_t* __restrict__ rrp, const int32_t* __restrict__ rci,
+                                 const VT* __restrict__ rv, const double* __restrict__ b,
+                                 const double* __restrict__ x, double* __restrict__ b1) {
+  pdl_wait();
+  long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int I = (int)(gt / VS), lane = (int)(gt % VS);
+  const bool ok = I < n1;
+  double s = 0.0;
+  if (ok) {
+    const int k1 = rrp[I + 1];
+    int k = rrp[I] + lane;
+    for (; k + 3 * VS < k1; k += 4 * VS) {
+      const int c0 = rci[k], c1 = rci[k + VS], c2 = rci[k + 2 * VS], c3 = rci[k + 3 * VS];
+      const double a0 = (double)rv[k], a1 = (double)rv[k + VS], a2 = (double)rv[k + 2 * VS], a3 = (double)rv[k + 3 * VS];
+      const double x0 = x[c0], x1 = x[c1], x2 = x[c2], x3 = x[c3];
+      s -= a0 * x0;
+      s -= a1 * x1;
+      s -= a2 * x2;
+      s -= a3 * x3;
+    }
+    for (; k < k1; k += VS) s -= (double)rv[k] * x[rci[k]];
+    for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += VS) s += b[pt_row[q]];
+  }
+#pragma unroll
+  for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
+  if (ok && lane == 0) b1[I] = s;
+}
+
 __global__ void k_gather_ptv(long long n, const int32_t* __restrict__ pt_idx,
                              const double* __restrict__ pv, double* __restrict__ ptv) {
   pdl_wait();
@@ -635,6 +686,18 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     upload(L.pt_ptr, tp);
     upload(L.pt_row, trow);
     upload(L.pt_idx, tidx);
+    if (level >= 1 && !smooth && cfg.fuse_restrict) {   // R = P^T A pattern: union of member rows
+      std::vector<std::vector<int32_t>> rows(nn);
+      parallel_for(nn, [&](int I) {
+        auto& r = rows[I];
+        for (int q = tp[I]; q < tp[I + 1]; ++q) {
+          const int i = trow[q];
+          r.insert(r.end(), A.ci.begin() + A.rp[i], A.ci.begin() + A.rp[i + 1]);
+        }
+      });
+      HPat Rp = finish(rows);
+      upload_csr(L.R, Rp);
+    }
     L.ptv.alloc(std::max<size_t>(tidx.size(), 1));
     L.ptvf.alloc(std::max<size_t>(tidx.size(), 1));
     L.P.vf.alloc(std::max<long long>(L.P.nnz, 1));
@@ -740,6 +803,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_REFRESH_SOLVES")) amg->refresh_solves = std::max(1, atoi(e));
   if (const char* e = getenv("HC_AMG_FUSE_ROWS")) amg->fuse_rows = atoi(e);
   if (const char* e = getenv("HC_AMG_FUSE_NNZ")) amg->fuse_nnz = atoll(e);
+  if (const char* e = getenv("HC_AMG_FUSE_RESTRICT")) amg->fuse_restrict = atoi(e) != 0;
   auto t0 = std::chrono::steady_clock::now();
   for (int f = 0; f < 2; ++f) {
     amg->blk[f].nu = amg->nu;
@@ -808,6 +872,14 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
       AmgLevel& L = B.levels[l];
       if (A.fp32_coarse && L.A.nnz) {
         launch(k_to_float, nblk(L.A.nnz), TPB, 0, s, L.A.nnz, L.A.v.p, L.A.vf.p); HC_COUNT();
+      }
+      if (L.R.nnz && l + 1 < B.levels.size()) {
+        const AmgLevel& U = B.levels[l + 1];
+        launch(k_pta_w, nblk(32LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, L.A.rp.p, L.A.ci.p, L.A.v.p,
+               L.R.rp.p, L.R.ci.p, L.R.v.p); HC_COUNT();
+        if (A.fp32_coarse) {
+          launch(k_to_float, nblk(L.R.nnz), TPB, 0, s, L.R.nnz, L.R.v.p, L.R.vf.p); HC_COUNT();
+        }
       }
     }
     AmgLevel& C = B.levels.back();
@@ -1057,17 +1129,39 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
       csr_sweep_x<0>(A, L, w, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.x2.p, 0, s);
       std::swap(L.x.p, L.x2.p);
     }
-    csr_sweep_x<0>(A, L, 0.0, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.res.p, 1, s);
-  } else {
-    // x0 = w D^-1 b and b - A x0 in one pass
-    csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.res.p, 1, s, L.x.p);
   }
-  if (A.fp32_coarse)
-    launch(k_restrict_v<float>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, (const float*)L.ptvf.p, L.res.p,
-           U.b.p);
-  else
-  launch(k_restrict_v<double>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, (const double*)L.ptv.p, L.res.p,
-                                               U.b.p); HC_COUNT();
+  if (pre >= 2 && L.R.nnz) {
+    // residual and restriction in one pass: U.b = P^T b - (P^T A) x
+    const double avg = U.n ? (double)L.R.nnz / U.n : 0.0;
+    auto go = [&](auto vs_tag, auto* vals) {
+      constexpr int VS = decltype(vs_tag)::value;
+      using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
+      launch(k_resid_restrict<VS, VT>, nblk((long long)VS * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p,
+             L.R.rp.p, L.R.ci.p, vals, L.b.p, L.x.p, U.b.p);
+      HC_COUNT();
+    };
+    if (A.fp32_coarse) {
+      if (avg <= 48.0) go(std::integral_constant<int, 8>{}, (const float*)L.R.vf.p);
+      else go(std::integral_constant<int, 32>{}, (const float*)L.R.vf.p);
+    } else {
+      if (avg <= 48.0) go(std::integral_constant<int, 8>{}, (const double*)L.R.v.p);
+      else go(std::integral_constant<int, 32>{}, (const double*)L.R.v.p);
+    }
+  } else {
+    if (pre >= 2) {
+      csr_sweep_x<0>(A, L, 0.0, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.res.p, 1, s);
+    } else {
+      // x0 = w D^-1 b and b - A x0 in one pass
+      csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.res.p, 1, s, L.x.p);
+    }
+    if (A.fp32_coarse)
+      launch(k_restrict_v<float>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p,
+             (const float*)L.ptvf.p, L.res.p, U.b.p);
+    else
+      launch(k_restrict_v<double>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p,
+             (const double*)L.ptv.p, L.res.p, U.b.p);
+    HC_COUNT();
+  }
   solve_level(A, B, l + 1, s);
   const bool tentative = L.P.nnz == (long long)L.n;  // one prolongator entry per row
   int post = B.post_c;

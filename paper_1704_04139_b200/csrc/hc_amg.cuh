@@ -22,6 +22,8 @@ struct AmgLevel {
   DBuf<int32_t> parent;                  // tentative aggregate of each row, -1 if empty
   Csr P;                                 // prolongator to the next level (smoothed aggregation)
   Csr AP;                                // A P (Galerkin intermediate)
+  Csr R;                                 // P^T A for a tentative P (levels >= 1): the member-row
+                                         // sums, so b_next = P^T b - R x is one pass (no residual vector)
   DBuf<int32_t> pt_ptr, pt_row, pt_idx;  // P^T: for each coarse unknown, (row, value index) pairs
   DBuf<double> ptv;                      // P^T values (gathered after every setup)
   DBuf<float> ptvf;                      // fp32 copy used by the cycle's restriction
@@ -82,6 +84,7 @@ struct Amg {
   int wmin = 1;
   int fuse_rows = 0;          // levels with at most this many rows ... (0: off, measured slower)
   long long fuse_nnz = 400000; // ... and nonzeros run as one cluster kernel (0 rows: off)
+  bool fuse_restrict = true;  // residual + restriction as one pass on tentative CSR levels (R = P^T A)
   int coarsen = 2;           // block growth factor of the transfers above level 1              // gamma cycles on CSR levels wmin..wdepth
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int refresh = 0;          // numeric setup every Newton iteration (1) or once per solve (0)
