@@ -64,6 +64,17 @@ __device__ __forceinline__ double fin_sum_block(const double* part, int nb) {
 
 __device__ void finish_in_last_block(int what, const double* part, double* ks, unsigned* ticket);
 
+// blocks per SM of the Krylov vector kernels (grid-stride loops over the voxels);
+// enough blocks that every thread has only a few elements in flight
+static int krylov_blocks_per_sm() {
+  static int b = 0;
+  if (!b) {
+    const char* e = getenv("HC_KRYLOV_BPSM");
+    b = std::max(1, e ? atoi(e) : 4);
+  }
+  return b;
+}
+
 __global__ void k_dev_dot2(long long n, double* ks, const double2* __restrict__ a,
                            const double2* __restrict__ b, const double2* __restrict__ c,
                            const double2* __restrict__ d, double* __restrict__ part, int what,
@@ -71,6 +82,7 @@ __global__ void k_dev_dot2(long long n, double* ks, const double2* __restrict__ 
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
   double s1 = 0.0, s2 = 0.0;
+#pragma unroll 2
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double2 x = a[i], y = b[i];
@@ -177,6 +189,7 @@ __global__ void k_dev_s(long long n, double* ks, const double2* __restrict__ r,
   if (ks[S_DONE] != 0.0) return;
   const double alpha = ks[S_ALPHA];
   double acc = 0.0;
+#pragma unroll 2
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double2 ri = r[i], vi = v[i];
@@ -199,6 +212,7 @@ __global__ void k_dev_xr(long long n, double* ks, const double2* __restrict__ ph
   if (ks[S_DONE] != 0.0) return;
   const double alpha = ks[S_ALPHA], omega = ks[S_OMEGA];
   double a1 = 0.0, a2 = 0.0;
+#pragma unroll 2
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double2 xi = x[i], pi = ph[i], si = sh[i], s0 = s[i], ti = t[i], h = rhat[i];
@@ -285,7 +299,7 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   if (!op.kg) op.kg = new KrylovGraphs();
   KrylovGraphs& G = *op.kg;
   const long long n = op.P.nvox;
-  const int nb = (int)std::min<long long>((n + TPB - 1) / TPB, 2LL * op.n_sm);
+  const int nb = (int)std::min<long long>((n + TPB - 1) / TPB, (long long)krylov_blocks_per_sm() * op.n_sm);
   if (!G.ks.p) {
     G.ks.alloc(S_NSLOT);
     G.part.alloc(4 * nb + 8);
@@ -422,7 +436,7 @@ void krylov_append(Operator& op, GraphBuilder& gb, const double2* b, double2* x,
   if (!op.kg) op.kg = new KrylovGraphs();
   KrylovGraphs& G = *op.kg;
   const long long n = op.P.nvox;
-  const int nb = (int)std::min<long long>((n + TPB - 1) / TPB, 2LL * op.n_sm);
+  const int nb = (int)std::min<long long>((n + TPB - 1) / TPB, (long long)krylov_blocks_per_sm() * op.n_sm);
   if (!G.ks.p) {
     G.ks.alloc(S_NSLOT);
     G.part.alloc(4 * nb + 8);
