@@ -2,7 +2,8 @@
 
 The device-resident Newton graph (Newton / line search / Krylov loops as conditional
 nodes), the device-side WHILE-node Krylov loop vs batched iteration graphs, the optional
-cluster-fused coarse multigrid cycle and the cp.async stencil path are
+cluster-fused coarse multigrid cycle, the block Gauss-Seidel preconditioner, the
+unfused coarse residual / restriction and the cp.async stencil path are
 execution strategies, not different algorithms: the Newton solution of one implicit
 step must agree to the Newton tolerance.  Each variant is selected by its environment
 switch before the operator (and its multigrid) is built."""
@@ -42,6 +43,9 @@ def _step_with(env):
     {"HC_KRYLOV_WHILE": "0"},
     {"HC_AMG_FUSE_ROWS": "4096"},
     {"HC_STENCIL": "2"},
+    {"HC_AMG_BDIAG": "0"},           # block Gauss-Seidel instead of the parallel block Jacobi
+    {"HC_AMG_FUSE_RESTRICT": "0"},   # separate residual and restriction passes
+    {"HC_AMG_PRE_C": "1"},           # zero-guess residual pass that also stores its iterate
 ])
 def test_variant_reaches_the_same_step(env):
     xr, nc, _ = _step_with({})
