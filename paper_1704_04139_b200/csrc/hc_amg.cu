@@ -1215,6 +1215,13 @@ __global__ void k_smooth0_s(long long n, double w, const double* __restrict__ di
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v < n) e[v] = w * dinv[v] * r[v];
 }
+// the same into one component of a double2 vector (stride 2)
+__global__ void k_smooth0_s2(long long n, double w, const double* __restrict__ dinv,
+                             const double* __restrict__ r, double* __restrict__ e) {
+  pdl_wait();
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v < n) e[2 * v] = w * dinv[v] * r[v];
+}
 template <class TV>
 __global__ void k_prolong0_s(long long n, double alpha, const int32_t* __restrict__ prp,
                              const int32_t* __restrict__ pci, const TV* __restrict__ pv,
@@ -1248,7 +1255,10 @@ __global__ void k_merge_s(long long n, const double* __restrict__ ec, const doub
 
 // one V-cycle for block f on the fine grid, scalar vectors: e = M_f^{-1} r.
 // Returns the buffer holding e (one of the block's two ping-pong vectors).
-static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, cudaStream_t s) {
+// dst (optional): the final sweep writes component f of that double2 vector instead
+// (stride-2 output), and nullptr is returned
+static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, cudaStream_t s,
+                           double2* dst = nullptr) {
   Amg& A = *op.amg;
   AmgBlock& B = A.blk[f];
   AmgLevel& L0 = B.levels[0];
@@ -1261,19 +1271,23 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   double* e = A.ea[f].p;
   double* e2 = A.eb[f].p;
   double* res = (f == 0 && A.bdiag) ? A.res_c.p : A.res.p;
-  auto sweep = [&](int epi, const double* in, double* out) {
+  auto sweep = [&](int epi, const double* in, double* out, int fl = 0) {
     if (f == 1) {
-      if (epi == EP_SMOOTH0) fine_launch_op<SM_PHI, EP_SMOOTH0>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
-      else if (epi == EP_SMOOTH) fine_launch_op<SM_PHI, EP_SMOOTH>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
-      else fine_launch_op<SM_PHI, EP_RESID>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
+      if (epi == EP_SMOOTH0) fine_launch_op<SM_PHI, EP_SMOOTH0>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, fl, nullptr, out, s);
+      else if (epi == EP_SMOOTH) fine_launch_op<SM_PHI, EP_SMOOTH>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, fl, nullptr, out, s);
+      else fine_launch_op<SM_PHI, EP_RESID>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, fl, nullptr, out, s);
     } else {
-      if (epi == EP_SMOOTH0) fine_launch_op<SM_CONC, EP_SMOOTH0>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
-      else if (epi == EP_SMOOTH) fine_launch_op<SM_CONC, EP_SMOOTH>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
-      else fine_launch_op<SM_CONC, EP_RESID>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, 0, nullptr, out, s);
+      if (epi == EP_SMOOTH0) fine_launch_op<SM_CONC, EP_SMOOTH0>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, fl, nullptr, out, s);
+      else if (epi == EP_SMOOTH) fine_launch_op<SM_CONC, EP_SMOOTH>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, fl, nullptr, out, s);
+      else fine_launch_op<SM_CONC, EP_RESID>(op, F, nullptr, in, r, L0.dinv.p, w, inv_dt, fl, nullptr, out, s);
     }
     HC_COUNT();
   };
   if (B.levels.size() == 1) {
+    if (dst) {
+      launch(k_smooth0_s2, nb, TPB, 0, s, nv, w, L0.dinv.p, r, reinterpret_cast<double*>(dst) + f); HC_COUNT();
+      return nullptr;
+    }
     launch(k_smooth0_s, nb, TPB, 0, s, nv, w, L0.dinv.p, r, e); HC_COUNT();
     return e;
   }
@@ -1307,6 +1321,11 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
     launch(k_prolong0_s<double>, nb, TPB, 0, s, nv, B.alpha, L0.P.rp.p, L0.P.ci.p, (const double*)L0.P.v.p, L1.x.p, e);
   HC_COUNT();
   for (int k = 0; k < B.nu; ++k) {
+    if (dst && k + 1 == B.nu) {
+      sweep(EP_SMOOTH, e, reinterpret_cast<double*>(dst) + f, FL_OSTRIDE2);
+      HC_CHECK_LAUNCH();
+      return nullptr;
+    }
     sweep(EP_SMOOTH, e, e2);
     std::swap(e, e2);
   }
@@ -1327,11 +1346,11 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
     // block Jacobi: fork the c-block V-cycle onto the side stream, join before the merge
     HC_CUDA(cudaEventRecord(A.ev_fork, s));
     HC_CUDA(cudaStreamWaitEvent(A.side, A.ev_fork, 0));
-    double* ec = vcycle_fine(op, 0, A.rs[0].p, inv_dt, A.side);
+    // each block's final sweep writes its component of z (no merge pass)
+    vcycle_fine(op, 0, A.rs[0].p, inv_dt, A.side, z);
     HC_CUDA(cudaEventRecord(A.ev_join, A.side));
-    double* ep = vcycle_fine(op, 1, A.rs[1].p, inv_dt, s);
+    vcycle_fine(op, 1, A.rs[1].p, inv_dt, s, z);
     HC_CUDA(cudaStreamWaitEvent(s, A.ev_join, 0));
-    launch(k_merge_s, nb, TPB, 0, s, nv, ec, ep, z); HC_COUNT();
     HC_CHECK_LAUNCH();
     return;
   }

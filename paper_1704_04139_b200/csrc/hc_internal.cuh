@@ -296,6 +296,9 @@ void scatter_packed(const Operator& op, const double* x, double2* xg, bool c_fil
 void gather_packed(const Operator& op, const double2* xg, double* x, cudaStream_t s);
 // residual in grid layout: parts bitmask
 enum : int { PART_LIN = 1, PART_BV = 2, PART_1C = 4, PART_BND = 8, PART_TIME = 16 };
+// scalar-mode stencil flag: write the output with stride 2, i.e. into one component of a
+// double2 (c, phi) vector (the preconditioner's final sweeps fill z directly)
+constexpr int FL_OSTRIDE2 = 1 << 16;
 void residual_grid(Operator& op, const double2* xg, const double* npl, double mu, double beta,
                    int parts, const double* cprev_scaled, double inv_dt, double2* out,
                    cudaStream_t s, int which = 3);  // which: 1 stencil kernel, 2 interface kernel

@@ -208,7 +208,7 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
     if constexpr (FULLM) wa = one_c_flag ? sw[buf * TN + cidx] : 0.0;
     if (!in_row) {
       if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
-      else out[v] = 0.0;
+      else out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = 0.0;
     } else {
       const int rk = (aw >> 3) - 1;
       const int a6 = a * 6;
@@ -305,9 +305,9 @@ k_fine_p(DevParams P, FineArgs F, const int32_t* __restrict__ lab4, const double
         out2[v] = make_double2(rc, rp);
       } else {
         if (MODE == SM_CONC) rp += inv_dt * va;
-        if (EPI == EP_STORE) out[v] = rp;
-        else if (EPI == EP_RESID || EPI == EP_RESID0) out[v] = rv - rp;
-        else out[v] = va + omega * dv_ * (rv - rp);   // SMOOTH and SMOOTH0
+        if (EPI == EP_STORE) out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = rp;
+        else if (EPI == EP_RESID || EPI == EP_RESID0) out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = rv - rp;
+        else out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = va + omega * dv_ * (rv - rp);   // SMOOTH and SMOOTH0
       }
     }
     if constexpr (EPI == EP_RESID0) reinterpret_cast<double*>(out2)[v] = va;

@@ -342,7 +342,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
       if constexpr (OC) wa = w_at(S0, 0);
       if (!in_row) {
         if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
-        else out[v] = 0.0;
+        else out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = 0.0;
       } else {
         const int a8 = a << 3;
         const bool elrow = a == TEL;
@@ -454,9 +454,9 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
           if (MODE == SM_PHI) rp += si;
           else rp = fma(elrow ? 1.0 - tp : 1.0, si, rp);   // (T J) on electrolyte c rows
           if (MODE == SM_CONC) rp = fma(inv_dt, va, rp);
-          if (EPI == EP_STORE) out[v] = rp;
-          else if (EPI == EP_RESID || EPI == EP_RESID0) out[v] = rv - rp;
-          else out[v] = va + omega * dv_ * (rv - rp);
+          if (EPI == EP_STORE) out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = rp;
+          else if (EPI == EP_RESID || EPI == EP_RESID0) out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = rv - rp;
+          else out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = va + omega * dv_ * (rv - rp);
         }
       }
       if constexpr (EPI == EP_RESID0) reinterpret_cast<double*>(out2)[v] = va;
