@@ -548,7 +548,7 @@ def run_rom(args, ws, rank, local):
             "e2e": {"value": n_steps / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": 8 * rom.k / n_steps,
                     "d2h_bytes_per_step": 16.0},
             "gpu_launches": int(n1.value - n0.value),
-            "roofline": {"bound": "latency (one CTA; k=%d dense LU per step)" % rom.k, "achieved": None,
+            "roofline": {"bound": "latency (one thread-block cluster; k=%d dense LU per step)" % rom.k, "achieved": None,
                          "peak": None, "unit": None, "frac": None, "traffic": None},
             "clocks": clk.summary()}
 
