@@ -308,6 +308,8 @@ void linearize(Operator& op, const double2* xg, const double* npl, double beta, 
 // 8 phi rows only (c rows written as 0)
 void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2* out,
               cudaStream_t s, int which = 3);
+int jvp_grid_dot(Operator& op, const double2* vg, double inv_dt, int flags, double2* out,
+                 const double2* a, double* part, int two, cudaStream_t s);
 double norm2_grid(Operator& op, const double2* v, int field_mask, cudaStream_t s);
 Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
                           const hc_params& hp);

@@ -62,6 +62,25 @@ __device__ __forceinline__ double fin_sum_block(const double* part, int nb) {
   return t;
 }
 
+// fixed-order sum of n partials, result in every thread (every block computes the same)
+__device__ __forceinline__ double block_sum_all(const double* part, int n) {
+  __shared__ double sh[33];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += __ldcg(part + i);
+  s = warp_sum(s);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = s;
+  __syncthreads();
+  if (w == 0) {
+    double t = l < (int)(blockDim.x >> 5) ? sh[l] : 0.0;
+    t = warp_sum(t);
+    if (l == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
 __device__ void finish_in_last_block(int what, const double* part, double* ks, unsigned* ticket);
 
 // blocks per SM of the Krylov vector kernels (grid-stride loops over the voxels);
@@ -184,10 +203,22 @@ __global__ void k_dev_p(long long n, double* ks, const double2* __restrict__ r,
 // s = r - alpha v, partial ||s||^2
 __global__ void k_dev_s(long long n, double* ks, const double2* __restrict__ r,
                         const double2* __restrict__ v, double2* __restrict__ s,
-                        double* __restrict__ part, unsigned* ticket, SplitOut so) {
+                        double* __restrict__ part, unsigned* ticket, SplitOut so,
+                        const double* __restrict__ jpart, int jnb) {
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
-  const double alpha = ks[S_ALPHA];
+  double alpha;
+  if (jnb > 0) {   // <rhat, v> from the J v epilogue's partials, summed by every block alike
+    const double rv = block_sum_all(jpart, jnb);
+    if (rv == 0.0 || !isfinite(rv)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) { ks[S_ERR] = 2; ks[S_DONE] = 1; }
+      return;
+    }
+    alpha = ks[S_RHO1] / rv;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ks[S_ALPHA] = alpha;
+  } else {
+    alpha = ks[S_ALPHA];
+  }
   double acc = 0.0;
 #pragma unroll 2
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -207,10 +238,26 @@ __global__ void k_dev_xr(long long n, double* ks, const double2* __restrict__ ph
                          const double2* __restrict__ sh, const double2* __restrict__ s,
                          const double2* __restrict__ t, const double2* __restrict__ rhat,
                          double2* __restrict__ x, double2* __restrict__ r, double* __restrict__ part,
-                         unsigned* ticket) {
+                         unsigned* ticket, const double* __restrict__ jpart, int jnb) {
   pdl_wait();
   if (ks[S_DONE] != 0.0) return;
-  const double alpha = ks[S_ALPHA], omega = ks[S_OMEGA];
+  const double alpha = ks[S_ALPHA];
+  double omega;
+  if (jnb > 0) {   // omega = <t, s> / <t, t> from the J v epilogue's partials (scalar_step 3)
+    if (ks[S_EARLY] != 0.0) {
+      omega = 0.0;
+    } else {
+      const double ts = block_sum_all(jpart, jnb), tt = block_sum_all(jpart + jnb, jnb);
+      if (tt == 0.0 || !isfinite(tt)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) { ks[S_ERR] = 3; ks[S_DONE] = 1; }
+        return;
+      }
+      omega = ts / tt;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ks[S_OMEGA] = omega;
+  } else {
+    omega = ks[S_OMEGA];
+  }
   double a1 = 0.0, a2 = 0.0;
 #pragma unroll 2
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -277,6 +324,7 @@ struct KrylovGraphs {
   unsigned long long n_kernels[2] = {0, 0};
   double2* x_ptr[2] = {nullptr, nullptr};
   DBuf<double> ks, part;
+  DBuf<double> jpart;      // per-CTA dot partials of the two J v launches (fused epilogue)
   DBuf<unsigned> ticket;   // last-block ticket of the fused reductions (self-resetting)
   double* ks_host = nullptr;
   ~KrylovGraphs() {
@@ -293,6 +341,44 @@ static void apply_A_dev(Operator& op, const double2* v, double2* out, double inv
   jvp_grid(op, v, inv_dt, mode == 0 ? (1 | 4) : 8, out, s);
 }
 
+// upper bound on the CTAs of one TMA J v launch (one per tile column and plane)
+static long long jpart_cap(const Operator& op) {
+  return (long long)((op.P.nx + VX - 1) / VX) * ((op.P.ny + VY - 1) / VY) * op.P.nz;
+}
+
+// one BiCGStab iteration (captured into the iteration / WHILE-body graphs).  On the TMA
+// path the two reductions after J v (<rhat, v>; <t, s>, <t, t>) come out of the J v
+// kernel's epilogue as per-CTA partials and the next vector kernel sums them, so
+// there is no separate reduction launch.
+static void bicgstab_iteration(Operator& op, Work& W, KrylovGraphs& G, const SplitOut& so, double2* x,
+                               double inv_dt, int mode, int nb, long long n, cudaStream_t s) {
+  double* ks = G.ks.p;
+  double* part = G.part.p;
+  unsigned* tk = G.ticket.p;
+  const int flags = mode == 0 ? (1 | 4) : 8;
+  const long long jcap = jpart_cap(op);
+  double* jp1 = G.jpart.p;
+  double* jp2 = G.jpart.p + jcap;
+  launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p, so); HC_COUNT();
+  amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s, true);
+  int j1 = jvp_grid_dot(op, W.kph.p, inv_dt, flags, W.kv.p, W.khat.p, jp1, 0, s);
+  if (!j1) {
+    apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part, 1, tk); HC_COUNT();
+  }
+  launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk, so, (const double*)jp1, j1);
+  HC_COUNT();
+  amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s, true);
+  int j2 = jvp_grid_dot(op, W.ksh.p, inv_dt, flags, W.kt.p, W.ks.p, jp2, 1, s);
+  if (!j2) {
+    apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
+    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part, 3, tk); HC_COUNT();
+  }
+  launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p, part, tk,
+         (const double*)jp2, j2);
+  HC_COUNT();
+}
+
 int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int mode, double rtol,
                  int maxit, cudaStream_t s) {
   Work& W = work(op);
@@ -303,6 +389,7 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   if (!G.ks.p) {
     G.ks.alloc(S_NSLOT);
     G.part.alloc(4 * nb + 8);
+    G.jpart.alloc(3 * jpart_cap(op));
     G.ticket.alloc(1);
     HC_CUDA(cudaMemset(G.ticket.p, 0, sizeof(unsigned)));
     HC_CUDA(cudaMallocHost(&G.ks_host, S_NSLOT * sizeof(double)));
@@ -318,21 +405,7 @@ int bicgstab_dev(Operator& op, const double2* b, double2* x, double inv_dt, int 
   launch(k_dev_init, 1, 256, 0, s, nb, G.part.p, G.ks.p, rtol * rtol); HC_COUNT();
   // the body of one BiCGStab iteration (captured, never run eagerly)
   const SplitOut so{op.labels.p, op.P.t_plus, op.amg->rs[0].p, op.amg->rs[1].p};
-  auto iteration = [&]() {
-    double* ks = G.ks.p;
-    double* part = G.part.p;
-    unsigned* tk = G.ticket.p;
-    launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p, so); HC_COUNT();
-    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s, true);
-    apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
-    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part, 1, tk); HC_COUNT();
-    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk, so); HC_COUNT();
-    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s, true);
-    apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
-    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part, 3, tk); HC_COUNT();
-    launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
-           part, tk); HC_COUNT();
-  };
+  auto iteration = [&]() { bicgstab_iteration(op, W, G, so, x, inv_dt, mode, nb, n, s); };
   const bool rebuild = !G.exec[mode] || G.inv_dt[mode] != inv_dt;
   if (rebuild) {
     if (G.exec[mode]) cudaGraphExecDestroy(G.exec[mode]);
@@ -440,6 +513,7 @@ void krylov_append(Operator& op, GraphBuilder& gb, const double2* b, double2* x,
   if (!G.ks.p) {
     G.ks.alloc(S_NSLOT);
     G.part.alloc(4 * nb + 8);
+    G.jpart.alloc(3 * jpart_cap(op));
     G.ticket.alloc(1);
     HC_CUDA(cudaMemset(G.ticket.p, 0, sizeof(unsigned)));
     HC_CUDA(cudaMallocHost(&G.ks_host, S_NSLOT * sizeof(double)));
@@ -465,16 +539,7 @@ void krylov_append(Operator& op, GraphBuilder& gb, const double2* b, double2* x,
   const SplitOut so{op.labels.p, op.P.t_plus, op.amg->rs[0].p, op.amg->rs[1].p};
   GraphBuilder body{s, gb.cond(h, cudaGraphCondTypeWhile), {}};
   body.capture([&] {
-    launch(k_dev_p, (int)((n + TPB - 1) / TPB), TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.kp.p, so); HC_COUNT();
-    amg_apply(op, W.kp.p, W.kph.p, inv_dt, mode, s, true);
-    apply_A_dev(op, W.kph.p, W.kv.p, inv_dt, mode, s);
-    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.khat.p, W.kv.p, nullptr, nullptr, part, 1, tk); HC_COUNT();
-    launch(k_dev_s, nb, TPB, 0, s, n, ks, W.kr.p, W.kv.p, W.ks.p, part, tk, so); HC_COUNT();
-    amg_apply(op, W.ks.p, W.ksh.p, inv_dt, mode, s, true);
-    apply_A_dev(op, W.ksh.p, W.kt.p, inv_dt, mode, s);
-    launch(k_dev_dot2, nb, TPB, 0, s, n, ks, W.kt.p, W.ks.p, W.kt.p, W.kt.p, part, 3, tk); HC_COUNT();
-    launch(k_dev_xr, nb, TPB, 0, s, n, ks, W.kph.p, W.ksh.p, W.ks.p, W.kt.p, W.khat.p, x, W.kr.p,
-           part, tk); HC_COUNT();
+    bicgstab_iteration(op, W, G, so, x, inv_dt, mode, nb, n, s);
     k_dev_cond<<<1, 32, 0, s>>>(ks, h, maxit);
   });
   gb.capture([&] { launch(k_dev_check, 1, 1, 0, s, (const double*)ks, maxit, ns); HC_COUNT(); });

@@ -529,6 +529,23 @@ void jvp_grid(Operator& op, const double2* vg, double inv_dt, int flags, double2
   HC_CHECK_LAUNCH();
 }
 
+// J v through the TMA stencil with the per-CTA partial dot products out.a (and out.out
+// when two) fused into its epilogue; returns the number of partials, 0 if the TMA path is
+// not available (nothing launched then)
+int jvp_grid_dot(Operator& op, const double2* vg, double inv_dt, int flags, double2* out,
+                 const double2* a, double* part, int two, cudaStream_t s) {
+  if (op.stencil_kind != 3 || !op.tma) return 0;
+  int nblk = 0;
+  FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
+             op.if_cslot.p, op.elz.p, nullptr, op.tp_off.p, a, part, two, &nblk};
+  if (!fine_launch_tma<SM_FULL, EP_STORE>(*op.tma, op.P, F, op.labt.p, vg, nullptr, nullptr, nullptr, 0.0,
+                                          inv_dt, flags, out, nullptr, op.n_sm, s))
+    return 0;
+  HC_COUNT();
+  HC_CHECK_LAUNCH();
+  return nblk;
+}
+
 double norm2_grid(Operator& op, const double2* v, int field_mask, cudaStream_t s) {
   int nb = std::min<long long>(blocks_for(op.P.nvox), 4 * op.n_sm);
   k_sumsq<<<nb, TPB, 0, s>>>(op.P.nvox, v, field_mask, op.red.p); HC_COUNT();

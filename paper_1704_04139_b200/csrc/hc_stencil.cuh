@@ -39,6 +39,13 @@ struct FineArgs {
   const int2* elz;        // TMA stencil: per 32 x 8 tile column, z range holding electrolyte (lo, hi)
   const double* islot;    // TMA residual: interface current per face slot, oriented from the row
   const int32_t* tp_off;  // TMA stencil: first face slot of every (32 x 8 tile, plane), + total
+  // TMA J v only: per-CTA partial dot products of the output with dot_a (and, dot_two,
+  // with itself) into dot_part[cta] / dot_part[n_cta + cta]; the launcher stores n_cta in
+  // *dot_nblk (host).  Lets BiCGStab drop its separate reduction pass after each J v.
+  const double2* dot_a = nullptr;
+  double* dot_part = nullptr;
+  int dot_two = 0;
+  int* dot_nblk = nullptr;
 };
 
 }  // namespace hc

@@ -285,6 +285,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
     logs_for(0);
     logs_for(1);
   }
+  double dacc1 = 0.0, dacc2 = 0.0;   // fused dot products (J v with F.dot_a)
   auto step = [&](int j, auto slotc, unsigned ph0, unsigned ph1) {
     constexpr int K = decltype(slotc)::value, K1 = (K + 1) % T_S;
     const unsigned char* S0 = base + K * L::SLOT;
@@ -450,6 +451,11 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
           if ((flags & 1) && crow) rc = fma(va.x, inv_dt, rc);
           if (flags & 8) rc = 0.0;
           out2[v] = make_double2(rc, rp);
+          if (MODE == SM_FULL && F.dot_a) {
+            const double2 da = F.dot_a[v];
+            dacc1 += rc * da.x + rp * da.y;
+            dacc2 += rc * rc + rp * rp;
+          }
         } else {
           if (MODE == SM_PHI) rp += si;
           else rp = fma(elrow ? 1.0 - tp : 1.0, si, rp);   // (T J) on electrolyte c rows
@@ -473,6 +479,31 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
       constexpr int K = decltype(kc)::value;
       if (jb + K < nplane) step(jb + K, kc, ph, K + 1 == T_S ? ph ^ 1 : ph);
     });
+  }
+  if constexpr (MODE == SM_FULL) {
+    if (F.dot_a) {   // CTA partials of the fused dot products (fixed order; compute warps only)
+      __shared__ double dsh[2][T_WARPS];
+      for (int o = 16; o > 0; o >>= 1) {
+        dacc1 += __shfl_down_sync(0xffffffffu, dacc1, o);
+        dacc2 += __shfl_down_sync(0xffffffffu, dacc2, o);
+      }
+      if (threadIdx.x == 0) {
+        dsh[0][threadIdx.y] = dacc1;
+        dsh[1][threadIdx.y] = dacc2;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(T_WARPS * VX) : "memory");   // the producer warp has left
+      if (tid == 0) {
+        double a1 = 0.0, a2 = 0.0;
+        for (int k = 0; k < T_WARPS; ++k) {
+          a1 += dsh[0][k];
+          a2 += dsh[1][k];
+        }
+        const int nb = gridDim.x * gridDim.y * gridDim.z;
+        const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        F.dot_part[b] = a1;
+        if (F.dot_two) F.dot_part[nb + b] = a2;
+      }
+    }
   }
 }
 
@@ -542,7 +573,9 @@ inline bool fine_launch_tma(TmaCache& cache, const DevParams& P, const FineArgs&
     }
     const int bz = pick_bz(bx, by, P.nz, per_sm, n_sm);
     const int zc = (P.nz + bz - 1) / bz;
-    launch(kern, dim3(bx, by, (P.nz + zc - 1) / zc), dim3(VX, L::THREADS / VX, 1), smem, s, P, M, F, labt,
+    const dim3 grid(bx, by, (P.nz + zc - 1) / zc);
+    if (F.dot_nblk) *F.dot_nblk = (int)(grid.x * grid.y * grid.z);
+    launch(kern, grid, dim3(VX, L::THREADS / VX, 1), smem, s, P, M, F, labt,
            V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
   };
   if (MODE == SM_FULL && (flags & 4)) go(std::true_type{});
