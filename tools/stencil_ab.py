@@ -36,7 +36,7 @@ for k in kinds:
     ms = (ctypes.c_double * 5)()
     xd, nd = _dev.to_dev(x), _dev.to_dev(npl)
     _native.check(_native.lib().hc_time_kernels(op.native.handle, _dev.ptr(xd), _dev.ptr(nd), beta,
-                                                1.0 / rs.dt, 20, 256 << 20, ms, _dev.stream()))
+                                                1.0 / rs.dt, 20, int(os.environ.get("FLUSH_MB", "256")) << 20, ms, _dev.stream()))
     nvox = grid.labels.size
     print(f"kind {k}: residual {ms[0]*1e3:.1f}+{ms[1]*1e3:.1f} us, jv {ms[2]*1e3:.1f}+{ms[3]*1e3:.1f} us, "
           f"copy {ms[4]*1e3:.1f} us ({nvox*32/ms[4]/1e6:.0f} GB/s)", flush=True)
