@@ -203,9 +203,10 @@ __global__ void k_ptap_w(int n_next, const int32_t* __restrict__ pt_ptr,
   }
 }
 
-// R = P^T A for a tentative P: row I is the sum of its member rows (warp per coarse row,
-// members in order, the same fixed summation order as k_ptap_w)
+// R = P^T A: row I is the P-weighted sum of the fine rows in P^T's row I (warp per
+// coarse row, fine rows in order, the same fixed summation order as k_ptap_w)
 __global__ void k_pta_w(int n_next, const int32_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_row,
+                        const int32_t* __restrict__ pt_idx, const double* __restrict__ pv,
                         const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
                         const double* __restrict__ av, const int32_t* __restrict__ rrp,
                         const int32_t* __restrict__ rci, double* __restrict__ rv) {
@@ -217,7 +218,8 @@ __global__ void k_pta_w(int n_next, const int32_t* __restrict__ pt_ptr, const in
   __syncwarp();
   for (int q = pt_ptr[I]; q < pt_ptr[I + 1]; ++q) {
     const int i = pt_row[q];
-    for (int m = arp[i] + lane; m < arp[i + 1]; m += 32) rv[find_col(rci, r0, r1, aci[m])] += av[m];
+    const double p = pv[pt_idx[q]];
+    for (int m = arp[i] + lane; m < arp[i + 1]; m += 32) rv[find_col(rci, r0, r1, aci[m])] += p * av[m];
     __syncwarp();
   }
 }
@@ -438,8 +440,9 @@ __global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
 template <int VS, class VT>
 __global__ void k_resid_restrict(int n1, const int32_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_row,
                                  const int32_t* __restrict__ rrp, const int32_t* __restrict__ rci,
-                                 const VT* __restrict__ rv, const double* __restrict__ b,
-                                 const double* __restrict__ x, double* __restrict__ b1) {
+                                 const VT* __restrict__ rv, const VT* __restrict__ ptv,
+                                 const double* __restrict__ b, const double* __restrict__ x,
+                                 double* __restrict__ b1) {
   pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int I = (int)(gt / VS), lane = (int)(gt % VS);
@@ -458,7 +461,7 @@ __global__ void k_resid_restrict(int n1, const int32_t* __restrict__ pt_ptr, con
       s -= a3 * x3;
     }
     for (; k < k1; k += VS) s -= (double)rv[k] * x[rci[k]];
-    for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += VS) s += b[pt_row[q]];
+    for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += VS) s += (double)ptv[q] * b[pt_row[q]];
   }
 #pragma unroll
   for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
@@ -686,7 +689,8 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     upload(L.pt_ptr, tp);
     upload(L.pt_row, trow);
     upload(L.pt_idx, tidx);
-    if (level >= 1 && !smooth && cfg.fuse_restrict) {   // R = P^T A pattern: union of member rows
+    if (level >= 1 && cfg.fuse_restrict && (!smooth || cfg.fuse_restrict_sa)) {
+      // R = P^T A pattern: union of the columns of the fine rows in each P^T row
       std::vector<std::vector<int32_t>> rows(nn);
       parallel_for(nn, [&](int I) {
         auto& r = rows[I];
@@ -804,6 +808,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_FUSE_ROWS")) amg->fuse_rows = atoi(e);
   if (const char* e = getenv("HC_AMG_FUSE_NNZ")) amg->fuse_nnz = atoll(e);
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT")) amg->fuse_restrict = atoi(e) != 0;
+  if (const char* e = getenv("HC_AMG_FUSE_RESTRICT_SA")) amg->fuse_restrict_sa = atoi(e) != 0;
   auto t0 = std::chrono::steady_clock::now();
   for (int f = 0; f < 2; ++f) {
     amg->blk[f].nu = amg->nu;
@@ -875,8 +880,8 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
       }
       if (L.R.nnz && l + 1 < B.levels.size()) {
         const AmgLevel& U = B.levels[l + 1];
-        launch(k_pta_w, nblk(32LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, L.A.rp.p, L.A.ci.p, L.A.v.p,
-               L.R.rp.p, L.R.ci.p, L.R.v.p); HC_COUNT();
+        launch(k_pta_w, nblk(32LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p,
+               (const double*)L.P.v.p, L.A.rp.p, L.A.ci.p, L.A.v.p, L.R.rp.p, L.R.ci.p, L.R.v.p); HC_COUNT();
         if (A.fp32_coarse) {
           launch(k_to_float, nblk(L.R.nnz), TPB, 0, s, L.R.nnz, L.R.v.p, L.R.vf.p); HC_COUNT();
         }
@@ -1136,8 +1141,10 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
     auto go = [&](auto vs_tag, auto* vals) {
       constexpr int VS = decltype(vs_tag)::value;
       using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
+      const VT* ptv = std::is_same<VT, float>::value ? (const VT*)(const void*)L.ptvf.p
+                                                     : (const VT*)(const void*)L.ptv.p;
       launch(k_resid_restrict<VS, VT>, nblk((long long)VS * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p,
-             L.R.rp.p, L.R.ci.p, vals, L.b.p, L.x.p, U.b.p);
+             L.R.rp.p, L.R.ci.p, vals, ptv, L.b.p, L.x.p, U.b.p);
       HC_COUNT();
     };
     if (A.fp32_coarse) {

@@ -84,7 +84,8 @@ struct Amg {
   int wmin = 1;
   int fuse_rows = 0;          // levels with at most this many rows ... (0: off, measured slower)
   long long fuse_nnz = 400000; // ... and nonzeros run as one cluster kernel (0 rows: off)
-  bool fuse_restrict = true;  // residual + restriction as one pass on tentative CSR levels (R = P^T A)
+  bool fuse_restrict = true;  // residual + restriction as one pass on CSR levels (R = P^T A) ...
+  bool fuse_restrict_sa = false;  // ... also where P is smoothed (HC_AMG_FUSE_RESTRICT_SA)
   int coarsen = 2;           // block growth factor of the transfers above level 1              // gamma cycles on CSR levels wmin..wdepth
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int refresh = 0;          // numeric setup every Newton iteration (1) or once per solve (0)
