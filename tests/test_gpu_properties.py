@@ -76,6 +76,22 @@ def test_setup_is_reproducible():
         assert np.array_equal(getattr(op, a), getattr(op2, a))
 
 
+def test_steps_are_bitwise_reproducible():
+    """No floating-point atomics and fixed-order reductions on the solver path (parallel
+    preconditioner branches, fused J v partials, last-block finishes): two runs from fresh
+    operators give bitwise identical states."""
+    P, rs, grid, params, _, mu = _cell("tiny")
+    out = []
+    for _ in range(2):
+        op = P.SystemOperator(P.build_dofmap(grid), params)
+        cfg = P.SolverConfig(dt_init=min(0.05, rs.dt), dt_max=rs.dt, linear_safety=0.3)
+        st = P.prepare_initial_state(op, params, mu, cfg)
+        for _ in range(3):
+            st, _, _, _ = P.step(op, st, rs.dt, mu, cfg)
+        out.append((st.x.copy(), st.n_pl.copy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
 @pytest.mark.parametrize("safety", [0.1, 0.3])
 def test_inexact_newton_curves_match_exact_on_tiny_config(safety):
     """BASELINE config 0 (tiny cell, 1C, dt = 1 s, 10 steps): the voltage, mean solid
