@@ -33,6 +33,7 @@ namespace hc {
 enum : int32_t { RF_BV = 0, RF_CE = 1, RF_STRIP = 2, RF_ELEL = 3 };
 constexpr int ROM_THREADS = 1024;
 constexpr int TK = 16;    // E G panel depth
+__host__ __device__ inline int rom_ld(int k) { return (k & 1) ? k : k + 1; }
 constexpr int ROM_ACC = 4; // J~ entries per thread: k <= 160 rows over >= 8 CTAs
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -115,14 +116,21 @@ k_rom_run(DevParams P, RomDev R, RomWork W, const double* __restrict__ mus, doub
   }
   extern __shared__ double sm[];
   const int k = R.k, m = R.m;
-  double* J = sm;                 // [k][k] LU factors (rank 0)
-  double* rr = J + k * k;         // [k] residual / Newton update (rank 0)
+  // [k][ld] LU factors (rank 0); odd row pitch so the column walks of the pivot search
+  // and the triangular solves hit distinct shared-memory banks (a pitch of k doubles
+  // put a warp's 32 rows on 2 banks: 16-way conflicts)
+  const int ld = rom_ld(k);
+  double* J = sm;
+  double* rr = J + k * ld;        // [k] residual / Newton update (rank 0)
   double* xo = rr + k;            // [k] x~ at the start of the step
   double* red = xo + k;           // [64] reduction scratch
   double* sx = red + 64;          // [k] x~ (this CTA's copy)
   double* pg = sx + k;            // [TK][k] panel of G
+  double* dgi = pg;               // [k] 1 / U_cc (rank 0; lives in the G panel, which is only
+                                  // used before the factorization that rewrites it)
   int* piv = reinterpret_cast<int*>(pg + TK * k);   // [k]
   int* ctl = piv + k;             // [4] control broadcast inside the CTA
+  int* perm = ctl + 4;            // [k] row permutation of the LU (all pivot swaps composed)
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   const int gtid = rank * nt + tid, gnt = ncta * nt;
@@ -242,14 +250,14 @@ k_rom_run(DevParams P, RomDev R, RomWork W, const double* __restrict__ mus, doub
       // phase E (rank 0): LU when fresh, solve, update x~, convergence flags
       if (rank == 0) {
         if (fresh) {
-          for (int idx = tid; idx < k * k; idx += nt) J[idx] = ldc(W.J + idx);
+          for (int idx = tid; idx < k * k; idx += nt) J[(idx / k) * ld + idx % k] = ldc(W.J + idx);
           __syncthreads();
           for (int c = 0; c < k; ++c) {   // LU with partial pivoting (column c)
             if (tid < 32) {
               double best = -1.0;
               int bi = c;
               for (int i = c + tid; i < k; i += 32) {
-                const double v = fabs(J[i * k + c]);
+                const double v = fabs(J[i * ld + c]);
                 if (v > best) { best = v; bi = i; }
               }
               for (int o = 16; o; o >>= 1) {
@@ -263,41 +271,45 @@ k_rom_run(DevParams P, RomDev R, RomWork W, const double* __restrict__ mus, doub
             const int p = piv[c];
             if (p != c)
               for (int j = tid; j < k; j += nt) {
-                const double t = J[c * k + j];
-                J[c * k + j] = J[p * k + j];
-                J[p * k + j] = t;
+                const double t = J[c * ld + j];
+                J[c * ld + j] = J[p * ld + j];
+                J[p * ld + j] = t;
               }
             __syncthreads();
-            const double d = J[c * k + c];
+            const double d = J[c * ld + c];
             for (int idx = tid; idx < (k - c - 1) * (k - c); idx += nt) {
               const int i = c + 1 + idx / (k - c), j = c + idx % (k - c);
               if (j == c) continue;
-              J[i * k + j] = fma(-(J[i * k + c] / d), J[c * k + j], J[i * k + j]);
+              J[i * ld + j] = fma(-(J[i * ld + c] / d), J[c * ld + j], J[i * ld + j]);
             }
             __syncthreads();
-            for (int i = c + 1 + tid; i < k; i += nt) J[i * k + c] /= d;
+            for (int i = c + 1 + tid; i < k; i += nt) J[i * ld + c] /= d;
             __syncthreads();
           }
-        }
-        if (tid < 32) {   // pivots, forward, backward on one warp
-          for (int j = tid; j < k; j += 32) rr[j] = ldc(W.rr + j);
-          __syncwarp();
-          if (tid == 0)
+          for (int c = tid; c < k; c += nt) dgi[c] = 1.0 / J[c * ld + c];   // U's reciprocal diagonal
+          if (tid == 0) {   // the pivot swaps composed into one gather: rhs_perm[i] = rhs[perm[i]]
+            for (int i = 0; i < k; ++i) perm[i] = i;
             for (int c = 0; c < k; ++c) {
               const int p = piv[c];
-              if (p != c) { const double t = rr[c]; rr[c] = rr[p]; rr[p] = t; }
+              if (p != c) { const int t = perm[c]; perm[c] = perm[p]; perm[p] = t; }
             }
+          }
+          __syncthreads();
+        }
+        if (tid < 32) {   // pivots, forward, backward on one warp
+          // the pivot swaps were composed into one permutation at factorization time
+          for (int j = tid; j < k; j += 32) rr[j] = ldc(W.rr + perm[j]);
           __syncwarp();
           for (int c = 0; c < k; ++c) {
             const double v = rr[c];
-            for (int i = c + 1 + tid; i < k; i += 32) rr[i] = fma(-J[i * k + c], v, rr[i]);
+            for (int i = c + 1 + tid; i < k; i += 32) rr[i] = fma(-J[i * ld + c], v, rr[i]);
             __syncwarp();
           }
           for (int c = k - 1; c >= 0; --c) {
-            if (tid == 0) rr[c] /= J[c * k + c];
+            if (tid == 0) rr[c] *= dgi[c];
             __syncwarp();
             const double v = rr[c];
-            for (int i = tid; i < c; i += 32) rr[i] = fma(-J[i * k + c], v, rr[i]);
+            for (int i = tid; i < c; i += 32) rr[i] = fma(-J[i * ld + c], v, rr[i]);
             __syncwarp();
           }
           // convergence per block: |delta_c| <= rtol |x~_c|, |delta_p| <= rtol (|x~_p| + 1)
@@ -375,8 +387,8 @@ void rom_run(const Operator& op, const hc_rom* rom, int n_par, double* xt, doubl
   DBuf<int32_t> st(np * 4);
   HC_CUDA(cudaMemsetAsync(st.p, 0, np * 4 * sizeof(int32_t), s));
   RomWork W{xt, xs.p, fq.p, fdq.p, nn.p, rr.p, G.p, J.p, npl, qoi, xt_steps, iters, st.p};
-  const size_t smem = ((size_t)R.k * R.k + 3 * R.k + 64 + (size_t)TK * R.k) * sizeof(double) +
-                      (R.k + 4) * sizeof(int);
+  const size_t smem = ((size_t)R.k * rom_ld(R.k) + 3 * R.k + 64 + (size_t)TK * R.k) * sizeof(double) +
+                      (2 * R.k + 4) * sizeof(int);
   HC_CUDA(cudaFuncSetAttribute(k_rom_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   static int cluster = 0;   // largest cluster the device schedules (16 non-portable, else 8)
   if (!cluster) {
