@@ -300,16 +300,46 @@ k_rom_run(DevParams P, RomDev R, RomWork W, const double* __restrict__ mus, doub
           // the pivot swaps were composed into one permutation at factorization time
           for (int j = tid; j < k; j += 32) rr[j] = ldc(W.rr + perm[j]);
           __syncwarp();
-          for (int c = 0; c < k; ++c) {
-            const double v = rr[c];
-            for (int i = c + 1 + tid; i < k; i += 32) rr[i] = fma(-J[i * ld + c], v, rr[i]);
+          // blocked by 32 columns: the sequential part of each diagonal block runs on
+          // lane-resident values broadcast by shuffle, the rows outside it take the block's
+          // 32 updates in one pass.  Every row receives its column updates in the same
+          // (ascending / descending) column order as the plain column sweep.
+          for (int b0 = 0; b0 < k; b0 += 32) {   // forward, unit lower L
+            const int nbk = min(32, k - b0);
+            double yb = tid < nbk ? rr[b0 + tid] : 0.0;
+            for (int cc = 0; cc < nbk; ++cc) {
+              const double l = (tid > cc && tid < nbk) ? J[(b0 + tid) * ld + b0 + cc] : 0.0;
+              yb = fma(-l, __shfl_sync(0xffffffffu, yb, cc), yb);
+            }
+            if (tid < nbk) rr[b0 + tid] = yb;
+            for (int i0 = b0 + nbk; i0 < k; i0 += 32) {
+              const int i = i0 + tid;
+              const bool ok = i < k;
+              double acc = ok ? rr[i] : 0.0;
+              for (int cc = 0; cc < nbk; ++cc) {
+                const double l = ok ? J[i * ld + b0 + cc] : 0.0;
+                acc = fma(-l, __shfl_sync(0xffffffffu, yb, cc), acc);
+              }
+              if (ok) rr[i] = acc;
+            }
             __syncwarp();
           }
-          for (int c = k - 1; c >= 0; --c) {
-            if (tid == 0) rr[c] *= dgi[c];
-            __syncwarp();
-            const double v = rr[c];
-            for (int i = tid; i < c; i += 32) rr[i] = fma(-J[i * ld + c], v, rr[i]);
+          for (int b0 = ((k - 1) / 32) * 32; b0 >= 0; b0 -= 32) {   // backward, U (1 / U_cc)
+            const int nbk = min(32, k - b0);
+            double yb = tid < nbk ? rr[b0 + tid] : 0.0;
+            for (int cc = nbk - 1; cc >= 0; --cc) {
+              if (tid == cc) yb *= dgi[b0 + cc];
+              const double u = tid < cc ? J[(b0 + tid) * ld + b0 + cc] : 0.0;
+              yb = fma(-u, __shfl_sync(0xffffffffu, yb, cc), yb);
+            }
+            if (tid < nbk) rr[b0 + tid] = yb;
+            for (int i0 = 0; i0 < b0; i0 += 32) {
+              const int i = i0 + tid;   // i < b0 always (b0 is a multiple of 32)
+              double acc = rr[i];
+              for (int cc = nbk - 1; cc >= 0; --cc)
+                acc = fma(-J[i * ld + b0 + cc], __shfl_sync(0xffffffffu, yb, cc), acc);
+              rr[i] = acc;
+            }
             __syncwarp();
           }
           // convergence per block: |delta_c| <= rtol |x~_c|, |delta_p| <= rtol (|x~_p| + 1)
