@@ -660,7 +660,9 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     }
     upload(L.parent, parent);
     // prolongator pattern: parent(i) plus (smoothed) the parents of row i's columns
-    const bool smooth = level < (field == 0 ? cfg.sa_levels_c : cfg.sa_levels);
+    const bool smooth = level < (field == 0 ? cfg.sa_levels_c : cfg.sa_levels) ||
+                        (field != 0 && level == cfg.sa_levels && n >= cfg.sa_rows_min && n <= cfg.sa_rows);
+    L.smoothed = smooth;
     HPat Pp;
     {
       std::vector<std::vector<int32_t>> rows(n);
@@ -795,6 +797,8 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_OMEGA")) amg->omega = atof(e);
   if (const char* e = getenv("HC_AMG_OMEGA_P")) amg->omega_p = atof(e);
   if (const char* e = getenv("HC_AMG_SA_LEVELS")) amg->sa_levels = atoi(e);
+  if (const char* e = getenv("HC_AMG_SA_ROWS")) amg->sa_rows = atoi(e);
+  if (const char* e = getenv("HC_AMG_SA_ROWS_MIN")) amg->sa_rows_min = atoi(e);
   if (const char* e = getenv("HC_AMG_ALPHA")) amg->alpha = atof(e);
   if (const char* e = getenv("HC_AMG_COARSE_MAX")) amg->coarse_max = atoi(e);
   if (const char* e = getenv("HC_AMG_GAMMA")) amg->gamma = atoi(e);
@@ -858,7 +862,7 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
       if (l > 0) {
         launch(k_dinv, nblk(L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p); HC_COUNT();
       }
-      launch(k_smooth_P, nblk(L.n), TPB, 0, s, L.n, (int)l < (f == 0 ? A.sa_levels_c : A.sa_levels), A.omega_p, L.A.rp.p, L.A.ci.p,
+      launch(k_smooth_P, nblk(L.n), TPB, 0, s, L.n, (int)L.smoothed, A.omega_p, L.A.rp.p, L.A.ci.p,
                                            L.A.v.p, L.dinv.p, L.parent.p, L.P.rp.p, L.P.ci.p,
                                            L.P.v.p); HC_COUNT();
       launch(k_gather_ptv, nblk((long long)L.P.nnz), TPB, 0, s, (long long)L.P.nnz, L.pt_idx.p, L.P.v.p,
