@@ -661,7 +661,8 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     upload(L.parent, parent);
     // prolongator pattern: parent(i) plus (smoothed) the parents of row i's columns
     const bool smooth = level < (field == 0 ? cfg.sa_levels_c : cfg.sa_levels) ||
-                        (field != 0 && level == cfg.sa_levels && n >= cfg.sa_rows_min && n <= cfg.sa_rows);
+                        (field != 0 && (cfg.sa_any ? level >= cfg.sa_levels : level == cfg.sa_levels) &&
+                         n >= cfg.sa_rows_min && n <= cfg.sa_rows);
     L.smoothed = smooth;
     HPat Pp;
     {
@@ -799,6 +800,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_SA_LEVELS")) amg->sa_levels = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_ROWS")) amg->sa_rows = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_ROWS_MIN")) amg->sa_rows_min = atoi(e);
+  if (const char* e = getenv("HC_AMG_SA_ANY")) amg->sa_any = atoi(e);
   if (const char* e = getenv("HC_AMG_ALPHA")) amg->alpha = atof(e);
   if (const char* e = getenv("HC_AMG_COARSE_MAX")) amg->coarse_max = atoi(e);
   if (const char* e = getenv("HC_AMG_GAMMA")) amg->gamma = atoi(e);

@@ -79,11 +79,13 @@ struct Amg {
   double omega = 0.9;        // Jacobi smoothing weight
   double omega_p = 2.0 / 3;  // prolongator smoothing weight
   int sa_levels = 2;         // smoothed prolongators on the first sa_levels transfers
-  // the transfer after the sa_levels smoothed ones is smoothed too when its fine level has
+  // transfers past the sa_levels smoothed ones are smoothed too when their fine level has
   // sa_rows_min..sa_rows rows (measured: medium cell, 10.6 k phi rows at level 2, 23.6 -> 15.6
-  // BiCGStab iterations per step and 101 -> 118 steps/s; the large cell's 83 k rows and the
-  // batched cells' smaller levels are faster without it)
+  // BiCGStab iterations per step and 101 -> 118 steps/s; large cell, 13.5 k rows at level 3,
+  // 36.3 -> 23.4 iterations and 13.4 -> 19.6 steps/s; its 83 k-row level 2 converges far worse
+  // smoothed, and the batched cells' levels are below the window)
   int sa_rows_min = 8192, sa_rows = 32768;
+  int sa_any = 1;            // 0: the size rule applies only to the transfer right after sa_levels
   double alpha = 1.0;
   int gamma = 1;             // cycles per coarse-level solve (2 = W-cycle)
   int wdepth = 3;
