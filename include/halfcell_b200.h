@@ -68,9 +68,10 @@ typedef struct hc_solver_config {
   double linear_safety;
 } hc_solver_config;
 
-/* Result record of one Newton solve / accepted time step. */
+/* Result record of one Newton solve / accepted time step.  status: HC_OK, or the error
+ * code of this cell in a batch (hc_step_batch). */
 typedef struct hc_newton_stats {
-  int32_t n_iter, krylov_iters, retries, pad_;
+  int32_t n_iter, krylov_iters, retries, status;
   double norm0, norm_final, tol, dt_used, dt_next, clamped_loss;
 } hc_newton_stats;
 
@@ -113,22 +114,68 @@ int hc_jvp(hc_operator* op, const double* x, const double* n_pl, double beta, do
 int hc_jacobian_csr(hc_operator* op, const double* x, const double* n_pl, double beta,
                     int64_t* nnz, int64_t* row_ptr, int64_t* col_idx, double* values);
 
+/* SystemOperator.A_lin (operator.py:221): the affine part's matrix in CSR, same calling
+ * convention as hc_jacobian_csr (two calls: size, then fill). */
+int hc_lin_csr(hc_operator* op, int64_t* nnz, int64_t* row_ptr, int64_t* col_idx, double* values);
+
+/* SystemOperator.strip_face_currents (operator.py:391-399): the stripping current (A/m^2)
+ * of every stripping face in the reference's face order, at packed state x (device) and
+ * plated inventory n_pl, with the implicit-inventory coupling beta; out[n_strip] (device).
+ * The matching plated slots are export selector 6, row 3. */
+int hc_strip_face_currents(hc_operator* op, const double* x, const double* n_pl, double beta,
+                           double* out, void* stream);
+
+/* RestrictedSubOperator.apply / .jacobian (operator.py:541-646): selected output rows of
+ * a nonlinear sub-operator evaluated from its stencil values only.  The face table is the
+ * one the reduced model's online kernel reads (hc_rom): n_f faces with f_kind (0 BV,
+ * 1 counter exchange, 2 stripping, 3 electrolyte-electrolyte), f_dof[n_f][4] stencil
+ * positions, f_slot plated slots; rows as CSR row_ptr[n_rows+1] -> (row_face, row_coef).
+ * x_st[n_s], n_pl (device); out[n_rows] (device) and, if jac != NULL, the dense local
+ * Jacobian jac[n_rows][n_s] (device, row-major). */
+int hc_restricted_eval(hc_operator* op, int32_t n_rows, int32_t n_f, int32_t n_s, const int32_t* f_kind,
+                       const int32_t* f_dof, const int32_t* f_slot, const int32_t* row_ptr,
+                       const int32_t* row_face, const double* row_coef, const double* x_st,
+                       const double* n_pl, double beta, double* out, double* jac, void* stream);
+
 /* newton_solve (fvm/newton.py:86-168): solves m (x - x_prev)/dt + A(x; mu) = 0
  * from x_guess; x_out receives the converged packed state (device). */
 int hc_newton_solve(hc_operator* op, const double* x_guess, double dt, const double* x_prev,
                     const double* n_pl, double mu, const hc_solver_config* cfg, double* x_out,
                     hc_newton_stats* stats, void* stream);
 
+/* newton_solve with its full signature and result (fvm/newton.py:86-168): `source`
+ * (packed, device, may be NULL) is added to every residual (newton.py:107-108);
+ * iterates[max_iterates][n_total] (device, may be NULL) receives every accepted Newton
+ * iterate (NewtonResult.iterates) and norms[max_norms] (host, may be NULL) the residual
+ * norm of the guess and of every iterate (NewtonResult.residual_norms); stats->n_iter
+ * is the number of iterates. */
+int hc_newton_solve_ex(hc_operator* op, const double* x_guess, double dt, const double* x_prev,
+                       const double* n_pl, double mu, const hc_solver_config* cfg, const double* source,
+                       double* iterates, int32_t max_iterates, double* norms, int32_t max_norms,
+                       double* x_out, hc_newton_stats* stats, void* stream);
+
 /* solve_initial_potential (fvm/newton.py:171-206): phi block at frozen c. */
 int hc_solve_initial_potential(hc_operator* op, const double* x0, const double* n_pl, double mu,
                                const hc_solver_config* cfg, double* x_out, hc_newton_stats* stats,
                                void* stream);
 
-/* step (fvm/timestepping.py:270-312): one accepted implicit-Euler step with
+/* step (fvm/timestepping.py:64-106): one accepted implicit-Euler step with
  * retry-on-failure, explicit plated-inventory update.  x and n_pl are updated
  * in place (device); stats carries dt_used / dt_next / retries / clamped loss. */
 int hc_step(hc_operator* op, double* x, double* n_pl, double t, double dt_suggest, double mu,
             const hc_solver_config* cfg, hc_newton_stats* stats, void* stream);
+
+/* hc_step that also returns the Newton iterates of the accepted solve (what step()
+ * hands to observers' on_iterates, timestepping.py:98-101): iterates[max_iterates][n_total]
+ * (device); stats->n_iter of them are written. */
+int hc_step_ex(hc_operator* op, double* x, double* n_pl, double t, double dt_suggest, double mu,
+               const hc_solver_config* cfg, double* iterates, int32_t max_iterates,
+               hc_newton_stats* stats, void* stream);
+
+/* Rebuild the multigrid preconditioner's Galerkin values at the next Newton iteration
+ * (they are otherwise refreshed once every 32 Newton solves and on every dt change; the
+ * Krylov method always applies the exact current Jacobian). */
+int hc_precond_refresh(hc_operator* op);
 
 /* Same step with HOST state buffers: copies in, steps on the device, copies out
  * (the reference-facing end-to-end call used by bench.py's e2e leg). */

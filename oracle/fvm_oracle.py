@@ -18,7 +18,7 @@ Reference citations (file:line under pkg/src/halfcell/):
   fvm/operator.py:331-389    apply and its parts             -> OracleOperator.apply*
   fvm/operator.py:402-471    analytic Jacobian               -> OracleOperator.jacobian
   fvm/newton.py:62-206       Newton, floor, initial potential-> newton_solve / solve_initial_potential
-  fvm/timestepping.py:260-312 step + plated update            -> step
+  fvm/timestepping.py:50-106  step + plated update             -> step
   fvm/state.py:44-69, qoi.py  initial fields, QoIs             -> initial_fields / qoi_vectors
 """
 
@@ -376,7 +376,7 @@ class OracleOperator:
                           shape=(self.n, self.n))
         return (self.A_lin + J).tocsr()
 
-    # -- plated fluxes (timestepping.py:260-267) -------------------------------------------
+    # -- plated fluxes (timestepping.py:50-57) -------------------------------------------
     def plated_flux(self, x, n_pl, beta):
         flux = np.zeros(n_pl.size)
         pp, ce, pe, slot = self.strip
@@ -504,7 +504,7 @@ def solve_initial_potential(op, x0, n_pl, mu, rtol=1e-9, atol=1e-10, max_iter=20
 
 
 def step(op, x, n_pl, dt, mu, implicit_plated=True, **kw):
-    """One fixed-size implicit-Euler step + explicit plated update (timestepping.py:270-312)."""
+    """One fixed-size implicit-Euler step + explicit plated update (timestepping.py:64-106)."""
     xn, it, _ = newton_solve(op, x, dt, x, n_pl, mu, implicit_plated=implicit_plated, **kw)
     beta = dt * op.face_area / op.p.F if implicit_plated else 0.0
     if n_pl.size:

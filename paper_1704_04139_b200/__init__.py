@@ -22,6 +22,7 @@ _LAZY = {
     "qoi_vectors": "qoi", "qoi_cell_voltage": "qoi", "qoi_mean_solid_conc": "qoi",
     "pod_gram": "pod", "pod_basis": "pod",
     "make_batch": "batch", "step_batch": "batch", "BatchCell": "batch",
+    "SubOperatorView": "suboperator", "RestrictedSubOperator": "suboperator",
 }
 
 

@@ -31,6 +31,11 @@ def to_dev(a, dtype=None):
     return t.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
 
 
+def numel(a) -> int:
+    """Element count of a numpy array or tensor."""
+    return int(a.numel()) if is_tensor(a) else int(np.size(a))
+
+
 def empty(n: int, dtype=None):
     t = torch()
     return t.empty(max(int(n), 0), dtype=dtype or t.float64, device="cuda")

@@ -38,7 +38,7 @@ class HcSolverConfig(ctypes.Structure):
 
 class HcNewtonStats(ctypes.Structure):
     _fields_ = [("n_iter", ctypes.c_int32), ("krylov_iters", ctypes.c_int32),
-                ("retries", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("retries", ctypes.c_int32), ("status", ctypes.c_int32),
                 ("norm0", ctypes.c_double), ("norm_final", ctypes.c_double),
                 ("tol", ctypes.c_double), ("dt_used", ctypes.c_double),
                 ("dt_next", ctypes.c_double), ("clamped_loss", ctypes.c_double)]
@@ -90,6 +90,24 @@ _SIGS = {
                                     ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                     ctypes.POINTER(HcSolverConfig),
                                     ctypes.POINTER(HcNewtonStats)]),
+    "hc_lin_csr": (ctypes.c_int, [ctypes.c_void_p, c_int64_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p]),
+    "hc_strip_face_currents": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
+    "hc_restricted_eval": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int32] + [ctypes.c_void_p] * 8
+                           + [ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "hc_newton_solve_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                          ctypes.POINTER(HcSolverConfig), ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                          ctypes.c_int32, ctypes.c_void_p,
+                                          ctypes.POINTER(HcNewtonStats), ctypes.c_void_p]),
+    "hc_step_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                  ctypes.c_double, ctypes.c_double, ctypes.POINTER(HcSolverConfig),
+                                  ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(HcNewtonStats),
+                                  ctypes.c_void_p]),
+    "hc_precond_refresh": (ctypes.c_int, [ctypes.c_void_p]),
     "hc_launch_count": (ctypes.c_int, [c_int64_p]),
     "hc_flush_l2": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p]),
     "hc_time_kernels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,

@@ -5,7 +5,7 @@ per cell, host threads drive the per-cell Newton control).
 This is the model-order-reduction use case of arXiv 1704.04139 (repeated
 full-order solves over a parameter domain); the per-cell physics and step
 semantics are exactly those of ``timestepping.step`` (reference
-``fvm/timestepping.py:270-312``).
+``fvm/timestepping.py:64-106``).
 """
 
 from __future__ import annotations
@@ -86,8 +86,11 @@ def step_batch(cells: list[BatchCell], dt: float, cfg: SolverConfig, n_threads: 
     stats = (_native.HcNewtonStats * n)()
     cc = cfg.to_c()
     _dev.torch().cuda.synchronize()
-    _native.check(_native.lib().hc_step_batch(ops, n, xs, ns, dts, mus, ctypes.byref(cc), stats,
-                                              int(n_threads)))
+    code = _native.lib().hc_step_batch(ops, n, xs, ns, dts, mus, ctypes.byref(cc), stats, int(n_threads))
+    # cells that stepped advance their clock even when another cell failed (a failed cell
+    # keeps its input state; stats[i].status carries its error code)
     for c, s in zip(cells, stats):
-        c.t += s.dt_used
+        if s.status == 0:
+            c.t += s.dt_used
+    _native.check(code)
     return list(stats)

@@ -101,6 +101,7 @@ struct Amg {
                             // 400-step medium / 200-step large runs: same Krylov totals as 8, 2-3 % faster
   long long solves = 0;
   double last_inv_dt = -1.0;
+  bool force = false;        // rebuild at the next Newton iteration (after a stale-hierarchy Krylov failure)
   DBuf<double> rs[2], ea[2], eb[2], res, rc2;   // fine-level scalar vectors per block
   DBuf<double> res_c;                           // the c block's fine residual (block Jacobi)
   // block-Jacobi preconditioner (default): the two blocks' V-cycles are independent, so

@@ -26,6 +26,10 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
                           const hc_params& hp);
 void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
               cudaStream_t s, bool rows);
+void restricted_eval(const Operator& op, int n_rows, int n_s, const int32_t* f_kind, const int32_t* f_dof,
+                     const int32_t* f_slot, const int32_t* row_ptr, const int32_t* row_face,
+                     const double* row_coef, const double* xs, const double* npl, double beta, double* out,
+                     double* jac, cudaStream_t s);
 void rom_run(const Operator& op, const hc_rom* rom, int n_par, double* xt, double* npl, const double* mus_dev,
              double dt, int32_t n_steps, double rtol, int32_t max_iter, int32_t refresh, int32_t jac_steps,
              double* qoi, int32_t* iters, double* xt_steps, int32_t* status_host, cudaStream_t s);
@@ -258,16 +262,20 @@ int hc_jvp(hc_operator* opq, const double* x, const double* n_pl, double beta, d
   });
 }
 
-// Host assembly of the analytic Jacobian in the reference's CSR convention:
-// duplicates summed, exact zeros of the sum dropped (scipy csr + csr).
-int hc_jacobian_csr(hc_operator* opq, const double* x, const double* n_pl, double beta,
-                    int64_t* nnz_out, int64_t* row_ptr, int64_t* col_idx, double* values) {
-  return guarded([&] {
-    Operator& op = *(Operator*)opq;
+}  // extern "C"
+
+// Host assembly of A_lin (operator.py:121-221, coo -> csr: duplicates summed) or of the
+// analytic Jacobian A_lin + J_nl (operator.py:458-471: scipy csr + csr, exact zeros of the
+// sum dropped).
+static void assemble_csr(Operator& op, const double* x, const double* n_pl, double beta, bool with_nl,
+                         int64_t* nnz_out, int64_t* row_ptr, int64_t* col_idx, double* values) {
+  {
     const DevParams& P = op.P;
     const long long nvox = P.nvox, nc = op.info.n_c, n = op.info.n_c + op.info.n_p;
-    scatter_packed(op, x, op.xg.p, true, 0);
-    linearize(op, op.xg.p, n_pl, beta, 0);
+    if (with_nl) {
+      scatter_packed(op, x, op.xg.p, true, 0);
+      linearize(op, op.xg.p, n_pl, beta, 0);
+    }
     HC_CUDA(cudaDeviceSynchronize());
     std::vector<uint8_t> lab(nvox);
     std::vector<int32_t> cd(nvox), pd(nvox), so(op.n_if), el(op.n_if);
@@ -276,8 +284,8 @@ int hc_jacobian_csr(hc_operator* opq, const double* x, const double* n_pl, doubl
     HC_CUDA(cudaMemcpy(lab.data(), op.labels.p, nvox, cudaMemcpyDeviceToHost));
     HC_CUDA(cudaMemcpy(cd.data(), op.cdof.p, nvox * 4, cudaMemcpyDeviceToHost));
     HC_CUDA(cudaMemcpy(pd.data(), op.pdof.p, nvox * 4, cudaMemcpyDeviceToHost));
-    HC_CUDA(cudaMemcpy(w.data(), op.inv_c.p, nvox * 8, cudaMemcpyDeviceToHost));
-    if (op.n_if) {
+    if (with_nl) HC_CUDA(cudaMemcpy(w.data(), op.inv_c.p, nvox * 8, cudaMemcpyDeviceToHost));
+    if (op.n_if && with_nl) {
       HC_CUDA(cudaMemcpy(so.data(), op.if_solid.p, op.n_if * 4, cudaMemcpyDeviceToHost));
       HC_CUDA(cudaMemcpy(el.data(), op.if_el.p, op.n_if * 4, cudaMemcpyDeviceToHost));
       HC_CUDA(cudaMemcpy(kd.data(), op.if_kind.p, op.n_if, cudaMemcpyDeviceToHost));
@@ -330,9 +338,9 @@ int hc_jacobian_csr(hc_operator* opq, const double* x, const double* n_pl, doubl
           }
     }
     // A_lin done: snapshot as its own summed matrix, then add the nonlinear part
-    std::vector<std::map<int64_t, double>> nl(n);
+    std::vector<std::map<int64_t, double>> nl(with_nl ? n : 0);
     auto addn = [&](long long r, long long c, double v) { nl[r][c] += v; };
-    for (long long f = 0; f < op.n_if; ++f) {
+    for (long long f = 0; with_nl && f < op.n_if; ++f) {
       long long s_ = so[f], e = el[f];
       double ca = coef[f], cb = coef[op.n_if + f], cg = coef[2 * op.n_if + f];
       if (kd[f] == IF_BV) {
@@ -361,7 +369,7 @@ int hc_jacobian_csr(hc_operator* opq, const double* x, const double* n_pl, doubl
         }
       }
     }
-    {
+    if (with_nl) {
       std::vector<int32_t> lo(op.info.n_elel), hi(op.info.n_elel);
       if (op.info.n_elel) {
         HC_CUDA(cudaMemcpy(lo.data(), op.elel_lo.p, lo.size() * 4, cudaMemcpyDeviceToHost));
@@ -380,9 +388,11 @@ int hc_jacobian_csr(hc_operator* opq, const double* x, const double* n_pl, doubl
     }
     long long nnz = 0;
     for (long long r = 0; r < n; ++r) {
-      for (auto& kv : nl[r]) rows[r][kv.first] += kv.second;
-      for (auto it = rows[r].begin(); it != rows[r].end();) {
-        if (it->second == 0.0) it = rows[r].erase(it); else ++it;
+      if (with_nl) {
+        for (auto& kv : nl[r]) rows[r][kv.first] += kv.second;
+        for (auto it = rows[r].begin(); it != rows[r].end();) {
+          if (it->second == 0.0) it = rows[r].erase(it); else ++it;
+        }
       }
       nnz += (long long)rows[r].size();
     }
@@ -398,25 +408,98 @@ int hc_jacobian_csr(hc_operator* opq, const double* x, const double* n_pl, doubl
       }
       row_ptr[r + 1] = k;
     }
-  });
+  }
 }
 
 static void load_prev(Operator& op, const double* x_prev, cudaStream_t s);
+// Clears the Newton trace / source settings of an operator on scope exit.
+struct TraceScope {
+  Operator& op;
+  ~TraceScope() {
+    op.iter_out = nullptr;
+    op.iter_max = 0;
+    op.trace_norms = false;
+    op.src = nullptr;
+  }
+};
+
+extern "C" {
+
+int hc_jacobian_csr(hc_operator* opq, const double* x, const double* n_pl, double beta,
+                    int64_t* nnz_out, int64_t* row_ptr, int64_t* col_idx, double* values) {
+  return guarded([&] {
+    assemble_csr(*(Operator*)opq, x, n_pl, beta, true, nnz_out, row_ptr, col_idx, values);
+  });
+}
+
+int hc_lin_csr(hc_operator* opq, int64_t* nnz_out, int64_t* row_ptr, int64_t* col_idx, double* values) {
+  return guarded([&] {
+    assemble_csr(*(Operator*)opq, nullptr, nullptr, 0.0, false, nnz_out, row_ptr, col_idx, values);
+  });
+}
+
+int hc_precond_refresh(hc_operator* opq) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    if (op.amg) op.amg->force = true;
+  });
+}
+
+int hc_strip_face_currents(hc_operator* opq, const double* x, const double* n_pl, double beta,
+                           double* out, void* stream) {
+  return guarded([&] {
+    Operator& op = *(Operator*)opq;
+    cudaStream_t s = S(stream);
+    if (!op.info.n_strip) return;
+    scatter_packed(op, x, op.xg.p, true, s);
+    strip_currents(op, op.xg.p, n_pl, beta, out, s);
+  });
+}
 
 int hc_newton_solve(hc_operator* opq, const double* x_guess, double dt, const double* x_prev,
                     const double* n_pl, double mu, const hc_solver_config* cfg, double* x_out,
                     hc_newton_stats* stats, void* stream) {
+  return hc_newton_solve_ex(opq, x_guess, dt, x_prev, n_pl, mu, cfg, nullptr, nullptr, 0, nullptr, 0,
+                            x_out, stats, stream);
+}
+
+int hc_newton_solve_ex(hc_operator* opq, const double* x_guess, double dt, const double* x_prev,
+                       const double* n_pl, double mu, const hc_solver_config* cfg, const double* source,
+                       double* iterates, int32_t max_iterates, double* norms, int32_t max_norms,
+                       double* x_out, hc_newton_stats* stats, void* stream) {
   return guarded([&] {
     Operator& op = *(Operator*)opq;
     StreamJoin join(op, S(stream));
     cudaStream_t s = op.stream;
     Work& W = work(op);
+    TraceScope trace{op};
     hc_newton_stats st{};
     load_prev(op, x_prev, s);
-    scatter_packed(op, x_guess, W.x.p, true, s);
-    newton_grid(op, n_pl, dt, mu, *cfg, st, s);
+    if (source) {
+      scatter_packed(op, source, op.vg.p, false, s);
+      op.src = op.vg.p;
+    }
+    op.iter_out = iterates;
+    op.iter_max = iterates ? std::max(0, max_iterates) : 0;
+    op.trace_norms = norms != nullptr;
+    for (int attempt = 0;; ++attempt) {
+      scatter_packed(op, x_guess, W.x.p, true, s);
+      op.krylov_fail_stale = false;
+      try {
+        newton_grid(op, n_pl, dt, mu, *cfg, st, s);
+      } catch (const Error& e) {
+        // a Krylov failure on a lagged multigrid hierarchy is the solver's, not the
+        // problem's: rebuild the hierarchy and solve again once
+        if (e.code != HC_ERR_NONCONVERGENCE || !op.krylov_fail_stale || attempt) throw;
+        op.amg->force = true;
+        continue;
+      }
+      break;
+    }
     gather_packed(op, W.x.p, x_out, s);
     HC_CUDA(cudaStreamSynchronize(s));
+    if (norms)
+      for (int i = 0; i < max_norms && i < (int)op.norm_log.size(); ++i) norms[i] = op.norm_log[i];
     if (stats) *stats = st;
   });
 }
@@ -440,12 +523,21 @@ int hc_solve_initial_potential(hc_operator* opq, const double* x0, const double*
 
 int hc_step(hc_operator* opq, double* x, double* n_pl, double t, double dt_suggest, double mu,
             const hc_solver_config* cfg, hc_newton_stats* stats, void* stream) {
+  return hc_step_ex(opq, x, n_pl, t, dt_suggest, mu, cfg, nullptr, 0, stats, stream);
+}
+
+int hc_step_ex(hc_operator* opq, double* x, double* n_pl, double t, double dt_suggest, double mu,
+               const hc_solver_config* cfg, double* iterates, int32_t max_iterates, hc_newton_stats* stats,
+               void* stream) {
   (void)t;
   return guarded([&] {
     Operator& op = *(Operator*)opq;
     StreamJoin join(op, S(stream));
     cudaStream_t s = op.stream;
     Work& W = work(op);
+    TraceScope trace{op};
+    op.iter_out = iterates;
+    op.iter_max = iterates ? std::max(0, max_iterates) : 0;
     hc_newton_stats st{};
     scatter_packed(op, x, W.x.p, true, s);
     step_grid(op, n_pl, dt_suggest, mu, *cfg, st, s);
@@ -541,7 +633,13 @@ int hc_step_batch(hc_operator* const* ops, int32_t n, double* const* x, double* 
     // here (253 -> 317 cell-steps/s), so it is the default for batches (HC_NEWTON_DEV=0 off)
     const char* nd = getenv("HC_NEWTON_DEV");
     const bool dev_newton = !nd || atoi(nd) != 0;
-    for (int i = 0; i < n; ++i) ((Operator*)ops[i])->newton_dev = dev_newton;
+    std::vector<char> saved(n);
+    for (int i = 0; i < n; ++i) {
+      saved[i] = ((Operator*)ops[i])->newton_dev;
+      ((Operator*)ops[i])->newton_dev = dev_newton;
+    }
+    if (stats)
+      for (int i = 0; i < n; ++i) stats[i] = hc_newton_stats{};
     std::atomic<int> next{0};
     std::mutex m;
     int first_code = HC_OK;
@@ -560,9 +658,13 @@ int hc_step_batch(hc_operator* const* ops, int32_t n, double* const* x, double* 
           HC_CUDA(cudaStreamSynchronize(s));
           if (stats) stats[i] = st;
         } catch (const Error& e) {
+          // the failed cell keeps its input state (x[i] is only written on success; n_pl is
+          // updated after the Newton solve only) and reports its code in status
+          if (stats) stats[i].status = e.code;
           std::lock_guard<std::mutex> g(m);
           if (first_code == HC_OK) { first_code = e.code; first_msg = "cell " + std::to_string(i) + ": " + e.what(); }
         } catch (const std::exception& e) {
+          if (stats) stats[i].status = HC_ERR_CUDA;
           std::lock_guard<std::mutex> g(m);
           if (first_code == HC_OK) { first_code = HC_ERR_CUDA; first_msg = e.what(); }
         }
@@ -571,6 +673,7 @@ int hc_step_batch(hc_operator* const* ops, int32_t n, double* const* x, double* 
     std::vector<std::thread> th;
     for (int t = 0; t < nt; ++t) th.emplace_back(worker);
     for (auto& t : th) t.join();
+    for (int i = 0; i < n; ++i) ((Operator*)ops[i])->newton_dev = saved[i];
     if (first_code != HC_OK) throw Error(first_code, first_msg);
   });
 }
@@ -605,6 +708,18 @@ int hc_pod_gram_rows(const double* Sm, const double* w, int64_t n_dof, int64_t n
   return guarded([&] {
     if (n_dof < 0 || n_snap < 0) throw Error(HC_ERR_ARGUMENT, "negative size");
     pod_gram(Sm, w, n_dof, n_snap, G, S(stream), true);
+  });
+}
+
+int hc_restricted_eval(hc_operator* opq, int32_t n_rows, int32_t n_f, int32_t n_s, const int32_t* f_kind,
+                       const int32_t* f_dof, const int32_t* f_slot, const int32_t* row_ptr,
+                       const int32_t* row_face, const double* row_coef, const double* x_st,
+                       const double* n_pl, double beta, double* out, double* jac, void* stream) {
+  return guarded([&] {
+    if (!opq || n_rows < 0 || n_f < 0 || n_s < 0) throw Error(HC_ERR_ARGUMENT, "bad restricted operator");
+    (void)n_f;
+    restricted_eval(*(Operator*)opq, n_rows, n_s, f_kind, f_dof, f_slot, row_ptr, row_face, row_coef, x_st,
+                    n_pl, beta, out, jac, S(stream));
   });
 }
 

@@ -283,9 +283,17 @@ struct Operator {
   KrylovGraphs* kg = nullptr;
   cudaStream_t stream = nullptr;   // private non-blocking stream (graph capture needs one)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  // optional callback after every accepted Newton iterate (grid layout)
-  void (*iterate_hook)(Operator&, const double2*) = nullptr;
-  void* hook_ctx = nullptr;
+  // Newton trace of newton_solve (its iterates and residual norms, newton.py:153-161)
+  // and its optional source term (newton.py:107-108).  While any of these is set the
+  // host-controlled Newton loop runs (the device graph records neither).
+  double* iter_out = nullptr;      // packed iterates [iter_max][n_total] (device) or null
+  int iter_max = 0, iter_count = 0;
+  bool trace_norms = false;
+  std::vector<double> norm_log;    // |F| of the guess and of every accepted iterate
+  const double2* src = nullptr;    // grid-layout source added to every residual, or null
+  // set when the last Newton failure was a Krylov failure on a preconditioner that was
+  // not rebuilt in that solve: the caller rebuilds it and retries at the same dt
+  bool krylov_fail_stale = false;
 
   ~Operator();
 };
@@ -303,6 +311,9 @@ void residual_grid(Operator& op, const double2* xg, const double* npl, double mu
                    int parts, const double* cprev_scaled, double inv_dt, double2* out,
                    cudaStream_t s, int which = 3);  // which: 1 stencil kernel, 2 interface kernel
 void linearize(Operator& op, const double2* xg, const double* npl, double beta, cudaStream_t s);
+// stripping current per stripping face (operator.py:391-399) into out[n_strip]
+void strip_currents(Operator& op, const double2* xg, const double* npl, double beta, double* out,
+                    cudaStream_t s);
 // J v with the linearization stored in op.  flags: 1 add mass (inv_dt on c rows),
 // 2 row transform T (electrolyte c row -= t+ phi row), 4 include 1/c terms,
 // 8 phi rows only (c rows written as 0)

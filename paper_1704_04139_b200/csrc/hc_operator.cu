@@ -323,6 +323,19 @@ __global__ void __launch_bounds__(TPB) k_residual_islot(
   islot[slot_of(e, dir_to(P, e, s))] = -q;
 }
 
+// Stripping current of every stripping face (operator.py:391-399), faces f0.. of the
+// unified list (bv | ce | strip), unscaled A/m^2.
+__global__ void k_strip_currents(DevParams P, long long f0, long long n, const int32_t* __restrict__ so,
+                                 const int32_t* __restrict__ el, const int32_t* __restrict__ slot,
+                                 const double2* __restrict__ X, const double* __restrict__ npl, double beta,
+                                 double* __restrict__ out) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const long long f = f0 + k;
+  const double2 xs = X[so[f]], xe = X[el[f]];
+  out[k] = strip_current_dev(xe.x, xs.y, xe.y, npl[slot[f]], beta, P, nullptr, nullptr);
+}
+
 // --------------------------------------------------------------- linearization
 __global__ void k_lin_iface(DevParams P, long long n_if, const int32_t* __restrict__ so,
                             const int32_t* __restrict__ el, const int32_t* __restrict__ slot,
@@ -464,6 +477,15 @@ void residual_grid(Operator& op, const double2* xg, const double* npl, double mu
     k_residual_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p,
                                                          op.if_el.p, op.if_slot.p, op.if_kind.p,
                                                          xg, npl, beta, out); HC_COUNT();
+  HC_CHECK_LAUNCH();
+}
+
+void strip_currents(Operator& op, const double2* xg, const double* npl, double beta, double* out,
+                    cudaStream_t s) {
+  const long long n = op.info.n_strip;
+  if (!n) return;
+  k_strip_currents<<<blocks_for(n), TPB, 0, s>>>(op.P, op.info.n_bv + op.info.n_ce, n, op.if_solid.p,
+                                                 op.if_el.p, op.if_slot.p, xg, npl, beta, out); HC_COUNT();
   HC_CHECK_LAUNCH();
 }
 

@@ -11,7 +11,7 @@
 //   J~   = M~/dt + A~ + E (dN_pi/dx_S) B_S                      (chord: refreshed per step)
 // then the dense k x k solve in shared memory (LU with partial pivoting).  After
 // convergence the plated inventory is advanced exactly (all stripping faces are in
-// the stencil, timestepping.py:260-267) and the two QoIs are recorded.  Nothing of
+// the stencil, timestepping.py:50-57, 89-96) and the two QoIs are recorded.  Nothing of
 // full-order length is touched online; per-step cost depends on (k, M, |S|) only.
 //
 // One thread-block cluster (16 CTAs of 1024 threads where the device schedules it,
@@ -455,6 +455,45 @@ void rom_run(const Operator& op, const hc_rom* rom, int n_par, double* xt, doubl
   HC_COUNT();
   HC_CUDA(cudaMemcpyAsync(status_host, st.p, np * 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   HC_CUDA(cudaStreamSynchronize(s));
+}
+
+// RestrictedSubOperator.apply / .jacobian (operator.py:598-646) from the same face
+// table and face kinetics (rom_face) the online kernel evaluates its EI rows with:
+// one thread per selected row, its faces in table order.
+__global__ void k_restricted_eval(DevParams P, int n_rows, int n_s, const int32_t* __restrict__ f_kind,
+                                  const int32_t* __restrict__ f_dof, const int32_t* __restrict__ f_slot,
+                                  const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ row_face,
+                                  const double* __restrict__ row_coef, const double* __restrict__ xs,
+                                  const double* __restrict__ npl, double beta, double* __restrict__ out,
+                                  double* __restrict__ jac) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  double acc = 0.0;
+  for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+    const int f = row_face[e];
+    const int32_t* dof = f_dof + 4 * f;
+    const int sl = f_slot[f];
+    double q, dq[4];
+    rom_face(P, f_kind[f], xs, dof, sl >= 0 ? npl[sl] : 0.0, beta, &q, dq);
+    const double c = row_coef[e];
+    acc += c * q;
+    if (jac)
+      for (int j = 0; j < 4; ++j)
+        if (dof[j] >= 0 && dq[j] != 0.0) jac[(long long)r * n_s + dof[j]] += c * dq[j];
+  }
+  out[r] = acc;
+}
+
+void restricted_eval(const Operator& op, int n_rows, int n_s, const int32_t* f_kind, const int32_t* f_dof,
+                     const int32_t* f_slot, const int32_t* row_ptr, const int32_t* row_face,
+                     const double* row_coef, const double* xs, const double* npl, double beta, double* out,
+                     double* jac, cudaStream_t s) {
+  if (n_rows <= 0) return;
+  if (jac) HC_CUDA(cudaMemsetAsync(jac, 0, (size_t)n_rows * n_s * sizeof(double), s));
+  k_restricted_eval<<<(n_rows + 127) / 128, 128, 0, s>>>(op.P, n_rows, n_s, f_kind, f_dof, f_slot, row_ptr,
+                                                        row_face, row_coef, xs, npl, beta, out, jac);
+  HC_COUNT();
+  HC_CHECK_LAUNCH();
 }
 
 }  // namespace hc

@@ -2,7 +2,7 @@
 // positivity guard and line search, stationary potential solve, and the
 // adaptive implicit-Euler step with the explicit plated-inventory update.
 //
-// Reference: fvm/newton.py:62-206, fvm/timestepping.py:260-312.
+// Reference: fvm/newton.py:62-206, fvm/timestepping.py:50-106.
 #include <chrono>
 #include <cmath>
 #include <algorithm>
@@ -186,7 +186,7 @@ __global__ void k_pos_min(DevParams P, const uint8_t* __restrict__ lab, const do
   }
 }
 
-// per plated slot: outflow (mol/s) through its stripping faces (timestepping.py:260-267),
+// per plated slot: outflow (mol/s) through its stripping faces (timestepping.py:50-57),
 // then n_new = max(0, n - dt*flux); part[] collects the clamped (negative) mass
 __global__ void k_plated_update(DevParams P, long long n_pl, const int32_t* __restrict__ pl_vox,
                                 const int32_t* __restrict__ if_rank, const int32_t* __restrict__ if_dir,
@@ -470,6 +470,9 @@ struct NewtonGraph {
   cudaGraphExec_t exec = nullptr;
   double dt = -1.0, mu = 0.0;
   const double* npl = nullptr;
+  // work-buffer addresses captured into the graph (the host loops swap W.x/W.xt and
+  // W.r/W.rt, so they are part of the key)
+  const double2 *px = nullptr, *pxt = nullptr, *pr = nullptr, *prt = nullptr;
   hc_solver_config cfg{};
   DBuf<double> ns;
   double* ns_host = nullptr;
@@ -581,13 +584,20 @@ static void build_newton_graph(Operator& op, NewtonGraph& NG, const double* npl,
   NG.mu = mu;
   NG.npl = npl;
   NG.cfg = cfg;
+  NG.px = W.x.p;
+  NG.pxt = W.xt.p;
+  NG.pr = W.r.p;
+  NG.prt = W.rt.p;
 }
 
 // returns false if the device path is unavailable (the caller runs the host loop)
 static bool newton_grid_dev(Operator& op, const double* npl, double dt, double mu,
                             const hc_solver_config& cfg, hc_newton_stats& st, cudaStream_t s) {
   Amg& A = *op.amg;
-  if (!op.newton_dev || A.refresh || op.iterate_hook || !op.dev_krylov || !op.krylov_while) return false;
+  if (!op.newton_dev || A.refresh || op.iter_out || op.trace_norms || op.src || !op.dev_krylov ||
+      !op.krylov_while)
+    return false;
+  Work& W = work(op);
   if (!op.ng) {
     op.ng = new NewtonGraph();
     op.ng->ns.alloc(NS_N);
@@ -595,7 +605,8 @@ static bool newton_grid_dev(Operator& op, const double* npl, double dt, double m
   }
   NewtonGraph& NG = *op.ng;
   const double inv_dt = 1.0 / dt;
-  if (!NG.exec || NG.dt != dt || NG.mu != mu || NG.npl != npl || !same_cfg(NG.cfg, cfg)) {
+  if (!NG.exec || NG.dt != dt || NG.mu != mu || NG.npl != npl || !same_cfg(NG.cfg, cfg) ||
+      NG.px != W.x.p || NG.pxt != W.xt.p || NG.pr != W.r.p || NG.prt != W.rt.p) {
     try {
       auto t0 = std::chrono::steady_clock::now();
       build_newton_graph(op, NG, npl, dt, mu, cfg, s);
@@ -609,7 +620,8 @@ static bool newton_grid_dev(Operator& op, const double* npl, double dt, double m
     }
   }
   ++A.solves;
-  const bool rebuild = A.solves % A.refresh_solves == 1 || A.refresh_solves == 1 || A.last_inv_dt != inv_dt;
+  const bool rebuild = A.force || A.solves % A.refresh_solves == 1 || A.refresh_solves == 1 ||
+                       A.last_inv_dt != inv_dt;
   NG.ns_host[NS_REBUILD] = rebuild ? 1.0 : 0.0;
   HC_CUDA(cudaMemcpyAsync(NG.ns.p + NS_REBUILD, NG.ns_host + NS_REBUILD, sizeof(double),
                           cudaMemcpyHostToDevice, s));
@@ -626,7 +638,14 @@ static bool newton_grid_dev(Operator& op, const double* npl, double dt, double m
     fprintf(stderr, "newton(dev): dt=%g status=%g it=%g kiters=%g norm0=%.3e tol=%.3e norm=%.3e lintol=%.3e rebuild=%d why=%g\n",
             dt, h[NS_STATUS], h[NS_IT], h[NS_KITERS], h[NS_NORM0], h[NS_TOL], h[NS_NORM], h[NS_LINTOL],
             (int)rebuild, h[NS_WHY]);
-  if (rebuild && h[NS_IT] + (h[NS_STATUS] == 1.0 ? 0.0 : 1.0) > 0.0) A.last_inv_dt = inv_dt;
+  // a solve that converged at its initial residual ran no Newton iteration: like the host
+  // loop it does not count towards the refresh period (and rebuilt nothing)
+  const bool iterated = h[NS_IT] + (h[NS_STATUS] == 1.0 ? 0.0 : 1.0) > 0.0;
+  if (!iterated) --A.solves;
+  if (rebuild && iterated) {
+    A.last_inv_dt = inv_dt;
+    A.force = false;
+  }
   count_graph_launch(NG.per_iter_kernels * (unsigned long long)std::max(1.0, h[NS_IT]));
   st.norm0 = h[NS_NORM0];
   st.tol = h[NS_TOL];
@@ -635,6 +654,7 @@ static bool newton_grid_dev(Operator& op, const double* npl, double dt, double m
   st.krylov_iters += (int)h[NS_KITERS];
   if (h[NS_STATUS] == 1.0) return true;
   const int why = (int)h[NS_WHY];
+  op.krylov_fail_stale = why >= 9 && !rebuild;
   char msg[200];
   if (why == 1)
     snprintf(msg, sizeof msg, "initial residual not evaluable: operator produced a non-finite value");
@@ -663,7 +683,14 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
   const double inv_dt = 1.0 / dt;
   const double beta = cfg.implicit_plated ? dt * op.info.face_area / op.host_params.faraday : 0.0;
   const int parts = PART_LIN | PART_BV | PART_1C | PART_BND | PART_TIME;
-  residual_grid(op, W.x.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.r.p, s);
+  // residual of newton.py:101-106: m (x - x_prev)/dt + A(x; mu) (+ source)
+  auto residual = [&](const double2* xg, double2* out) {
+    residual_grid(op, xg, npl, mu, beta, parts, W.cprev.p, inv_dt, out, s);
+    if (op.src) { k_axpy<<<nb, TPB, 0, s>>>(n, out, 1.0, op.src, out); HC_COUNT(); }
+  };
+  op.iter_count = 0;
+  op.norm_log.clear();
+  residual(W.x.p, W.r.p);
   double norm0 = norm_checked(op, W.r.p, 3, s);
   if (!std::isfinite(norm0))
     throw Error(HC_ERR_NONCONVERGENCE, "initial residual not evaluable: operator produced a non-finite value");
@@ -672,8 +699,10 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
   st.tol = tol;
   st.n_iter = 0;
   st.norm_final = norm0;
+  if (op.trace_norms) op.norm_log.push_back(norm0);
   if (norm0 <= tol) return;
   double norm = norm0;
+  bool rebuilt = false;
   for (int it = 1; it <= cfg.newton_max_iter; ++it) {
     linearize(op, W.x.p, npl, beta, s);
     // the preconditioner is rebuilt at the first Newton iteration of every solve; later
@@ -685,18 +714,25 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
       // the Galerkin hierarchy is rebuilt for the first Newton iteration of every
       // refresh_solves-th solve (and always when dt changed); Krylov always sees the
       // exact current Jacobian, the preconditioner may lag
-      bool rebuild = A.refresh || (first && (A.solves % A.refresh_solves == 1 ||
+      bool rebuild = A.refresh || (first && (A.force || A.solves % A.refresh_solves == 1 ||
                                              A.refresh_solves == 1 || A.last_inv_dt != inv_dt));
       if (rebuild) {
         amg_update(op, inv_dt, 3, s);
         A.last_inv_dt = inv_dt;
+        A.force = false;
+        rebuilt = true;
       }
     }
     k_neg<<<nb, TPB, 0, s>>>(n, W.r.p, W.b.p); HC_COUNT();
     const double lin_tol = std::min(0.1, std::max(cfg.linear_rtol, cfg.linear_safety * tol / norm));
-    st.krylov_iters += op.dev_krylov
-        ? bicgstab_dev(op, W.b.p, W.d.p, inv_dt, 0, lin_tol, cfg.krylov_max_iter, s)
-        : bicgstab(op, W.b.p, W.d.p, inv_dt, 0, lin_tol, cfg.krylov_max_iter, s);
+    try {
+      st.krylov_iters += op.dev_krylov
+          ? bicgstab_dev(op, W.b.p, W.d.p, inv_dt, 0, lin_tol, cfg.krylov_max_iter, s)
+          : bicgstab(op, W.b.p, W.d.p, inv_dt, 0, lin_tol, cfg.krylov_max_iter, s);
+    } catch (const Error& e) {
+      op.krylov_fail_stale = e.code == HC_ERR_NONCONVERGENCE && !rebuilt;
+      throw;
+    }
     // positivity guard on the concentration block
     double alpha = 1.0;
     {
@@ -714,14 +750,14 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
     double norm_try = INFINITY;
     for (int h = 0; h <= 8; ++h) {
       k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p); HC_COUNT();
-      residual_grid(op, W.xt.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.rt.p, s);
+      residual(W.xt.p, W.rt.p);
       norm_try = norm_checked(op, W.rt.p, 3, s);
       if (std::isfinite(norm_try) && (norm_try <= norm || norm_try <= tol)) { accepted = true; break; }
       alpha *= 0.5;
     }
     if (!accepted) {
       k_axpy<<<nb, TPB, 0, s>>>(n, W.x.p, alpha, W.d.p, W.xt.p); HC_COUNT();
-      residual_grid(op, W.xt.p, npl, mu, beta, parts, W.cprev.p, inv_dt, W.rt.p, s);
+      residual(W.xt.p, W.rt.p);
       norm_try = norm_checked(op, W.rt.p, 3, s);
       if (!std::isfinite(norm_try))
         throw Error(HC_ERR_NONCONVERGENCE, "residual not evaluable under damping");
@@ -731,7 +767,10 @@ void newton_grid(Operator& op, const double* npl, double dt, double mu, const hc
     norm = norm_try;
     st.n_iter = it;
     st.norm_final = norm;
-    if (op.iterate_hook) op.iterate_hook(op, W.x.p);
+    if (op.trace_norms) op.norm_log.push_back(norm);
+    if (op.iter_out && op.iter_count < op.iter_max)
+      gather_packed(op, W.x.p, op.iter_out + (long long)op.iter_count * (op.info.n_c + op.info.n_p), s);
+    ++op.iter_count;
     if (norm <= tol) return;
   }
   char msg[200];
@@ -786,7 +825,7 @@ void initial_potential_grid(Operator& op, const double* npl, double mu, const hc
   throw Error(HC_ERR_NONCONVERGENCE, msg);
 }
 
-// step (timestepping.py:270-312) on the grid layout: W.x holds the state on
+// step (timestepping.py:64-106) on the grid layout: W.x holds the state on
 // entry (also x_prev) and the accepted state on exit; npl updated in place.
 void step_grid(Operator& op, double* npl, double dt_suggest, double mu, const hc_solver_config& cfg,
                hc_newton_stats& st, cudaStream_t s) {
@@ -799,11 +838,23 @@ void step_grid(Operator& op, double* npl, double dt_suggest, double mu, const hc
   if (!xprev.p) xprev.alloc(n);
   HC_CUDA(cudaMemcpyAsync(xprev.p, W.x.p, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
   st.krylov_iters = 0;
+  bool stale_retry = false;
   while (true) {
     try {
+      op.krylov_fail_stale = false;
       newton_grid(op, npl, dt, mu, cfg, st, s);
     } catch (const Error& e) {
       if (e.code != HC_ERR_NONCONVERGENCE) throw;
+      if (op.krylov_fail_stale && !stale_retry) {
+        // the Krylov solve failed on a lagged multigrid hierarchy: rebuild it and retry the
+        // same dt (the reference's direct solve never fails here, so this is not a retry of
+        // the step-size control)
+        stale_retry = true;
+        op.amg->force = true;
+        HC_CUDA(cudaMemcpyAsync(W.x.p, xprev.p, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        continue;
+      }
+      stale_retry = true;   // a fresh hierarchy failed too: shrink dt as the reference does
       if (dt <= cfg.dt_min * (1.0 + 1e-12)) {
         char msg[256];
         snprintf(msg, sizeof msg, "time step underflow (dt=%.3e): %s", dt, e.what());

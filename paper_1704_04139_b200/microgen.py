@@ -1,13 +1,13 @@
 """Seeded microstructure setup for the BASELINE configurations.
 
 The reference generates half cells with a Laguerre / Gaussian-random-field
-pipeline (``src/halfcell/microgen/generate.py:244-305``).  BASELINE.json's
+pipeline (``src/halfcell/microgen/generate.py:87-153``).  BASELINE.json's
 configurations instead specify a union of balls with Poisson centres and
 Gamma-distributed radii thresholded to a target porosity; that is what
 :func:`generate_cell` builds.  The slab assembly (working collector at z = 0,
 a pore layer capping the electrode, pruning of graphite not connected to the
 collector) and the germ-grain plated-lithium layer follow the reference
-(``generate.py:223-236,291-305`` and ``plating.py:53-109``), so every grid is
+(``generate.py:71-84,131-135`` and ``plating.py:53-109``), so every grid is
 a valid reference ``PhaseGrid`` and can be fed to both the reference operator
 and this package.
 
@@ -125,7 +125,7 @@ def plate_germs(grid: PhaseGrid, intensity: float, grain_radius: float,
 
 def prune_disconnected_graphite(labels: np.ndarray, z_contact: int) -> np.ndarray:
     """Graphite not 6-connected to the collector contact layer becomes electrolyte
-    (reference ``generate.py:223-236``)."""
+    (reference ``generate.py:71-84``)."""
     gr = labels == Phase.GRAPHITE
     comp, n = ndimage.label(gr, structure=ndimage.generate_binary_structure(3, 1))
     if n == 0:

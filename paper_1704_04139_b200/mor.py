@@ -62,7 +62,7 @@ def collect_snapshots(op, x0, n_pl0, mu: float, dt: float, n_steps: int, cfg=Non
     c = cfg.to_c()
     st = _native.HcNewtonStats()
     x = _dev.to_dev(x0).clone()
-    npl = _dev.to_dev(n_pl0 if np.size(n_pl0) else np.zeros(1)).clone()
+    npl = _dev.to_dev(n_pl0 if _dev.numel(n_pl0) else np.zeros(1)).clone()
     beta = dt * op.face_area / op.p.constants.F
     n = op.dof.n_total
     X = t.empty((n, n_steps + 1), dtype=t.float64, device="cuda")
@@ -334,7 +334,7 @@ def solve_rom(op, rom: ReducedModel, xt0, n_pl0, mu: float, dt: float, n_steps: 
     Jacobian is refreshed every ``jac_steps`` steps (chord Newton in between)."""
     t = _dev.torch()
     xt = _dev.to_dev(xt0).clone()
-    npl = _dev.to_dev(n_pl0 if np.size(n_pl0) else np.zeros(1)).clone()
+    npl = _dev.to_dev(n_pl0 if _dev.numel(n_pl0) else np.zeros(1)).clone()
     qoi = t.empty(2 * max(n_steps, 1), dtype=t.float64, device="cuda")
     its = t.empty(max(n_steps, 1), dtype=t.int32, device="cuda")
     states = t.empty((max(n_steps, 1), rom.k), dtype=t.float64, device="cuda") if keep_states else None
@@ -363,7 +363,7 @@ def solve_rom_batch(op, rom: ReducedModel, xt0, n_pl0, mus, dt: float, n_steps: 
     mus = np.asarray(mus, dtype=float)
     n_par = int(mus.size)
     xt = _dev.to_dev(xt0).reshape(1, -1).repeat(n_par, 1).contiguous()
-    npl1 = np.asarray(n_pl0 if np.size(n_pl0) else np.zeros(1), dtype=float)
+    npl1 = np.asarray(n_pl0 if _dev.numel(n_pl0) else np.zeros(1), dtype=float)
     npl = _dev.to_dev(np.tile(npl1, (n_par, 1)))
     mu_d = _dev.to_dev(mus)
     qoi = t.empty((n_par, 2 * max(n_steps, 1)), dtype=t.float64, device="cuda")

@@ -79,28 +79,38 @@ class NewtonResult:
 
 def newton_solve(op, x_guess, dt: float, x_prev, n_pl, mu: float, cfg: SolverConfig,
                  source=None) -> NewtonResult:
-    """Solve ``m (x - x_prev)/dt + A(x; mu) = 0`` (reference ``newton.py:86-168``)."""
+    """Solve ``m (x - x_prev)/dt + A(x; mu) + source = 0`` (reference ``newton.py:86-168``).
+
+    Returns every accepted iterate (``NewtonResult.iterates``, the snapshot source of the
+    reduction stage) and every residual norm, like the reference.  Inputs may be numpy
+    arrays or CUDA tensors; outputs follow ``x_guess``.
+    """
     if dt <= 0:
         raise ValueError("dt must be positive")
-    if source is not None:
-        raise NotImplementedError("source terms are not supported by the device Newton solver")
+    n = op.dof.n_total
     xg, xp = _dev.to_dev(x_guess), _dev.to_dev(x_prev)
-    nd = _dev.to_dev(n_pl) if np.size(n_pl) else _dev.to_dev(np.zeros(1))
-    out = _dev.empty(op.dof.n_total)
+    nd = _dev.to_dev(n_pl) if _dev.numel(n_pl) else _dev.to_dev(np.zeros(1))
+    src = _dev.to_dev(source) if source is not None else None
+    out = _dev.empty(n)
+    m = int(cfg.newton_max_iter)
+    its = _dev.torch().empty((max(m, 1), n), dtype=_dev.torch().float64, device="cuda")
+    norms = (ctypes.c_double * (m + 1))()
     st = _native.HcNewtonStats()
     c = cfg.to_c()
-    _native.check(_native.lib().hc_newton_solve(op.native.handle, _dev.ptr(xg), float(dt),
-                                                _dev.ptr(xp), _dev.ptr(nd), float(mu),
-                                                ctypes.byref(c), _dev.ptr(out),
-                                                ctypes.byref(st), _dev.stream()))
+    _native.check(_native.lib().hc_newton_solve_ex(
+        op.native.handle, _dev.ptr(xg), float(dt), _dev.ptr(xp), _dev.ptr(nd), float(mu), ctypes.byref(c),
+        _dev.ptr(src) if src is not None else None, _dev.ptr(its), m, norms, m + 1, _dev.ptr(out),
+        ctypes.byref(st), _dev.stream()))
+    k = int(st.n_iter)
     x = _dev.like_input(out, x_guess)
-    return NewtonResult(x, [], int(st.n_iter), [st.norm0, st.norm_final], int(st.krylov_iters))
+    iterates = [_dev.like_input(its[i], x_guess) for i in range(k)]
+    return NewtonResult(x, iterates, k, [float(norms[i]) for i in range(k + 1)], int(st.krylov_iters))
 
 
 def solve_initial_potential(op, x0, n_pl, mu: float, cfg: SolverConfig):
     """Stationary potential solve at frozen c (reference ``newton.py:171-206``)."""
     xd = _dev.to_dev(x0)
-    nd = _dev.to_dev(n_pl) if np.size(n_pl) else _dev.to_dev(np.zeros(1))
+    nd = _dev.to_dev(n_pl) if _dev.numel(n_pl) else _dev.to_dev(np.zeros(1))
     out = _dev.empty(op.dof.n_total)
     st = _native.HcNewtonStats()
     c = cfg.to_c()

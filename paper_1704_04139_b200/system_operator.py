@@ -8,9 +8,10 @@ the face lists and coefficients, same ``apply*`` decomposition
 
 (``operator.py:9-18``) and the same sign conventions.  Inputs may be numpy
 arrays (copied to the device, result returned as numpy) or CUDA fp64 tensors
-(result stays on the device).  The Jacobian is matrix-free: :meth:`jvp`
-applies it, :meth:`jacobian` returns a linear-operator object whose
-``tocsr()`` assembles the reference's CSR (for sparsity parity).
+(result stays on the device).  :meth:`jacobian` returns the reference's
+``scipy.sparse.csr_matrix`` (assembled from the device linearization, for API and
+sparsity parity); the solver path never assembles it and applies the Jacobian
+matrix-free instead (:meth:`jvp`, :meth:`jacobian_operator`).
 """
 
 from __future__ import annotations
@@ -157,21 +158,62 @@ class SystemOperator:
     def jvp(self, x, n_pl, v, beta: float = 0.0, inv_dt: float = 0.0):
         """(jacobian(x) + diag(inv_dt on c rows)) @ v, matrix-free on the GPU."""
         xd, vd = _dev.to_dev(x), _dev.to_dev(v)
-        nd = _dev.to_dev(n_pl) if n_pl is not None and np.size(n_pl) else _dev.to_dev(np.zeros(1))
+        nd = _dev.to_dev(n_pl) if n_pl is not None and _dev.numel(n_pl) else _dev.to_dev(np.zeros(1))
         out = _dev.empty(self.dof.n_total)
         _native.check(_native.lib().hc_jvp(self.native.handle, _dev.ptr(xd), _dev.ptr(nd),
                                            float(beta), float(inv_dt), _dev.ptr(vd),
                                            _dev.ptr(out), _dev.stream()))
         return _dev.like_input(out, v)
 
-    def jacobian(self, x, n_pl, mu: float = 0.0, beta: float = 0.0) -> JacobianOperator:
-        """Analytic Jacobian of :meth:`apply` (operator.py:458-471) as a matrix-free operator."""
-        return JacobianOperator(self, x, n_pl, beta)
+    def jacobian(self, x, n_pl, mu: float = 0.0, beta: float = 0.0):
+        """Analytic Jacobian of :meth:`apply` as ``scipy.sparse.csr_matrix``
+        (operator.py:458-471: A_lin + J_nl, duplicates summed, exact zeros dropped)."""
+        return self.jacobian_csr(x, n_pl, beta=beta)
+
+    def jacobian_operator(self, x, n_pl, beta: float = 0.0, inv_dt: float = 0.0) -> JacobianOperator:
+        """``jacobian(x) + diag(inv_dt on c rows)`` as a matrix-free operator on the GPU."""
+        return JacobianOperator(self, x, n_pl, beta, inv_dt)
+
+    @property
+    def A_lin(self):
+        """The affine part's matrix (operator.py:221) as ``scipy.sparse.csr_matrix``."""
+        if "A_lin" not in self._lists:
+            import scipy.sparse as sp
+            L = _native.lib()
+            nnz = ctypes.c_int64(0)
+            _native.check(L.hc_lin_csr(self.native.handle, ctypes.byref(nnz), None, None, None))
+            n = self.dof.n_total
+            rp = np.empty(n + 1, dtype=np.int64)
+            ci = np.empty(nnz.value, dtype=np.int64)
+            va = np.empty(nnz.value, dtype=np.float64)
+            _native.check(L.hc_lin_csr(self.native.handle, ctypes.byref(nnz), rp.ctypes.data,
+                                       ci.ctypes.data, va.ctypes.data))
+            self._lists["A_lin"] = sp.csr_matrix((va, ci, rp), shape=(n, n))
+        return self._lists["A_lin"]
+
+    def strip_face_currents(self, x, n_pl, beta: float = 0.0):
+        """(stripping current A/m^2, plated slot) for every stripping face (operator.py:391-399)."""
+        slots = self.strip_slot
+        if slots.size == 0:
+            return (_dev.empty(0) if _dev.is_tensor(x) else np.empty(0)), slots
+        xd = _dev.to_dev(x)
+        nd = _dev.to_dev(n_pl)
+        out = _dev.empty(slots.size)
+        _native.check(_native.lib().hc_strip_face_currents(self.native.handle, _dev.ptr(xd), _dev.ptr(nd),
+                                                           float(beta), _dev.ptr(out), _dev.stream()))
+        return _dev.like_input(out, x), slots
+
+    def sub_operator(self, name: str):
+        """Uniform full / restricted access to one nonlinear sub-operator (operator.py:476-479)."""
+        from .suboperator import SubOperatorView
+        if name not in ("bv", "one_over_c"):
+            raise KeyError(name)
+        return SubOperatorView(self, name)
 
     def jacobian_csr(self, x, n_pl, beta: float = 0.0):
         import scipy.sparse as sp
         xd = _dev.to_dev(x)
-        nd = _dev.to_dev(n_pl) if n_pl is not None and np.size(n_pl) else _dev.to_dev(np.zeros(1))
+        nd = _dev.to_dev(n_pl) if n_pl is not None and _dev.numel(n_pl) else _dev.to_dev(np.zeros(1))
         L = _native.lib()
         nnz = ctypes.c_int64(0)
         _native.check(L.hc_jacobian_csr(self.native.handle, _dev.ptr(xd), _dev.ptr(nd),

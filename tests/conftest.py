@@ -17,8 +17,16 @@ def pytest_configure(config):
 
 
 def golden_cases():
+    """The operator fixtures of make_golden.py (refgen_*, balls_*)."""
     return sorted(os.path.splitext(os.path.basename(p))[0]
-                  for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+                  for pat in ("refgen_*.npz", "balls_*.npz")
+                  for p in glob.glob(os.path.join(GOLDEN, pat)))
+
+
+def config_cases():
+    """The whole-run fixtures of make_golden_configs.py (config_*)."""
+    return sorted(os.path.splitext(os.path.basename(p))[0][len("config_"):]
+                  for p in glob.glob(os.path.join(GOLDEN, "config_*.npz")))
 
 
 def load_golden(name):
@@ -36,3 +44,27 @@ def scaled_err(a, b, scale):
     """max_i |a_i - b_i| / max(scale_i, tiny): relative agreement per row."""
     scale = np.maximum(np.abs(scale), 1e-300)
     return float(np.max(np.abs(np.asarray(a) - np.asarray(b)) / scale)) if np.size(a) else 0.0
+
+
+def assert_newton_solution(x, ref, nc, orc=None, x_prev=None, n_pl=None, mu=None, dt=None,
+                           beta=None, source=None, rtol=1e-9, atol=1e-10):
+    """A Newton solution agrees with the reference's: (1) it meets the reference's own
+    convergence test |F(x)| <= max(atol, rtol |F(x0)|, floor) (newton.py:111-113) evaluated
+    by the CPU oracle, when given; (2) c within 1e-6 relative and phi within 1e-6 of the
+    phi scale of the reference solution.  A Krylov-solved Newton step leaves an error in the
+    weakly determined modes (the floating electrode potential) that the residual test does
+    not see; the reference's direct solve leaves a different one, so the converged states
+    agree to the curve bar, not to 1e-8."""
+    x, ref = np.asarray(x), np.asarray(ref)
+    assert np.max(np.abs(x[:nc] - ref[:nc]) / np.abs(ref[:nc])) < 1e-6
+    assert np.max(np.abs(x[nc:] - ref[nc:])) < 1e-6 * np.max(np.abs(ref[nc:]))
+    if orc is not None:
+        from oracle import fvm_oracle as O
+
+        def F(z):
+            r = orc.apply(z, n_pl, mu, beta)
+            r[:nc] += (z[:nc] - x_prev[:nc]) / dt
+            return r + (source if source is not None else 0.0)
+        norm0 = float(np.linalg.norm(F(x_prev)))
+        tol = max(atol, rtol * norm0, O._floor(orc, x_prev, 1.0 / dt))
+        assert float(np.linalg.norm(F(x))) <= tol * (1.0 + 1e-6)

@@ -4,9 +4,14 @@
 
 Each fixture ``<case>.npz`` holds the reference's own outputs on a small grid:
 labels, Dofmap arrays, face lists, operator parts at a perturbed state, a
-Jacobian-vector product, the Jacobian sparsity pattern and a short transient
-(cell voltage, mean solid concentration, plated inventory per step).  The
-files are committed; the GPU box never reads /root/reference.
+Jacobian-vector product, the Jacobian sparsity pattern, ``A_lin`` (operator.py:221),
+the stripping face currents (operator.py:391-399), restricted sub-operator rows and
+their local Jacobians (operator.py:476-646), one Newton solve with its iterates and
+residual norms and one with a source term (newton.py:86-168), and a short transient
+(cell voltage, mean solid concentration, plated inventory per step).  The files are
+committed; the GPU box never reads /root/reference.  ``balls_16x16x24`` is built by
+this package's ``generate_cell`` (the spec is stored; tests/test_microgen.py checks the
+generator still reproduces the labels bit for bit).
 """
 
 from __future__ import annotations
@@ -41,7 +46,27 @@ def cases():
     yield "balls_16x16x24", g2.labels, g2.voxel_size, p2, -8.0, 0.5
 
 
+def plating_cases():
+    """Reference germ-grain plating (microgen/plating.py:53-109) on ball-union anodes."""
+    import dataclasses
+    from halfcell.microgen.plating import plate_germs as ref_plate
+    out = {}
+    for k, (seed, intensity, radius, h) in enumerate([(5, 0.05, 2.2, 1.0), (6, 0.02, 3.0, 1.0),
+                                                       (7, 0.08, 1.5, 0.75)]):
+        spec = CellSpec(24, 20, 32, 16, 6, seed=seed, radius_mean=3.0, porosity=0.4,
+                        plating_intensity=0.0, voxel_size=h)
+        base = generate_cell(dataclasses.replace(spec))
+        plated = ref_plate(PhaseGrid(base.labels, h), intensity, radius, np.random.default_rng(100 + k))
+        out[f"in_{k}"] = base.labels
+        out[f"out_{k}"] = plated.labels
+        out[f"args_{k}"] = np.array([intensity, radius, h, 100 + k])
+    path = os.path.join(HERE, "plating_ref.npz")
+    np.savez_compressed(path, **out)
+    print("plating_ref ->", os.path.getsize(path), "bytes")
+
+
 def main():
+    plating_cases()
     for name, labels, h, params, mu, dt in cases():
         grid = PhaseGrid(labels, h)
         dof = build_dofmap(grid)
@@ -58,7 +83,11 @@ def main():
         v = rng.standard_normal(dof.n_total)
         J = op.jacobian(x, n_pl, mu, beta=beta).tocsr()
         J.sort_indices()
+        A = op.A_lin.tocsr()
+        A.sort_indices()
+        cur, slot = op.strip_face_currents(x, n_pl, beta=beta)
         out = dict(
+            a_indptr=A.indptr, a_indices=A.indices, a_data=A.data, strip_current=cur, strip_slot=slot,
             labels=labels, voxel_size=h, mu=mu, dt=dt, beta=beta,
             params=np.array([params.soc_init, params.i00_plel]),
             c_dof=dof.c_dof, p_dof=dof.p_dof, plated=dof.plated_voxels, dirichlet=dof.dirichlet,
@@ -76,6 +105,26 @@ def main():
         res = newton_solve(op, x, dt, x, n_pl, mu, cfg)
         out["newton_x"] = res.x
         out["newton_iters"] = res.n_iter
+        out["newton_iterates"] = np.stack(res.iterates)
+        out["newton_norms"] = np.array(res.residual_norms)
+        # a solve with a source term (newton.py:107-108)
+        # a gentle volumetric source on the concentration rows (1e-3 relative per step)
+        src = np.zeros(dof.n_total)
+        src[: dof.n_c] = 1e-3 * x[: dof.n_c] / dt * rng.standard_normal(dof.n_c)
+        res_s = newton_solve(op, x, dt, x, n_pl, mu, cfg, source=src)
+        out.update(source=src, source_x=res_s.x, source_iters=res_s.n_iter)
+        # restricted sub-operators (the empirical-interpolation access path)
+        for which in ("bv", "one_over_c"):
+            view = op.sub_operator(which)
+            cand = view.output_dofs()
+            rows = np.sort(rng.choice(cand, size=min(40, cand.size), replace=False))
+            rs = view.restricted(rows)
+            xs = x[rs.stencil]
+            out[f"sub_{which}_rows"] = rs.rows
+            out[f"sub_{which}_stencil"] = rs.stencil
+            out[f"sub_{which}_apply"] = rs.apply(xs, n_pl, beta=beta)
+            out[f"sub_{which}_jac"] = rs.jacobian(xs, n_pl, beta=beta).toarray()
+            out[f"sub_{which}_output_dofs"] = cand
         # short transient with fixed steps from the stationary initial state
         state = prepare_initial_state(op, params, mu, cfg)
         traj_v, traj_c, traj_n, xs = [], [], [], [state.x]

@@ -1,4 +1,4 @@
-"""GPU: time-step control semantics of the reference (timestepping.py:270-382):
+"""GPU: time-step control semantics of the reference (timestepping.py:64-176):
 retry with a halved step on Newton failure, SimulationError at dt_min, schedule
 knots hit exactly, run_transient trajectory bookkeeping."""
 

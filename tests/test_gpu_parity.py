@@ -8,7 +8,7 @@ relative to the sum of |contributions|); voltage / plated-lithium curves within
 import numpy as np
 import pytest
 
-from conftest import golden_cases, load_golden, oracle_params, scaled_err
+from conftest import assert_newton_solution, golden_cases, load_golden, oracle_params, scaled_err
 from oracle import fvm_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -94,10 +94,9 @@ def test_newton_solve(case):
     P, _ = _pkg()
     x, n_pl = g["x"], g["n_pl"]
     res = P.newton_solve(op, x, float(g["dt"]), x, n_pl, float(g["mu"]), P.SolverConfig())
-    nc = dof.n_c
-    ref = g["newton_x"]
-    assert np.max(np.abs(res.x[:nc] - ref[:nc]) / np.abs(ref[:nc])) < 1e-8
-    assert np.max(np.abs(res.x[nc:] - ref[nc:])) < 1e-8
+    orc = case[4]
+    assert_newton_solution(res.x, g["newton_x"], dof.n_c, orc, x, n_pl, float(g["mu"]), float(g["dt"]),
+                           float(g["beta"]))
 
 
 @pytest.mark.parametrize("linear_safety", [0.0, 0.1, 0.3])

@@ -78,3 +78,35 @@ def test_generation_is_deterministic_and_seeded():
     assert np.array_equal(a.labels, b.labels)
     c = generate_cell(dataclasses.replace(spec, seed=spec.seed + 1))
     assert not np.array_equal(a.labels, c.labels)
+
+
+# ---- pinned to the reference (fixtures written by tests/golden/make_golden*.py)
+from conftest import GOLDEN, config_cases, load_golden  # noqa: E402
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_plate_germs_bit_exact_vs_reference(k):
+    """Germ-grain plating vs the reference's plate_germs (microgen/plating.py:53-109) on the
+    same input grid and seeded generator: labels bit-exact."""
+    g = load_golden("plating_ref")
+    intensity, radius, h, seed = g[f"args_{k}"]
+    out = plate_germs(PhaseGrid(g[f"in_{k}"], float(h)), float(intensity), float(radius),
+                      np.random.default_rng(int(seed)))
+    assert np.array_equal(out.labels, g[f"out_{k}"])
+    assert (out.labels == Phase.PLATED_LI).sum() > (g[f"in_{k}"] == Phase.PLATED_LI).sum()
+
+
+def test_fixture_geometry_is_reproducible():
+    """The generator still reproduces the labels the reference fixtures were computed on."""
+    spec = CellSpec(16, 16, 24, 12, 4, seed=3, radius_mean=3.0, porosity=0.35, plating_intensity=0.05)
+    assert np.array_equal(generate_cell(spec).labels, load_golden("balls_16x16x24")["labels"])
+
+
+@pytest.mark.parametrize("name", config_cases())
+def test_config_fixture_geometry_is_reproducible(name):
+    import sys
+    import os
+    sys.path.insert(0, GOLDEN)
+    from make_golden_configs import case_settings
+    spec = case_settings(name)[0]
+    assert np.array_equal(generate_cell(spec).labels, load_golden(f"config_{name}")["labels"])
