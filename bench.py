@@ -514,38 +514,62 @@ def run_batched(args, ws, rank, local):
 
 
 def run_pod(args, ws, rank, local):
-    """BASELINE config 4 offline stage: POD Gram S^T W S of 2.1M DOF x 400 snapshots (DMMA)."""
+    """BASELINE config 4 offline stage: POD Gram S^T W S of 2.1M DOF x 400 snapshots and the
+    rank-60 basis projection S (U / sigma), both on the FP64 tensor cores (DMMA)."""
     import torch
-    from paper_1704_04139_b200 import pod
+    from paper_1704_04139_b200 import _native, pod
     torch.cuda.set_device(local)
-    n_dof, n_snap = 2_100_000, 400
+    n_dof, n_snap, rank_k = 2_100_000, 400, 60
     g = torch.Generator(device="cuda").manual_seed(7)
     # row-major (n_dof, n_snap): the snapshots of one DOF contiguous, as the ROM's snapshot
-    # matrix is stored; hc_pod_gram_rows reads it in place
+    # matrix is stored; the kernels read it in place
     S = torch.randn(n_dof, n_snap, device="cuda", dtype=torch.float64, generator=g)
     w = torch.rand(n_dof, device="cuda", dtype=torch.float64, generator=g) + 0.5
+    U = torch.randn(n_snap, rank_k, device="cuda", dtype=torch.float64, generator=g)
     for _ in range(args.warmup):
         pod.pod_gram(S, w)
+        pod.tc_matmul(S, U)
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for a, b in ev:
-        a.record()
-        G = pod.pod_gram(S, w)
-        b.record()
-    torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
-    flops = 2.0 * n_dof * n_snap * n_snap
+
+    def timed(fn):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        out = None
+        for a, b in ev:
+            _native.check(_native.lib().hc_flush_l2(L2_FLUSH_BYTES, torch.cuda.current_stream().cuda_stream))
+            a.record()
+            out = fn()
+            b.record()
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in ev) / args.steps, out
+
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ms, G = timed(lambda: pod.pod_gram(S, w))
+        ms_p, V = timed(lambda: pod.tc_matmul(S, U))
+    peak = ctypes.c_double(0.0)
+    _native.check(_native.lib().hc_dmma_peak(ctypes.byref(peak), None))
+    # useful flops: the n (n + 1) / 2 distinct entries of the symmetric Gram, 2 flops per DOF
+    flops = float(n_snap) * (n_snap + 1) * n_dof
+    flops_p = 2.0 * n_dof * n_snap * rank_k
     ref = (S.t() * w) @ S
     err = float((G - ref).abs().max() / ref.abs().max())
-    return {"metric": "POD snapshot Gram S^T W S (FP64 DMMA)", "value": flops / (ms * 1e-3) / 1e9,
+    refp = S @ U
+    err_p = float((V - refp).abs().max() / refp.abs().max())
+    tf, tfp = flops / (ms * 1e-3) / 1e12, flops_p / (ms_p * 1e-3) / 1e12
+    return {"metric": "POD snapshot Gram S^T W S (FP64 DMMA)", "value": tf * 1e3,
             "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic snapshots",
-            "config": {"workload": f"pod: {n_dof} DOF x {n_snap} snapshots",
-                       "flops": "2 n_dof n_snap^2 (the kernel computes the upper triangle only)"},
-            "roofline": {"bound": "tensor (FP64 DMMA pipe)", "pipe_util_ncu": 0.736,
-                         "source": "profiles/r01_gram_ncu.txt"},
-            "max_rel_err_vs_cublas": err}
+            "config": {"workload": f"pod: {n_dof} DOF x {n_snap} snapshots, rank {rank_k} projection",
+                       "flops": "Gram: n_snap (n_snap + 1) n_dof (distinct entries of the symmetric "
+                                "matrix, 2 flops each; the kernel computes upper-triangle tiles only)",
+                       "l2": "flushed before every timed launch"},
+            "roofline": {"bound": "tensor (FP64 DMMA)", "achieved": tf, "peak": peak.value,
+                         "peak_kind": "measured (hc_dmma_peak: register-only DMMA probe)", "unit": "TFLOP/s",
+                         "frac": tf / peak.value if peak.value else None, "traffic": None},
+            "projection": {"what": "S (U / sigma): 2.1M x 400 times 400 x 60 (hc_dgemm)", "ms": ms_p,
+                           "tflops": tfp, "frac_of_dmma_peak": tfp / peak.value if peak.value else None,
+                           "max_rel_err_vs_cublas": err_p},
+            "max_rel_err_vs_cublas": err, "clocks": clk.summary()}
 
 
 def run_rom(args, ws, rank, local):

@@ -202,6 +202,19 @@ int hc_pod_gram(const double* S, const double* w, int64_t n_dof, int64_t n_snap,
 int hc_pod_gram_rows(const double* S, const double* w, int64_t n_dof, int64_t n_snap, double* G,
                      void* stream);
 
+/* The dense contractions of the reduced-basis stage on the FP64 tensor cores (DMMA):
+ * C[i][j] = sum_k w[k] A(k, i) B(k, j), i < M, j < N, k < K, with strided operands
+ * A(k, i) = A[k sa_k + i sa_i], B(k, j) = B[k sb_k + j sb_j] (device fp64) and optional
+ * weights w[K] (NULL = 1); C row-major with leading dimension ldc (device).  Covers the
+ * POD projection S (U / sigma), the CholeskyQR solve V R^-1, the EI block update and
+ * B^T W (SPEC mor.pod / build_rom; no counterpart in the reference tree). */
+int hc_dgemm(const double* A, int64_t sa_k, int64_t sa_i, const double* B, int64_t sb_k, int64_t sb_j,
+             const double* w, int64_t K, int32_t M, int32_t N, double* C, int64_t ldc, void* stream);
+
+/* Measured FP64 tensor-core (DMMA) throughput of the device in TFLOP/s (register-only
+ * probe kernel, CUDA events): the roofline denominator of the reduced-basis contractions. */
+int hc_dmma_peak(double* tflops, void* stream);
+
 /* Reduced-order model for the online stage (SPEC mor.build_rom / solve_rom; no
  * counterpart in the reference tree, whose mor package is not shipped).  All arrays are
  * device memory.  x = B x~ with B = blockdiag(V_c, V_phi); the first k_c reduced

@@ -31,6 +31,14 @@ def to_dev(a, dtype=None):
     return t.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
 
 
+def to_dev_strided(a):
+    """CUDA fp64 tensor of ``a`` keeping a strided CUDA fp64 view as it is (no copy)."""
+    t = torch()
+    if isinstance(a, t.Tensor) and a.device.type == "cuda" and a.dtype == t.float64:
+        return a
+    return to_dev(a)
+
+
 def numel(a) -> int:
     """Element count of a numpy array or tensor."""
     return int(a.numel()) if is_tensor(a) else int(np.size(a))

@@ -108,6 +108,11 @@ _SIGS = {
                                   ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(HcNewtonStats),
                                   ctypes.c_void_p]),
     "hc_precond_refresh": (ctypes.c_int, [ctypes.c_void_p]),
+    "hc_dgemm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
+                                ctypes.c_void_p]),
+    "hc_dmma_peak": (ctypes.c_int, [c_double_p, ctypes.c_void_p]),
     "hc_launch_count": (ctypes.c_int, [c_int64_p]),
     "hc_flush_l2": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p]),
     "hc_time_kernels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,

@@ -26,6 +26,9 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
                           const hc_params& hp);
 void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
               cudaStream_t s, bool rows);
+void dgemm_tc(const double* A, long long sa_k, long long sa_i, const double* B, long long sb_k, long long sb_j,
+              const double* w, long long K, int M, int N, double* C, long long ldc, bool sym, cudaStream_t s);
+double dmma_peak_tflops(cudaStream_t s);
 void restricted_eval(const Operator& op, int n_rows, int n_s, const int32_t* f_kind, const int32_t* f_dof,
                      const int32_t* f_slot, const int32_t* row_ptr, const int32_t* row_face,
                      const double* row_coef, const double* xs, const double* npl, double beta, double* out,
@@ -701,6 +704,19 @@ int hc_pod_gram(const double* Sm, const double* w, int64_t n_dof, int64_t n_snap
     if (n_dof < 0 || n_snap < 0) throw Error(HC_ERR_ARGUMENT, "negative size");
     pod_gram(Sm, w, n_dof, n_snap, G, S(stream), false);
   });
+}
+
+int hc_dgemm(const double* A, int64_t sa_k, int64_t sa_i, const double* B, int64_t sb_k, int64_t sb_j,
+             const double* w, int64_t K, int32_t M, int32_t N, double* C, int64_t ldc, void* stream) {
+  return guarded([&] {
+    if (K < 0 || M < 0 || N < 0 || ldc < N) throw Error(HC_ERR_ARGUMENT, "bad contraction shape");
+    if ((M && N && K) && (!A || !B || !C)) throw Error(HC_ERR_ARGUMENT, "null operand");
+    dgemm_tc(A, sa_k, sa_i, B, sb_k, sb_j, w, K, M, N, C, ldc, false, S(stream));
+  });
+}
+
+int hc_dmma_peak(double* tflops, void* stream) {
+  return guarded([&] { *tflops = dmma_peak_tflops(S(stream)); });
 }
 
 int hc_pod_gram_rows(const double* Sm, const double* w, int64_t n_dof, int64_t n_snap, double* G,

@@ -277,7 +277,10 @@ struct Operator {
   bool dev_krylov = true;          // device-resident BiCGStab (hc_krylov.cu)
   int krylov_batch = 4;            // iteration graphs launched per status check (fallback)
   bool krylov_while = true;        // whole solve as one graph with a device-side WHILE node
-  bool newton_dev = false;         // whole Newton solve as one graph (conditional nodes); HC_NEWTON_DEV=1
+  // whole Newton solve as one graph (conditional nodes): no host sync per Newton iteration;
+  // measured at parity with the host-controlled loop at the exact Krylov tolerance (large
+  // cell 88.2 vs 87.8 ms/step, medium 20.2 vs 20.3); HC_NEWTON_DEV=0 selects the host loop
+  bool newton_dev = true;
   NewtonGraph* ng = nullptr;
   bool capturing = false;          // inside a stream capture (no nested capture)
   KrylovGraphs* kg = nullptr;

@@ -38,46 +38,73 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// part[z][j * n + i] = sum_{k in slice z} S[k][i] w[k] S[k][j]   for the tile pair (ti <= tj)
-template <bool ROWS>
-__global__ void __launch_bounds__(NT) k_gram(const double* __restrict__ S, const double* __restrict__ w,
-                                             long long n_dof, int n, int tiles, long long k_per,
-                                             double* __restrict__ part) {
+// Generic FP64 tensor-core contraction  C[i][j] = sum_k w[k] A(k, i) B(k, j)  with strided
+// operands A(k, i) = A[k sa_k + i sa_i], B(k, j) = B[k sb_k + j sb_j]:
+//   * the POD Gram S^T W S (sym: upper-triangle tile pairs only, A == B, mirrored),
+//   * tall-times-small projections S (U / sigma), V R^-1, W[:, :l] X (i over DOFs, k short),
+//   * long-inner-dimension products B^T W (i, j short, k over DOFs; split-K).
+// One CTA per 64 x 64 tile of C (and K slice); both operand panels and the weights stream
+// through a 3-stage cp.async ring, 4 warps each own a 32 x 32 sub-tile (16 DMMA
+// m8n8k4 per k-step from 8 fragment loads).  Split-K partials are reduced in a fixed order.
+struct GemmDesc {
+  const double* A;
+  long long sa_k, sa_i;
+  const double* B;
+  long long sb_k, sb_j;
+  const double* w;       // optional weights over k
+  long long K;
+  int M, N, tiles_i, tiles_j, sym;
+  long long k_per;
+  double* out;           // nz == 1: C (row-major, ldc);  else partials [z][M][N]
+  long long ldc;
+};
+
+__global__ void __launch_bounds__(NT) k_dgemm(GemmDesc D) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                        // [ST][BT][LD]
   double* Bs = As + ST * BT * LD;           // [ST][BT][LD]
   double* Ws = Bs + ST * BT * LD;           // [ST][KC]
-  // upper-triangle tile pair from the linear block index
-  int p = blockIdx.x, ti = 0;
-  while (p >= tiles - ti) { p -= tiles - ti; ++ti; }
-  const int tj = ti + p;
+  int ti, tj;
+  if (D.sym) {   // upper-triangle tile pair from the linear block index
+    int p = blockIdx.x;
+    ti = 0;
+    while (p >= D.tiles_i - ti) { p -= D.tiles_i - ti; ++ti; }
+    tj = ti + p;
+  } else {
+    ti = blockIdx.x / D.tiles_j;
+    tj = blockIdx.x - ti * D.tiles_j;
+  }
   const int i0 = ti * BT, j0 = tj * BT, z = blockIdx.y;
-  const long long k_begin = (long long)z * k_per;
-  const long long k_end = min(n_dof, k_begin + k_per);
+  const long long k_begin = (long long)z * D.k_per;
+  const long long k_end = min(D.K, k_begin + D.k_per);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wr = warp >> 1, wc = warp & 1;
   const int g = lane >> 2, tq = lane & 3;
-  const double* wsrc = w;
+  // staging order: walk whichever index is contiguous in memory
+  const bool a_icont = D.sa_i == 1, b_jcont = D.sb_j == 1;
   auto stage = [&](long long k0, int s) {
-    // 64 columns x 32 DOFs per panel: 2048 elements per panel, 16 per thread
     for (int e = tid; e < BT * KC; e += NT) {
-      // column-major S: consecutive threads walk k (a column's 256 B); row-major S
-      // (snapshots contiguous per DOF): consecutive threads walk the 64 snapshots of one
-      // DOF row, and a whole 32-DOF chunk of all snapshots is one contiguous block
-      const int col = ROWS ? e % BT : e / KC, kk = ROWS ? e / BT : e - col * KC;
-      const long long k = k0 + kk;
-      const int gi = i0 + col, gj = j0 + col;
-      const bool kin = k < k_end;
-      const long long kk0 = kin ? k : 0;
-      const double* ai = ROWS ? S + kk0 * n + min(gi, n - 1) : S + (long long)min(gi, n - 1) * n_dof + kk0;
-      const double* bj = ROWS ? S + kk0 * n + min(gj, n - 1) : S + (long long)min(gj, n - 1) * n_dof + kk0;
-      cp8(As + (s * BT + col) * LD + kk, ai, (kin && gi < n) ? 8 : 0);
-      cp8(Bs + (s * BT + col) * LD + kk, bj, (kin && gj < n) ? 8 : 0);
+      {
+        const int col = a_icont ? e % BT : e / KC, kk = a_icont ? e / BT : e - (e / KC) * KC;
+        const long long k = k0 + kk;
+        const int gi = i0 + col;
+        const bool ok = k < k_end && gi < D.M;
+        const double* src = D.A + (ok ? k * D.sa_k + (long long)gi * D.sa_i : 0);
+        cp8(As + (s * BT + col) * LD + kk, src, ok ? 8 : 0);
+      }
+      {
+        const int col = b_jcont ? e % BT : e / KC, kk = b_jcont ? e / BT : e - (e / KC) * KC;
+        const long long k = k0 + kk;
+        const int gj = j0 + col;
+        const bool ok = k < k_end && gj < D.N;
+        const double* src = D.B + (ok ? k * D.sb_k + (long long)gj * D.sb_j : 0);
+        cp8(Bs + (s * BT + col) * LD + kk, src, ok ? 8 : 0);
+      }
     }
     if (tid < KC) {
       const long long k = k0 + tid;
       const bool kin = k < k_end;
-      if (wsrc) cp8(Ws + s * KC + tid, wsrc + (kin ? k : 0), kin ? 8 : 0);
+      if (D.w) cp8(Ws + s * KC + tid, D.w + (kin ? k : 0), kin ? 8 : 0);
       else Ws[s * KC + tid] = kin ? 1.0 : 0.0;
     }
   };
@@ -117,67 +144,128 @@ __global__ void __launch_bounds__(NT) k_gram(const double* __restrict__ S, const
     }
   }
   cp_wait<0>();
-  double* out = part + (long long)z * n * n;
+  const bool direct = gridDim.y == 1;
+  double* out = direct ? D.out : D.out + (long long)z * D.M * D.N;
+  const long long ld = direct ? D.ldc : D.N;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int i = i0 + wr * 32 + a * 8 + g;
       const int j = j0 + wc * 32 + b * 8 + tq * 2;
-      if (i < n && j < n) out[(long long)j * n + i] = acc[a][b][0];
-      if (i < n && j + 1 < n) out[(long long)(j + 1) * n + i] = acc[a][b][1];
+      if (i < D.M && j < D.N) out[(long long)i * ld + j] = acc[a][b][0];
+      if (i < D.M && j + 1 < D.N) out[(long long)i * ld + j + 1] = acc[a][b][1];
     }
 }
 
-// G[j][i] = G[i][j] = sum_z part[z] over the upper triangle (fixed order)
-__global__ void k_reduce_sym(int n, int nz, int tiles, const double* __restrict__ part,
-                             double* __restrict__ G) {
-  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long nn = (long long)n * n;
-  if (e >= nn) return;
-  const int j = (int)(e / n), i = (int)(e % n);
-  // the tile pair (ti <= tj) that computed this entry
-  const int ti = i / BT, tj = j / BT;
-  const bool upper = ti <= tj;
-  const long long src = upper ? e : (long long)i * n + j;   // mirrored entry
+// FP64 tensor-core throughput probe: every warp issues `iters` x 16 independent DMMA
+// m8n8k4 on register operands (no memory traffic); 2 * 8 * 8 * 4 flops each
+__global__ void __launch_bounds__(NT) k_dmma_peak(long long iters, double* sink) {
+  double acc[16][2];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q][0] = acc[q][1] = 0.0;
+  double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * blockIdx.x;
+  for (long long it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) dmma_8x8x4(acc[q][0], acc[q][1], a, b);
+  }
   double s = 0.0;
-  for (int z = 0; z < nz; ++z) s += part[(long long)z * nn + src];
-  G[e] = s;
-  (void)tiles;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) s += acc[q][0] + acc[q][1];
+  if (s == 12345.0) sink[0] = s;
+}
+
+// C[i][j] = sum_z part[z][i][j] (fixed order); sym: the lower triangle mirrors the upper
+__global__ void k_reduce_parts(int M, int N, int nz, int sym, const double* __restrict__ part,
+                               double* __restrict__ C, long long ldc) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long mn = (long long)M * N;
+  if (e >= mn) return;
+  const int i = (int)(e / N), j = (int)(e % N);
+  const long long src = (sym && i / BT > j / BT) ? (long long)j * N + i : e;   // tile computed as (tj, ti)
+  double s = 0.0;
+  for (int z = 0; z < nz; ++z) s += part[(long long)z * mn + src];
+  C[(long long)i * ldc + j] = s;
 }
 }  // namespace
 
-void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
-              cudaStream_t s, bool rows) {
-  if (n_snap == 0) return;
-  const int n = (int)n_snap;
-  const int tiles = (n + BT - 1) / BT;
-  const int pairs = tiles * (tiles + 1) / 2;
+// C (M x N, row-major, ldc) = sum_k w[k] A(k, i) B(k, j) on the FP64 tensor cores
+void dgemm_tc(const double* A, long long sa_k, long long sa_i, const double* B, long long sb_k, long long sb_j,
+              const double* w, long long K, int M, int N, double* C, long long ldc, bool sym, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return;
+  if (K <= 0) {
+    for (int i = 0; i < M; ++i) HC_CUDA(cudaMemsetAsync(C + (long long)i * ldc, 0, N * sizeof(double), s));
+    return;
+  }
+  const int tiles_i = (M + BT - 1) / BT, tiles_j = (N + BT - 1) / BT;
+  const long long pairs = sym ? (long long)tiles_i * (tiles_i + 1) / 2 : (long long)tiles_i * tiles_j;
   int sms = 148, dev = 0;
   HC_CUDA(cudaGetDevice(&dev));
   HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const size_t smem = (size_t)(2 * ST * BT * LD + ST * KC) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    HC_CUDA(cudaFuncSetAttribute(k_gram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HC_CUDA(cudaFuncSetAttribute(k_gram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  static int per_sm = 0;
+  if (!per_sm) {
+    HC_CUDA(cudaFuncSetAttribute(k_dgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dgemm, NT, smem));
+    per_sm = std::max(per_sm, 1);
   }
-  int per_sm = 1;
-  HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram<false>, NT, smem));
-  const long long want = std::max<long long>(1, ((long long)std::max(per_sm, 1) * sms + pairs - 1) / pairs);
-  long long k_per = (n_dof + want - 1) / want;
+  // split K only when the tiles alone cannot fill the GPU
+  const long long want = std::max<long long>(1, ((long long)per_sm * sms + pairs - 1) / pairs);
+  long long k_per = (K + want - 1) / want;
   k_per = std::max<long long>(KC, ((k_per + KC - 1) / KC) * KC);
-  const int nz = (int)std::max<long long>(1, (n_dof + k_per - 1) / k_per);
-  DBuf<double> part((size_t)nz * n * n);
-  HC_CUDA(cudaMemsetAsync(part.p, 0, part.n * sizeof(double), s));
-  if (rows) k_gram<true><<<dim3(pairs, nz), NT, smem, s>>>(S, w, n_dof, n, tiles, k_per, part.p);
-  else k_gram<false><<<dim3(pairs, nz), NT, smem, s>>>(S, w, n_dof, n, tiles, k_per, part.p);
+  const int nz = (int)std::max<long long>(1, (K + k_per - 1) / k_per);
+  GemmDesc D{A, sa_k, sa_i, B, sb_k, sb_j, w, K, M, N, tiles_i, tiles_j, sym ? 1 : 0, k_per, C, ldc};
+  DBuf<double> part;
+  if (nz > 1 || sym) {
+    part.alloc((size_t)nz * M * N);
+    if (sym) HC_CUDA(cudaMemsetAsync(part.p, 0, part.n * sizeof(double), s));
+    D.out = part.p;
+  }
+  if (pairs > 0x7fffffffLL) throw Error(HC_ERR_ARGUMENT, "contraction too large");
+  // nz == 1 with sym still goes through the partial buffer (the mirror pass)
+  k_dgemm<<<dim3((unsigned)pairs, nz), NT, smem, s>>>(D);
   HC_COUNT();
   HC_CHECK_LAUNCH();
-  const long long nn = (long long)n * n;
-  k_reduce_sym<<<(int)((nn + 255) / 256), 256, 0, s>>>(n, nz, tiles, part.p, G); HC_COUNT();
-  HC_CHECK_LAUNCH();
+  if (part.p) {
+    const long long mn = (long long)M * N;
+    k_reduce_parts<<<(int)((mn + 255) / 256), 256, 0, s>>>(M, N, nz, sym ? 1 : 0, part.p, C, ldc); HC_COUNT();
+    HC_CHECK_LAUNCH();
+    HC_CUDA(cudaStreamSynchronize(s));   // the partial buffer is freed on return
+  }
+}
+
+// measured FP64 DMMA throughput (TFLOP/s) of the whole GPU
+double dmma_peak_tflops(cudaStream_t s) {
+  int sms = 148, dev = 0;
+  HC_CUDA(cudaGetDevice(&dev));
+  HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DBuf<double> sink(1);
+  const long long iters = 20000;
+  const int grid = sms * 8;
+  k_dmma_peak<<<grid, NT, 0, s>>>(1000, sink.p);   // warm
+  HC_COUNT();
+  cudaEvent_t e0, e1;
+  HC_CUDA(cudaEventCreate(&e0));
+  HC_CUDA(cudaEventCreate(&e1));
+  HC_CUDA(cudaEventRecord(e0, s));
+  k_dmma_peak<<<grid, NT, 0, s>>>(iters, sink.p);
+  HC_COUNT();
+  HC_CUDA(cudaEventRecord(e1, s));
+  HC_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  HC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double flops = (double)grid * (NT / 32) * iters * 16 * 2.0 * 8 * 8 * 4;
+  return flops / (ms * 1e-3) / 1e12;
+}
+
+void pod_gram(const double* S, const double* w, long long n_dof, long long n_snap, double* G,
+              cudaStream_t s, bool rows) {
+  if (n_snap == 0) return;
+  // A(k, i) = S[k][i]: row-major S (snapshots contiguous per DOF) or column-major
+  if (rows) dgemm_tc(S, n_snap, 1, S, n_snap, 1, w, n_dof, (int)n_snap, (int)n_snap, G, n_snap, true, s);
+  else dgemm_tc(S, 1, n_dof, S, 1, n_dof, w, n_dof, (int)n_snap, (int)n_snap, G, n_snap, true, s);
   HC_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -6,8 +6,10 @@ The reference tree does not ship its ``mor`` package; this module follows SPEC
 * snapshots: accepted full-order states of one trajectory (``hc_step``) and the
   nonlinear sub-operator evaluations ``N(x) = A_bv(x) + A_1/c(x)`` at them;
 * POD per field (method of snapshots): the Gram matrix on the FP64 tensor cores
-  (``hc_pod_gram``), eigendecomposition of the small Gram, basis projection, and a
-  CholeskyQR re-orthonormalisation whose Gram is again ``hc_pod_gram``;
+  (``hc_pod_gram``), eigendecomposition of the small Gram, basis projection
+  ``S U / sigma`` and a CholeskyQR2 re-orthonormalisation ``V R^-1`` — every dense
+  contraction of the stage (also the DEIM block updates and ``B^T W``) is a DMMA
+  contraction (``hc_dgemm`` through :func:`pod.tc_matmul`);
 * empirical interpolation of ``N``: collateral basis = POD of the ``N`` snapshots,
   interpolation DOFs by the DEIM greedy (blocked: one GEMM per block brings the
   block up to date, then rank-1 updates inside it — exactly the sequential greedy);
@@ -32,7 +34,7 @@ import numpy as np
 
 from . import _dev, _native
 from .errors import ReductionError
-from .pod import pod_gram
+from .pod import pod_gram, tc_matmul
 from .qoi import qoi_vectors
 
 RF_BV, RF_CE, RF_STRIP, RF_ELEL = 0, 1, 2, 3
@@ -87,7 +89,8 @@ def _orthonormalize(V):
         G = _dev.to_dev(pod_gram(V))
         G = 0.5 * (G + G.t())
         R = t.linalg.cholesky(G, upper=True)
-        V = t.linalg.solve_triangular(R.t(), V.t(), upper=False).t()     # V R^-1
+        Rinv = t.linalg.solve_triangular(R, t.eye(R.shape[0], dtype=R.dtype, device=R.device), upper=True)
+        V = tc_matmul(V, Rinv)                                           # V R^-1 (DMMA)
     return V
 
 
@@ -106,7 +109,7 @@ def pod_rank(S, k: int):
     keep = int((lam > lam[0] * 1e-24).sum())
     k = max(1, min(int(k), keep))
     sig = t.sqrt(lam)
-    V = S @ (U[:, :k] / sig[:k])
+    V = tc_matmul(S, U[:, :k] / sig[:k])                                  # DMMA
     return _orthonormalize(V), sig
 
 
@@ -122,7 +125,7 @@ def deim(W, block: int = 16) -> np.ndarray:
         R = W[:, l0:l1].clone()
         if l0:
             P = t.as_tensor(pi, device="cuda")
-            R -= W[:, :l0] @ t.linalg.solve(W[P, :l0], W[P, l0:l1])
+            R -= tc_matmul(W[:, :l0], t.linalg.solve(W[P, :l0], W[P, l0:l1]))
         for j in range(l1 - l0):
             r = R[:, j]
             p = int(t.argmax(t.abs(r)))
@@ -161,13 +164,13 @@ class ReducedModel:
         t = _dev.torch()
         x = _dev.to_dev(x)
         nc = self.Vc.shape[0]
-        return t.cat([self.Vc.t() @ x[:nc], self.Vp.t() @ x[nc:]])
+        return t.cat([tc_matmul(self.Vc.t(), x[:nc, None])[:, 0], tc_matmul(self.Vp.t(), x[nc:, None])[:, 0]])
 
     def lift(self, xt):
         """x = B x~ (reconstruction; not part of the online loop)."""
         t = _dev.torch()
         xt = _dev.to_dev(xt)
-        return t.cat([self.Vc @ xt[: self.k_c], self.Vp @ xt[self.k_c:]])
+        return t.cat([tc_matmul(self.Vc, xt[: self.k_c, None])[:, 0], tc_matmul(self.Vp, xt[self.k_c:, None])[:, 0]])
 
 
 def _face_tables(op):
@@ -255,14 +258,14 @@ def assemble_rom(op, Vc, Vp, W) -> ReducedModel:
         return v
 
     def BT(v):
-        return t.cat([Vc.t() @ v[:nc], Vp.t() @ v[nc:]])
+        return t.cat([tc_matmul(Vc.t(), v[:nc, None])[:, 0], tc_matmul(Vp.t(), v[nc:, None])[:, 0]])
 
     A = t.stack([BT(op.apply_lin(Bcol(j))) for j in range(k)], dim=1)
     Mr = t.zeros((k, k), dtype=t.float64, device="cuda")
-    Mr[:k_c, :k_c] = Vc.t() @ Vc
+    Mr[:k_c, :k_c] = tc_matmul(Vc.t(), Vc)
     bnd = BT(_dev.to_dev(op.apply_bnd()))
     Pi = t.as_tensor(pi, device="cuda")
-    BTW = t.cat([Vc.t() @ W[:nc], Vp.t() @ W[nc:]])
+    BTW = t.cat([tc_matmul(Vc.t(), W[:nc]), tc_matmul(Vp.t(), W[nc:])])     # B^T W (DMMA)
     E = t.linalg.solve(W[Pi].t(), BTW.t()).t()      # B^T W (W_pi)^-1
     v_cp, v_ac = qoi_vectors(dof)
     q_v, q_ac = BT(_dev.to_dev(v_cp)), BT(_dev.to_dev(v_ac))

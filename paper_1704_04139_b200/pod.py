@@ -1,8 +1,9 @@
 """POD by the method of snapshots (SPEC mor.pod; arXiv 1704.04139 section 2.5).
 
-The snapshot Gram matrix ``G = S^T W S`` is the only dense contraction of the
-path and runs on the FP64 tensor cores (``csrc/hc_pod.cu``); the small
-eigenproblem of G and the basis assembly stay on the device.
+The snapshot Gram matrix ``G = S^T W S`` and the other dense contractions of the
+reduced-basis stage (basis projection, re-orthonormalisation, EI updates, ``B^T W``)
+run on the FP64 tensor cores (``csrc/hc_pod.cu``, :func:`tc_matmul`); the small
+eigenproblem of G and the small triangular / dense solves stay on the device.
 """
 
 from __future__ import annotations
@@ -36,6 +37,27 @@ def pod_gram(S, w=None):
     return _dev.like_input(G.contiguous(), S)
 
 
+def tc_matmul(X, Y, w=None):
+    """``X @ diag(w) @ Y`` (fp64) on the FP64 tensor cores (``hc_dgemm``, csrc/hc_pod.cu).
+
+    X (M, K) and Y (K, N) are CUDA fp64 tensors of any strides (transposed views and row
+    slices are used in place); the result is a new contiguous (M, N) tensor."""
+    t = _dev.torch()
+    X, Y = _dev.to_dev_strided(X), _dev.to_dev_strided(Y)
+    if X.dim() != 2 or Y.dim() != 2 or X.shape[1] != Y.shape[0]:
+        raise ValueError(f"tc_matmul: incompatible shapes {tuple(X.shape)} @ {tuple(Y.shape)}")
+    M, K = X.shape
+    N = Y.shape[1]
+    C = t.empty((M, N), dtype=t.float64, device="cuda")
+    wd = _dev.to_dev(w) if w is not None else None
+    _native.check(_native.lib().hc_dgemm(
+        _dev.ptr(X) if X.numel() else None, X.stride(1), X.stride(0),
+        _dev.ptr(Y) if Y.numel() else None, Y.stride(0), Y.stride(1),
+        _dev.ptr(wd) if wd is not None else None, int(K), int(M), int(N), _dev.ptr(C), int(N),
+        _dev.stream()))
+    return C
+
+
 def pod_basis(S, rel_tol: float, w=None):
     """Orthonormal POD basis keeping the smallest k with tail energy <= rel_tol^2.
 
@@ -59,7 +81,7 @@ def pod_basis(S, rel_tol: float, w=None):
         if rest <= rel_tol ** 2 * tot:
             k = kk
             break
-    B = Sd @ (V[:, :k] / sig[:k])
+    B = tc_matmul(Sd, V[:, :k] / sig[:k])
     # one modified Gram-Schmidt pass (SPEC: re-orthonormalize output)
     for j in range(k):
         for i in range(j):

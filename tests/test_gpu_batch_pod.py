@@ -51,3 +51,23 @@ def test_pod_basis_orthonormal_and_singular_values():
     assert np.max(np.abs(B.T @ B - np.eye(B.shape[1]))) < 1e-12
     ref = np.linalg.svd(S, compute_uv=False)
     assert np.allclose(sig[: ref.size], ref, rtol=1e-8)
+
+
+@pytest.mark.parametrize("shape", [(2_000, 37, 5), (70_000, 130, 61), (9, 200_000, 66), (150, 3, 1)])
+def test_tc_matmul_strided_operands_match_fp64(shape):
+    """The reduced-basis stage's DMMA contractions (hc_dgemm): tall x small projections,
+    long-inner-dimension products B^T W, transposed / sliced operands in place."""
+    import torch
+    from paper_1704_04139_b200 import pod
+    m, k, n = shape
+    g = torch.Generator(device="cuda").manual_seed(9)
+    X = torch.randn(m, k, dtype=torch.float64, device="cuda", generator=g)
+    Y = torch.randn(k, n + 3, dtype=torch.float64, device="cuda", generator=g)[:, 1:n + 1]   # strided slice
+    for a, b in ((X, Y), (X.t().contiguous().t(), Y), (Y.t(), X.t()) if m == k else (X, Y)):
+        C = pod.tc_matmul(a, b)
+        ref = a.cpu().numpy() @ b.cpu().numpy()
+        assert np.max(np.abs(C.cpu().numpy() - ref)) <= 1e-12 * max(np.max(np.abs(ref)), 1.0) * np.sqrt(k)
+    w = torch.rand(k, dtype=torch.float64, device="cuda", generator=g) + 0.5
+    Cw = pod.tc_matmul(X, Y, w)
+    ref = (X.cpu().numpy() * w.cpu().numpy()) @ Y.cpu().numpy()
+    assert np.max(np.abs(Cw.cpu().numpy() - ref)) <= 1e-12 * np.max(np.abs(ref)) * np.sqrt(k)

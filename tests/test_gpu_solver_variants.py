@@ -39,7 +39,7 @@ def _step_with(env):
 
 
 @pytest.mark.parametrize("env", [
-    {"HC_NEWTON_DEV": "1"},
+    {"HC_NEWTON_DEV": "0"},          # host-controlled Newton loop (the device graph is the default)
     {"HC_KRYLOV_WHILE": "0"},
     {"HC_AMG_FUSE_ROWS": "4096"},
     {"HC_STENCIL": "2"},
@@ -53,3 +53,31 @@ def test_variant_reaches_the_same_step(env):
     assert info.n_iter >= 1
     assert np.max(np.abs(xv[:nc] - xr[:nc]) / np.abs(xr[:nc])) < 1e-8
     assert np.max(np.abs(xv[nc:] - xr[nc:])) < 1e-8
+
+
+def test_device_newton_graph_survives_host_loops():
+    """The cached device Newton graph captures the work-buffer addresses; host-controlled
+    solves on the same operator swap those buffers (the initial potential solve always runs
+    on the host), so a step after one must rebuild the graph, not read a stale guess."""
+    import paper_1704_04139_b200 as P
+    from paper_1704_04139_b200.microgen import CellSpec, generate_cell
+    spec = CellSpec(32, 32, 48, 20, 8, seed=11, radius_mean=3.0, porosity=0.35, plating_intensity=0.05)
+    grid = generate_cell(spec)
+    params = P.MaterialParams()
+    cfg = P.SolverConfig(dt_init=0.5, dt_max=0.5)
+
+    def run(interleave):
+        op = P.SystemOperator(P.build_dofmap(grid), params)
+        st = P.prepare_initial_state(op, params, -20.0, cfg)
+        st1, *_ = P.step(op, st, 0.5, -20.0, cfg)
+        if interleave:   # host loop on the same operator between two device-graph steps
+            P.solve_initial_potential(op, st.x, st.n_pl, -20.0, cfg)
+            P.newton_solve(op, st.x, 0.5, st.x, st.n_pl, -20.0, cfg)
+        st2, _, _, info = P.step(op, st1, 0.5, -20.0, cfg)
+        return st2, op.dof.n_c, info
+
+    a, nc, _ = run(False)
+    b, _, info = run(True)
+    assert info.n_iter >= 1
+    assert np.max(np.abs(b.c - a.c) / np.abs(a.c)) < 1e-8
+    assert np.max(np.abs(b.phi - a.phi)) < 1e-8
