@@ -318,6 +318,60 @@ __global__ void k_to_float(long long n, const double* __restrict__ a, float* __r
   if (i < n) b[i] = (float)a[i];
 }
 
+// sliced-ELL values from the CSR fp32 values (after every numeric setup)
+__global__ void k_sell_gather(long long n, const int32_t* __restrict__ map, const float* __restrict__ vf,
+                              float* __restrict__ out) {
+  pdl_wait();
+  long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q < n) {
+    const int m = map[q];
+    out[q] = m >= 0 ? vf[m] : 0.0f;
+  }
+}
+
+// The k_csr_x sweep on the sliced-ELL copy: one thread per row, a warp per 32-row slice
+// (uniform trip count), entries in the row's CSR order
+template <int XM>
+__global__ void k_sell_x(int n, double w, double alpha, const int32_t* __restrict__ sp,
+                         const int32_t* __restrict__ sc, const float* __restrict__ sv,
+                         const double* __restrict__ dinv, const double* __restrict__ b,
+                         const double* __restrict__ x, const int32_t* __restrict__ parent,
+                         const double* __restrict__ xc, double* __restrict__ y, int resid,
+                         double* __restrict__ x0) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slice = i >> 5;
+  if (slice * 32 >= n) return;
+  auto xin = [&](int j) -> double {
+    if (XM == 0) return x[j];
+    if (XM == 1) return w * dinv[j] * b[j];
+    return x[j] + alpha * xc[parent[j]];
+  };
+  const int base = sp[slice], width = (sp[slice + 1] - base) >> 5;
+  const int r = i & 31;
+  const int32_t* cp = sc + base + r;
+  const float* vp = sv + base + r;
+  double s = 0.0;
+  int k = 0;
+  for (; k + 3 < width; k += 4) {
+    const int c0 = cp[0], c1 = cp[32], c2 = cp[64], c3 = cp[96];
+    const double a0 = vp[0], a1 = vp[32], a2 = vp[64], a3 = vp[96];
+    const double x0_ = xin(c0), x1 = xin(c1), x2 = xin(c2), x3 = xin(c3);
+    s += a0 * x0_;
+    s += a1 * x1;
+    s += a2 * x2;
+    s += a3 * x3;
+    cp += 128;
+    vp += 128;
+  }
+  for (; k < width; ++k, cp += 32, vp += 32) s += (double)*vp * xin(*cp);
+  if (i < n) {
+    const double xi = xin(i);
+    y[i] = resid ? b[i] - s : xi + w * dinv[i] * (b[i] - s);
+    if (x0) x0[i] = xi;
+  }
+}
+
 // VS lanes per row (VS = 1, 8 or 32), chosen per level from the mean row length
 template <int VS, class VT>
 __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
@@ -527,6 +581,41 @@ void upload_csr(Csr& c, const HPat& p) {
 
 }  // namespace
 
+// sliced-ELL pattern (see Csr::sl_*) from a host CSR pattern
+static void build_sell(Csr& c, const HPat& p) {
+  const int n = p.n(), ns = (n + 31) / 32;
+  std::vector<int32_t> ptr(ns + 1, 0);
+  for (int sl = 0; sl < ns; ++sl) {
+    int wmax = 0;
+    for (int r = sl * 32; r < std::min(n, sl * 32 + 32); ++r) wmax = std::max(wmax, p.rp[r + 1] - p.rp[r]);
+    ptr[sl + 1] = ptr[sl] + 32 * wmax;
+  }
+  std::vector<int32_t> col(ptr[ns]), map(ptr[ns]);
+  for (int sl = 0; sl < ns; ++sl) {
+    const int width = (ptr[sl + 1] - ptr[sl]) / 32;
+    for (int r = 0; r < 32; ++r) {
+      const int i = sl * 32 + r;
+      const int len = i < n ? p.rp[i + 1] - p.rp[i] : 0;
+      for (int k = 0; k < width; ++k) {
+        const int q = ptr[sl] + k * 32 + r;
+        if (k < len) {
+          col[q] = p.ci[p.rp[i] + k];
+          map[q] = p.rp[i] + k;
+        } else {
+          col[q] = i < n ? i : 0;
+          map[q] = -1;
+        }
+      }
+    }
+  }
+  upload(c.sl_ptr, ptr);
+  upload(c.sl_col, col);
+  upload(c.sl_map, map);
+  c.sl_vf.alloc(std::max<size_t>(col.size(), 1));
+  c.sl_nnz = (long long)col.size();
+  c.sl_n = n;
+}
+
 // ============================================================== host: patterns
 static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int field,
                         const Amg& cfg, AmgBlock& B) {
@@ -587,6 +676,9 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     const int n = A.n();
     L.n = n;
     upload_csr(L.A, A);
+    if (level >= 1 && cfg.sell_max_avg > 0 && n >= cfg.sell_min_rows &&
+        (double)A.ci.size() <= (double)cfg.sell_max_avg * n)
+      build_sell(L.A, A);
     L.dinv.alloc(std::max(n, 1));
     int active = 0;
     for (int i = 0; i < n; ++i) active += A.rp[i + 1] > A.rp[i];
@@ -815,6 +907,8 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_FUSE_NNZ")) amg->fuse_nnz = atoll(e);
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT")) amg->fuse_restrict = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT_SA")) amg->fuse_restrict_sa = atoi(e) != 0;
+  if (const char* e = getenv("HC_AMG_SELL")) amg->sell_max_avg = atoi(e);
+  if (const char* e = getenv("HC_AMG_SELL_ROWS")) amg->sell_min_rows = atoi(e);
   auto t0 = std::chrono::steady_clock::now();
   for (int f = 0; f < 2; ++f) {
     amg->blk[f].nu = amg->nu;
@@ -883,6 +977,10 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
       AmgLevel& L = B.levels[l];
       if (A.fp32_coarse && L.A.nnz) {
         launch(k_to_float, nblk(L.A.nnz), TPB, 0, s, L.A.nnz, L.A.v.p, L.A.vf.p); HC_COUNT();
+        if (L.A.sl_n) {
+          launch(k_sell_gather, nblk(L.A.sl_nnz), TPB, 0, s, L.A.sl_nnz, L.A.sl_map.p, L.A.vf.p, L.A.sl_vf.p);
+          HC_COUNT();
+        }
       }
       if (L.R.nnz && l + 1 < B.levels.size()) {
         const AmgLevel& U = B.levels[l + 1];
@@ -1111,6 +1209,12 @@ template <int XM>
 static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha, const double* b,
                         const double* x, const int32_t* parent, const double* xc, double* y,
                         int resid, cudaStream_t s, double* x0 = nullptr) {
+  if (A.fp32_coarse && L.A.sl_n) {
+    launch(k_sell_x<XM>, nblk(L.n), TPB, 0, s, L.n, w, alpha, L.A.sl_ptr.p, L.A.sl_col.p,
+           (const float*)L.A.sl_vf.p, L.dinv.p, b, x, parent, xc, y, resid, x0);
+    HC_COUNT();
+    return;
+  }
   double avg = L.n ? (double)L.A.nnz / L.n : 0.0;
   const int VSsel = avg <= 12.0 ? 1 : (avg <= 48.0 ? 8 : 32);
   auto go = [&](auto vs_tag, auto* vals) {

@@ -44,9 +44,11 @@ RF_BV, RF_CE, RF_STRIP, RF_ELEL = 0, 1, 2, 3
 @dataclass
 class Snapshots:
     X: object                  # (n_dof, n_s) device states
-    N: object                  # (n_dof, n_s) device nonlinear evaluations
+    N: object                  # (n_dof, n_s) device nonlinear evaluations N = N_bv + N_1c
     n_pl: list = field(default_factory=list)
     beta: float = 0.0
+    Nb: object = None          # (n_dof, n_s) A_bv part (separate EI spaces, SPEC build_rom)
+    Nc: object = None          # (n_dof, n_s) A_1/c part
 
 
 def nonlinear_part(op, x, n_pl, beta: float):
@@ -68,7 +70,8 @@ def collect_snapshots(op, x0, n_pl0, mu: float, dt: float, n_steps: int, cfg=Non
     beta = dt * op.face_area / op.p.constants.F
     n = op.dof.n_total
     X = t.empty((n, n_steps + 1), dtype=t.float64, device="cuda")
-    N = t.empty_like(X)
+    Nb = t.empty_like(X)
+    Nc = t.empty_like(X)
     pls = []
     for s in range(n_steps + 1):
         if s:
@@ -76,9 +79,10 @@ def collect_snapshots(op, x0, n_pl0, mu: float, dt: float, n_steps: int, cfg=Non
                                                 float(mu), ctypes.byref(c), ctypes.byref(st),
                                                 _dev.stream()))
         X[:, s] = x
-        N[:, s] = nonlinear_part(op, x, npl, beta)
+        Nb[:, s] = op.apply_bv(x, npl, beta=beta)
+        Nc[:, s] = op.apply_one_over_c(x)
         pls.append(npl.clone())
-    return Snapshots(X, N, pls, beta)
+    return Snapshots(X, Nb + Nc, pls, beta, Nb, Nc)
 
 
 # ------------------------------------------------------------------ POD / DEIM
@@ -94,9 +98,11 @@ def _orthonormalize(V):
     return V
 
 
-def pod_rank(S, k: int):
-    """Orthonormal POD basis of rank <= k of the columns of S (n, n_s), method of
-    snapshots; returns (V (n, k'), singular values)."""
+def pod_rank(S, k: int | None = None, rel_tol: float | None = None):
+    """Orthonormal POD basis of the columns of S (n, n_s), method of snapshots; returns
+    (V (n, k'), singular values).  The rank is at most ``k`` and, with ``rel_tol``, the
+    smallest one whose discarded energy sum_{i>k} s_i^2 / sum s_i^2 <= rel_tol^2 (SPEC
+    mor.pod; the paper uses 1e-7)."""
     t = _dev.torch()
     S = _dev.to_dev(S)
     if not float(t.linalg.vector_norm(S)) > 0.0:
@@ -107,7 +113,13 @@ def pod_rank(S, k: int):
     lam, U = lam.flip(0), U.flip(1)
     lam = t.clamp(lam, min=0.0)
     keep = int((lam > lam[0] * 1e-24).sum())
-    k = max(1, min(int(k), keep))
+    if rel_tol is not None:
+        if not 0.0 < rel_tol < 1.0:
+            raise ReductionError("rel_tol must lie in (0, 1)")
+        tail = t.flip(t.cumsum(t.flip(lam, [0]), 0), [0])       # tail[j] = sum_{i >= j} lam_i
+        ok = (tail <= rel_tol ** 2 * tail[0]).nonzero()
+        keep = min(keep, int(ok[0]) if ok.numel() else keep)
+    k = max(1, min(int(k) if k is not None else keep, keep))
     sig = t.sqrt(lam)
     V = tc_matmul(S, U[:, :k] / sig[:k])                                  # DMMA
     return _orthonormalize(V), sig
@@ -210,11 +222,24 @@ def _face_tables(op):
             cat([i[2] for i in inc], float))
 
 
-def build_rom(op, snaps: Snapshots, k_c: int, k_p: int, m: int) -> ReducedModel:
-    """Offline stage: POD bases, EI data, projected blocks, restricted stencil."""
+def build_rom(op, snaps: Snapshots, k_c: int, k_p: int, m: int, rel_tol: float | None = None,
+              separate_ei: bool = False, m_c: int | None = None) -> ReducedModel:
+    """Offline stage: POD bases, EI data, projected blocks, restricted stencil.
+
+    ``rel_tol`` truncates each POD basis by its discarded energy (ranks k_c, k_p are then
+    upper bounds).  ``separate_ei`` interpolates the interface-current sub-operator A_bv
+    (M = m points) and the chemical-potential sub-operator A_1/c (M = m_c, default m) in
+    their own EI spaces, as SPEC build_rom's (M^(bv), M^(1/c)); the default is one EI space
+    for their sum."""
     nc = op.dof.n_c
-    Vc, _ = pod_rank(snaps.X[:nc], k_c)
-    Vp, _ = pod_rank(snaps.X[nc:], k_p)
+    Vc, _ = pod_rank(snaps.X[:nc], k_c, rel_tol)
+    Vp, _ = pod_rank(snaps.X[nc:], k_p, rel_tol)
+    if separate_ei:
+        if snaps.Nb is None:
+            raise ReductionError("separate EI spaces need the per-sub-operator snapshots")
+        Wb, _ = pod_rank(snaps.Nb, m)
+        Wc, _ = pod_rank(snaps.Nc, m_c or m)
+        return assemble_rom(op, Vc, Vp, None, spaces=[(Wb, (RF_BV, RF_CE, RF_STRIP)), (Wc, (RF_ELEL,))])
     W, _ = pod_rank(snaps.N, m)
     return assemble_rom(op, Vc, Vp, W)
 
@@ -237,8 +262,12 @@ def build_rom_twin(op, snaps: Snapshots, k_c: int, k_p: int, m: int, keep_fracti
     return rom, twin
 
 
-def assemble_rom(op, Vc, Vp, W) -> ReducedModel:
-    """Projected blocks, EI rows / projection and the restricted stencil for given bases."""
+def assemble_rom(op, Vc, Vp, W, spaces=None) -> ReducedModel:
+    """Projected blocks, EI rows / projection and the restricted stencil for given bases.
+
+    ``spaces``: list of (collateral basis, face kinds) EI spaces; default one space W for
+    all face kinds.  Each space contributes its DEIM rows (evaluated from its faces only)
+    and its block of E = B^T W (W_pi)^-1."""
     t = _dev.torch()
     dof = op.dof
     nc, n = dof.n_c, dof.n_total
@@ -246,8 +275,11 @@ def assemble_rom(op, Vc, Vp, W) -> ReducedModel:
     k = k_c + k_p
     if k > 160:
         raise ReductionError("reduced dimension exceeds HC_ROM_MAX_K (160)")
-    m = W.shape[1]
-    pi = deim(W)
+    if spaces is None:
+        spaces = [(W, (RF_BV, RF_CE, RF_STRIP, RF_ELEL))]
+    pis = [deim(Ws) for Ws, _ in spaces]
+    m = sum(Ws.shape[1] for Ws, _ in spaces)
+    pi = np.concatenate(pis)
     # ---- affine blocks: A~ = B^T A_lin B, M~ = B^T diag(c rows) B, b~ = B^T b_bnd
     def Bcol(j):
         v = t.zeros(n, dtype=t.float64, device="cuda")
@@ -264,17 +296,27 @@ def assemble_rom(op, Vc, Vp, W) -> ReducedModel:
     Mr = t.zeros((k, k), dtype=t.float64, device="cuda")
     Mr[:k_c, :k_c] = tc_matmul(Vc.t(), Vc)
     bnd = BT(_dev.to_dev(op.apply_bnd()))
-    Pi = t.as_tensor(pi, device="cuda")
-    BTW = t.cat([tc_matmul(Vc.t(), W[:nc]), tc_matmul(Vp.t(), W[nc:])])     # B^T W (DMMA)
-    E = t.linalg.solve(W[Pi].t(), BTW.t()).t()      # B^T W (W_pi)^-1
+    Es = []
+    for (Ws, _), pis_ in zip(spaces, pis):
+        Pi = t.as_tensor(pis_, device="cuda")
+        BTW = t.cat([tc_matmul(Vc.t(), Ws[:nc]), tc_matmul(Vp.t(), Ws[nc:])])     # B^T W (DMMA)
+        Es.append(t.linalg.solve(Ws[Pi].t(), BTW.t()).t())                       # B^T W (W_pi)^-1
+    E = t.cat(Es, dim=1)
     v_cp, v_ac = qoi_vectors(dof)
     q_v, q_ac = BT(_dev.to_dev(v_cp)), BT(_dev.to_dev(v_ac))
     # ---- restricted stencil: faces of the EI rows + every stripping face
     kind, fdof, fslot, inc_row, inc_face, inc_coef = _face_tables(op)
-    row_of = np.full(n, -1, np.int64)
-    row_of[pi] = np.arange(m)
-    sel = row_of[inc_row] >= 0
-    r_m, r_f, r_c = row_of[inc_row[sel]], inc_face[sel], inc_coef[sel]
+    rms, rfs, rcs = [], [], []
+    off = 0
+    for (Ws, kinds), pis_ in zip(spaces, pis):   # each EI row reads its own space's faces
+        row_of = np.full(n, -1, np.int64)
+        row_of[pis_] = off + np.arange(pis_.size)
+        sel = (row_of[inc_row] >= 0) & np.isin(kind[inc_face], kinds)
+        rms.append(row_of[inc_row[sel]])
+        rfs.append(inc_face[sel])
+        rcs.append(inc_coef[sel])
+        off += pis_.size
+    r_m, r_f, r_c = np.concatenate(rms), np.concatenate(rfs), np.concatenate(rcs)
     active = np.union1d(np.unique(r_f), np.flatnonzero(kind == RF_STRIP))
     loc_face = np.full(kind.size, -1, np.int64)
     loc_face[active] = np.arange(active.size)

@@ -134,3 +134,27 @@ def test_batched_rom_equals_single_trajectories(cell):
         assert np.allclose(v[i], tr.voltage, rtol=1e-13, atol=1e-15)
         assert np.allclose(c[i], tr.mean_solid_c, rtol=1e-13)
         assert np.allclose(xt[i].cpu().numpy(), tr.xt.cpu().numpy(), rtol=1e-12, atol=1e-12)
+
+
+def test_separate_ei_spaces_and_tolerance_truncation(cell):
+    """SPEC build_rom / pod: A_bv and A_1/c interpolated in their own EI spaces (each row
+    reads only its sub-operator's faces), POD ranks from the discarded-energy tolerance;
+    the online kernel still equals the CPU restatement and follows the training run."""
+    from paper_1704_04139_b200 import mor
+    from paper_1704_04139_b200.qoi import qoi_vectors
+    from oracle import rom_oracle as R
+    op, snaps, st = cell["op"], cell["snaps"], cell["st"]
+    Vc, sig = mor.pod_rank(snaps.X[: op.dof.n_c], None, rel_tol=1e-7)
+    lam = (sig.cpu().numpy() ** 2)
+    k = Vc.shape[1]
+    assert lam[k:].sum() <= 1e-14 * lam.sum() and (k == 1 or lam[k - 1:].sum() > 1e-14 * lam.sum())
+    rom = mor.build_rom(op, snaps, 10, 10, 12, separate_ei=True, m_c=12)
+    assert rom.m == 24 and rom.W is None
+    xt0 = rom.project(st.x)
+    tr = mor.solve_rom(op, rom, xt0, st.n_pl, cell["mu"], cell["dt"], N_TRAIN)
+    xo, no, qo, io = R.rom_run(cell["orc"], rom.host(), xt0.cpu().numpy(), st.n_pl, cell["mu"], cell["dt"], N_TRAIN)
+    assert np.array_equal(tr.newton_iters, io)
+    assert np.allclose(tr.voltage, qo[:, 0], rtol=1e-10, atol=1e-12)
+    v_cp, _ = qoi_vectors(op.dof)
+    fom_v = v_cp @ snaps.X.cpu().numpy()[:, 1:]
+    assert np.max(np.abs(tr.voltage - fom_v)) <= 1e-3 * np.max(np.abs(fom_v))
