@@ -311,6 +311,33 @@ def config0_line():
     return out
 
 
+def other_configs(args):
+    """BASELINE configs[3] (batched study) and configs[4] (POD Gram + projection; ROM online
+    stage) measured in the same run as the headline, with shortened step counts, so the
+    driver's bench line carries them (each leg guarded: a failure is reported, not fatal)."""
+    import copy
+    out = {}
+    legs = (("batched", run_batched, dict(steps=5, warmup=3)),
+            ("pod", run_pod, dict(steps=3, warmup=1)),
+            ("rom", run_rom, dict(steps=500, warmup=1)))
+    for name, fn, over in legs:
+        a = copy.copy(args)
+        for k, v in over.items():
+            setattr(a, k, v)
+        a.config = name
+        t0 = time.perf_counter()
+        try:
+            r = fn(a, 1, 0, int(os.environ.get("LOCAL_RANK", "0")))
+            keep = ("metric", "value", "unit", "steps", "ms_per_step", "config", "roofline", "projection",
+                    "krylov_iters_per_cell_step", "newton_iters_per_step", "parameter_batch",
+                    "qoi_max_rel_dev_vs_fom_training_window", "offline", "max_rel_err_vs_cublas", "e2e")
+            out[name] = {k: r[k] for k in keep if k in r}
+        except Exception as e:  # noqa: BLE001
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        out[name]["wall_s"] = time.perf_counter() - t0
+    return out
+
+
 def run_ours(args, ws, rank, local):
     import torch
     import paper_1704_04139_b200 as P
@@ -465,6 +492,8 @@ def run_ours(args, ws, rank, local):
         }
         if not args.no_config0:
             out["config0"] = config0_line()
+        if ws == 1 and not args.no_other_configs:
+            out["other_configs"] = other_configs(args)
     if ws > 1:
         torch.distributed.destroy_process_group()
     return out
@@ -701,6 +730,8 @@ def main():
     ap.add_argument("--no-at-scale", action="store_true", help="skip the large-grid kernel roofline")
     ap.add_argument("--no-inexact", action="store_true", help="skip the inexact-Newton figure")
     ap.add_argument("--no-config0", action="store_true", help="skip the tiny-config line")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the batched / POD / ROM legs appended to the headline line")
     ap.add_argument("--cells", type=int, default=128)
     ap.add_argument("--rom-snapshots", type=int, default=400)
     ap.add_argument("--rom-rank", type=int, default=60)

@@ -152,11 +152,18 @@ __global__ void k_smooth_P(int n, int smooth, double w, const int32_t* __restric
   int p0 = prp[i], p1 = prp[i + 1];
   if (p0 == p1) return;
   for (int k = p0; k < p1; ++k) pv[k] = 0.0;
-  pv[find_col(pci, p0, p1, parent[i])] += 1.0;
+  const int self = find_col(pci, p0, p1, parent[i]);
+  pv[self] += 1.0;
   if (!smooth) return;
   double s = -w * dinv[i];
-  for (int k = arp[i]; k < arp[i + 1]; ++k)
-    pv[find_col(pci, p0, p1, parent[aci[k]])] += s * av[k];
+  // filtered smoothing (smooth == 2): couplings whose aggregate is not in the row's pattern
+  // (weak, cross-phase ones) are lumped onto the diagonal, A^F = A - weak + diag(weak)
+  for (int k = arp[i]; k < arp[i + 1]; ++k) {
+    const int32_t c = parent[aci[k]];
+    int q = find_col(pci, p0, p1, c);
+    if (q >= p1 || pci[q] != c) q = self;
+    pv[q] += s * av[k];
+  }
 }
 
 // Warp-per-row variants of the two Galerkin passes.  Within one (fine row, P row) pair
@@ -755,7 +762,11 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     const bool smooth = level < (field == 0 ? cfg.sa_levels_c : cfg.sa_levels) ||
                         (field != 0 && (cfg.sa_any ? level >= cfg.sa_levels : level == cfg.sa_levels) &&
                          n >= cfg.sa_rows_min && n <= cfg.sa_rows);
+    // filtered smoothing: the prolongator reaches only the aggregates of strong (same-phase
+    // connectivity graph G) neighbours
+    const bool filt = smooth && field != 0 && level < 30 && ((cfg.sa_filter >> level) & 1);
     L.smoothed = smooth;
+    L.filtered = filt;
     HPat Pp;
     {
       std::vector<std::vector<int32_t>> rows(n);
@@ -763,7 +774,12 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
         if (parent[i] < 0) return;
         rows[i].push_back(parent[i]);
         if (smooth)
-          for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) rows[i].push_back(parent[A.ci[k]]);
+          for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const int j = A.ci[k];
+            if (filt && j != i && !std::binary_search(G.ci.begin() + G.rp[i], G.ci.begin() + G.rp[i + 1], j))
+              continue;
+            if (parent[j] >= 0) rows[i].push_back(parent[j]);
+          }
       });
       Pp = finish(rows);
     }
@@ -908,6 +924,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT")) amg->fuse_restrict = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT_SA")) amg->fuse_restrict_sa = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_SELL")) amg->sell_max_avg = atoi(e);
+  if (const char* e = getenv("HC_AMG_SA_FILTER")) amg->sa_filter = atoi(e);
   if (const char* e = getenv("HC_AMG_SELL_ROWS")) amg->sell_min_rows = atoi(e);
   auto t0 = std::chrono::steady_clock::now();
   for (int f = 0; f < 2; ++f) {

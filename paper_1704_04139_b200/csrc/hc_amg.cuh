@@ -30,6 +30,7 @@ struct AmgLevel {
   DBuf<double> dinv;
   DBuf<int32_t> parent;                  // tentative aggregate of each row, -1 if empty
   bool smoothed = false;                 // P is a smoothed (not tentative) prolongator
+  bool filtered = false;                 // ... smoothed with the filtered (strong-graph) operator
   Csr P;                                 // prolongator to the next level (smoothed aggregation)
   Csr AP;                                // A P (Galerkin intermediate)
   Csr R;                                 // P^T A for a tentative P (levels >= 1): the member-row
@@ -105,6 +106,7 @@ struct Amg {
   bool fuse_restrict_sa = false;  // ... also where P is smoothed (HC_AMG_FUSE_RESTRICT_SA)
   int coarsen = 2;           // block growth factor of the transfers above level 1              // gamma cycles on CSR levels wmin..wdepth
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
+  int sa_filter = 0;         // bit l: filtered smoothing of the phi transfer from level l
   int sell_max_avg = 48;     // levels with at most this many nonzeros per row (and >= sell_min_rows
   int sell_min_rows = 131072; // rows) sweep through the sliced-ELL copy (0: off); measured: large cell
                              // 88.0 -> 83.7 ms per step, medium cell (70 k-row level) 20.2 -> 21.4 at 16 k
