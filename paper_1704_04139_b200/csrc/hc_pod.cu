@@ -18,7 +18,7 @@ namespace hc {
 
 namespace {
 constexpr int BT = 64;      // tile of G
-constexpr int KC = 32;      // DOF chunk per stage
+constexpr int KC = 16;      // K chunk per stage (16: 55 KB of ring per CTA, 4 CTAs / 16 warps per SM)
 constexpr int ST = 3;       // pipeline stages
 constexpr int LD = KC + 2;  // padded row of a staged panel
 constexpr int NT = 128;     // 4 warps: 2 x 2 sub-tiles of 32 x 32
