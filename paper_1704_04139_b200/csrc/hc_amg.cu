@@ -127,7 +127,7 @@ __global__ void k_assemble0(DevParams P, int field, const uint8_t* __restrict__ 
 }
 
 __global__ void k_dinv(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                       const double* __restrict__ v, double* __restrict__ dinv) {
+                       const double* __restrict__ v, double* __restrict__ dinv, CV* __restrict__ dinvc) {
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -138,6 +138,7 @@ __global__ void k_dinv(int n, const int32_t* __restrict__ rp, const int32_t* __r
     if (k < r1 && ci[k] == i) d = v[k];
   }
   dinv[i] = d != 0.0 ? 1.0 / d : 0.0;
+  if (dinvc) dinvc[i] = (CV)dinv[i];
 }
 
 // P = (I - w D^-1 A) P0 (smoothed) or P0 (tentative) — one thread per row
@@ -299,21 +300,21 @@ __global__ void k_dense_inverse(int n, const double* __restrict__ A, double* __r
 }
 
 // x = Ainv b, one warp per row
-__global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const double* __restrict__ b,
-                               double* __restrict__ x) {
+__global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const CV* __restrict__ b,
+                               CV* __restrict__ x) {
   pdl_wait();
   int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
   if (row >= n) return;
   double s = 0.0;
-  for (int j = lane; j < n; j += 32) s += Ainv[row * n + j] * b[j];
+  for (int j = lane; j < n; j += 32) s += Ainv[row * n + j] * (double)b[j];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-  if (lane == 0) x[row] = s;
+  if (lane == 0) x[row] = (CV)s;
 }
 
 // ---- cycle kernels ------------------------------------------------------------
 
-__global__ void k_csr_smooth0(int n, double w, const double* __restrict__ dinv,
-                              const double* __restrict__ b, double* __restrict__ x) {
+__global__ void k_csr_smooth0(int n, double w, const CV* __restrict__ dinv,
+                              const CV* __restrict__ b, CV* __restrict__ x) {
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = w * dinv[i] * b[i];
@@ -341,18 +342,18 @@ __global__ void k_sell_gather(long long n, const int32_t* __restrict__ map, cons
 template <int XM>
 __global__ void k_sell_x(int n, double w, double alpha, const int32_t* __restrict__ sp,
                          const int32_t* __restrict__ sc, const float* __restrict__ sv,
-                         const double* __restrict__ dinv, const double* __restrict__ b,
-                         const double* __restrict__ x, const int32_t* __restrict__ parent,
-                         const double* __restrict__ xc, double* __restrict__ y, int resid,
-                         double* __restrict__ x0) {
+                         const CV* __restrict__ dinv, const CV* __restrict__ b,
+                         const CV* __restrict__ x, const int32_t* __restrict__ parent,
+                         const CV* __restrict__ xc, CV* __restrict__ y, int resid,
+                         CV* __restrict__ x0) {
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int slice = i >> 5;
   if (slice * 32 >= n) return;
   auto xin = [&](int j) -> double {
-    if (XM == 0) return x[j];
-    if (XM == 1) return w * dinv[j] * b[j];
-    return x[j] + alpha * xc[parent[j]];
+    if (XM == 0) return (double)x[j];
+    if (XM == 1) return w * (double)dinv[j] * (double)b[j];
+    return (double)x[j] + alpha * (double)xc[parent[j]];
   };
   const int base = sp[slice], width = (sp[slice + 1] - base) >> 5;
   const int r = i & 31;
@@ -373,9 +374,9 @@ __global__ void k_sell_x(int n, double w, double alpha, const int32_t* __restric
   }
   for (; k < width; ++k, cp += 32, vp += 32) s += (double)*vp * xin(*cp);
   if (i < n) {
-    const double xi = xin(i);
-    y[i] = resid ? b[i] - s : xi + w * dinv[i] * (b[i] - s);
-    if (x0) x0[i] = xi;
+    const double xi = xin(i), bi = b[i];
+    y[i] = (CV)(resid ? bi - s : xi + w * (double)dinv[i] * (bi - s));
+    if (x0) x0[i] = (CV)xi;
   }
 }
 
@@ -383,8 +384,8 @@ __global__ void k_sell_x(int n, double w, double alpha, const int32_t* __restric
 template <int VS, class VT>
 __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
                                const int32_t* __restrict__ cl, const VT* __restrict__ v,
-                               const double* __restrict__ dinv, const double* __restrict__ b,
-                               const double* __restrict__ x, double* __restrict__ y, int resid) {
+                               const CV* __restrict__ dinv, const CV* __restrict__ b,
+                               const CV* __restrict__ x, CV* __restrict__ y, int resid) {
   pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int i = (int)(gt / VS), lane = (int)(gt % VS);
@@ -396,14 +397,14 @@ __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
   for (; k + VS < k1; k += 2 * VS) {   // two independent gathers in flight per lane
     const int c0 = cl[k], c1 = cl[k + VS];
     const double a0 = (double)v[k], a1 = (double)v[k + VS];
-    s += a0 * x[c0];
-    s2 += a1 * x[c1];
+    s += a0 * (double)x[c0];
+    s2 += a1 * (double)x[c1];
   }
-  if (k < k1) s += (double)v[k] * x[cl[k]];
+  if (k < k1) s += (double)v[k] * (double)x[cl[k]];
   s += s2;
 #pragma unroll
   for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
-  if (lane == 0) y[i] = resid ? b[i] - s : x[i] + w * dinv[i] * (b[i] - s);
+  if (lane == 0) y[i] = (CV)(resid ? (double)b[i] - s : (double)x[i] + w * (double)dinv[i] * ((double)b[i] - s));
 }
 
 // Generalized sweep: y = xin + w D^-1 (b - A xin)  (resid: y = b - A xin) where the
@@ -415,18 +416,18 @@ __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
 template <int VS, class VT, int XM>
 __global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict__ rp,
                         const int32_t* __restrict__ cl, const VT* __restrict__ v,
-                        const double* __restrict__ dinv, const double* __restrict__ b,
-                        const double* __restrict__ x, const int32_t* __restrict__ parent,
-                        const double* __restrict__ xc, double* __restrict__ y, int resid,
-                        double* __restrict__ x0) {
+                        const CV* __restrict__ dinv, const CV* __restrict__ b,
+                        const CV* __restrict__ x, const int32_t* __restrict__ parent,
+                        const CV* __restrict__ xc, CV* __restrict__ y, int resid,
+                        CV* __restrict__ x0) {
   pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int i = (int)(gt / VS), lane = (int)(gt % VS);
   if (i >= n) return;
   auto xin = [&](int j) -> double {
-    if (XM == 0) return x[j];
-    if (XM == 1) return w * dinv[j] * b[j];
-    return x[j] + alpha * xc[parent[j]];
+    if (XM == 0) return (double)x[j];
+    if (XM == 1) return w * (double)dinv[j] * (double)b[j];
+    return (double)x[j] + alpha * (double)xc[parent[j]];
   };
   double s = 0.0;
   // four nonzeros per trip with all index / value loads issued before the gathers (the
@@ -447,35 +448,36 @@ __global__ void k_csr_x(int n, double w, double alpha, const int32_t* __restrict
 #pragma unroll
   for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
   if (lane == 0) {
-    const double xi = xin(i);
-    y[i] = resid ? b[i] - s : xi + w * dinv[i] * (b[i] - s);
-    if (x0) x0[i] = xi;   // residual of the zero-guess iterate: also store that iterate
+    const double xi = xin(i), bi = b[i];
+    y[i] = (CV)(resid ? bi - s : xi + w * (double)dinv[i] * (bi - s));
+    if (x0) x0[i] = (CV)xi;   // residual of the zero-guess iterate: also store that iterate
   }
 }
 
 template <class TV>
 __global__ void k_csr_prolong(int n, double alpha, const int32_t* __restrict__ prp,
                               const int32_t* __restrict__ pci, const TV* __restrict__ pv,
-                              const double* __restrict__ xn, double* __restrict__ x) {
+                              const CV* __restrict__ xn, CV* __restrict__ x) {
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
-  for (int m = prp[i]; m < prp[i + 1]; ++m) s += (double)pv[m] * xn[pci[m]];
-  x[i] += alpha * s;
+  for (int m = prp[i]; m < prp[i + 1]; ++m) s += (double)pv[m] * (double)xn[pci[m]];
+  x[i] = (CV)((double)x[i] + alpha * s);
 }
 
-__global__ void k_vec_add(int n, const double* __restrict__ a, double* __restrict__ x) {
+__global__ void k_vec_add(int n, const CV* __restrict__ a, CV* __restrict__ x) {
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] += a[i];
+  if (i < n) x[i] = (CV)((double)x[i] + (double)a[i]);
 }
 
-// b[I] = sum_q ptv[q] res[pt_row[q]] (P^T res), 8 lanes per coarse row
-template <class TV>
+// b[I] = sum_q ptv[q] res[pt_row[q]] (P^T res), 8 lanes per coarse row; res is the fine
+// level's fp64 residual (RT double) or a coarse level's (RT = CV)
+template <class TV, class RT>
 __global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
                              const int32_t* __restrict__ pt_row, const TV* __restrict__ ptv,
-                             const double* __restrict__ res, double* __restrict__ b1) {
+                             const RT* __restrict__ res, CV* __restrict__ b1) {
   pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int I = (int)(gt >> 3), lane = (int)(gt & 7);
@@ -490,11 +492,11 @@ __global__ void k_restrict_v(int n1, const int32_t* __restrict__ pt_ptr,
     s += a0 * x0;
     s += a1 * x1;
   }
-  for (; q < q1; q += 8) s += (double)ptv[q] * res[pt_row[q]];
+  for (; q < q1; q += 8) s += (double)ptv[q] * (double)res[pt_row[q]];
   s += __shfl_down_sync(0xffffffffu, s, 4, 8);
   s += __shfl_down_sync(0xffffffffu, s, 2, 8);
   s += __shfl_down_sync(0xffffffffu, s, 1, 8);
-  if (lane == 0) b1[I] = s;
+  if (lane == 0) b1[I] = (CV)s;
 }
 // fused residual + restriction for a tentative prolongator: b1[I] = sum of b over the
 // aggregate's members - (R x)_I with R = P^T A (VS lanes per coarse row)
@@ -502,8 +504,8 @@ template <int VS, class VT>
 __global__ void k_resid_restrict(int n1, const int32_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_row,
                                  const int32_t* __restrict__ rrp, const int32_t* __restrict__ rci,
                                  const VT* __restrict__ rv, const VT* __restrict__ ptv,
-                                 const double* __restrict__ b, const double* __restrict__ x,
-                                 double* __restrict__ b1) {
+                                 const CV* __restrict__ b, const CV* __restrict__ x,
+                                 CV* __restrict__ b1) {
   pdl_wait();
   long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int I = (int)(gt / VS), lane = (int)(gt % VS);
@@ -521,12 +523,12 @@ __global__ void k_resid_restrict(int n1, const int32_t* __restrict__ pt_ptr, con
       s -= a2 * x2;
       s -= a3 * x3;
     }
-    for (; k < k1; k += VS) s -= (double)rv[k] * x[rci[k]];
-    for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += VS) s += (double)ptv[q] * b[pt_row[q]];
+    for (; k < k1; k += VS) s -= (double)rv[k] * (double)x[rci[k]];
+    for (int q = pt_ptr[I] + lane; q < pt_ptr[I + 1]; q += VS) s += (double)ptv[q] * (double)b[pt_row[q]];
   }
 #pragma unroll
   for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
-  if (ok && lane == 0) b1[I] = s;
+  if (ok && lane == 0) b1[I] = (CV)s;
 }
 
 __global__ void k_gather_ptv(long long n, const int32_t* __restrict__ pt_idx,
@@ -854,7 +856,7 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
   for (size_t l = 1; l < B.levels.size(); ++l) {
     AmgLevel& L = B.levels[l];
     int m = std::max(L.n, 1);
-    L.x.alloc(m); L.x2.alloc(m); L.b.alloc(m); L.res.alloc(m); L.acc.alloc(m);
+    L.x.alloc(m); L.x2.alloc(m); L.b.alloc(m); L.res.alloc(m); L.acc.alloc(m); L.dinvc.alloc(m);
   }
   int nc = B.levels.back().n;
   if (nc > HC_COARSE_MAX)
@@ -882,7 +884,7 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
       c.rp = L.A.rp.p; c.ci = L.A.ci.p;
       c.vf = cfg.fp32_coarse ? L.A.vf.p : nullptr;
       c.vd = L.A.v.p;
-      c.dinv = L.dinv.p;
+      c.dinv = L.dinvc.p;
       c.b = L.b.p; c.x = L.x.p; c.x2 = L.x2.p; c.res = L.res.p;
       c.tentative = L.P.nnz == (long long)L.n;
       c.parent = L.parent.p;
@@ -973,7 +975,7 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
       AmgLevel& L = B.levels[l];
       AmgLevel& U = B.levels[l + 1];
       if (l > 0) {
-        launch(k_dinv, nblk(L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p); HC_COUNT();
+        launch(k_dinv, nblk(L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.dinv.p, L.dinvc.p); HC_COUNT();
       }
       launch(k_smooth_P, nblk(L.n), TPB, 0, s, L.n, (int)L.smoothed, A.omega_p, L.A.rp.p, L.A.ci.p,
                                            L.A.v.p, L.dinv.p, L.parent.p, L.P.rp.p, L.P.ci.p,
@@ -1010,7 +1012,7 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
     }
     AmgLevel& C = B.levels.back();
     if (B.levels.size() > 1) {
-      launch(k_dinv, nblk(C.n), TPB, 0, s, C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, C.dinv.p); HC_COUNT();
+      launch(k_dinv, nblk(C.n), TPB, 0, s, C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, C.dinv.p, C.dinvc.p); HC_COUNT();
     }
     launch(k_dense_from_csr, nblk(C.n), TPB, 0, s, C.n, C.A.rp.p, C.A.ci.p, C.A.v.p, B.dense.p); HC_COUNT();
     size_t smem = (size_t)C.n * C.n * sizeof(double) + (size_t)C.n * sizeof(int);
@@ -1037,17 +1039,17 @@ namespace {
 constexpr int CC_THREADS = 1024;
 
 template <int XM>
-__device__ void cc_sweep(const CoarseLev& L, int gt, int gn, double w, double alpha, const double* x,
-                         const double* xc, double* y, int resid) {
+__device__ void cc_sweep(const CoarseLev& L, int gt, int gn, double w, double alpha, const CV* x,
+                         const CV* xc, CV* y, int resid) {
   const int lane = gt & 7;
   // warp-uniform trip count (the 8-lane shuffles need all 32 lanes of the warp)
   for (int i0 = (gt >> 5) * 4; i0 < L.n; i0 += (gn >> 5) * 4) {
     const int i = i0 + ((gt & 31) >> 3);
     const bool ok = i < L.n;
     auto xin = [&](int j) -> double {
-      if (XM == 0) return __ldcg(x + j);
-      if (XM == 1) return w * L.dinv[j] * __ldcg(L.b + j);
-      return __ldcg(x + j) + alpha * __ldcg(xc + L.parent[j]);
+      if (XM == 0) return (double)__ldcg(x + j);
+      if (XM == 1) return w * (double)L.dinv[j] * (double)__ldcg(L.b + j);
+      return (double)__ldcg(x + j) + alpha * (double)__ldcg(xc + L.parent[j]);
     };
     double s = 0.0;
     if (ok)
@@ -1058,7 +1060,7 @@ __device__ void cc_sweep(const CoarseLev& L, int gt, int gn, double w, double al
     s += __shfl_down_sync(0xffffffffu, s, 1, 8);
     if (ok && lane == 0) {
       const double bi = __ldcg(L.b + i);
-      y[i] = resid ? bi - s : xin(i) + w * L.dinv[i] * (bi - s);
+      y[i] = (CV)(resid ? bi - s : xin(i) + w * (double)L.dinv[i] * (bi - s));
     }
   }
 }
@@ -1070,8 +1072,8 @@ k_coarse_cycle(const CoarseLev* __restrict__ levs, int nlev, const double* __res
   cg::cluster_group cl = cg::this_cluster();
   const int gt = (int)cl.block_rank() * blockDim.x + threadIdx.x;
   const int gn = (int)cl.num_blocks() * blockDim.x;
-  __shared__ double* xs[16];     // current / scratch iterate per level (uniform pointer swaps)
-  __shared__ double* x2s[16];
+  __shared__ CV* xs[16];     // current / scratch iterate per level (uniform pointer swaps)
+  __shared__ CV* x2s[16];
   if (threadIdx.x < nlev) {
     xs[threadIdx.x] = levs[threadIdx.x].x;
     x2s[threadIdx.x] = levs[threadIdx.x].x2;
@@ -1080,20 +1082,20 @@ k_coarse_cycle(const CoarseLev* __restrict__ levs, int nlev, const double* __res
   // down: pre-smoothing from the zero guess, residual, restriction
   for (int l = 0; l + 1 < nlev; ++l) {
     const CoarseLev L = levs[l];
-    double*& x = xs[l];
-    double*& x2 = x2s[l];
+    CV*& x = xs[l];
+    CV*& x2 = x2s[l];
     if (nu >= 2) {
       cc_sweep<1>(L, gt, gn, w, 0.0, nullptr, nullptr, x, 0);
       cl.sync();
       for (int k = 2; k < nu; ++k) {
         cc_sweep<0>(L, gt, gn, w, 0.0, x, nullptr, x2, 0);
         cl.sync();
-        if (threadIdx.x == 0) { double* t = x; x = x2; x2 = t; }
+        if (threadIdx.x == 0) { CV* t = x; x = x2; x2 = t; }
         __syncthreads();
       }
       cc_sweep<0>(L, gt, gn, 0.0, 0.0, x, nullptr, L.res, 1);
     } else {
-      for (int i = gt; i < L.n; i += gn) x[i] = w * L.dinv[i] * __ldcg(L.b + i);
+      for (int i = gt; i < L.n; i += gn) x[i] = (CV)(w * (double)L.dinv[i] * (double)__ldcg(L.b + i));
       cl.sync();
       cc_sweep<1>(L, gt, gn, w, 0.0, nullptr, nullptr, L.res, 1);
     }
@@ -1104,11 +1106,11 @@ k_coarse_cycle(const CoarseLev* __restrict__ levs, int nlev, const double* __res
       const int I = I0 + ((gt & 31) >> 3);
       double s = 0.0;
       if (I < U.n)
-        for (int q = L.pt_ptr[I] + lane; q < L.pt_ptr[I + 1]; q += 8) s += L.ptv[q] * __ldcg(L.res + L.pt_row[q]);
+        for (int q = L.pt_ptr[I] + lane; q < L.pt_ptr[I + 1]; q += 8) s += L.ptv[q] * (double)__ldcg(L.res + L.pt_row[q]);
       s += __shfl_down_sync(0xffffffffu, s, 4, 8);
       s += __shfl_down_sync(0xffffffffu, s, 2, 8);
       s += __shfl_down_sync(0xffffffffu, s, 1, 8);
-      if (I < U.n && lane == 0) U.b[I] = s;
+      if (I < U.n && lane == 0) U.b[I] = (CV)s;
     }
     cl.sync();
   }
@@ -1117,37 +1119,37 @@ k_coarse_cycle(const CoarseLev* __restrict__ levs, int nlev, const double* __res
     const int lane = gt & 31;
     for (int row = gt >> 5; row < C.n; row += gn >> 5) {
       double s = 0.0;
-      for (int j = lane; j < C.n; j += 32) s += dense_inv[row * C.n + j] * __ldcg(C.b + j);
+      for (int j = lane; j < C.n; j += 32) s += dense_inv[row * C.n + j] * (double)__ldcg(C.b + j);
       for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-      if (lane == 0) xs[nlev - 1][row] = s;
+      if (lane == 0) xs[nlev - 1][row] = (CV)s;
     }
     cl.sync();
   }
   // up: coarse correction (fused into the first post-sweep for tentative prolongators)
   for (int l = nlev - 2; l >= 0; --l) {
     const CoarseLev L = levs[l];
-    double*& x = xs[l];
-    double*& x2 = x2s[l];
-    const double* xc = xs[l + 1];
+    CV*& x = xs[l];
+    CV*& x2 = x2s[l];
+    const CV* xc = xs[l + 1];
     int post = nu;
     if (L.tentative && post >= 1) {
       cc_sweep<2>(L, gt, gn, w, alpha, x, xc, x2, 0);
       cl.sync();
-      if (threadIdx.x == 0) { double* t = x; x = x2; x2 = t; }
+      if (threadIdx.x == 0) { CV* t = x; x = x2; x2 = t; }
       __syncthreads();
       --post;
     } else {
       for (int i = gt; i < L.n; i += gn) {
         double s = 0.0;
-        for (int m = L.prp[i]; m < L.prp[i + 1]; ++m) s += L.pv[m] * __ldcg(xc + L.pci[m]);
-        x[i] = __ldcg(x + i) + alpha * s;
+        for (int m = L.prp[i]; m < L.prp[i + 1]; ++m) s += L.pv[m] * (double)__ldcg(xc + L.pci[m]);
+        x[i] = (CV)((double)__ldcg(x + i) + alpha * s);
       }
       cl.sync();
     }
     for (int k = 0; k < post; ++k) {
       cc_sweep<0>(L, gt, gn, w, 0.0, x, nullptr, x2, 0);
       cl.sync();
-      if (threadIdx.x == 0) { double* t = x; x = x2; x2 = t; }
+      if (threadIdx.x == 0) { CV* t = x; x = x2; x2 = t; }
       __syncthreads();
     }
   }
@@ -1198,15 +1200,15 @@ static void coarse_cycle_launch(const Amg& A, AmgBlock& B, cudaStream_t s) {
 static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s);
 
 // y = x + w D^-1 (b - A x)  or  (resid) y = b - A x, with lanes-per-row from the density
-static void csr_sweep(const Amg& A, const AmgLevel& L, double w, const double* b, const double* x,
-                      double* y, int resid, cudaStream_t s) {
+static void csr_sweep(const Amg& A, const AmgLevel& L, double w, const CV* b, const CV* x,
+                      CV* y, int resid, cudaStream_t s) {
   double avg = L.n ? (double)L.A.nnz / L.n : 0.0;
   const bool f32 = A.fp32_coarse;
   auto go = [&](auto vs_tag, auto* vals) {
     constexpr int VS = decltype(vs_tag)::value;
     using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
     launch(k_csr_jacobi_v<VS, VT>, nblk((long long)VS * L.n), TPB, 0, s, L.n, w, L.A.rp.p, L.A.ci.p, vals,
-                                                                      L.dinv.p, b, x, y, resid);
+                                                                      L.dinvc.p, b, x, y, resid);
     HC_COUNT();
   };
   if (avg <= 12.0) {
@@ -1223,12 +1225,12 @@ static void csr_sweep(const Amg& A, const AmgLevel& L, double w, const double* b
 
 // generalized sweep launcher (see k_csr_x)
 template <int XM>
-static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha, const double* b,
-                        const double* x, const int32_t* parent, const double* xc, double* y,
-                        int resid, cudaStream_t s, double* x0 = nullptr) {
+static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha, const CV* b,
+                        const CV* x, const int32_t* parent, const CV* xc, CV* y,
+                        int resid, cudaStream_t s, CV* x0 = nullptr) {
   if (A.fp32_coarse && L.A.sl_n) {
     launch(k_sell_x<XM>, nblk(L.n), TPB, 0, s, L.n, w, alpha, L.A.sl_ptr.p, L.A.sl_col.p,
-           (const float*)L.A.sl_vf.p, L.dinv.p, b, x, parent, xc, y, resid, x0);
+           (const float*)L.A.sl_vf.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
     HC_COUNT();
     return;
   }
@@ -1238,7 +1240,7 @@ static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha,
     constexpr int VS = decltype(vs_tag)::value;
     using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;
     launch(k_csr_x<VS, VT, XM>, nblk((long long)VS * L.n), TPB, 0, s, 
-        L.n, w, alpha, L.A.rp.p, L.A.ci.p, vals, L.dinv.p, b, x, parent, xc, y, resid, x0);
+        L.n, w, alpha, L.A.rp.p, L.A.ci.p, vals, L.dinvc.p, b, x, parent, xc, y, resid, x0);
     HC_COUNT();
   };
   const float* vf = L.A.vf.p;
@@ -1289,10 +1291,10 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
       csr_sweep_x<1>(A, L, w, 0.0, L.b.p, nullptr, nullptr, nullptr, L.res.p, 1, s, L.x.p);
     }
     if (A.fp32_coarse)
-      launch(k_restrict_v<float>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p,
+      launch(k_restrict_v<float, CV>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p,
              (const float*)L.ptvf.p, L.res.p, U.b.p);
     else
-      launch(k_restrict_v<double>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p,
+      launch(k_restrict_v<double, CV>, nblk(8LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p,
              (const double*)L.ptv.p, L.res.p, U.b.p);
     HC_COUNT();
   }
@@ -1333,7 +1335,7 @@ static void solve_level(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   cycle_once(A, B, l, s);
   int g = ((int)l >= A.wmin && (int)l <= A.wdepth) ? A.gamma : 1;
   for (int k = 1; k < g; ++k) {
-    HC_CUDA(cudaMemcpyAsync(L.acc.p, L.x.p, L.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    HC_CUDA(cudaMemcpyAsync(L.acc.p, L.x.p, L.n * sizeof(CV), cudaMemcpyDeviceToDevice, s));
     csr_sweep(A, L, 0.0, L.b.p, L.acc.p, L.res.p, 1, s);
     std::swap(L.b.p, L.res.p);
     cycle_once(A, B, l, s);
@@ -1359,7 +1361,7 @@ __global__ void k_smooth0_s2(long long n, double w, const double* __restrict__ d
 template <class TV>
 __global__ void k_prolong0_s(long long n, double alpha, const int32_t* __restrict__ prp,
                              const int32_t* __restrict__ pci, const TV* __restrict__ pv,
-                             const double* __restrict__ x1, double* __restrict__ e) {
+                             const CV* __restrict__ x1, double* __restrict__ e) {
   pdl_wait();
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= n) return;
@@ -1443,10 +1445,10 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   }
   if (B.nu >= 2) sweep(EP_RESID, e, res);
   if (A.fp32_coarse)
-    launch(k_restrict_v<float>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const float*)L0.ptvf.p,
+    launch(k_restrict_v<float, double>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const float*)L0.ptvf.p,
            res, L1.b.p);
   else
-  launch(k_restrict_v<double>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const double*)L0.ptv.p, res,
+  launch(k_restrict_v<double, double>, nblk(8LL * L1.n), TPB, 0, s, L1.n, L0.pt_ptr.p, L0.pt_row.p, (const double*)L0.ptv.p, res,
                                                 L1.b.p); HC_COUNT();
   solve_level(A, B, 1, s);
   if (A.fp32_coarse)

@@ -7,6 +7,11 @@
 
 namespace hc {
 
+// element type of the coarse-level cycle vectors (levels >= 1: iterates, right-hand
+// sides, residuals, D^-1); sums are accumulated in fp64, the vectors stored in fp32 (the
+// preconditioner needs no more; the Krylov method works in fp64)
+using CV = float;
+
 struct Csr {
   int n = 0;
   long long nnz = 0;
@@ -38,7 +43,8 @@ struct AmgLevel {
   DBuf<int32_t> pt_ptr, pt_row, pt_idx;  // P^T: for each coarse unknown, (row, value index) pairs
   DBuf<double> ptv;                      // P^T values (gathered after every setup)
   DBuf<float> ptvf;                      // fp32 copy used by the cycle's restriction
-  DBuf<double> x, x2, b, res, acc;       // cycle vectors (levels >= 1)
+  DBuf<CV> x, x2, b, res, acc;           // cycle vectors (levels >= 1)
+  DBuf<CV> dinvc;                        // D^-1 for the cycle (levels >= 1)
 };
 
 // device view of one CSR level for the cluster-fused coarse cycle (hc_amg.cu)
@@ -47,8 +53,8 @@ struct CoarseLev {
   const int32_t *rp, *ci;
   const float* vf;              // fp32 values (or null: vd)
   const double* vd;
-  const double* dinv;
-  double *b, *x, *x2, *res;
+  const CV* dinv;
+  CV *b, *x, *x2, *res;
   int tentative;                // prolongator is the tentative one (one entry of 1 per row)
   const int32_t* parent;
   const int32_t *prp, *pci;
