@@ -337,9 +337,11 @@ __global__ void k_sell_gather(long long n, const int32_t* __restrict__ map, cons
   }
 }
 
-// The k_csr_x sweep on the sliced-ELL copy: one thread per row, a warp per 32-row slice
-// (uniform trip count), entries in the row's CSR order
-template <int XM>
+// The k_csr_x sweep on the sliced-ELL copy: T lanes per row, a warp per slice of 32 / T
+// rows; entry j of slice row r sits at base + ((j / T) * (32 / T) + r) * T + j % T, so every
+// k-step of the warp is one coalesced 32-entry load and the rows' k-th columns (mostly
+// consecutive) are gathered together; the T partial sums are combined by shuffles
+template <int T, int XM>
 __global__ void k_sell_x(int n, double w, double alpha, const int32_t* __restrict__ sp,
                          const int32_t* __restrict__ sc, const float* __restrict__ sv,
                          const CV* __restrict__ dinv, const CV* __restrict__ b,
@@ -347,18 +349,20 @@ __global__ void k_sell_x(int n, double w, double alpha, const int32_t* __restric
                          const CV* __restrict__ xc, CV* __restrict__ y, int resid,
                          CV* __restrict__ x0) {
   pdl_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int slice = i >> 5;
-  if (slice * 32 >= n) return;
+  constexpr int R = 32 / T;   // rows per slice
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int slice = (int)(gt >> 5);
+  if ((long long)slice * R >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int i = slice * R + lane / T;
   auto xin = [&](int j) -> double {
     if (XM == 0) return (double)x[j];
     if (XM == 1) return w * (double)dinv[j] * (double)b[j];
     return (double)x[j] + alpha * (double)xc[parent[j]];
   };
-  const int base = sp[slice], width = (sp[slice + 1] - base) >> 5;
-  const int r = i & 31;
-  const int32_t* cp = sc + base + r;
-  const float* vp = sv + base + r;
+  const int base = sp[slice], width = (sp[slice + 1] - base) >> 5;   // k-steps of 32 entries
+  const int32_t* cp = sc + base + lane;
+  const float* vp = sv + base + lane;
   double s = 0.0;
   int k = 0;
   for (; k + 3 < width; k += 4) {
@@ -373,7 +377,9 @@ __global__ void k_sell_x(int n, double w, double alpha, const int32_t* __restric
     vp += 128;
   }
   for (; k < width; ++k, cp += 32, vp += 32) s += (double)*vp * xin(*cp);
-  if (i < n) {
+#pragma unroll
+  for (int o = T / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, T);
+  if (lane % T == 0 && i < n) {
     const double xi = xin(i), bi = b[i];
     y[i] = (CV)(resid ? bi - s : xi + w * (double)dinv[i] * (bi - s));
     if (x0) x0[i] = (CV)xi;
@@ -590,33 +596,37 @@ void upload_csr(Csr& c, const HPat& p) {
 
 }  // namespace
 
-// sliced-ELL pattern (see Csr::sl_*) from a host CSR pattern
-static void build_sell(Csr& c, const HPat& p) {
-  const int n = p.n(), ns = (n + 31) / 32;
+// sliced-ELL pattern (see Csr::sl_*, k_sell_x) with T lanes per row from a host CSR pattern
+static void build_sell(Csr& c, const HPat& p, int T) {
+  const int R = 32 / T;
+  const int n = p.n(), ns = (n + R - 1) / R;
   std::vector<int32_t> ptr(ns + 1, 0);
   for (int sl = 0; sl < ns; ++sl) {
     int wmax = 0;
-    for (int r = sl * 32; r < std::min(n, sl * 32 + 32); ++r) wmax = std::max(wmax, p.rp[r + 1] - p.rp[r]);
-    ptr[sl + 1] = ptr[sl] + 32 * wmax;
+    for (int r = sl * R; r < std::min(n, sl * R + R); ++r) wmax = std::max(wmax, p.rp[r + 1] - p.rp[r]);
+    ptr[sl + 1] = ptr[sl] + 32 * ((wmax + T - 1) / T);
   }
   std::vector<int32_t> col(ptr[ns]), map(ptr[ns]);
   for (int sl = 0; sl < ns; ++sl) {
     const int width = (ptr[sl + 1] - ptr[sl]) / 32;
-    for (int r = 0; r < 32; ++r) {
-      const int i = sl * 32 + r;
+    for (int r = 0; r < R; ++r) {
+      const int i = sl * R + r;
       const int len = i < n ? p.rp[i + 1] - p.rp[i] : 0;
-      for (int k = 0; k < width; ++k) {
-        const int q = ptr[sl] + k * 32 + r;
-        if (k < len) {
-          col[q] = p.ci[p.rp[i] + k];
-          map[q] = p.rp[i] + k;
-        } else {
-          col[q] = i < n ? i : 0;
-          map[q] = -1;
+      for (int k = 0; k < width; ++k)
+        for (int t = 0; t < T; ++t) {
+          const int j = k * T + t;
+          const int q = ptr[sl] + (k * R + r) * T + t;
+          if (j < len) {
+            col[q] = p.ci[p.rp[i] + j];
+            map[q] = p.rp[i] + j;
+          } else {
+            col[q] = i < n ? i : 0;
+            map[q] = -1;
+          }
         }
-      }
     }
   }
+  c.sl_t = T;
   upload(c.sl_ptr, ptr);
   upload(c.sl_col, col);
   upload(c.sl_map, map);
@@ -685,9 +695,15 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     const int n = A.n();
     L.n = n;
     upload_csr(L.A, A);
-    if (level >= 1 && cfg.sell_max_avg > 0 && n >= cfg.sell_min_rows &&
-        (double)A.ci.size() <= (double)cfg.sell_max_avg * n)
-      build_sell(L.A, A);
+    if (level >= 1 && cfg.sell_max_avg > 0 && n > 0) {
+      // lanes per row: enough that each lane keeps ~sell_lane_nnz entries, and enough
+      // threads in flight (n T >= sell_min_rows) for the sliced copy to pay
+      const double avg = (double)A.ci.size() / n;
+      int T = 1;
+      while (T < 32 && avg / T > cfg.sell_lane_nnz) T *= 2;
+      if (cfg.sell_force_t) T = cfg.sell_force_t;
+      if ((long long)n * T >= cfg.sell_min_rows && avg <= cfg.sell_max_avg) build_sell(L.A, A, T);
+    }
     L.dinv.alloc(std::max(n, 1));
     int active = 0;
     for (int i = 0; i < n; ++i) active += A.rp[i + 1] > A.rp[i];
@@ -928,6 +944,8 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_SELL")) amg->sell_max_avg = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_FILTER")) amg->sa_filter = atoi(e);
   if (const char* e = getenv("HC_AMG_SELL_ROWS")) amg->sell_min_rows = atoi(e);
+  if (const char* e = getenv("HC_AMG_SELL_LANE")) amg->sell_lane_nnz = atof(e);
+  if (const char* e = getenv("HC_AMG_SELL_T")) amg->sell_force_t = atoi(e);
   auto t0 = std::chrono::steady_clock::now();
   for (int f = 0; f < 2; ++f) {
     amg->blk[f].nu = amg->nu;
@@ -1229,9 +1247,21 @@ static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha,
                         const CV* x, const int32_t* parent, const CV* xc, CV* y,
                         int resid, cudaStream_t s, CV* x0 = nullptr) {
   if (A.fp32_coarse && L.A.sl_n) {
-    launch(k_sell_x<XM>, nblk(L.n), TPB, 0, s, L.n, w, alpha, L.A.sl_ptr.p, L.A.sl_col.p,
-           (const float*)L.A.sl_vf.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
-    HC_COUNT();
+    auto go = [&](auto t_tag) {
+      constexpr int T = decltype(t_tag)::value;
+      const long long threads = ((long long)L.n + 32 / T - 1) / (32 / T) * 32;
+      launch(k_sell_x<T, XM>, nblk(threads), TPB, 0, s, L.n, w, alpha, L.A.sl_ptr.p, L.A.sl_col.p,
+             (const float*)L.A.sl_vf.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
+      HC_COUNT();
+    };
+    switch (L.A.sl_t) {
+      case 1: go(std::integral_constant<int, 1>{}); break;
+      case 2: go(std::integral_constant<int, 2>{}); break;
+      case 4: go(std::integral_constant<int, 4>{}); break;
+      case 8: go(std::integral_constant<int, 8>{}); break;
+      case 16: go(std::integral_constant<int, 16>{}); break;
+      default: go(std::integral_constant<int, 32>{}); break;
+    }
     return;
   }
   double avg = L.n ? (double)L.A.nnz / L.n : 0.0;

@@ -23,6 +23,7 @@ struct Csr {
   // read by one coalesced load, and their columns are mostly consecutive, so the x gathers
   // touch few sectors.  Padding entries hold column = row and value 0.
   int sl_n = 0;                    // rows (0: no sliced copy)
+  int sl_t = 1;                    // lanes per row
   DBuf<int32_t> sl_ptr, sl_col;    // slice offsets [n / 32 + 1], columns
   DBuf<int32_t> sl_map;            // CSR position of every sliced entry, -1 for padding
   DBuf<float> sl_vf;               // values, gathered from vf after every numeric setup
@@ -113,9 +114,13 @@ struct Amg {
   int coarsen = 2;           // block growth factor of the transfers above level 1              // gamma cycles on CSR levels wmin..wdepth
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int sa_filter = 0;         // bit l: filtered smoothing of the phi transfer from level l
-  int sell_max_avg = 48;     // levels with at most this many nonzeros per row (and >= sell_min_rows
-  int sell_min_rows = 131072; // rows) sweep through the sliced-ELL copy (0: off); measured: large cell
-                             // 88.0 -> 83.7 ms per step, medium cell (70 k-row level) 20.2 -> 21.4 at 16 k
+  int sell_max_avg = 512;    // levels with at most this many nonzeros per row and at least
+  int sell_min_rows = 131072; // sell_min_rows threads (rows x lanes per row) sweep through the
+                              // sliced-ELL copy (0: off); measured at one lane per row: large cell
+                              // 88.0 -> 83.7 ms per step, medium (70 k-row level) 20.2 -> 21.4 at 16 k;
+                              // with 4 lanes per row on phi level 2 (183 nonzeros): 76.9 -> 75.7
+  double sell_lane_nnz = 48;  // lanes per row: the smallest power of two with <= this many entries per lane
+  int sell_force_t = 0;       // force the lanes per row (0: by the rule above)
   int refresh = 0;          // numeric setup every Newton iteration (1) or once per solve (0)
   int refresh_solves = 32;  // rebuild once every this many Newton solves (and when dt changes);
                             // 400-step medium / 200-step large runs: same Krylov totals as 8, 2-3 % faster
