@@ -10,7 +10,7 @@ namespace hc {
 // element type of the coarse-level cycle vectors (levels >= 1: iterates, right-hand
 // sides, residuals, D^-1); sums are accumulated in fp64, the vectors stored in fp32 (the
 // preconditioner needs no more; the Krylov method works in fp64)
-using CV = float;
+using CV = double;
 
 struct Csr {
   int n = 0;

@@ -243,7 +243,8 @@ struct Operator {
 
   DBuf<uint8_t> labels;        // [nvox]
   DBuf<int32_t> lab4;          // labels widened to 32 bit (cp.async staging)
-  DBuf<int32_t> labt;          // TMA label word: (phase + 1) | (rank + 1) << 3, 0 = outside
+  DBuf<int32_t> labt;          // TMA face word (hc_tma.cuh), 0 = outside
+  DBuf<int2> if_fslot;         // TMA stencil: per interface face, its slot on the solid / electrolyte side
   TmaCache* tma = nullptr;     // tensor maps of the TMA stencils
   DBuf<int32_t> cdof, pdof;    // [nvox], -1 where absent
   DBuf<int32_t> c_vox, p_vox;  // packed index -> voxel

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(TPB) k_residual_iface(
 // +i, electrolyte -i), for the TMA residual stencil to gather: no atomics.
 __global__ void __launch_bounds__(TPB) k_residual_islot(
     DevParams P, long long n_if, const int32_t* __restrict__ so, const int32_t* __restrict__ el,
-    const int32_t* __restrict__ slot, const int8_t* __restrict__ kind, const int32_t* __restrict__ labt,
+    const int32_t* __restrict__ slot, const int8_t* __restrict__ kind, const int2* __restrict__ fslot,
     const double2* __restrict__ X, const double* __restrict__ npl, double beta,
     double* __restrict__ islot) {
   long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -315,12 +315,9 @@ __global__ void __launch_bounds__(TPB) k_residual_islot(
     i = strip_current_dev(xe.x, xs.y, xe.y, npl[slot[f]], beta, P, nullptr, nullptr);
   }
   const double q = P.sc * i;
-  auto slot_of = [&](int v, int d) -> long long {
-    const unsigned w = (unsigned)labt[v];
-    return (long long)(w >> 9) + __popc(((w >> 3) & 63u) & ((1u << d) - 1u));
-  };
-  islot[slot_of(s, dir_to(P, s, e))] = q;
-  islot[slot_of(e, dir_to(P, e, s))] = -q;
+  const int2 fs = fslot[f];
+  islot[fs.x] = q;
+  islot[fs.y] = -q;
 }
 
 // Stripping current of every stripping face (operator.py:391-399), faces f0.. of the
@@ -387,17 +384,14 @@ __global__ void k_lin_scatter(DevParams P, long long n_if, const int32_t* __rest
 // triple + pad; a voxel's slots are consecutive in direction order, first slot in its
 // label word)
 __global__ void k_lin_scatter_c(DevParams P, long long n_if, const int32_t* __restrict__ so,
-                                const int32_t* __restrict__ el, const int32_t* __restrict__ labt,
+                                const int32_t* __restrict__ el, const int2* __restrict__ fslot,
                                 const double* __restrict__ coef, double* __restrict__ cs) {
   long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (f >= n_if) return;
   const int s = so[f], e = el[f];
   const double ca = coef[f], cb = coef[n_if + f], cg = coef[2 * n_if + f];
-  auto slot = [&](int v, int d) -> long long {
-    const unsigned w = (unsigned)labt[v];
-    return (long long)(w >> 9) + __popc(((w >> 3) & 63u) & ((1u << d) - 1u));
-  };
-  const long long is = 4 * slot(s, dir_to(P, s, e)), ie = 4 * slot(e, dir_to(P, e, s));
+  const int2 fs = fslot[f];
+  const long long is = 4LL * fs.x, ie = 4LL * fs.y;
   cs[is] = ca; cs[is + 1] = cb; cs[is + 2] = cg;
   cs[ie] = -cb; cs[ie + 1] = -ca; cs[ie + 2] = cg;
 }
@@ -458,7 +452,7 @@ void residual_grid(Operator& op, const double2* xg, const double* npl, double mu
     // deterministic: face currents into per-slot storage, gathered by the stencil
     if ((which & 2) && (parts & PART_BV) && op.n_if)
       k_residual_islot<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
-                                                           op.if_slot.p, op.if_kind.p, op.labt.p, xg,
+                                                           op.if_slot.p, op.if_kind.p, op.if_fslot.p, xg,
                                                            npl, beta, op.if_islot.p); HC_COUNT();
     if ((which & 1) && res_launch_tma(op, xg, mu, parts, cprev, inv_dt, out, s)) {
       HC_COUNT();
@@ -496,7 +490,7 @@ void linearize(Operator& op, const double2* xg, const double* npl, double beta, 
                                                     op.if_coef.p); HC_COUNT();
     if (op.tma)
       k_lin_scatter_c<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
-                                                          op.labt.p, op.if_coef.p, op.if_cslot.p); HC_COUNT();
+                                                          op.if_fslot.p, op.if_coef.p, op.if_cslot.p); HC_COUNT();
     long long nslot = (long long)op.if_dir.n;
     k_lin_scatter<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p, op.if_el.p,
                                                       op.if_rank.p, op.if_coef.p, nslot,
@@ -841,11 +835,14 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
     op->lab4.alloc(nvox);
     HC_CUDA(cudaMemcpy(op->lab4.p, l4.data(), nvox * 4, cudaMemcpyHostToDevice));
     if (tma_grid_ok(P)) {
-      // TMA label word: (phase + 1) | interface-direction mask << 3 | first slot << 9 —
-      // phase + 1 so that the TMA zero fill reads as "outside"; the slots of a voxel's
-      // interface faces are consecutive in the compact coefficient array
+      // TMA face word (hc_tma.cuh): (phase + 1) | interface mask << 3 | same-phase
+      // conduction mask << 9 | contact flag | grounded-row flag | tile-plane-local first
+      // slot << 17 — phase + 1 so that the TMA zero fill reads as "outside"; the slots of a
+      // voxel's interface faces are consecutive in direction order
       std::vector<int32_t> dirs(op->if_dir.n);
       HC_CUDA(cudaMemcpy(dirs.data(), op->if_dir.p, dirs.size() * 4, cudaMemcpyDeviceToHost));
+      // per interface face: its slot on the solid side and on the electrolyte side
+      std::vector<int2> fslot(std::max<long long>(op->n_if, 1), make_int2(0, 0));
       // slots numbered tile-plane by tile-plane (32 x 8 tile, plane z), so the slots a
       // TMA stencil CTA needs for one plane are one contiguous block (bulk-copied by its
       // producer warp); tp_off[tile-plane] = first slot of that block
@@ -856,15 +853,37 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
       for (int z = 0; z < nz; ++z)
         for (int ty = 0; ty < tby0; ++ty)
           for (int tx = 0; tx < tbx0; ++tx) {
+            const long long tp0 = slot;
             tp_off[((size_t)z * tby0 + ty) * tbx0 + tx] = (int32_t)slot;
             for (int y = ty * VY; y < std::min(ny, ty * VY + VY); ++y)
               for (int x = tx * VX; x < std::min(nx, tx * VX + VX); ++x) {
                 const long long v = ((long long)z * ny + y) * nx + x;
-                int mask = 0;
+                const uint8_t a = labels_host[v];
+                int mask = 0, smask = 0, contact = 0;
+                const long long nb[6] = {x > 0 ? v - 1 : -1, x + 1 < nx ? v + 1 : -1,
+                                         y > 0 ? v - nx : -1, y + 1 < ny ? v + nx : -1,
+                                         z > 0 ? v - (long long)nx * ny : -1,
+                                         z + 1 < nz ? v + (long long)nx * ny : -1};
+                for (int d = 0; d < 6; ++d) {
+                  if (nb[d] < 0) continue;
+                  const uint8_t k = kind_of(a, labels_host[nb[d]]);
+                  if (k == K_CONT) smask |= 1 << d;
+                  if (k == K_CONTACT) contact = 1;
+                }
                 if (rank[v] >= 0)
-                  for (int d = 0; d < 6; ++d) mask |= (dirs[6LL * rank[v] + d] >= 0) << d;
-                if (slot >= (1LL << 23)) fits = false;
-                l4[v] = ((int32_t)labels_host[v] + 1) | (mask << 3) | (int32_t)((slot & ((1 << 23) - 1)) << 9);
+                  for (int d = 0; d < 6; ++d) {
+                    const int32_t f = dirs[6LL * rank[v] + d];
+                    if (f < 0) continue;
+                    mask |= 1 << d;
+                    if (a == EL) fslot[f].y = (int)(slot + __builtin_popcount(mask) - 1);
+                    else fslot[f].x = (int)(slot + __builtin_popcount(mask) - 1);
+                  }
+                const long long loc = slot - tp0;
+                if (loc >= (1LL << 15) || slot + 6 >= (1LL << 31)) fits = false;
+                const int grounded = (z == nz - 1 && a == CC) ? 1 : 0;
+                l4[v] = (int32_t)((uint32_t)(a + 1) | (uint32_t)mask << 3 | (uint32_t)smask << 9 |
+                                  (uint32_t)contact << 15 | (uint32_t)grounded << 16 |
+                                  (uint32_t)(loc & 0x7fff) << 17);
                 slot += __builtin_popcount(mask);
               }
           }
@@ -878,6 +897,8 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
         HC_CUDA(cudaMemcpy(op->tp_off.p, tp_off.data(), tp_off.size() * 4, cudaMemcpyHostToDevice));
         op->if_islot.alloc(std::max<long long>(slot, 1));
         HC_CUDA(cudaMemset(op->if_islot.p, 0, op->if_islot.n * sizeof(double)));
+        op->if_fslot.alloc(fslot.size());
+        HC_CUDA(cudaMemcpy(op->if_fslot.p, fslot.data(), fslot.size() * sizeof(int2), cudaMemcpyHostToDevice));
         const int tbx = (nx + VX - 1) / VX, tby = (ny + VY - 1) / VY;
         std::vector<int2> ez(tbx * tby, make_int2(nz, -1));
         for (long long v = 0; v < nvox; ++v)

@@ -11,9 +11,9 @@
 // missing neighbours contribute nothing — the reference's face enumeration
 // (operator.py:121-242) without a single boundary branch.
 //
-// Label word (labt): (phase + 1) | interface-direction mask << 3 | first face slot << 9,
-// 0 = outside; the slots hold row-oriented (alpha, beta, gamma) triples (cslot).
-// Face-coefficient tables are indexed (a << 3) | b in that encoding.
+// Face word (labt, below): phase, interface and same-phase conduction masks, and the
+// tile-plane-local first face slot, 0 = outside; the slots hold row-oriented
+// (alpha, beta, gamma) triples (cslot).  The contact-face table is indexed (a << 3) | b.
 #pragma once
 
 #include <cuda.h>
@@ -29,6 +29,16 @@ namespace hc {
 
 // phases in the TMA label encoding
 enum : int { TV = 0, TEL = EL + 1, TGR = GR + 1, TCC = CC + 1, TCW = CW + 1 };
+// face word (one int32 per voxel, built once per geometry):
+//   (phase + 1) | interface mask << 3 | same-phase conduction mask << FW_SELF |
+//   contact flag | grounded-row flag | tile-plane-local first face slot << FW_SLOT
+// Direction bits: 0 x-1, 1 x+1, 2 y-1, 3 y+1, 4 z-1, 5 z+1.  The conduction mask holds the
+// in-domain neighbours of the same phase (kind K_CONT): their faces use the row phase's own
+// (P, C), so the stencil reads no neighbour label and no pair table.  A voxel with a
+// contact face (two different conductor phases, harmonic-mean conductance) takes the
+// table path on all its faces.
+constexpr int FW_SELF = 9, FW_SLOT = 17;
+constexpr int FW_CONTACT = 1 << 15, FW_GROUND = 1 << 16;
 // operator value (residual) mode of the TMA stencil: parts in `flags`, mu in `omega`,
 // c_prev in `r`, interface currents per face slot in F.islot
 constexpr int SM_RES = 4;
@@ -149,7 +159,8 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
   extern __shared__ __align__(16) unsigned char smem_dyn[];
   // 128-byte aligned ring (the launch adds 128 bytes of slack)
   unsigned char* ring = smem_dyn + ((128 - ((unsigned)__cvta_generic_to_shared(smem_dyn) & 127)) & 127);
-  __shared__ __align__(16) double2 sPC[64];   // (P, C) per (a << 3 | b)
+  __shared__ __align__(16) double2 sPC[64];   // (P, C) per (a << 3 | b): contact voxels
+  __shared__ __align__(16) double2 sSelf[8];  // (P, C) of a phase's same-phase faces, per a
   __shared__ __align__(8) unsigned long long full[T_S], empty[T_S], ready[T_S];
   __shared__ int tp_start[T_S];   // first global face slot of the tile-plane staged in each ring slot
   const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
@@ -174,6 +185,10 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
     const bool ok = a >= 1 && a <= N_PHASES && b >= 1 && b <= N_PHASES;
     const int i = (a - 1) * 6 + (b - 1);
     sPC[tid] = ok ? make_double2(P.gP[i], P.gC[i]) : make_double2(0.0, 0.0);
+    if (tid < 8) {
+      const bool sk = tid >= 1 && tid <= N_PHASES;
+      sSelf[tid] = sk ? make_double2(P.gP[7 * (tid - 1)], P.gC[7 * (tid - 1)]) : make_double2(0.0, 0.0);
+    }
   }
   // producer warp: face-slot block of plane j = lane + 32 r of this tile column (loaded
   // lane-parallel; the first batch before the barrier so its latency overlaps the setup)
@@ -213,7 +228,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         // residual slots are 8 B: start the bulk copy at the 16-byte aligned slot below
         const int sta = RES ? (st & ~1) : st;
         const unsigned sbytes = RES ? (unsigned)(((cnt + (st - sta)) * 8 + 15) & ~15) : 32u * cnt;
-        tp_start[slot] = sta;
+        tp_start[slot] = st;   // true first slot (the residual copy starts at the 16-byte aligned sta)
         mbar_expect_tx(b, tx + (wtile ? T_DN * 8 : 0) + (cnt ? sbytes : 0u));
         tma_load3(s + L::LAB, &M.lab, x0 - T_LOFF, y0 - 1, zz, b);
         if constexpr (X0) {
@@ -285,8 +300,34 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
     logs_for(0);
     logs_for(1);
   }
+  auto lab_at = [&](const unsigned char* Sx, int o) -> int {
+    return *reinterpret_cast<const int*>(Sx + lofs + 4 * o);
+  };
+  auto val_at = [&](const unsigned char* Sx, int o) -> VT {
+    if constexpr (X0)
+      return omega * *reinterpret_cast<const double*>(Sx + L::AUX2 + aofs + 8 * o) *
+             *reinterpret_cast<const double*>(Sx + L::AUX + aofs + 8 * o);
+    else
+      return *reinterpret_cast<const VT*>(Sx + vofs + (int)sizeof(VT) * o);
+  };
+  auto w_at = [&](const unsigned char* Sx, int o) -> double {
+    return *reinterpret_cast<const double*>(Sx + L::AUX + aofs + 8 * o);
+  };
+  auto lg = [&](const unsigned char* Sx, int o) -> double {
+    return reinterpret_cast<const double*>(Sx + L::LOG)[vidx_t + o];
+  };
+  // the own voxel of plane z0; afterwards it is carried from the previous plane's z + 1 read
+  int aw = 0;
+  VT va{};
+  double wa = 0.0;
+  mbar_wait((RES ? ready0 : full0), 0);
+  aw = lab_at(base, 0);
+  va = val_at(base, 0);
+  if constexpr (OC) wa = w_at(base, 0);
+  if constexpr (RES) wa = lg(base, 0);
+
   double dacc1 = 0.0, dacc2 = 0.0;   // fused dot products (J v with F.dot_a)
-  auto step = [&](int j, auto slotc, unsigned ph0, unsigned ph1) {
+  auto step = [&](int j, auto slotc, unsigned ph1) {
     constexpr int K = decltype(slotc)::value, K1 = (K + 1) % T_S;
     const unsigned char* S0 = base + K * L::SLOT;
     const unsigned char* S1 = base + K1 * L::SLOT;
@@ -302,137 +343,145 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
       if (active && (flags & PART_TIME)) rv = r[v];   // c_prev
     }
     if constexpr (RES) logs_for(j + 2);
-    mbar_wait((RES ? ready0 : full0) + 8 * K, ph0);
+    // plane j was waited for as the previous step's z + 1
     mbar_wait((RES ? ready0 : full0) + 8 * K1, ph1);
-    auto lab_at = [&](const unsigned char* Sx, int o) -> int {
-      return *reinterpret_cast<const int*>(Sx + lofs + 4 * o);
-    };
-    auto val_at = [&](const unsigned char* Sx, int o) -> VT {
-      if constexpr (X0)
-        return omega * *reinterpret_cast<const double*>(Sx + L::AUX2 + aofs + 8 * o) *
-               *reinterpret_cast<const double*>(Sx + L::AUX + aofs + 8 * o);
-      else
-        return *reinterpret_cast<const VT*>(Sx + vofs + (int)sizeof(VT) * o);
-    };
-    auto w_at = [&](const unsigned char* Sx, int o) -> double {
-      return *reinterpret_cast<const double*>(Sx + L::AUX + aofs + 8 * o);
-    };
-    // neighbour d: 0 x-1, 1 x+1, 2 y-1, 3 y+1, 4 z-1 (registers), 5 z+1 (next slot)
+    // own column at z + 1: the z + 1 neighbour now, the own voxel of the next plane
+    const int aw1 = lab_at(S1, 0);
+    const VT v1 = val_at(S1, 0);
+    double w1 = 0.0;
+    if constexpr (OC) w1 = w_at(S1, 0);
+    if constexpr (RES) w1 = lg(S1, 0);
+    // neighbour d: 0 x-1, 1 x+1, 2 y-1, 3 y+1, 4 z-1 (registers), 5 z+1 (registers)
     auto nb_lab = [&](int d) -> int {
       if (d == 4) return lm;
-      if (d == 5) return lab_at(S1, 0) & 7;
+      if (d == 5) return aw1 & 7;
       return lab_at(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -T_LW : T_LW))) & 7;
     };
     auto nb_val = [&](int d) -> VT {
       if (d == 4) return vm;
-      if (d == 5) return val_at(S1, 0);
+      if (d == 5) return v1;
       return val_at(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -VW : VW)));
     };
     auto nb_w = [&](int d) -> double {
       if (d == 4) return wm;
-      if (d == 5) return w_at(S1, 0);
+      if (d == 5) return w1;
       return w_at(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -T_DW : T_DW)));
     };
+    auto nb_lg = [&](int d) -> double {
+      if (d == 4) return wm;
+      if (d == 5) return w1;
+      return lg(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -T_QW : T_QW)));
+    };
+    const int a = aw & 7;
     if (active) {
-      const int aw = lab_at(S0, 0);
-      const int a = aw & 7;
-      const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == TGR || a == TEL)
-                                                             : !(z == nz - 1 && a == TCC);
-      const VT va = val_at(S0, 0);
-      double wa = 0.0;
-      if constexpr (OC) wa = w_at(S0, 0);
+      const bool in_row = (MODE == SM_CONC || MODE == SM_CP) ? (a == TGR || a == TEL) : !(aw & FW_GROUND);
       if (!in_row) {
         if constexpr (FULLM) out2[v] = make_double2(0.0, 0.0);
         else out[(size_t)v * ((flags & FL_OSTRIDE2) ? 2 : 1)] = 0.0;
       } else {
-        const int a8 = a << 3;
         const bool elrow = a == TEL;
-        // linear faces from the (P, C) table.  Electrolyte rows also carry migration and
-        // chemical-potential couplings, which equal t+ times their phi-row terms
-        // (operator.py:216-227), so only P and C are looked up.
+        const unsigned sm = ((unsigned)aw >> FW_SELF) & 63u;   // same-phase conduction faces
         double rc = 0.0, rp = 0.0;
-        if constexpr (RES) {
-          // linear two-point fluxes and the chemical-potential faces gX (log c_a - log c_b)
-          // between electrolyte voxels (operator.py:322-327)
-          const bool lin = flags & PART_LIN, lc = (flags & PART_1C) && elrow;
-          auto lg = [&](const unsigned char* Sx, int o) -> double {
-            return reinterpret_cast<const double*>(Sx + L::LOG)[vidx_t + o];
-          };
-          const double la = lg(S0, 0);
-          double q = 0.0;
-#pragma unroll
-          for (int d = 0; d < 6; ++d) {
-            const int b = nb_lab(d);
-            const double2 vb = nb_val(d);
-            if (lin) {
-              const double2 pc = sPC[a8 | b];
-              rp = fma(pc.x, va.y - vb.y, rp);
-              rc = fma(pc.y, va.x - vb.x, rc);
-            }
-            if (lc && b == TEL) {
-              const double lb = d == 4 ? wm : (d == 5 ? lg(S1, 0)
-                                : lg(S0, d == 0 ? -1 : (d == 1 ? 1 : (d == 2 ? -T_QW : T_QW))));
-              q += la - lb;
-            }
-          }
-          wa = la;
-          rp = fma(P.gX, q, rp);
-        } else if constexpr (FULLM) {
-          double q = 0.0;
-          int nel = 0;
-#pragma unroll
-          for (int d = 0; d < 6; ++d) {
-            const int b = nb_lab(d);
-            const double2 vb = nb_val(d);
-            const double2 pc = sPC[a8 | b];
-            rp = fma(pc.x, va.y - vb.y, rp);
-            rc = fma(pc.y, va.x - vb.x, rc);
-            if constexpr (OC) {   // gX/c is zero off the electrolyte and in the zero-filled halo
-              q = fma(-nb_w(d), vb.x, q);
-              nel += b == TEL;
-            }
-          }
-          if constexpr (OC) {
-            q = fma((double)nel, wa * va.x, q);
-            rp += elrow ? q : 0.0;
-          }
-        } else if (MODE == SM_PHI || MODE == SM_CONC) {
+        if (aw & FW_CONTACT) {
+          // rare (solid conductors touching another conductor phase): the (P, C) table of
+          // the face's phase pair on every face.  Never an electrolyte row.
+          const int a8 = a << 3;
+          const bool lin = !RES || (flags & PART_LIN);
 #pragma unroll
           for (int d = 0; d < 6; ++d) {
             const double2 pc = sPC[a8 | nb_lab(d)];
-            rp = fma(MODE == SM_PHI ? pc.x : pc.y, va - nb_val(d), rp);
+            const VT vbd = nb_val(d);
+            if constexpr (FULLM) {
+              if (lin) {
+                rp = fma(pc.x, va.y - vbd.y, rp);
+                rc = fma(pc.y, va.x - vbd.x, rc);
+              }
+            } else if (MODE == SM_PHI || MODE == SM_CONC) {
+              rp = fma(MODE == SM_PHI ? pc.x : pc.y, va - vbd, rp);
+            }
+          }
+        } else {
+          // same-phase faces share the row phase's coefficients: sum the differences
+          // over the conduction mask, scale once.  Electrolyte rows also carry migration
+          // and chemical-potential couplings, which equal t+ times their phi-row terms
+          // (operator.py:216-227), so only P and C are needed.
+          const double2 ps = sSelf[a];
+          if constexpr (RES) {
+            // linear two-point fluxes and the chemical-potential faces gX (log c_a - log c_b)
+            // between electrolyte voxels (operator.py:322-327)
+            double dp = 0.0, dc = 0.0, q = 0.0;
+#pragma unroll
+            for (int d = 0; d < 6; ++d)
+              if (sm & (1u << d)) {
+                const double2 vbd = nb_val(d);
+                dp += va.y - vbd.y;
+                dc += va.x - vbd.x;
+                q += wa - nb_lg(d);
+              }
+            if (flags & PART_LIN) {
+              rp = ps.x * dp;
+              rc = ps.y * dc;
+            }
+            if ((flags & PART_1C) && elrow) rp = fma(P.gX, q, rp);
+          } else if constexpr (FULLM) {
+            double dp = 0.0, dc = 0.0, q = 0.0;
+#pragma unroll
+            for (int d = 0; d < 6; ++d)
+              if (sm & (1u << d)) {
+                const double2 vbd = nb_val(d);
+                dp += va.y - vbd.y;
+                dc += va.x - vbd.x;
+                if constexpr (OC) q = fma(-nb_w(d), vbd.x, q);   // gX/c: electrolyte rows only
+              }
+            rp = ps.x * dp;
+            rc = ps.y * dc;
+            if constexpr (OC) {
+              q = fma((double)__popc(sm), wa * va.x, q);
+              rp += elrow ? q : 0.0;
+            }
+          } else if (MODE == SM_PHI || MODE == SM_CONC) {
+            double dq = 0.0;
+#pragma unroll
+            for (int d = 0; d < 6; ++d)
+              if (sm & (1u << d)) dq += va - nb_val(d);
+            rp = (MODE == SM_PHI ? ps.x : ps.y) * dq;
           }
         }
-        // interface kinetics: six row-oriented coefficient triples (zero off-interface);
-        // face d adds alpha c_a + beta c_b + gamma (phi_a - phi_b) to the phi row
+        // interface kinetics: the voxel's face slots, consecutive in direction order from the
+        // tile-plane-local index in its word (staged with the plane; global past capacity)
         double si = 0.0;
         const unsigned mask = ((unsigned)aw >> 3) & 63u;
-        if constexpr (RES) {
-          // interface currents, one per face slot, oriented from this row (k_residual_islot)
-          if (mask && (flags & PART_BV)) {
-            const int gs = (int)((unsigned)aw >> 9), loc = gs - tp_start[K];
-            const int n = __popc(mask);
-            const double* c = loc + n <= T_SLOTCAP ? reinterpret_cast<const double*>(S0 + L::SLT) + loc
-                                                   : F.islot + gs;
-            for (int k = 0; k < n; ++k) si += c[k];
-          }
-        } else if (mask) {
-          // the tile-plane's slots were bulk-copied with the plane (global if over capacity)
-          const int gs = (int)((unsigned)aw >> 9), loc = gs - tp_start[K];
-          const double* c = loc + __popc(mask) <= T_SLOTCAP
-                                 ? reinterpret_cast<const double*>(S0 + L::SLT) + 4 * loc
-                                 : F.cslot + 4LL * gs;
-#pragma unroll
-          for (int d = 0; d < 6; ++d) {
-            if (mask & (1u << d)) {
-              const VT vb = nb_val(d);
-              const double2 ab = *reinterpret_cast<const double2*>(c);
-              const double g = c[2];
-              if constexpr (FULLM) si += ab.x * va.x + ab.y * vb.x + g * (va.y - vb.y);
-              else if (MODE == SM_CONC) si += ab.x * va + ab.y * vb;
-              else si += g * (va - vb);
-              c += 4;
+        if (mask) {
+          const int loc = (int)((unsigned)aw >> FW_SLOT), n = __popc(mask);
+          if constexpr (RES) {
+            // interface currents, one per face slot, oriented from this row (k_residual_islot)
+            if (flags & PART_BV) {
+              if (loc + n <= T_SLOTCAP) {
+                const double* c = reinterpret_cast<const double*>(S0 + L::SLT) + loc + (tp_start[K] & 1);
+                for (int k = 0; k < n; ++k) si += c[k];
+              } else {
+                const double* c = F.islot + tp_start[K] + loc;
+                for (int k = 0; k < n; ++k) si += c[k];
+              }
             }
+          } else {
+            // face d adds alpha c_a + beta c_b + gamma (phi_a - phi_b) to the phi row
+            auto faces = [&](const double* c) {
+#pragma unroll
+              for (int d = 0; d < 6; ++d) {
+                if (mask & (1u << d)) {
+                  const double2 ab = *reinterpret_cast<const double2*>(c);
+                  const double g = c[2];
+                  const VT vbd = nb_val(d);
+                  if constexpr (FULLM) si += ab.x * va.x + ab.y * vbd.x + g * (va.y - vbd.y);
+                  else if (MODE == SM_CONC) si += ab.x * va + ab.y * vbd;
+                  else si += g * (va - vbd);
+                  c += 4;
+                }
+              }
+            };
+            if (loc + n <= T_SLOTCAP) faces(reinterpret_cast<const double*>(S0 + L::SLT) + 4 * loc);
+            else faces(F.cslot + 4LL * (tp_start[K] + loc));
           }
         }
         if constexpr (RES) {
@@ -466,10 +515,13 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
         }
       }
       if constexpr (EPI == EP_RESID0) reinterpret_cast<double*>(out2)[v] = va;
-      lm = a;
-      vm = va;
-      if constexpr (OC || RES) wm = wa;
     }
+    lm = a;
+    vm = va;
+    if constexpr (OC || RES) wm = wa;
+    aw = aw1;
+    va = v1;
+    wa = w1;
     __syncwarp();
     if (threadIdx.x == 0) mbar_arrive(empty0 + 8 * K);   // this warp is done with plane j
   };
@@ -477,7 +529,7 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
     const unsigned ph = (jb / T_S) & 1;
     static_for<T_S>([&](auto kc) {
       constexpr int K = decltype(kc)::value;
-      if (jb + K < nplane) step(jb + K, kc, ph, K + 1 == T_S ? ph ^ 1 : ph);
+      if (jb + K < nplane) step(jb + K, kc, K + 1 == T_S ? ph ^ 1 : ph);
     });
   }
   if constexpr (MODE == SM_FULL) {
