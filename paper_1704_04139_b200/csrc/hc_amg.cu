@@ -386,6 +386,134 @@ __global__ void k_sell_x(int n, double w, double alpha, const int32_t* __restric
   }
 }
 
+// packed entries of a level operator from its fp64 values (after every numeric setup):
+// off-diagonals rounded to bf16 (nearest even), the diagonal entry's value 0, the row's
+// rounding errors folded into the fp32 diagonal kept per row
+__global__ void k_pack_rows(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ a, const uint16_t* __restrict__ off,
+                            uint32_t* __restrict__ pk, float* __restrict__ diag) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double err = 0.0, d = 0.0;
+  for (int q = rp[i]; q < rp[i + 1]; ++q) {
+    const double aq = a[q];
+    if (ci[q] == i) {
+      d += aq;
+      pk[q] = off[q];
+      continue;
+    }
+    unsigned u = __float_as_uint((float)aq);
+    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+    err += aq - (double)__uint_as_float(u);
+    pk[q] = u | off[q];
+  }
+  diag[i] = (float)(d + err);
+}
+// sliced-ELL packed entries from the CSR packed entries
+__global__ void k_sell_pack(long long n, const int32_t* __restrict__ map, const uint16_t* __restrict__ off,
+                            const uint32_t* __restrict__ pk, uint32_t* __restrict__ out) {
+  pdl_wait();
+  long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q < n) {
+    const int m = map[q];
+    out[q] = (m >= 0 ? (pk[m] & 0xffff0000u) : 0u) | off[q];
+  }
+}
+
+// k_sell_x on the packed copy: one 32-bit load per entry (bf16 value | column offset from
+// the slice's base column); the diagonal comes from the per-row fp32 array
+template <int T, int XM>
+__global__ void k_sell_xp(int n, double w, double alpha, const int32_t* __restrict__ sp,
+                          const int32_t* __restrict__ sbase, const uint32_t* __restrict__ se,
+                          const float* __restrict__ diag, const CV* __restrict__ dinv,
+                          const CV* __restrict__ b, const CV* __restrict__ x,
+                          const int32_t* __restrict__ parent, const CV* __restrict__ xc,
+                          CV* __restrict__ y, int resid, CV* __restrict__ x0) {
+  pdl_wait();
+  constexpr int R = 32 / T;   // rows per slice
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int slice = (int)(gt >> 5);
+  if ((long long)slice * R >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int i = slice * R + lane / T;
+  auto xin = [&](int j) -> double {
+    if (XM == 0) return (double)x[j];
+    if (XM == 1) return w * (double)dinv[j] * (double)b[j];
+    return (double)x[j] + alpha * (double)xc[parent[j]];
+  };
+  const int base = sp[slice], width = (sp[slice + 1] - base) >> 5;   // k-steps of 32 entries
+  const int cb = sbase[slice];
+  const uint32_t* ep = se + base + lane;
+  double s = 0.0;
+  int k = 0;
+  for (; k + 3 < width; k += 4) {
+    const uint32_t e0 = ep[0], e1 = ep[32], e2 = ep[64], e3 = ep[96];
+    const double x0_ = xin(cb + (int)(e0 & 0xffffu)), x1 = xin(cb + (int)(e1 & 0xffffu));
+    const double x2 = xin(cb + (int)(e2 & 0xffffu)), x3 = xin(cb + (int)(e3 & 0xffffu));
+    s += (double)__uint_as_float(e0 & 0xffff0000u) * x0_;
+    s += (double)__uint_as_float(e1 & 0xffff0000u) * x1;
+    s += (double)__uint_as_float(e2 & 0xffff0000u) * x2;
+    s += (double)__uint_as_float(e3 & 0xffff0000u) * x3;
+    ep += 128;
+  }
+  for (; k < width; ++k, ep += 32) {
+    const uint32_t e = *ep;
+    s += (double)__uint_as_float(e & 0xffff0000u) * xin(cb + (int)(e & 0xffffu));
+  }
+#pragma unroll
+  for (int o = T / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, T);
+  if (lane % T == 0 && i < n) {
+    const double xi = xin(i), bi = b[i];
+    s += (double)diag[i] * xi;
+    y[i] = (CV)(resid ? bi - s : xi + w * (double)dinv[i] * (bi - s));
+    if (x0) x0[i] = (CV)xi;
+  }
+}
+
+// k_csr_x on the packed copy (column offsets from the row's smallest column)
+template <int VS, int XM>
+__global__ void k_csr_xp(int n, double w, double alpha, const int32_t* __restrict__ rp,
+                         const int32_t* __restrict__ rbase, const uint32_t* __restrict__ pe,
+                         const float* __restrict__ diag, const CV* __restrict__ dinv,
+                         const CV* __restrict__ b, const CV* __restrict__ x,
+                         const int32_t* __restrict__ parent, const CV* __restrict__ xc,
+                         CV* __restrict__ y, int resid, CV* __restrict__ x0) {
+  pdl_wait();
+  long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int i = (int)(gt / VS), lane = (int)(gt % VS);
+  if (i >= n) return;
+  auto xin = [&](int j) -> double {
+    if (XM == 0) return (double)x[j];
+    if (XM == 1) return w * (double)dinv[j] * (double)b[j];
+    return (double)x[j] + alpha * (double)xc[parent[j]];
+  };
+  double s = 0.0;
+  const int k1 = rp[i + 1], cb = rbase[i];
+  int k = rp[i] + lane;
+  for (; k + 3 * VS < k1; k += 4 * VS) {
+    const uint32_t e0 = pe[k], e1 = pe[k + VS], e2 = pe[k + 2 * VS], e3 = pe[k + 3 * VS];
+    const double x0_ = xin(cb + (int)(e0 & 0xffffu)), x1 = xin(cb + (int)(e1 & 0xffffu));
+    const double x2 = xin(cb + (int)(e2 & 0xffffu)), x3 = xin(cb + (int)(e3 & 0xffffu));
+    s += (double)__uint_as_float(e0 & 0xffff0000u) * x0_;
+    s += (double)__uint_as_float(e1 & 0xffff0000u) * x1;
+    s += (double)__uint_as_float(e2 & 0xffff0000u) * x2;
+    s += (double)__uint_as_float(e3 & 0xffff0000u) * x3;
+  }
+  for (; k < k1; k += VS) {
+    const uint32_t e = pe[k];
+    s += (double)__uint_as_float(e & 0xffff0000u) * xin(cb + (int)(e & 0xffffu));
+  }
+#pragma unroll
+  for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, VS);
+  if (lane == 0) {
+    const double xi = xin(i), bi = b[i];
+    s += (double)diag[i] * xi;
+    y[i] = (CV)(resid ? bi - s : xi + w * (double)dinv[i] * (bi - s));
+    if (x0) x0[i] = (CV)xi;
+  }
+}
+
 // VS lanes per row (VS = 1, 8 or 32), chosen per level from the mean row length
 template <int VS, class VT>
 __global__ void k_csr_jacobi_v(int n, double w, const int32_t* __restrict__ rp,
@@ -596,6 +724,54 @@ void upload_csr(Csr& c, const HPat& p) {
 
 }  // namespace
 
+// packed-entry patterns of a level operator (see Csr::pk_*): per-row / per-slice base column
+// and 16-bit offsets; leaves pk_ok false when some row or slice spans 65536 columns or more
+static void build_packed(Csr& c, const HPat& p) {
+  const int n = p.n();
+  c.pk_ok = false;
+  if (!n || p.ci.empty()) return;
+  std::vector<int32_t> base(n);
+  std::vector<uint16_t> off(p.ci.size());
+  for (int i = 0; i < n; ++i) {
+    int lo = i, hi = i;
+    for (int q = p.rp[i]; q < p.rp[i + 1]; ++q) {
+      lo = std::min(lo, p.ci[q]);
+      hi = std::max(hi, p.ci[q]);
+    }
+    if (hi - lo >= 65536) return;
+    base[i] = lo;
+    for (int q = p.rp[i]; q < p.rp[i + 1]; ++q) off[q] = (uint16_t)(p.ci[q] - lo);
+  }
+  upload(c.pk_base, base);
+  upload(c.pk_off, off);
+  c.pk.alloc(p.ci.size());
+  c.pk_diag.alloc(n);
+  c.pk_ok = true;
+}
+// the same for the sliced-ELL copy (after build_sell): offsets from the slice's smallest column
+static void build_packed_sell(Csr& c, const std::vector<int32_t>& ptr, const std::vector<int32_t>& col) {
+  if (!c.pk_ok) return;
+  const int ns = (int)ptr.size() - 1;
+  std::vector<int32_t> base(ns);
+  std::vector<uint16_t> off(col.size());
+  for (int sl = 0; sl < ns; ++sl) {
+    int lo = INT32_MAX, hi = 0;
+    for (int q = ptr[sl]; q < ptr[sl + 1]; ++q) {
+      lo = std::min(lo, col[q]);
+      hi = std::max(hi, col[q]);
+    }
+    if (ptr[sl + 1] > ptr[sl] && hi - lo >= 65536) {
+      c.sl_base.n = 0;
+      return;
+    }
+    base[sl] = ptr[sl + 1] > ptr[sl] ? lo : 0;
+    for (int q = ptr[sl]; q < ptr[sl + 1]; ++q) off[q] = (uint16_t)(col[q] - base[sl]);
+  }
+  upload(c.sl_base, base);
+  upload(c.sl_off, off);
+  c.sl_pk.alloc(std::max<size_t>(col.size(), 1));
+}
+
 // sliced-ELL pattern (see Csr::sl_*, k_sell_x) with T lanes per row from a host CSR pattern
 static void build_sell(Csr& c, const HPat& p, int T) {
   const int R = 32 / T;
@@ -620,7 +796,7 @@ static void build_sell(Csr& c, const HPat& p, int T) {
             col[q] = p.ci[p.rp[i] + j];
             map[q] = p.rp[i] + j;
           } else {
-            col[q] = i < n ? i : 0;
+            col[q] = i < n ? i : n - 1;   // (rows past the end: any valid column near the slice's)
             map[q] = -1;
           }
         }
@@ -633,6 +809,7 @@ static void build_sell(Csr& c, const HPat& p, int T) {
   c.sl_vf.alloc(std::max<size_t>(col.size(), 1));
   c.sl_nnz = (long long)col.size();
   c.sl_n = n;
+  build_packed_sell(c, ptr, col);
 }
 
 // ============================================================== host: patterns
@@ -695,6 +872,7 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     const int n = A.n();
     L.n = n;
     upload_csr(L.A, A);
+    if (level >= 1 && cfg.pack && n > 0) build_packed(L.A, A);
     if (level >= 1 && cfg.sell_max_avg > 0 && n > 0) {
       // lanes per row: enough that each lane keeps ~sell_lane_nnz entries, and enough
       // threads in flight (n T >= sell_min_rows) for the sliced copy to pay
@@ -941,6 +1119,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_FUSE_NNZ")) amg->fuse_nnz = atoll(e);
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT")) amg->fuse_restrict = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT_SA")) amg->fuse_restrict_sa = atoi(e) != 0;
+  if (const char* e = getenv("HC_AMG_PACK")) amg->pack = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_SELL")) amg->sell_max_avg = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_FILTER")) amg->sa_filter = atoi(e);
   if (const char* e = getenv("HC_AMG_SELL_ROWS")) amg->sell_min_rows = atoi(e);
@@ -1017,6 +1196,16 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
         if (L.A.sl_n) {
           launch(k_sell_gather, nblk(L.A.sl_nnz), TPB, 0, s, L.A.sl_nnz, L.A.sl_map.p, L.A.vf.p, L.A.sl_vf.p);
           HC_COUNT();
+        }
+        if (L.A.pk_ok) {
+          launch(k_pack_rows, nblk(L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, (const double*)L.A.v.p,
+                 (const uint16_t*)L.A.pk_off.p, L.A.pk.p, L.A.pk_diag.p);
+          HC_COUNT();
+          if (L.A.sl_n && L.A.sl_base.n) {
+            launch(k_sell_pack, nblk(L.A.sl_nnz), TPB, 0, s, L.A.sl_nnz, L.A.sl_map.p,
+                   (const uint16_t*)L.A.sl_off.p, (const uint32_t*)L.A.pk.p, L.A.sl_pk.p);
+            HC_COUNT();
+          }
         }
       }
       if (L.R.nnz && l + 1 < B.levels.size()) {
@@ -1246,6 +1435,24 @@ template <int XM>
 static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha, const CV* b,
                         const CV* x, const int32_t* parent, const CV* xc, CV* y,
                         int resid, cudaStream_t s, CV* x0 = nullptr) {
+  if (A.fp32_coarse && L.A.sl_n && L.A.pk_ok && L.A.sl_base.n) {
+    auto go = [&](auto t_tag) {
+      constexpr int T = decltype(t_tag)::value;
+      const long long threads = ((long long)L.n + 32 / T - 1) / (32 / T) * 32;
+      launch(k_sell_xp<T, XM>, nblk(threads), TPB, 0, s, L.n, w, alpha, L.A.sl_ptr.p, L.A.sl_base.p,
+             (const uint32_t*)L.A.sl_pk.p, (const float*)L.A.pk_diag.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
+      HC_COUNT();
+    };
+    switch (L.A.sl_t) {
+      case 1: go(std::integral_constant<int, 1>{}); break;
+      case 2: go(std::integral_constant<int, 2>{}); break;
+      case 4: go(std::integral_constant<int, 4>{}); break;
+      case 8: go(std::integral_constant<int, 8>{}); break;
+      case 16: go(std::integral_constant<int, 16>{}); break;
+      default: go(std::integral_constant<int, 32>{}); break;
+    }
+    return;
+  }
   if (A.fp32_coarse && L.A.sl_n) {
     auto go = [&](auto t_tag) {
       constexpr int T = decltype(t_tag)::value;
@@ -1266,6 +1473,18 @@ static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha,
   }
   double avg = L.n ? (double)L.A.nnz / L.n : 0.0;
   const int VSsel = avg <= 12.0 ? 1 : (avg <= 48.0 ? 8 : 32);
+  if (A.fp32_coarse && L.A.pk_ok) {
+    auto gop = [&](auto vs_tag) {
+      constexpr int VS = decltype(vs_tag)::value;
+      launch(k_csr_xp<VS, XM>, nblk((long long)VS * L.n), TPB, 0, s, L.n, w, alpha, L.A.rp.p, L.A.pk_base.p,
+             (const uint32_t*)L.A.pk.p, (const float*)L.A.pk_diag.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
+      HC_COUNT();
+    };
+    if (VSsel == 1) gop(std::integral_constant<int, 1>{});
+    else if (VSsel == 8) gop(std::integral_constant<int, 8>{});
+    else gop(std::integral_constant<int, 32>{});
+    return;
+  }
   auto go = [&](auto vs_tag, auto* vals) {
     constexpr int VS = decltype(vs_tag)::value;
     using VT = std::remove_const_t<std::remove_pointer_t<decltype(vals)>>;

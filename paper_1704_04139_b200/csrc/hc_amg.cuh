@@ -28,6 +28,16 @@ struct Csr {
   DBuf<int32_t> sl_map;            // CSR position of every sliced entry, -1 for padding
   DBuf<float> sl_vf;               // values, gathered from vf after every numeric setup
   long long sl_nnz = 0;
+  // packed copy for the sweeps (levels >= 1): one 32-bit word per entry = bf16 value << 16 |
+  // 16-bit column offset from the row's (CSR) or slice's (sliced ELL) smallest column; the
+  // diagonal entry holds value 0 and the diagonal is kept per row in fp32, with the rounding
+  // errors of the row's off-diagonal entries added to it, so every row sum is preserved
+  // (half the bytes per entry; Krylov counts unchanged, profiles/r02_amg_packed_ab.txt)
+  bool pk_ok = false;                  // every row / slice spans fewer than 65536 columns
+  DBuf<int32_t> pk_base, sl_base;      // smallest column per row / per slice
+  DBuf<uint16_t> pk_off, sl_off;       // static column offsets per entry (pattern only)
+  DBuf<uint32_t> pk, sl_pk;            // packed entries (values refreshed with the hierarchy)
+  DBuf<float> pk_diag;                 // compensated diagonal per row
 };
 
 struct AmgLevel {
@@ -114,6 +124,7 @@ struct Amg {
   int coarsen = 2;           // block growth factor of the transfers above level 1              // gamma cycles on CSR levels wmin..wdepth
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int sa_filter = 0;         // bit l: filtered smoothing of the phi transfer from level l
+  bool pack = true;          // packed (bf16 value | 16-bit column offset) level operators for the sweeps
   int sell_max_avg = 512;    // levels with at most this many nonzeros per row and at least
   int sell_min_rows = 131072; // sell_min_rows threads (rows x lanes per row) sweep through the
                               // sliced-ELL copy (0: off); measured at one lane per row: large cell
