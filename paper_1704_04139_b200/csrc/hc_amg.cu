@@ -410,6 +410,36 @@ __global__ void k_pack_rows(int n, const int32_t* __restrict__ rp, const int32_t
   }
   diag[i] = (float)(d + err);
 }
+// the same into the sparsified pattern (AmgLevel::As): kept entries packed in order, every
+// other entry of the row lumped onto the diagonal
+__global__ void k_pack_rows_sp(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               const double* __restrict__ a, const uint8_t* __restrict__ keep,
+                               const int32_t* __restrict__ rps, const uint16_t* __restrict__ offs,
+                               uint32_t* __restrict__ pks, float* __restrict__ diag) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double err = 0.0, d = 0.0;
+  int qs = rps[i];
+  for (int q = rp[i]; q < rp[i + 1]; ++q) {
+    const double aq = a[q];
+    if (!keep[q]) {
+      err += aq;
+      continue;
+    }
+    if (ci[q] == i) {
+      d += aq;
+      pks[qs] = offs[qs];
+    } else {
+      unsigned u = __float_as_uint((float)aq);
+      u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+      err += aq - (double)__uint_as_float(u);
+      pks[qs] = u | offs[qs];
+    }
+    ++qs;
+  }
+  diag[i] = (float)(d + err);
+}
 // sliced-ELL packed entries from the CSR packed entries
 __global__ void k_sell_pack(long long n, const int32_t* __restrict__ map, const uint16_t* __restrict__ off,
                             const uint32_t* __restrict__ pk, uint32_t* __restrict__ out) {
@@ -665,6 +695,35 @@ __global__ void k_resid_restrict(int n1, const int32_t* __restrict__ pt_ptr, con
   if (ok && lane == 0) b1[I] = (CV)s;
 }
 
+// experiment (HC_AMG_PROUND=m): transfer values rounded to m mantissa bits, except each row's
+// largest entry, which absorbs the row's rounding errors (row sums of P preserved); the
+// transposed copy is gathered from the rounded values
+__global__ void k_round_lead(int n, int drop, const int32_t* __restrict__ rp, const double* __restrict__ a,
+                             float* __restrict__ b) {
+  pdl_wait();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int ql = -1;
+  double big = -1.0;
+  for (int q = rp[i]; q < rp[i + 1]; ++q)
+    if (fabs(a[q]) > big) { big = fabs(a[q]); ql = q; }
+  double err = 0.0;
+  for (int q = rp[i]; q < rp[i + 1]; ++q) {
+    if (q == ql) continue;
+    unsigned u = __float_as_uint((float)a[q]);
+    u = (u + (1u << (drop - 1))) & ~((1u << drop) - 1u);
+    const float v = __uint_as_float(u);
+    err += a[q] - (double)v;
+    b[q] = v;
+  }
+  if (ql >= 0) b[ql] = (float)(a[ql] + err);
+}
+__global__ void k_gather_f(long long n, const int32_t* __restrict__ idx, const float* __restrict__ v,
+                           float* __restrict__ out) {
+  pdl_wait();
+  long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q < n) out[q] = v[idx[q]];
+}
 __global__ void k_gather_ptv(long long n, const int32_t* __restrict__ pt_idx,
                              const double* __restrict__ pv, double* __restrict__ ptv) {
   pdl_wait();
@@ -1120,6 +1179,8 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT")) amg->fuse_restrict = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT_SA")) amg->fuse_restrict_sa = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_PACK")) amg->pack = atoi(e) != 0;
+  if (const char* e = getenv("HC_AMG_SPARSIFY")) amg->sparsify = atof(e);
+  if (const char* e = getenv("HC_AMG_SPARSIFY_AVG")) amg->sparsify_avg = atof(e);
   if (const char* e = getenv("HC_AMG_SELL")) amg->sell_max_avg = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_FILTER")) amg->sa_filter = atoi(e);
   if (const char* e = getenv("HC_AMG_SELL_ROWS")) amg->sell_min_rows = atoi(e);
@@ -1159,6 +1220,62 @@ Amg* build_amg(const Operator& op) {
 }
 
 // Numeric setup for the current linearization (op.if_coef) and dt.
+// Decide the sparsified sweep patterns of a block (AmgLevel::As) from the level operators'
+// current values: eager, once, at the block's first numeric setup.  Levels handled by the
+// cluster-fused coarse cycle keep their full operators.
+static void sparsify_block(const Amg& A, AmgBlock& B, cudaStream_t s) {
+  HC_CUDA(cudaStreamSynchronize(s));
+  const size_t lend = B.fuse_from >= 1 ? (size_t)B.fuse_from : B.levels.size() - 1;
+  for (size_t l = 1; l < lend && l + 1 < B.levels.size(); ++l) {
+    AmgLevel& L = B.levels[l];
+    if (!L.A.pk_ok || !L.n || (double)L.A.nnz / L.n <= A.sparsify_avg) continue;
+    std::vector<int32_t> rp(L.n + 1), ci(L.A.nnz);
+    std::vector<double> v(L.A.nnz);
+    HC_CUDA(cudaMemcpy(rp.data(), L.A.rp.p, rp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    HC_CUDA(cudaMemcpy(ci.data(), L.A.ci.p, ci.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    HC_CUDA(cudaMemcpy(v.data(), L.A.v.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<uint8_t> keep(L.A.nnz, 0);
+    HPat sp;
+    sp.rp.assign(L.n + 1, 0);
+    for (int i = 0; i < L.n; ++i) {
+      double aii = 0.0;
+      for (int q = rp[i]; q < rp[i + 1]; ++q)
+        if (ci[q] == i) aii = std::fabs(v[q]);
+      int cnt = 0;
+      for (int q = rp[i]; q < rp[i + 1]; ++q)
+        if (ci[q] == i || std::fabs(v[q]) >= A.sparsify * aii) {
+          keep[q] = 1;
+          ++cnt;
+        }
+      sp.rp[i + 1] = sp.rp[i] + cnt;
+    }
+    sp.ci.resize(sp.rp[L.n]);
+    for (int i = 0, qs = 0; i < L.n; ++i)
+      for (int q = rp[i]; q < rp[i + 1]; ++q)
+        if (keep[q]) sp.ci[qs++] = ci[q];
+    if (sp.ci.size() * 10 > ci.size() * 9) continue;   // under 10 % to drop: not worth a second copy
+    Csr& S = L.As;
+    S.n = L.n;
+    S.nnz = (long long)sp.ci.size();
+    upload(S.rp, sp.rp);
+    upload(S.ci, sp.ci);
+    build_packed(S, sp);
+    if (!S.pk_ok) continue;
+    if (A.sell_max_avg > 0) {
+      const double avg = (double)sp.ci.size() / L.n;
+      int T = 1;
+      while (T < 32 && avg / T > A.sell_lane_nnz) T *= 2;
+      if (A.sell_force_t) T = A.sell_force_t;
+      if ((long long)L.n * T >= A.sell_min_rows && avg <= A.sell_max_avg) build_sell(S, sp, T);
+    }
+    upload(L.sp_keep, keep);
+    L.sp_ok = true;
+    if (getenv("HC_AMG_VERBOSE"))
+      fprintf(stderr, "amg field %d level %zu: sweeps on %zu of %zu entries (drop tolerance %g)\n", B.field, l,
+              sp.ci.size(), ci.size(), A.sparsify);
+  }
+}
+
 void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
   Amg& A = *op.amg;
   for (int f = 0; f < 2; ++f) {
@@ -1180,14 +1297,27 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
       launch(k_gather_ptv, nblk((long long)L.P.nnz), TPB, 0, s, (long long)L.P.nnz, L.pt_idx.p, L.P.v.p,
                                                            L.ptv.p); HC_COUNT();
       if (A.fp32_coarse && L.P.nnz) {   // fp32 transfer values for the cycle (restriction / prolongation)
+        static const int pround = getenv("HC_AMG_PROUND") ? atoi(getenv("HC_AMG_PROUND")) : 0;
+        if (pround > 0) {
+          launch(k_round_lead, nblk(L.n), TPB, 0, s, L.n, 23 - pround, L.P.rp.p, (const double*)L.P.v.p, L.P.vf.p); HC_COUNT();
+          launch(k_gather_f, nblk(L.P.nnz), TPB, 0, s, (long long)L.P.nnz, L.pt_idx.p, (const float*)L.P.vf.p, L.ptvf.p); HC_COUNT();
+        } else {
         launch(k_to_float, nblk(L.P.nnz), TPB, 0, s, (long long)L.P.nnz, (const double*)L.ptv.p, L.ptvf.p); HC_COUNT();
         launch(k_to_float, nblk(L.P.nnz), TPB, 0, s, (long long)L.P.nnz, (const double*)L.P.v.p, L.P.vf.p); HC_COUNT();
+        }
       }
       launch(k_ap_w, nblk(32LL * L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.P.rp.p, L.P.ci.p, L.P.v.p,
                                      L.AP.rp.p, L.AP.ci.p, L.AP.v.p); HC_COUNT();
       launch(k_ptap_w, nblk(32LL * U.n), TPB, 0, s, U.n, L.pt_ptr.p, L.pt_row.p, L.pt_idx.p, L.P.v.p,
                                             L.AP.rp.p, L.AP.ci.p, L.AP.v.p, U.A.rp.p, U.A.ci.p,
                                             U.A.v.p); HC_COUNT();
+    }
+    if (!B.sp_done) {
+      // the sweep patterns are fixed at the block's first numeric setup, which must be an
+      // eager one (the solver runs one before it captures its graphs); a block first set up
+      // inside a capture keeps its full operators for good
+      B.sp_done = true;
+      if (!op.capturing && A.sparsify > 0.0 && A.pack && A.fp32_coarse) sparsify_block(A, B, s);
     }
     for (size_t l = 1; l < B.levels.size(); ++l) {
       AmgLevel& L = B.levels[l];
@@ -1197,7 +1327,17 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
           launch(k_sell_gather, nblk(L.A.sl_nnz), TPB, 0, s, L.A.sl_nnz, L.A.sl_map.p, L.A.vf.p, L.A.sl_vf.p);
           HC_COUNT();
         }
-        if (L.A.pk_ok) {
+        if (L.sp_ok) {
+          Csr& S = L.As;
+          launch(k_pack_rows_sp, nblk(L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, (const double*)L.A.v.p,
+                 (const uint8_t*)L.sp_keep.p, S.rp.p, (const uint16_t*)S.pk_off.p, S.pk.p, S.pk_diag.p);
+          HC_COUNT();
+          if (S.sl_n && S.sl_base.n) {
+            launch(k_sell_pack, nblk(S.sl_nnz), TPB, 0, s, S.sl_nnz, S.sl_map.p, (const uint16_t*)S.sl_off.p,
+                   (const uint32_t*)S.pk.p, S.sl_pk.p);
+            HC_COUNT();
+          }
+        } else if (L.A.pk_ok) {
           launch(k_pack_rows, nblk(L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, (const double*)L.A.v.p,
                  (const uint16_t*)L.A.pk_off.p, L.A.pk.p, L.A.pk_diag.p);
           HC_COUNT();
@@ -1435,15 +1575,16 @@ template <int XM>
 static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha, const CV* b,
                         const CV* x, const int32_t* parent, const CV* xc, CV* y,
                         int resid, cudaStream_t s, CV* x0 = nullptr) {
-  if (A.fp32_coarse && L.A.sl_n && L.A.pk_ok && L.A.sl_base.n) {
+  const Csr& S = L.sp_ok ? L.As : L.A;   // the sweeps' operator: sparsified copy where there is one
+  if (A.fp32_coarse && S.sl_n && S.pk_ok && S.sl_base.n) {
     auto go = [&](auto t_tag) {
       constexpr int T = decltype(t_tag)::value;
       const long long threads = ((long long)L.n + 32 / T - 1) / (32 / T) * 32;
-      launch(k_sell_xp<T, XM>, nblk(threads), TPB, 0, s, L.n, w, alpha, L.A.sl_ptr.p, L.A.sl_base.p,
-             (const uint32_t*)L.A.sl_pk.p, (const float*)L.A.pk_diag.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
+      launch(k_sell_xp<T, XM>, nblk(threads), TPB, 0, s, L.n, w, alpha, S.sl_ptr.p, S.sl_base.p,
+             (const uint32_t*)S.sl_pk.p, (const float*)S.pk_diag.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
       HC_COUNT();
     };
-    switch (L.A.sl_t) {
+    switch (S.sl_t) {
       case 1: go(std::integral_constant<int, 1>{}); break;
       case 2: go(std::integral_constant<int, 2>{}); break;
       case 4: go(std::integral_constant<int, 4>{}); break;
@@ -1453,7 +1594,7 @@ static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha,
     }
     return;
   }
-  if (A.fp32_coarse && L.A.sl_n) {
+  if (A.fp32_coarse && L.A.sl_n && !L.sp_ok) {
     auto go = [&](auto t_tag) {
       constexpr int T = decltype(t_tag)::value;
       const long long threads = ((long long)L.n + 32 / T - 1) / (32 / T) * 32;
@@ -1471,13 +1612,13 @@ static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha,
     }
     return;
   }
-  double avg = L.n ? (double)L.A.nnz / L.n : 0.0;
+  double avg = L.n ? (double)S.nnz / L.n : 0.0;
   const int VSsel = avg <= 12.0 ? 1 : (avg <= 48.0 ? 8 : 32);
-  if (A.fp32_coarse && L.A.pk_ok) {
+  if (A.fp32_coarse && S.pk_ok) {
     auto gop = [&](auto vs_tag) {
       constexpr int VS = decltype(vs_tag)::value;
-      launch(k_csr_xp<VS, XM>, nblk((long long)VS * L.n), TPB, 0, s, L.n, w, alpha, L.A.rp.p, L.A.pk_base.p,
-             (const uint32_t*)L.A.pk.p, (const float*)L.A.pk_diag.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
+      launch(k_csr_xp<VS, XM>, nblk((long long)VS * L.n), TPB, 0, s, L.n, w, alpha, S.rp.p, S.pk_base.p,
+             (const uint32_t*)S.pk.p, (const float*)S.pk_diag.p, L.dinvc.p, b, x, parent, xc, y, resid, x0);
       HC_COUNT();
     };
     if (VSsel == 1) gop(std::integral_constant<int, 1>{});
@@ -1513,7 +1654,7 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
       std::swap(L.x.p, L.x2.p);
     }
   }
-  if (pre >= 2 && L.R.nnz) {
+  if (pre >= 2 && L.R.nnz && !L.sp_ok) {
     // residual and restriction in one pass: U.b = P^T b - (P^T A) x
     const double avg = U.n ? (double)L.R.nnz / U.n : 0.0;
     auto go = [&](auto vs_tag, auto* vals) {

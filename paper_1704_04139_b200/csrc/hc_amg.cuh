@@ -56,6 +56,13 @@ struct AmgLevel {
   DBuf<float> ptvf;                      // fp32 copy used by the cycle's restriction
   DBuf<CV> x, x2, b, res, acc;           // cycle vectors (levels >= 1)
   DBuf<CV> dinvc;                        // D^-1 for the cycle (levels >= 1)
+  // sparsified sweep operator (levels >= 1 with long rows): the entries with |a_ij| >=
+  // sparsify * |a_ii| at the first numeric setup keep their place, everything else is lumped
+  // onto the diagonal at every setup (row sums preserved).  Only the sweeps read it (packed
+  // copies only); the Galerkin products keep the full pattern.
+  bool sp_ok = false;
+  Csr As;                                // rp / ci of the kept pattern + packed copies
+  DBuf<uint8_t> sp_keep;                 // per entry of A: kept (1) or lumped (0)
 };
 
 // device view of one CSR level for the cluster-fused coarse cycle (hc_amg.cu)
@@ -79,6 +86,7 @@ struct AmgBlock {
   int field = 0;                  // 0: c block of T J, 1: phi block of J
   double alpha = 1.0;             // coarse-correction scaling
   std::vector<AmgLevel> levels;   // levels[0] is the fine grid
+  bool sp_done = false;           // the sparsified sweep patterns were decided (first numeric setup)
   DBuf<double> dense, dense_inv;  // coarsest matrix and its inverse
   int fuse_from = -1;             // levels >= fuse_from run as one cluster kernel (-1: none)
   DBuf<CoarseLev> clev;           // their device views
@@ -124,6 +132,8 @@ struct Amg {
   int coarsen = 2;           // block growth factor of the transfers above level 1              // gamma cycles on CSR levels wmin..wdepth
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int sa_filter = 0;         // bit l: filtered smoothing of the phi transfer from level l
+  double sparsify = 0.003;   // drop tolerance of the sparsified sweep operators (0: off; HC_AMG_SPARSIFY)
+  double sparsify_avg = 40;  // ... on levels with more nonzeros per row than this (HC_AMG_SPARSIFY_AVG)
   bool pack = true;          // packed (bf16 value | 16-bit column offset) level operators for the sweeps
   int sell_max_avg = 512;    // levels with at most this many nonzeros per row and at least
   int sell_min_rows = 131072; // sell_min_rows threads (rows x lanes per row) sweep through the

@@ -503,6 +503,13 @@ static void build_newton_graph(Operator& op, NewtonGraph& NG, const double* npl,
   double* ns = NG.ns.p;
   cudaGraph_t outer;
   HC_CUDA(cudaGraphCreate(&outer, 0));
+  // the multigrid's sparsified sweep patterns are decided at each block's first numeric
+  // setup, which has to be an eager one: run it here when no solve has done so yet
+  if (op.amg && !(op.amg->blk[0].sp_done && op.amg->blk[1].sp_done)) {
+    linearize(op, W.x.p, npl, beta, s);
+    amg_update(op, inv_dt, 3, s);
+    op.amg->force = true;   // (the first solve still rebuilds the hierarchy at its own state)
+  }
   const unsigned long long c0 = t_launch_count;
   op.capturing = true;
   try {
