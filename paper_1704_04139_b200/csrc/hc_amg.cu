@@ -695,35 +695,6 @@ __global__ void k_resid_restrict(int n1, const int32_t* __restrict__ pt_ptr, con
   if (ok && lane == 0) b1[I] = (CV)s;
 }
 
-// experiment (HC_AMG_PROUND=m): transfer values rounded to m mantissa bits, except each row's
-// largest entry, which absorbs the row's rounding errors (row sums of P preserved); the
-// transposed copy is gathered from the rounded values
-__global__ void k_round_lead(int n, int drop, const int32_t* __restrict__ rp, const double* __restrict__ a,
-                             float* __restrict__ b) {
-  pdl_wait();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int ql = -1;
-  double big = -1.0;
-  for (int q = rp[i]; q < rp[i + 1]; ++q)
-    if (fabs(a[q]) > big) { big = fabs(a[q]); ql = q; }
-  double err = 0.0;
-  for (int q = rp[i]; q < rp[i + 1]; ++q) {
-    if (q == ql) continue;
-    unsigned u = __float_as_uint((float)a[q]);
-    u = (u + (1u << (drop - 1))) & ~((1u << drop) - 1u);
-    const float v = __uint_as_float(u);
-    err += a[q] - (double)v;
-    b[q] = v;
-  }
-  if (ql >= 0) b[ql] = (float)(a[ql] + err);
-}
-__global__ void k_gather_f(long long n, const int32_t* __restrict__ idx, const float* __restrict__ v,
-                           float* __restrict__ out) {
-  pdl_wait();
-  long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (q < n) out[q] = v[idx[q]];
-}
 __global__ void k_gather_ptv(long long n, const int32_t* __restrict__ pt_idx,
                              const double* __restrict__ pv, double* __restrict__ ptv) {
   pdl_wait();
@@ -1297,14 +1268,8 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
       launch(k_gather_ptv, nblk((long long)L.P.nnz), TPB, 0, s, (long long)L.P.nnz, L.pt_idx.p, L.P.v.p,
                                                            L.ptv.p); HC_COUNT();
       if (A.fp32_coarse && L.P.nnz) {   // fp32 transfer values for the cycle (restriction / prolongation)
-        static const int pround = getenv("HC_AMG_PROUND") ? atoi(getenv("HC_AMG_PROUND")) : 0;
-        if (pround > 0) {
-          launch(k_round_lead, nblk(L.n), TPB, 0, s, L.n, 23 - pround, L.P.rp.p, (const double*)L.P.v.p, L.P.vf.p); HC_COUNT();
-          launch(k_gather_f, nblk(L.P.nnz), TPB, 0, s, (long long)L.P.nnz, L.pt_idx.p, (const float*)L.P.vf.p, L.ptvf.p); HC_COUNT();
-        } else {
         launch(k_to_float, nblk(L.P.nnz), TPB, 0, s, (long long)L.P.nnz, (const double*)L.ptv.p, L.ptvf.p); HC_COUNT();
         launch(k_to_float, nblk(L.P.nnz), TPB, 0, s, (long long)L.P.nnz, (const double*)L.P.v.p, L.P.vf.p); HC_COUNT();
-        }
       }
       launch(k_ap_w, nblk(32LL * L.n), TPB, 0, s, L.n, L.A.rp.p, L.A.ci.p, L.A.v.p, L.P.rp.p, L.P.ci.p, L.P.v.p,
                                      L.AP.rp.p, L.AP.ci.p, L.AP.v.p); HC_COUNT();
