@@ -1152,6 +1152,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_PACK")) amg->pack = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_SPARSIFY")) amg->sparsify = atof(e);
   if (const char* e = getenv("HC_AMG_SPARSIFY_AVG")) amg->sparsify_avg = atof(e);
+  if (const char* e = getenv("HC_AMG_SPARSIFY_ROWS")) amg->sparsify_min_rows = atoi(e);
   if (const char* e = getenv("HC_AMG_SELL")) amg->sell_max_avg = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_FILTER")) amg->sa_filter = atoi(e);
   if (const char* e = getenv("HC_AMG_SELL_ROWS")) amg->sell_min_rows = atoi(e);
@@ -1199,7 +1200,7 @@ static void sparsify_block(const Amg& A, AmgBlock& B, cudaStream_t s) {
   const size_t lend = B.fuse_from >= 1 ? (size_t)B.fuse_from : B.levels.size() - 1;
   for (size_t l = 1; l < lend && l + 1 < B.levels.size(); ++l) {
     AmgLevel& L = B.levels[l];
-    if (!L.A.pk_ok || !L.n || (double)L.A.nnz / L.n <= A.sparsify_avg) continue;
+    if (!L.A.pk_ok || L.n < A.sparsify_min_rows || (double)L.A.nnz / L.n <= A.sparsify_avg) continue;
     std::vector<int32_t> rp(L.n + 1), ci(L.A.nnz);
     std::vector<double> v(L.A.nnz);
     HC_CUDA(cudaMemcpy(rp.data(), L.A.rp.p, rp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));

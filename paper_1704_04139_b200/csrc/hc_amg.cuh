@@ -133,6 +133,7 @@ struct Amg {
   bool fp32_coarse = true;   // coarse-level sweeps read fp32 matrix values
   int sa_filter = 0;         // bit l: filtered smoothing of the phi transfer from level l
   double sparsify = 0.003;   // drop tolerance of the sparsified sweep operators (0: off; HC_AMG_SPARSIFY)
+  int sparsify_min_rows = 1024;   // ... and at least this many rows (smaller levels are latency-bound)
   double sparsify_avg = 20;  // ... on levels with more nonzeros per row than this (HC_AMG_SPARSIFY_AVG)
   bool pack = true;          // packed (bf16 value | 16-bit column offset) level operators for the sweeps
   int sell_max_avg = 512;    // levels with at most this many nonzeros per row and at least
