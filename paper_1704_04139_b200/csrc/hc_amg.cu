@@ -1150,6 +1150,7 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT")) amg->fuse_restrict = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_FUSE_RESTRICT_SA")) amg->fuse_restrict_sa = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_PACK")) amg->pack = atoi(e) != 0;
+  if (const char* e = getenv("HC_AMG_SKIP_PLANES")) amg->skip_planes = atoi(e) != 0;
   if (const char* e = getenv("HC_AMG_SPARSIFY")) amg->sparsify = atof(e);
   if (const char* e = getenv("HC_AMG_SPARSIFY_AVG")) amg->sparsify_avg = atof(e);
   if (const char* e = getenv("HC_AMG_SPARSIFY_ROWS")) amg->sparsify_min_rows = atoi(e);
@@ -1178,12 +1179,19 @@ Amg* build_amg(const Operator& op) {
     amg->rs[f].alloc(nvox);
     amg->ea[f].alloc(nvox);
     amg->eb[f].alloc(nvox);
+    // (zeroed: the c-block sweeps skip the planes without c rows and rely on zeros there)
+    HC_CUDA(cudaMemset(amg->rs[f].p, 0, nvox * sizeof(double)));
+    HC_CUDA(cudaMemset(amg->ea[f].p, 0, nvox * sizeof(double)));
+    HC_CUDA(cudaMemset(amg->eb[f].p, 0, nvox * sizeof(double)));
   }
   amg->res.alloc(nvox);
   amg->rc2.alloc(nvox);
+  HC_CUDA(cudaMemset(amg->res.p, 0, nvox * sizeof(double)));
+  HC_CUDA(cudaMemset(amg->rc2.p, 0, nvox * sizeof(double)));
   if (const char* e = getenv("HC_AMG_BDIAG")) amg->bdiag = atoi(e) != 0;
   if (amg->bdiag) {
     amg->res_c.alloc(nvox);
+    HC_CUDA(cudaMemset(amg->res_c.p, 0, nvox * sizeof(double)));
     HC_CUDA(cudaStreamCreateWithFlags(&amg->side, cudaStreamNonBlocking));
     HC_CUDA(cudaEventCreateWithFlags(&amg->ev_fork, cudaEventDisableTiming));
     HC_CUDA(cudaEventCreateWithFlags(&amg->ev_join, cudaEventDisableTiming));
@@ -1759,6 +1767,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   const int nb = nblk(nv);
   FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
              op.if_cslot.p, op.elz.p, nullptr, op.tp_off.p};
+  if (A.skip_planes) F.cz = op.cz;
   const dim3 vg = vox_grid(op.P), vb = vox_block();
   double* e = A.ea[f].p;
   double* e2 = A.eb[f].p;
@@ -1854,6 +1863,7 @@ static void amg_apply_impl(Operator& op, const double2* r, double2* z, double in
   // c-block right-hand side: T r_c - (T J)_cp e_phi
   FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
              op.if_cslot.p, op.elz.p, nullptr, op.tp_off.p};
+  if (A.skip_planes) F.cz = op.cz;
   fine_launch_op<SM_CP, EP_RESID>(op, F, nullptr, ep, A.rs[0].p, nullptr, 0.0, inv_dt, 0,
                                   nullptr, A.rc2.p, s);
   HC_COUNT();

@@ -135,6 +135,7 @@ struct Amg {
   double sparsify = 0.003;   // drop tolerance of the sparsified sweep operators (0: off; HC_AMG_SPARSIFY)
   int sparsify_min_rows = 1024;   // ... and at least this many rows (smaller levels are latency-bound)
   double sparsify_avg = 20;  // ... on levels with more nonzeros per row than this (HC_AMG_SPARSIFY_AVG)
+  bool skip_planes = true;   // c-block fine sweeps only over the planes that hold c rows (HC_AMG_SKIP_PLANES)
   bool pack = true;          // packed (bf16 value | 16-bit column offset) level operators for the sweeps
   int sell_max_avg = 512;    // levels with at most this many nonzeros per row and at least
   int sell_min_rows = 131072; // sell_min_rows threads (rows x lanes per row) sweep through the

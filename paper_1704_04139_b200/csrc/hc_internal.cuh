@@ -268,6 +268,7 @@ struct Operator {
   DBuf<int2> elz;              // TMA stencil: electrolyte z range per 32 x 8 tile column
   DBuf<double> if_islot;       // TMA residual: interface current per face slot
   DBuf<int32_t> tp_off;        // TMA stencil: first slot per (tile, plane), slots tile-plane ordered
+  int2 cz = {0, 0};            // planes [cz.x, cz.y) hold every c row (electrolyte / graphite voxels)
   DBuf<double> inv_c;          // gX / c per electrolyte voxel (linearized)
   DBuf<double> red;            // reduction scratch
   DBuf<double> host_x, host_npl;  // staging for the host-buffer entry point

@@ -908,6 +908,19 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
             t.x = std::min(t.x, z);
             t.y = std::max(t.y, z);
           }
+        {
+          int zlo = nz, zhi = -1;
+          for (int z = 0; z < nz; ++z) {
+            bool any = false;
+            for (long long v = (long long)z * nx * ny; v < (long long)(z + 1) * nx * ny && !any; ++v)
+              any = labels_host[v] == EL || labels_host[v] == GR;
+            if (any) {
+              zlo = std::min(zlo, z);
+              zhi = std::max(zhi, z);
+            }
+          }
+          op->cz = zhi >= zlo ? make_int2(zlo, zhi + 1) : make_int2(0, 0);
+        }
         op->elz.alloc(ez.size());
         HC_CUDA(cudaMemcpy(op->elz.p, ez.data(), ez.size() * sizeof(int2), cudaMemcpyHostToDevice));
         op->tma = new TmaCache();

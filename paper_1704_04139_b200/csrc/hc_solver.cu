@@ -332,7 +332,12 @@ Work& work(Operator& op) {
 
 Work::Work(long long nvox)
     : x(nvox), xt(nvox), r(nvox), rt(nvox), d(nvox), b(nvox), kr(nvox), khat(nvox), kp(nvox),
-      kv(nvox), ks(nvox), kt(nvox), kph(nvox), ksh(nvox), cprev(nvox), part(8192), parth(8192) {}
+      kv(nvox), ks(nvox), kt(nvox), kph(nvox), ksh(nvox), cprev(nvox), part(8192), parth(8192) {
+  // zeroed: the multigrid's c-block sweeps write only the planes that hold c rows; the c
+  // entries of every other plane are zero in all Krylov vectors and stay so
+  for (DBuf<double2>* b : {&x, &xt, &r, &rt, &d, &this->b, &kr, &khat, &kp, &kv, &ks, &kt, &kph, &ksh})
+    HC_CUDA(cudaMemset(b->p, 0, (size_t)nvox * sizeof(double2)));
+}
 
 static int red_blocks(const Operator& op) {
   return (int)std::min<long long>(nblk(op.P.nvox), 4LL * op.n_sm);

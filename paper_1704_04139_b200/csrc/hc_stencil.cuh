@@ -46,6 +46,9 @@ struct FineArgs {
   double* dot_part = nullptr;
   int dot_two = 0;
   int* dot_nblk = nullptr;
+  // TMA c-block sweeps (CONC / CP): planes [cz.x, cz.y) hold every c row (electrolyte and
+  // graphite voxels); empty (0, 0): sweep the whole grid
+  int2 cz = {0, 0};
 };
 
 }  // namespace hc

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(TmaLayout<MODE, EPI>::THREADS, HC_TMA_MINB)
 k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int32_t* __restrict__ labt,
            const double2* __restrict__ V, const double* __restrict__ e, const double* __restrict__ r,
            const double* __restrict__ dinv, double omega, double inv_dt, int flags,
-           double2* __restrict__ out2, double* __restrict__ out, int zc) {
+           double2* __restrict__ out2, double* __restrict__ out, int zc, int zb, int ze) {
   using L = TmaLayout<MODE, EPI>;
   constexpr bool FULLM = L::FULLM, X0 = L::X0;
   constexpr bool RES = MODE == SM_RES;
@@ -165,7 +165,8 @@ k_fine_tma(DevParams P, const __grid_constant__ TmaMaps M, FineArgs F, const int
   __shared__ int tp_start[T_S];   // first global face slot of the tile-plane staged in each ring slot
   const int nx = P.nx, ny = P.ny, nz = P.nz, nxy = (int)P.nxy;
   const int x0 = blockIdx.x * VX, y0 = blockIdx.y * VY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);   // planes z0 .. z1 are staged
+  // planes zb .. ze - 1 are computed (the whole grid, or the z range holding the field's rows)
+  const int z0 = zb + blockIdx.z * zc, z1 = min(z0 + zc, ze);   // planes z0 .. z1 are staged
   const int nplane = z1 - z0;                                // computed planes
   const unsigned full0 = (unsigned)__cvta_generic_to_shared(full);
   const unsigned empty0 = (unsigned)__cvta_generic_to_shared(empty);
@@ -623,12 +624,16 @@ inline bool fine_launch_tma(TmaCache& cache, const DevParams& P, const FineArgs&
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, smem);
       if (per_sm < 1) per_sm = 1;
     }
-    const int bz = pick_bz(bx, by, P.nz, per_sm, n_sm);
-    const int zc = (P.nz + bz - 1) / bz;
-    const dim3 grid(bx, by, (P.nz + zc - 1) / zc);
+    // the c-block modes sweep only the planes that hold c rows (F.cz; the buffers they write
+    // are zero outside and stay so: nothing else ever writes those entries)
+    const bool crange = (MODE == SM_CONC || MODE == SM_CP) && F.cz.y > F.cz.x;
+    const int zb = crange ? F.cz.x : 0, ze = crange ? F.cz.y : P.nz, nzr = ze - zb;
+    const int bz = pick_bz(bx, by, nzr, per_sm, n_sm);
+    const int zc = (nzr + bz - 1) / bz;
+    const dim3 grid(bx, by, (nzr + zc - 1) / zc);
     if (F.dot_nblk) *F.dot_nblk = (int)(grid.x * grid.y * grid.z);
     launch(kern, grid, dim3(VX, L::THREADS / VX, 1), smem, s, P, M, F, labt,
-           V, e, r, dinv, omega, inv_dt, flags, out2, out, zc);
+           V, e, r, dinv, omega, inv_dt, flags, out2, out, zc, zb, ze);
   };
   if (MODE == SM_FULL && (flags & 4)) go(std::true_type{});
   else go(std::false_type{});
