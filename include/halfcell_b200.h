@@ -89,6 +89,12 @@ int hc_operator_create(const uint8_t* labels_host, int32_t nx, int32_t ny, int32
                        double voxel_size_um, const hc_params* params, hc_operator** out);
 int hc_operator_destroy(hc_operator* op);
 int hc_operator_info(const hc_operator* op, hc_info* out);
+/* SystemOperator(dofmap, params) on a geometry that build_dofmap already classified
+ * (fvm/operator.py:109-119: the reference also keeps the Dofmap and only reads the material
+ * parameters in its constructor): replaces the operator's material parameters.  The geometry
+ * (DOF numbering, face lists, slots) does not depend on them; every parameter-dependent
+ * cache (multigrid values, captured solver graphs) is dropped. */
+int hc_operator_set_params(hc_operator* op, const hc_params* params);
 
 /* Export index arrays in the reference's layout into host int64 buffers.
  * what: 0 c_dof[n_vox], 1 p_dof[n_vox], 2 plated_voxels[n_plated], 3 dirichlet[n_dirichlet],

@@ -64,6 +64,7 @@ _SIGS = {
                                           ctypes.POINTER(HcParams),
                                           ctypes.POINTER(ctypes.c_void_p)]),
     "hc_operator_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "hc_operator_set_params": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "hc_operator_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HcInfo)]),
     "hc_operator_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
     "hc_apply": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,

@@ -137,6 +137,24 @@ int hc_operator_destroy(hc_operator* op) {
   return guarded([&] { delete (Operator*)op; });
 }
 
+int hc_operator_set_params(hc_operator* opq, const hc_params* params) {
+  return guarded([&] {
+    if (!opq || !params) throw Error(HC_ERR_ARGUMENT, "null argument");
+    Operator& op = *(Operator*)opq;
+    set_params(op, *params);
+    // everything derived from the old parameters: captured graphs hold DevParams by value,
+    // the multigrid hierarchy its Galerkin values
+    destroy_krylov_graphs(op.kg);
+    op.kg = nullptr;
+    destroy_newton_graph(op.ng);
+    op.ng = nullptr;
+    delete op.amg;
+    op.amg = nullptr;
+    delete op.work;
+    op.work = nullptr;
+  });
+}
+
 int hc_operator_info(const hc_operator* op, hc_info* out) {
   return guarded([&] { *out = ((const Operator*)op)->info; });
 }

@@ -238,6 +238,7 @@ void destroy_krylov_graphs(KrylovGraphs* g);
 struct Operator {
   DevParams P;
   hc_params host_params;
+  double voxel_um = 1.0;
   hc_info info;
   int n_sm = 148;
 
@@ -267,6 +268,7 @@ struct Operator {
   DBuf<double> if_cslot;       // TMA stencil: (alpha, beta, gamma) per interface face slot
   DBuf<int2> elz;              // TMA stencil: electrolyte z range per 32 x 8 tile column
   DBuf<double> if_islot;       // TMA residual: interface current per face slot
+  DBuf<double> if_cur;         // cp.async residual: interface current per face
   DBuf<int32_t> tp_off;        // TMA stencil: first slot per (tile, plane), slots tile-plane ordered
   int2 cz = {0, 0};            // planes [cz.x, cz.y) hold every c row (electrolyte / graphite voxels)
   DBuf<double> inv_c;          // gX / c per electrolyte voxel (linearized)
@@ -329,6 +331,8 @@ int jvp_grid_dot(Operator& op, const double2* vg, double inv_dt, int flags, doub
 double norm2_grid(Operator& op, const double2* v, int field_mask, cudaStream_t s);
 Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, double voxel_um,
                           const hc_params& hp);
+// new material parameters on the same geometry (DevParams, info); the caller drops the caches
+void set_params(Operator& op, const hc_params& hp);
 
 }  // namespace hc
 

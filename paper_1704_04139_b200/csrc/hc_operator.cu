@@ -264,12 +264,13 @@ __global__ void k_gather(int n_c, int n_p, const int32_t* __restrict__ c_vox,
   if (i < n_p) x[n_c + i] = xg[p_vox[i]].y;
 }
 
-// Interface currents over the compacted face list (operator.py:331-357).
+// Interface currents over the compacted face list (operator.py:331-357), cp.async stencil
+// path (grids without tensor-map tiles): one current per face ...
 __global__ void __launch_bounds__(TPB) k_residual_iface(
     DevParams P, long long n_if, const int32_t* __restrict__ so, const int32_t* __restrict__ el,
     const int32_t* __restrict__ slot, const int8_t* __restrict__ kind,
     const double2* __restrict__ X, const double* __restrict__ npl, double beta,
-    double2* __restrict__ out) {
+    double* __restrict__ cur) {
   long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (f >= n_if) return;
   int32_t s = so[f], e = el[f];
@@ -285,11 +286,37 @@ __global__ void __launch_bounds__(TPB) k_residual_iface(
   } else {
     i = strip_current_dev(xe.x, xs.y, xe.y, npl[slot[f]], beta, P, nullptr, nullptr);
   }
-  double q = P.sc * i;
-  if (k == IF_BV) atomicAdd(&out[s].x, q);
-  atomicAdd(&out[s].y, q);
-  atomicAdd(&out[e].x, -q);
-  atomicAdd(&out[e].y, -q);
+  cur[f] = P.sc * i;
+}
+// ... gathered per interface voxel over its faces in direction order (fixed order, no
+// floating-point atomics): the solid row takes +i (its c row only on BV faces), the
+// electrolyte row -i on both equations
+__global__ void __launch_bounds__(TPB) k_residual_iface_gather(
+    long long nvox, const int32_t* __restrict__ rank, const int32_t* __restrict__ dirs,
+    const int32_t* __restrict__ so, const int8_t* __restrict__ kind, const double* __restrict__ cur,
+    double2* __restrict__ out) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= nvox) return;
+  const int rk = rank[v];
+  if (rk < 0) return;
+  double dc = 0.0, dp = 0.0;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    const int f = dirs[6LL * rk + d];
+    if (f < 0) continue;
+    const double q = cur[f];
+    if (so[f] == (int32_t)v) {
+      if (kind[f] == IF_BV) dc += q;
+      dp += q;
+    } else {
+      dc -= q;
+      dp -= q;
+    }
+  }
+  double2 o = out[v];
+  o.x += dc;
+  o.y += dp;
+  out[v] = o;
 }
 
 // The same currents written once per face slot, oriented from each side's row (solid
@@ -467,10 +494,14 @@ void residual_grid(Operator& op, const double2* xg, const double* npl, double mu
     res_launch_p(op.P, op.lab4.p, xg, mu, parts, cprev, inv_dt, out, op.n_sm, s);
     HC_COUNT();
   }
-  if ((which & 2) && (parts & PART_BV) && op.n_if)
+  if ((which & 2) && (parts & PART_BV) && op.n_if) {
     k_residual_iface<<<blocks_for(op.n_if), TPB, 0, s>>>(op.P, op.n_if, op.if_solid.p,
                                                          op.if_el.p, op.if_slot.p, op.if_kind.p,
-                                                         xg, npl, beta, out); HC_COUNT();
+                                                         xg, npl, beta, op.if_cur.p); HC_COUNT();
+    k_residual_iface_gather<<<blocks_for(op.P.nvox), TPB, 0, s>>>(op.P.nvox, op.if_rank.p, op.if_dir.p,
+                                                                  op.if_solid.p, op.if_kind.p,
+                                                                  op.if_cur.p, out); HC_COUNT();
+  }
   HC_CHECK_LAUNCH();
 }
 
@@ -695,6 +726,7 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
 
   auto op = std::make_unique<Operator>();
   op->host_params = hp;
+  op->voxel_um = voxel_um;
   op->P = make_dev_params(hp, nx, ny, nz, voxel_um);
   int dev = 0;
   HC_CUDA(cudaGetDevice(&dev));
@@ -963,12 +995,21 @@ Operator* create_operator(const uint8_t* labels_host, int nx, int ny, int nz, do
   op->cprev.alloc(nvox);
   op->inv_c.alloc(nvox);
   op->if_coef.alloc(std::max<long long>(3 * op->n_if, 1));
+  op->if_cur.alloc(std::max<long long>(op->n_if, 1));
   op->if_vcoef.alloc(3 * op->if_dir.n);
   HC_CUDA(cudaMemset(op->if_vcoef.p, 0, op->if_vcoef.n * sizeof(double)));
   op->npl.alloc(std::max<long long>(op->info.n_plated, 1));
   op->red.alloc(4096);
   HC_CUDA(cudaDeviceSynchronize());
   return op.release();
+}
+
+void set_params(Operator& op, const hc_params& hp) {
+  HC_CUDA(cudaDeviceSynchronize());
+  op.host_params = hp;
+  op.P = make_dev_params(hp, op.P.nx, op.P.ny, op.P.nz, op.voxel_um);
+  op.info.n_const = op.P.n_const;
+  op.info.scale = op.P.sc;
 }
 
 }  // namespace hc

@@ -11,7 +11,7 @@ no counter collector to ground) runs in the CUDA library and raises the same
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -36,6 +36,13 @@ class NativeOperator:
         info = _native.HcInfo()
         _native.check(L.hc_operator_info(h, ctypes.byref(info)))
         self.info = info
+
+    def set_params(self, params: MaterialParams) -> None:
+        """New material parameters on the same classified geometry (``hc_operator_set_params``)."""
+        cp = to_c_params(params)
+        _native.check(_native.lib().hc_operator_set_params(self.handle, ctypes.byref(cp)))
+        self._cp = cp
+        _native.check(_native.lib().hc_operator_info(self.handle, ctypes.byref(self.info)))
 
     def export(self, what: int, length: int) -> np.ndarray:
         out = np.empty(max(length, 0), dtype=np.int64)
@@ -64,6 +71,14 @@ class Dofmap:
     n_p: int
     plated_voxels: np.ndarray
     dirichlet: np.ndarray
+    # the device operator build_dofmap classified the geometry with; the first SystemOperator
+    # built on this Dofmap takes it over (new parameters, same geometry) instead of
+    # classifying the grid a second time
+    _nat: "NativeOperator | None" = field(default=None, repr=False, compare=False)
+
+    def take_native(self) -> "NativeOperator | None":
+        nat, self._nat = self._nat, None
+        return nat
 
     @property
     def n_total(self) -> int:
@@ -101,6 +116,9 @@ def build_dofmap(grid: PhaseGrid) -> Dofmap:
     """Number the DOFs and validate the grid (reference ``dofmap.py:71-101``)."""
     nat = NativeOperator(grid, MaterialParams())
     try:
-        return dofmap_from_native(grid, nat)
-    finally:
+        dof = dofmap_from_native(grid, nat)
+    except BaseException:
         nat.close()
+        raise
+    dof._nat = nat
+    return dof

@@ -67,7 +67,12 @@ class SystemOperator:
         self.voxel_volume = self.h ** 3
         self.n_const = params.n_const(self.face_area)
         self._scale = 1.0 / (params.constants.F * self.h)
-        self.native = NativeOperator(dofmap.grid, params)
+        nat = dofmap.take_native()
+        if nat is not None:
+            nat.set_params(params)   # same geometry: no second classification pass
+            self.native = nat
+        else:
+            self.native = NativeOperator(dofmap.grid, params)
         info = self.native.info
         if int(info.n_c) != dofmap.n_c or int(info.n_p) != dofmap.n_p:
             raise ModelError("dofmap does not belong to this grid")

@@ -182,3 +182,30 @@ def test_device_resident_state_steps_like_host_state(case):
     assert np.allclose(hb.c, a.c, rtol=1e-9, atol=0) and np.allclose(hb.phi, a.phi, rtol=0, atol=1e-9)
     assert np.allclose(hb.n_pl, a.n_pl, rtol=1e-9, atol=0)
     assert P.qoi_cell_voltage(b, dof) == pytest.approx(P.qoi_cell_voltage(a, dof), rel=1e-9)
+
+
+def test_system_operator_takes_over_the_dofmap_geometry():
+    """``SystemOperator(dofmap, params)`` re-parametrises the device geometry that
+    ``build_dofmap`` classified (``hc_operator_set_params``) instead of classifying the grid
+    twice; it must equal an operator built from scratch with those parameters, bit for bit,
+    after work that depends on the parameters (multigrid, solver graphs) has run."""
+    P = _P()
+    g = load_golden(golden_cases()[0])
+    soc, i00pl = g["params"]
+    params = P.MaterialParams(soc_init=float(soc), i00_plel=float(i00pl), kappa_el=0.8, i00_grel=3.0e-4)
+    grid = P.PhaseGrid(g["labels"], float(g["voxel_size"]))
+    dof = P.build_dofmap(grid)
+    assert dof._nat is not None
+    handed = P.SystemOperator(dof, params)      # takes the Dofmap's device operator
+    assert dof._nat is None
+    fresh = P.SystemOperator(dof, params)       # nothing left to take: classifies again
+    assert handed.native is not fresh.native
+    x, n_pl, mu, beta, v, dt = g["x"], g["n_pl"], float(g["mu"]), float(g["beta"]), g["v"], float(g["dt"])
+    assert handed.n_const == fresh.n_const and handed.gX == fresh.gX
+    assert np.array_equal(handed.apply(x, n_pl, mu, beta=beta), fresh.apply(x, n_pl, mu, beta=beta))
+    assert np.array_equal(handed.jvp(x, n_pl, v, beta=beta), fresh.jvp(x, n_pl, v, beta=beta))
+    cfg = P.SolverConfig()
+    a = P.newton_solve(handed, x, dt, x, n_pl, mu, cfg)
+    b = P.newton_solve(fresh, x, dt, x, n_pl, mu, cfg)
+    assert a.n_iter == b.n_iter and a.krylov_iters == b.krylov_iters
+    assert np.array_equal(a.x, b.x)
