@@ -7,7 +7,9 @@ for v in "$@"; do
   make -s -C $C clean >/dev/null
   make -s -j8 -C $C EXTRA="$v" >/dev/null 2>&1 || { echo "[$v] build failed"; continue; }
   regs=$(grep -A3 "k_fine_tmaILi0ELi0ELb1" $C/hc_operator.o.ptxas.log | grep -o "Used [0-9]* registers" | head -1)
+  spill=$(grep -A3 "k_fine_tmaILi0ELi0ELb1" $C/hc_operator.o.ptxas.log | grep -o "[0-9]* bytes spill stores" | head -1)
+  k=$(timeout 200 python tools/jv_time.py large 20 2>&1 | tail -1)
   r=$(bash tools/quick_bench.sh --steps ${STEPS:-10} --warmup 3 2>&1 | tail -1)
-  echo "[$v] $regs | $r"
+  echo "[$v] $regs, $spill | $k | $r"
 done
 make -s -C $C clean >/dev/null; make -s -j8 -C $C >/dev/null 2>&1
