@@ -1130,6 +1130,14 @@ Amg* build_amg(const Operator& op) {
   if (const char* e = getenv("HC_AMG_NU_C")) amg->nu_c = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_C")) amg->sa_levels_c = atoi(e);
   if (const char* e = getenv("HC_AMG_OMEGA")) amg->omega = atof(e);
+  amg->w_pre = amg->w_post0 = amg->w_post1 = amg->wf_pre = amg->wf_post = amg->omega;
+  if (const char* e = getenv("HC_AMG_W_PRE")) amg->w_pre = atof(e);
+  if (const char* e = getenv("HC_AMG_W_POST0")) amg->w_post0 = atof(e);
+  if (const char* e = getenv("HC_AMG_W_POST1")) amg->w_post1 = atof(e);
+  if (const char* e = getenv("HC_AMG_WF_PRE")) amg->wf_pre = atof(e);
+  if (const char* e = getenv("HC_AMG_WF_POST")) amg->wf_post = atof(e);
+  amg->wf_post1 = amg->omega;
+  if (const char* e = getenv("HC_AMG_WF_POST1")) amg->wf_post1 = atof(e);
   if (const char* e = getenv("HC_AMG_OMEGA_P")) amg->omega_p = atof(e);
   if (const char* e = getenv("HC_AMG_SA_LEVELS")) amg->sa_levels = atoi(e);
   if (const char* e = getenv("HC_AMG_SA_ROWS")) amg->sa_rows = atoi(e);
@@ -1618,7 +1626,11 @@ static void csr_sweep_x(const Amg& A, const AmgLevel& L, double w, double alpha,
 static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   AmgLevel& L = B.levels[l];
   AmgLevel& U = B.levels[l + 1];
-  const double w = A.omega;
+  // per-sweep Jacobi weights (all A.omega unless set): two post sweeps with the reciprocals of
+  // the degree-2 Chebyshev roots of [lmax / a, lmax] damp that interval by the Chebyshev
+  // polynomial instead of (1 - w l)^2
+  const double w = A.w_pre;
+  auto wpost = [&](int k) { return k == 0 ? A.w_post0 : (k == 1 ? A.w_post1 : A.omega); };
   // pre-smoothing from a zero guess: the first sweep materialises x0 = w D^-1 b itself
   int pre = B.pre_c;
   if (pre >= 2) {
@@ -1664,10 +1676,10 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
   }
   solve_level(A, B, l + 1, s);
   const bool tentative = L.P.nnz == (long long)L.n;  // one prolongator entry per row
-  int post = B.post_c;
+  int post = B.post_c, kp = 0;
   if (tentative && post >= 1) {
     // prolongation fused into the first post-sweep (P0 entries are all 1)
-    csr_sweep_x<2>(A, L, w, B.alpha, L.b.p, L.x.p, L.parent.p, U.x.p, L.x2.p, 0, s);
+    csr_sweep_x<2>(A, L, wpost(kp++), B.alpha, L.b.p, L.x.p, L.parent.p, U.x.p, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
     --post;
   } else {
@@ -1679,7 +1691,7 @@ static void cycle_once(const Amg& A, AmgBlock& B, size_t l, cudaStream_t s) {
                                             L.x.p); HC_COUNT();
   }
   for (int k = 0; k < post; ++k) {
-    csr_sweep_x<0>(A, L, w, 0.0, L.b.p, L.x.p, nullptr, nullptr, L.x2.p, 0, s);
+    csr_sweep_x<0>(A, L, wpost(kp++), 0.0, L.b.p, L.x.p, nullptr, nullptr, L.x2.p, 0, s);
     std::swap(L.x.p, L.x2.p);
   }
 }
@@ -1763,7 +1775,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
   AmgBlock& B = A.blk[f];
   AmgLevel& L0 = B.levels[0];
   const long long nv = op.P.nvox;
-  const double w = A.omega;
+  double w = A.wf_pre;   // weight of the sweep being launched (pre, then post)
   const int nb = nblk(nv);
   FineArgs F{op.labels.p, op.if_rank.p, op.if_vcoef.p, (long long)op.if_dir.n, op.inv_c.p,
              op.if_cslot.p, op.elz.p, nullptr, op.tp_off.p};
@@ -1822,6 +1834,7 @@ static double* vcycle_fine(Operator& op, int f, const double* r, double inv_dt, 
     launch(k_prolong0_s<double>, nb, TPB, 0, s, nv, B.alpha, L0.P.rp.p, L0.P.ci.p, (const double*)L0.P.v.p, L1.x.p, e);
   HC_COUNT();
   for (int k = 0; k < B.nu; ++k) {
+    w = k == 0 ? A.wf_post : A.wf_post1;
     if (dst && k + 1 == B.nu) {
       sweep(EP_SMOOTH, e, reinterpret_cast<double*>(dst) + f, FL_OSTRIDE2);
       HC_CHECK_LAUNCH();

@@ -112,6 +112,9 @@ struct Amg {
   int nu_c = 2;              // smoothing sweeps on the CSR levels
   int sa_levels_c = 0;       // smoothed transfers of the c block (plain aggregation suffices)
   double omega = 0.9;        // Jacobi smoothing weight
+  // per-sweep weights (default omega): CSR-level zero-guess pre-sweep, first / second post-sweep;
+  // fine-level pre (zero-guess) and post sweeps
+  double w_pre = 0.9, w_post0 = 0.9, w_post1 = 0.9, wf_pre = 0.9, wf_post = 0.9, wf_post1 = 0.9;
   double omega_p = 2.0 / 3;  // prolongator smoothing weight
   int sa_levels = 2;         // smoothed prolongators on the first sa_levels transfers
   // transfers past the sa_levels smoothed ones are smoothed too when their fine level has
