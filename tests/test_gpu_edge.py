@@ -1,5 +1,6 @@
 """GPU edge cases vs the CPU oracle: 1-D column cells, no plated lithium, plated
-lithium everywhere on the surface, ragged (non-multiple-of-tile) grid sizes."""
+lithium everywhere on the surface, ragged (non-multiple-of-tile) grid sizes on both
+stencil paths (cp.async for nx % 4 != 0, tensor-map tiles otherwise)."""
 
 import numpy as np
 import pytest
@@ -41,6 +42,12 @@ CASES = {
     "column_1x1x12": column(),
     "ragged_7x5x14_no_plating": slab(7, 5, 14, plated=False, seed=1),
     "ragged_33x9x17_plated": slab(33, 9, 17, plated=True, seed=2),
+    # tensor-map (TMA) stencil path, nx % 4 == 0, on grids that are not multiples of the
+    # 32 x 8 tile: the narrowest grid the path takes, partial tiles in x and y with zero-filled
+    # halos, and fewer planes than one CTA's ring of staged planes
+    "tma_4x4x10_plated": slab(4, 4, 10, plated=True, seed=4),
+    "tma_36x12x9_plated": slab(36, 12, 9, plated=True, seed=5),
+    "tma_40x3x21_no_plating": slab(40, 3, 21, plated=False, seed=6),
 }
 
 
