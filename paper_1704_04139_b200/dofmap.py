@@ -74,7 +74,7 @@ class Dofmap:
     # the device operator build_dofmap classified the geometry with; the first SystemOperator
     # built on this Dofmap takes it over (new parameters, same geometry) instead of
     # classifying the grid a second time
-    _nat: "NativeOperator | None" = field(default=None, repr=False, compare=False)
+    _nat: "NativeOperator | None" = field(default=None, init=False, repr=False, compare=False)
 
     def take_native(self) -> "NativeOperator | None":
         nat, self._nat = self._nat, None
