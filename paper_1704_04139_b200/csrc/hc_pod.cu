@@ -11,6 +11,7 @@
 // per k-step from 8 fragment loads).  Slices are reduced in a fixed order and the
 // triangle mirrored, so the result is deterministic and exactly symmetric.
 #include <algorithm>
+#include <cstdint>
 
 #include "hc_internal.cuh"
 
@@ -20,7 +21,9 @@ namespace {
 constexpr int BT = 64;      // tile of G
 constexpr int KC = 16;      // K chunk per stage (16: 55 KB of ring per CTA, 4 CTAs / 16 warps per SM)
 constexpr int ST = 3;       // pipeline stages
-constexpr int LD = KC + 2;  // padded row of a staged panel
+constexpr int LD = KC + 2;  // padded row of a staged panel, [col][k] layout (k contiguous in memory or generic strides)
+constexpr int LDI = BT + 4; // padded row of a staged panel, [k][col] layout (tile index contiguous in memory):
+                            // 16-byte copies of column pairs; LDI mod 16 == 4 keeps the fragment loads conflict-free
 constexpr int NT = 128;     // 4 warps: 2 x 2 sub-tiles of 32 x 32
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
@@ -33,6 +36,11 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 __device__ __forceinline__ void cp8(void* smem, const void* gmem, int src_bytes) {
   unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+// 16-byte async copy (two doubles); src_bytes 8 copies one and zero-fills the other, 0 zero-fills both
+__device__ __forceinline__ void cp16(void* smem, const void* gmem, int src_bytes) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -59,11 +67,19 @@ struct GemmDesc {
   long long ldc;
 };
 
+// AI / BJ: the tile index of A / B is the contiguous one in memory (stride 1, even k stride,
+// 16-byte aligned base): that panel is staged [k][col] with 16-byte copies of column pairs — a
+// thread keeps its column pair and walks k, so the copy loop is a pointer increment per copy
+// instead of the generic path's per-element index arithmetic (which issued more instructions
+// than the DMMA loop itself).
+constexpr int PANEL = ST * (BT * LD > KC * LDI ? BT * LD : KC * LDI);   // doubles per operand ring
+
+template <bool AI, bool BJ>
 __global__ void __launch_bounds__(NT) k_dgemm(GemmDesc D) {
   extern __shared__ __align__(16) double smem[];
-  double* As = smem;                        // [ST][BT][LD]
-  double* Bs = As + ST * BT * LD;           // [ST][BT][LD]
-  double* Ws = Bs + ST * BT * LD;           // [ST][KC]
+  double* As = smem;                        // [ST][BT][LD] or [ST][KC][LDI]
+  double* Bs = As + PANEL;
+  double* Ws = Bs + PANEL;                  // [ST][KC]
   int ti, tj;
   if (D.sym) {   // upper-triangle tile pair from the linear block index
     int p = blockIdx.x;
@@ -82,23 +98,42 @@ __global__ void __launch_bounds__(NT) k_dgemm(GemmDesc D) {
   const int g = lane >> 2, tq = lane & 3;
   // staging order: walk whichever index is contiguous in memory
   const bool a_icont = D.sa_i == 1, b_jcont = D.sb_j == 1;
+  // [k][col] staging of a tile-contiguous panel: thread = (column pair, k mod 4)
+  auto stage_pairs = [&](const double* base, long long sk, int t0, int lim, double* dst, long long k0, int s) {
+    const int cp = tid & 31, kq = tid >> 5;
+    const int gt = t0 + 2 * cp;
+    const int full = gt + 1 < lim ? 16 : (gt < lim ? 8 : 0);
+    const double* src = base + (k0 + kq) * sk + gt;
+    double* d = dst + (s * KC + kq) * LDI + 2 * cp;
+#pragma unroll
+    for (int it = 0; it < KC / 4; ++it) {
+      const int bytes = k0 + kq + 4 * it < k_end ? full : 0;
+      cp16(d, bytes ? src : base, bytes);
+      src += 4 * sk;
+      d += 4 * LDI;
+    }
+  };
   auto stage = [&](long long k0, int s) {
-    for (int e = tid; e < BT * KC; e += NT) {
-      {
-        const int col = a_icont ? e % BT : e / KC, kk = a_icont ? e / BT : e - (e / KC) * KC;
-        const long long k = k0 + kk;
-        const int gi = i0 + col;
-        const bool ok = k < k_end && gi < D.M;
-        const double* src = D.A + (ok ? k * D.sa_k + (long long)gi * D.sa_i : 0);
-        cp8(As + (s * BT + col) * LD + kk, src, ok ? 8 : 0);
-      }
-      {
-        const int col = b_jcont ? e % BT : e / KC, kk = b_jcont ? e / BT : e - (e / KC) * KC;
-        const long long k = k0 + kk;
-        const int gj = j0 + col;
-        const bool ok = k < k_end && gj < D.N;
-        const double* src = D.B + (ok ? k * D.sb_k + (long long)gj * D.sb_j : 0);
-        cp8(Bs + (s * BT + col) * LD + kk, src, ok ? 8 : 0);
+    if constexpr (AI) stage_pairs(D.A, D.sa_k, i0, D.M, As, k0, s);
+    if constexpr (BJ) stage_pairs(D.B, D.sb_k, j0, D.N, Bs, k0, s);
+    if constexpr (!AI || !BJ) {
+      for (int e = tid; e < BT * KC; e += NT) {
+        if constexpr (!AI) {
+          const int col = a_icont ? e % BT : e / KC, kk = a_icont ? e / BT : e - (e / KC) * KC;
+          const long long k = k0 + kk;
+          const int gi = i0 + col;
+          const bool ok = k < k_end && gi < D.M;
+          const double* src = D.A + (ok ? k * D.sa_k + (long long)gi * D.sa_i : 0);
+          cp8(As + (s * BT + col) * LD + kk, src, ok ? 8 : 0);
+        }
+        if constexpr (!BJ) {
+          const int col = b_jcont ? e % BT : e / KC, kk = b_jcont ? e / BT : e - (e / KC) * KC;
+          const long long k = k0 + kk;
+          const int gj = j0 + col;
+          const bool ok = k < k_end && gj < D.N;
+          const double* src = D.B + (ok ? k * D.sb_k + (long long)gj * D.sb_j : 0);
+          cp8(Bs + (s * BT + col) * LD + kk, src, ok ? 8 : 0);
+        }
       }
     }
     if (tid < KC) {
@@ -126,17 +161,19 @@ __global__ void __launch_bounds__(NT) k_dgemm(GemmDesc D) {
     if (cn < nchunks) stage(k_begin + cn * KC, (int)(cn % ST));
     cp_commit();
     const int s = (int)(c % ST);
-    const double* A = As + s * BT * LD;
-    const double* B = Bs + s * BT * LD;
+    const double* A = As + s * (AI ? KC * LDI : BT * LD);
+    const double* B = Bs + s * (BJ ? KC * LDI : BT * LD);
     const double* W = Ws + s * KC;
 #pragma unroll
     for (int ks = 0; ks < KC; ks += 4) {
       const double wk = W[ks + tq];
       double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) af[a] = A[(wr * 32 + a * 8 + g) * LD + ks + tq] * wk;
+      for (int a = 0; a < 4; ++a)
+        af[a] = (AI ? A[(ks + tq) * LDI + wr * 32 + a * 8 + g] : A[(wr * 32 + a * 8 + g) * LD + ks + tq]) * wk;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = B[(wc * 32 + b * 8 + g) * LD + ks + tq];
+      for (int b = 0; b < 4; ++b)
+        bf[b] = BJ ? B[(ks + tq) * LDI + wc * 32 + b * 8 + g] : B[(wc * 32 + b * 8 + g) * LD + ks + tq];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -202,11 +239,19 @@ void dgemm_tc(const double* A, long long sa_k, long long sa_i, const double* B, 
   int sms = 148, dev = 0;
   HC_CUDA(cudaGetDevice(&dev));
   HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const size_t smem = (size_t)(2 * ST * BT * LD + ST * KC) * sizeof(double);
-  static int per_sm = 0;
+  const size_t smem = (size_t)(2 * PANEL + ST * KC) * sizeof(double);
+  // tile-contiguous operands with 16-byte aligned column pairs take the [k][col] staging
+  auto pairable = [](const double* p, long long s_k, long long s_t) {
+    return s_t == 1 && s_k % 2 == 0 && reinterpret_cast<uintptr_t>(p) % 16 == 0;
+  };
+  const bool ai = pairable(A, sa_k, sa_i), bj = pairable(B, sb_k, sb_j);
+  void (*kern)(GemmDesc) = ai ? (bj ? k_dgemm<true, true> : k_dgemm<true, false>)
+                              : (bj ? k_dgemm<false, true> : k_dgemm<false, false>);
+  static int per_sm_v[4] = {0, 0, 0, 0};
+  int& per_sm = per_sm_v[(ai ? 2 : 0) | (bj ? 1 : 0)];
   if (!per_sm) {
-    HC_CUDA(cudaFuncSetAttribute(k_dgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dgemm, NT, smem));
+    HC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     per_sm = std::max(per_sm, 1);
   }
   // split K only when the tiles alone cannot fill the GPU
@@ -223,7 +268,7 @@ void dgemm_tc(const double* A, long long sa_k, long long sa_i, const double* B, 
   }
   if (pairs > 0x7fffffffLL) throw Error(HC_ERR_ARGUMENT, "contraction too large");
   // nz == 1 with sym still goes through the partial buffer (the mirror pass)
-  k_dgemm<<<dim3((unsigned)pairs, nz), NT, smem, s>>>(D);
+  kern<<<dim3((unsigned)pairs, nz), NT, smem, s>>>(D);
   HC_COUNT();
   HC_CHECK_LAUNCH();
   if (part.p) {
