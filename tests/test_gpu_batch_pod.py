@@ -35,8 +35,8 @@ def test_pod_gram_matches_fp64_reference():
     import torch
     from paper_1704_04139_b200 import pod
     rng = np.random.default_rng(3)
-    # 7 / 130 snapshots take 64 x 64 tiles, 80 / 153 / 400 the 80 x 80 ones (less padding); odd
-    # counts exercise the half-filled 16-byte column pairs at the edge of a panel
+    # partial edge tiles (7, 130, 80, 153, 400 snapshots on 64 x 64 tiles); odd counts exercise
+    # the half-filled 16-byte column pairs at the edge of a staged panel
     for n_dof, n_snap in ((1000, 7), (50_000, 130), (3_000, 80), (2_500, 153), (4_000, 400)):
         S = rng.standard_normal((n_dof, n_snap))
         w = rng.uniform(0.5, 1.5, n_dof)
@@ -56,7 +56,7 @@ def test_pod_basis_orthonormal_and_singular_values():
 
 
 @pytest.mark.parametrize("shape", [(2_000, 37, 5), (70_000, 130, 61), (9, 200_000, 66), (150, 3, 1),
-                                   (80, 1_000, 80), (5_000, 33, 75)])   # the last two take 80 x 80 tiles
+                                   (80, 1_000, 80), (5_000, 33, 75)])
 def test_tc_matmul_strided_operands_match_fp64(shape):
     """The reduced-basis stage's DMMA contractions (hc_dgemm): tall x small projections,
     long-inner-dimension products B^T W, transposed / sliced operands in place."""
