@@ -311,6 +311,94 @@ __global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const CV*
   if (lane == 0) x[row] = (CV)s;
 }
 
+// ---- coarsest levels above HC_COARSE_MAX rows: blocked Gauss-Jordan on [A | I] in global memory.
+// Pivot blocks of GJ_B rows are inverted by k_dense_inverse (partial pivoting inside the block; the
+// Galerkin operators are diagonally dominant enough that blocks need no pivoting between them);
+// every block step is five launches whatever the size, so the whole inverse stays a short kernel
+// chain that a graph capture can hold.
+constexpr int GJ_B = 64;
+__global__ void k_gj_init(int n, const double* __restrict__ A, double* __restrict__ G) {
+  pdl_wait();
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)n * 2 * n) return;
+  const int i = (int)(e / (2 * n)), j = (int)(e % (2 * n));
+  G[e] = j < n ? A[(long long)i * n + j] : (j - n == i ? 1.0 : 0.0);
+}
+// the column panel k0 .. k0 + bw of G (all rows) into C [n][bw], its diagonal block also into P [bw][bw]
+__global__ void k_gj_col(int n, int k0, int bw, const double* __restrict__ G, double* __restrict__ C,
+                         double* __restrict__ P) {
+  pdl_wait();
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)n * bw) return;
+  const int i = (int)(e / bw), j = (int)(e % bw);
+  const double v = G[(long long)i * 2 * n + k0 + j];
+  C[e] = v;
+  if (i >= k0 && i < k0 + bw) P[(long long)(i - k0) * bw + j] = v;
+}
+// Out[i][j] = beta Out[i][j] + alpha sum_k A[i][k] B[k][j] for rows i < m outside [skip0, skip0 + skipn),
+// columns j0 <= j < j1 (A [m][kd], B and Out with leading dimension ld): 64 x 64 tiles, 4 x 4 per thread
+__global__ void __launch_bounds__(256) k_gj_gemm(int m, int kd, int j0, int j1, int ld, double alpha,
+                                                const double* __restrict__ A, const double* __restrict__ B,
+                                                double beta, double* __restrict__ Out, int skip0, int skipn) {
+  pdl_wait();
+  constexpr int KC = 32;   // k chunk staged in shared memory
+  __shared__ double As[KC][64 + 1], Bs[KC][64];
+  const int i0 = blockIdx.y * 64, c0 = j0 + blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4] = {};
+  for (int kc = 0; kc < kd; kc += KC) {
+    const int kn = min(KC, kd - kc);
+    for (int e = threadIdx.x; e < 64 * kn; e += 256) {
+      const int r = e / kn, k = e - r * kn;
+      As[k][r] = i0 + r < m ? A[(long long)(i0 + r) * kd + kc + k] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kn * 64; e += 256) {
+      const int k = e >> 6, c = e & 63;
+      Bs[k][c] = c0 + c < j1 ? B[(long long)(kc + k) * ld + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < kn; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[q] = As[k][ty * 4 + q], b[q] = Bs[k][tx * 4 + q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[q][r] = fma(a[q], b[r], acc[q][r]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ty * 4 + q;
+    if (i >= m || (i >= skip0 && i < skip0 + skipn)) continue;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int j = c0 + tx * 4 + r;
+      if (j < j1) {
+        double* o = Out + (long long)i * ld + j;
+        *o = (beta != 0.0 ? beta * *o : 0.0) + alpha * acc[q][r];
+      }
+    }
+  }
+}
+// rows k0 .. k0 + bw of G, columns j0 .. j1, from R (same leading dimension)
+__global__ void k_gj_row(int n, int k0, int bw, int j0, int j1, const double* __restrict__ R, double* __restrict__ G) {
+  pdl_wait();
+  const int w = j1 - j0;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)bw * w) return;
+  const int i = (int)(e / w), j = j0 + (int)(e % w);
+  G[(long long)(k0 + i) * 2 * n + j] = R[(long long)i * 2 * n + j];
+}
+__global__ void k_gj_out(int n, const double* __restrict__ G, double* __restrict__ Ainv) {
+  pdl_wait();
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)n * n) return;
+  const int i = (int)(e / n), j = (int)(e % n);
+  Ainv[e] = G[(long long)i * 2 * n + n + j];
+}
+
 // ---- cycle kernels ------------------------------------------------------------
 
 __global__ void k_csr_smooth0(int n, double w, const CV* __restrict__ dinv,
@@ -850,6 +938,13 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
   B.field = field;
   B.alpha = cfg.alpha;
   B.levels.clear();
+  // rows of the dense coarsest level: cfg.coarse_max if set, else by grid size — its inverse costs
+  // O(n^3) per hierarchy refresh, which small cells amortise over cheap steps (measured: batched
+  // 48 x 48 x 96 cells 269 cell-steps/s at 1600 rows against 253 at 4000; medium and large cells
+  // 13.7 / 59.7 ms per step at 4000 against 14.0 / 61.3 at 1600 / 1200)
+  const int coarse_rows = cfg.coarse_max > 0
+                              ? cfg.coarse_max
+                              : (int)std::min<long long>(4000, std::max<long long>(1600, nvox / 128));
   auto in_field = [&](long long v) {
     uint8_t a = lab[v];
     if (field == 0) return a == GR || a == EL;
@@ -916,7 +1011,10 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     int active = 0;
     for (int i = 0; i < n; ++i) active += A.rp[i + 1] > A.rp[i];
     bool can = sx > 1 || sy > 1 || sz > 1;
-    if (active <= cfg.coarse_max || !can) break;
+    // stop at the first aggregated level small enough for the dense inverse (the voxel-indexed fine
+    // level only when it is tiny: a one-level hierarchy is a plain Jacobi sweep)
+    const int stop = level >= 1 ? coarse_rows : std::min(coarse_rows, 128);
+    if ((active <= stop && n <= HC_COARSE_CAP) || !can) break;
     // tentative aggregation: connected components (in the strong same-phase graph G)
     // of the unknowns sharing a (2x2x2 block, phase) key
     const int cf = level == 0 ? 2 : cfg.coarsen;   // block growth factor of this transfer
@@ -1083,11 +1181,17 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     L.x.alloc(m); L.x2.alloc(m); L.b.alloc(m); L.res.alloc(m); L.acc.alloc(m); L.dinvc.alloc(m);
   }
   int nc = B.levels.back().n;
-  if (nc > HC_COARSE_MAX)
+  if (nc > HC_COARSE_CAP)
     throw Error(HC_ERR_CUDA, "aggregation hierarchy left " + std::to_string(nc) +
-                                 " coarsest unknowns (limit " + std::to_string(HC_COARSE_MAX) + ")");
+                                 " coarsest unknowns (limit " + std::to_string(HC_COARSE_CAP) + ")");
   B.dense.alloc((size_t)std::max(nc, 1) * std::max(nc, 1));
   B.dense_inv.alloc((size_t)std::max(nc, 1) * std::max(nc, 1));
+  if (nc > HC_COARSE_MAX) {   // blocked Gauss-Jordan work space: [A | I], a column panel, a row panel, a pivot block
+    B.gj_aug.alloc((size_t)nc * 2 * nc);
+    B.gj_col.alloc((size_t)nc * GJ_B);
+    B.gj_row.alloc((size_t)GJ_B * 2 * nc);
+    B.gj_piv.alloc((size_t)2 * GJ_B * GJ_B);
+  }
   // cluster-fused tail of the cycle: the deepest run of CSR levels that are all small
   // (and plain V-cycle levels), if it spans at least two levels
   const int nl = (int)B.levels.size();
@@ -1351,7 +1455,30 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
                                    (int)((size_t)HC_COARSE_MAX * HC_COARSE_MAX * 8 + HC_COARSE_MAX * 4)));
       attr = true;
     }
-    launch(k_dense_inverse, 1, 256, smem, s, C.n, B.dense.p, B.dense_inv.p); HC_COUNT();
+    if (C.n <= HC_COARSE_MAX) {
+      launch(k_dense_inverse, 1, 256, smem, s, C.n, B.dense.p, B.dense_inv.p); HC_COUNT();
+    } else {
+      const int n = C.n;
+      double* G = B.gj_aug.p;
+      double* piv = B.gj_piv.p;
+      double* pinv = piv + GJ_B * GJ_B;
+      launch(k_gj_init, nblk(2LL * n * n), TPB, 0, s, n, (const double*)B.dense.p, G); HC_COUNT();
+      for (int k0 = 0; k0 < n; k0 += GJ_B) {
+        const int bw = std::min(GJ_B, n - k0);
+        // columns that hold anything but the untouched parts of [A | I] at this step
+        const int j0 = k0, j1 = n + k0 + bw;
+        launch(k_gj_col, nblk((long long)n * bw), TPB, 0, s, n, k0, bw, (const double*)G, B.gj_col.p, piv); HC_COUNT();
+        launch(k_dense_inverse, 1, 256, (size_t)bw * bw * sizeof(double) + (size_t)bw * sizeof(int), s, bw,
+               (const double*)piv, pinv); HC_COUNT();
+        // row panel R = D G[k rows]; every other row i -= G[i][k cols] R; then the panel itself
+        launch(k_gj_gemm, dim3((j1 - j0 + 63) / 64, 1), 256, 0, s, bw, bw, j0, j1, 2 * n, 1.0, (const double*)pinv,
+               (const double*)(G + (long long)k0 * 2 * n), 0.0, B.gj_row.p, 0, 0); HC_COUNT();
+        launch(k_gj_gemm, dim3((j1 - j0 + 63) / 64, (n + 63) / 64), 256, 0, s, n, bw, j0, j1, 2 * n, -1.0,
+               (const double*)B.gj_col.p, (const double*)B.gj_row.p, 1.0, G, k0, bw); HC_COUNT();
+        launch(k_gj_row, nblk((long long)bw * (j1 - j0)), TPB, 0, s, n, k0, bw, j0, j1, (const double*)B.gj_row.p, G); HC_COUNT();
+      }
+      launch(k_gj_out, nblk((long long)n * n), TPB, 0, s, n, (const double*)G, B.dense_inv.p); HC_COUNT();
+    }
     HC_CHECK_LAUNCH();
   }
 }

@@ -3,7 +3,8 @@
 
 #include "hc_internal.cuh"
 
-#define HC_COARSE_MAX 160
+#define HC_COARSE_MAX 160    /* largest coarsest level inverted in shared memory (one CTA) */
+#define HC_COARSE_CAP 4096   /* largest dense coarsest level at all (blocked Gauss-Jordan in global memory) */
 
 namespace hc {
 
@@ -88,6 +89,7 @@ struct AmgBlock {
   std::vector<AmgLevel> levels;   // levels[0] is the fine grid
   bool sp_done = false;           // the sparsified sweep patterns were decided (first numeric setup)
   DBuf<double> dense, dense_inv;  // coarsest matrix and its inverse
+  DBuf<double> gj_aug, gj_col, gj_row, gj_piv;   // blocked Gauss-Jordan work space (coarsest levels above HC_COARSE_MAX rows)
   int fuse_from = -1;             // levels >= fuse_from run as one cluster kernel (-1: none)
   DBuf<CoarseLev> clev;           // their device views
 };
@@ -107,7 +109,13 @@ struct Amg {
   bool use_graphs = true;
   std::vector<AmgGraph> graphs;
   AmgBlock blk[2];
-  int coarse_max = 128;       // <= HC_COARSE_MAX (the coarsest inverse lives in shared memory)
+  // coarsening stops at the first level with at most this many rows; that level is inverted densely
+  // (<= HC_COARSE_MAX rows in shared memory, up to HC_COARSE_CAP by blocked Gauss-Jordan in global
+  // memory) and every coarse solve is one dense mat-vec.  Measured against 128: the exact solve on a
+  // few thousand rows replaces the 2-3 smallest levels' launch chains AND converges faster — tiny cell
+  // 6.34 -> 3.3 ms per step (37.7 -> 15.6 BiCGStab iterations), medium 18.0 -> 13.7 (39.1 -> 32.5),
+  // large 64.1 -> 59.8 (39.8 -> 36.9), batched 200 -> 269 cell-steps/s (48.5 -> 34.5)
+  int coarse_max = 0;         // 0: by grid size, clamp(n_vox / 128, 1600, 4000) (HC_AMG_COARSE_MAX)
   int nu = 1;                // smoothing sweeps on the fine level (measured: 1 beats 2 on the medium cell)
   int nu_c = 2;              // smoothing sweeps on the CSR levels
   int sa_levels_c = 0;       // smoothed transfers of the c block (plain aggregation suffices)
