@@ -312,8 +312,8 @@ __global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const CV*
 }
 
 // ---- coarsest levels above HC_COARSE_MAX rows: blocked Gauss-Jordan on [A | I] in global memory.
-// Pivot blocks of GJ_B rows are inverted by k_dense_inverse (partial pivoting inside the block; the
-// Galerkin operators are diagonally dominant enough that blocks need no pivoting between them);
+// Pivot blocks of GJ_B rows are inverted in shared memory (k_gj_pivot_inverse); the Galerkin operators
+// are diagonally dominant enough to need no pivoting;
 // every block step is five launches whatever the size, so the whole inverse stays a short kernel
 // chain that a graph capture can hold.
 constexpr int GJ_B = 64;
@@ -335,42 +335,81 @@ __global__ void k_gj_col(int n, int k0, int bw, const double* __restrict__ G, do
   C[e] = v;
   if (i >= k0 && i < k0 + bw) P[(long long)(i - k0) * bw + j] = v;
 }
+// inverse of one pivot block (bw <= GJ_B) in shared memory: in-place Gauss-Jordan by all 256 threads,
+// two barriers per pivot (the one-CTA LU of k_dense_inverse spent ~250 us per block, most of the
+// whole inverse).  No pivoting: the Galerkin operators' diagonal blocks are diagonally dominant; a
+// zero pivot (a row without entries) leaves a zero row and column, like k_dense_inverse.
+__global__ void __launch_bounds__(256) k_gj_pivot_inverse(int bw, const double* __restrict__ P, double* __restrict__ D) {
+  pdl_wait();
+  __shared__ double M[GJ_B][GJ_B + 1], colk[GJ_B], rowk[GJ_B];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < bw * bw; e += 256) M[e / bw][e % bw] = P[e];
+  for (int k = 0; k < bw; ++k) {
+    __syncthreads();
+    const double d = M[k][k];
+    const double p = d != 0.0 ? 1.0 / d : 0.0;
+    if (tid < bw) {
+      colk[tid] = M[tid][k];
+      rowk[tid] = (tid == k ? 1.0 : M[k][tid]) * p;
+    }
+    __syncthreads();
+    for (int e = tid; e < bw * bw; e += 256) {
+      const int i = e / bw, j = e - i * bw;
+      M[i][j] = i == k ? rowk[j] : (j == k ? 0.0 : M[i][j]) - colk[i] * rowk[j];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < bw * bw; e += 256) D[e] = M[e / bw][e % bw];
+}
 // Out[i][j] = beta Out[i][j] + alpha sum_k A[i][k] B[k][j] for rows i < m outside [skip0, skip0 + skipn),
-// columns j0 <= j < j1 (A [m][kd], B and Out with leading dimension ld): 64 x 64 tiles, 4 x 4 per thread
+// columns j0 <= j < j1 (A [m][kd], B and Out with leading dimension ld): 128 x 64 tiles, 8 x 4 per
+// thread, operands staged per 16-deep k chunk and read back as double2 (the 16 threads of a row
+// group share their A values: broadcast loads)
+constexpr int GJ_TM = 128, GJ_TN = 64, GJ_KC = 16;
 __global__ void __launch_bounds__(256) k_gj_gemm(int m, int kd, int j0, int j1, int ld, double alpha,
                                                 const double* __restrict__ A, const double* __restrict__ B,
                                                 double beta, double* __restrict__ Out, int skip0, int skipn) {
   pdl_wait();
-  constexpr int KC = 32;   // k chunk staged in shared memory
-  __shared__ double As[KC][64 + 1], Bs[KC][64];
-  const int i0 = blockIdx.y * 64, c0 = j0 + blockIdx.x * 64;
+  __shared__ __align__(16) double As[GJ_KC][GJ_TM + 2], Bs[GJ_KC][GJ_TN];
+  const int i0 = blockIdx.y * GJ_TM, c0 = j0 + blockIdx.x * GJ_TN;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4] = {};
-  for (int kc = 0; kc < kd; kc += KC) {
-    const int kn = min(KC, kd - kc);
-    for (int e = threadIdx.x; e < 64 * kn; e += 256) {
-      const int r = e / kn, k = e - r * kn;
-      As[k][r] = i0 + r < m ? A[(long long)(i0 + r) * kd + kc + k] : 0.0;
+  double acc[8][4] = {};
+  for (int kc = 0; kc < kd; kc += GJ_KC) {
+    const int kn = min(GJ_KC, kd - kc);
+    for (int e = threadIdx.x; e < GJ_TM * GJ_KC; e += 256) {   // A tile: k fastest in memory
+      const int r = e / GJ_KC, k = e % GJ_KC;
+      As[k][r] = (k < kn && i0 + r < m) ? A[(long long)(i0 + r) * kd + kc + k] : 0.0;
     }
-    for (int e = threadIdx.x; e < kn * 64; e += 256) {
-      const int k = e >> 6, c = e & 63;
-      Bs[k][c] = c0 + c < j1 ? B[(long long)(kc + k) * ld + c0 + c] : 0.0;
+    for (int e = threadIdx.x; e < GJ_KC * GJ_TN; e += 256) {
+      const int k = e / GJ_TN, c = e % GJ_TN;
+      Bs[k][c] = (k < kn && c0 + c < j1) ? B[(long long)(kc + k) * ld + c0 + c] : 0.0;
     }
     __syncthreads();
-    for (int k = 0; k < kn; ++k) {
-      double a[4], b[4];
+#pragma unroll 4
+    for (int k = 0; k < GJ_KC; ++k) {
+      double a[8], b[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) a[q] = As[k][ty * 4 + q], b[q] = Bs[k][tx * 4 + q];
+      for (int q = 0; q < 4; ++q) {
+        const double2 t = *reinterpret_cast<const double2*>(&As[k][ty * 8 + 2 * q]);
+        a[2 * q] = t.x;
+        a[2 * q + 1] = t.y;
+      }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 2; ++q) {
+        const double2 t = *reinterpret_cast<const double2*>(&Bs[k][tx * 4 + 2 * q]);
+        b[2 * q] = t.x;
+        b[2 * q + 1] = t.y;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc[q][r] = fma(a[q], b[r], acc[q][r]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = i0 + ty * 4 + q;
+  for (int q = 0; q < 8; ++q) {
+    const int i = i0 + ty * 8 + q;
     if (i >= m || (i >= skip0 && i < skip0 + skipn)) continue;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -1468,12 +1507,11 @@ void amg_update(Operator& op, double inv_dt, int blocks, cudaStream_t s) {
         // columns that hold anything but the untouched parts of [A | I] at this step
         const int j0 = k0, j1 = n + k0 + bw;
         launch(k_gj_col, nblk((long long)n * bw), TPB, 0, s, n, k0, bw, (const double*)G, B.gj_col.p, piv); HC_COUNT();
-        launch(k_dense_inverse, 1, 256, (size_t)bw * bw * sizeof(double) + (size_t)bw * sizeof(int), s, bw,
-               (const double*)piv, pinv); HC_COUNT();
+        launch(k_gj_pivot_inverse, 1, 256, 0, s, bw, (const double*)piv, pinv); HC_COUNT();
         // row panel R = D G[k rows]; every other row i -= G[i][k cols] R; then the panel itself
-        launch(k_gj_gemm, dim3((j1 - j0 + 63) / 64, 1), 256, 0, s, bw, bw, j0, j1, 2 * n, 1.0, (const double*)pinv,
+        launch(k_gj_gemm, dim3((j1 - j0 + GJ_TN - 1) / GJ_TN, 1), 256, 0, s, bw, bw, j0, j1, 2 * n, 1.0, (const double*)pinv,
                (const double*)(G + (long long)k0 * 2 * n), 0.0, B.gj_row.p, 0, 0); HC_COUNT();
-        launch(k_gj_gemm, dim3((j1 - j0 + 63) / 64, (n + 63) / 64), 256, 0, s, n, bw, j0, j1, 2 * n, -1.0,
+        launch(k_gj_gemm, dim3((j1 - j0 + GJ_TN - 1) / GJ_TN, (n + GJ_TM - 1) / GJ_TM), 256, 0, s, n, bw, j0, j1, 2 * n, -1.0,
                (const double*)B.gj_col.p, (const double*)B.gj_row.p, 1.0, G, k0, bw); HC_COUNT();
         launch(k_gj_row, nblk((long long)bw * (j1 - j0)), TPB, 0, s, n, k0, bw, j0, j1, (const double*)B.gj_row.p, G); HC_COUNT();
       }

@@ -260,10 +260,14 @@ void dgemm_tc(const double* A, long long sa_k, long long sa_i, const double* B, 
   k_per = std::max<long long>(KC, ((k_per + KC - 1) / KC) * KC);
   const int nz = (int)std::max<long long>(1, (K + k_per - 1) / k_per);
   GemmDesc D{A, sa_k, sa_i, B, sb_k, sb_j, w, K, M, N, tiles_i, tiles_j, sym ? 1 : 0, k_per, C, ldc};
-  DBuf<double> part;
-  if (nz > 1 || sym) {
-    part.alloc((size_t)nz * M * N);
-    if (sym) HC_CUDA(cudaMemsetAsync(part.p, 0, part.n * sizeof(double), s));
+  // split-K partials: a per-thread buffer that only grows (a cudaMalloc / cudaFree pair per call
+  // cost up to 10 ms of the 20 ms Gram when the allocator had to map fresh memory); this function
+  // synchronises the stream before it returns whenever the buffer was used, so reuse is safe
+  static thread_local DBuf<double> part;
+  const size_t need = (nz > 1 || sym) ? (size_t)nz * M * N : 0;
+  if (need) {
+    if (part.n < need) part.alloc(need);
+    if (sym) HC_CUDA(cudaMemsetAsync(part.p, 0, need * sizeof(double), s));
     D.out = part.p;
   }
   if (pairs > 0x7fffffffLL) throw Error(HC_ERR_ARGUMENT, "contraction too large");
@@ -271,11 +275,11 @@ void dgemm_tc(const double* A, long long sa_k, long long sa_i, const double* B, 
   kern<<<dim3((unsigned)pairs, nz), NT, smem, s>>>(D);
   HC_COUNT();
   HC_CHECK_LAUNCH();
-  if (part.p) {
+  if (need) {
     const long long mn = (long long)M * N;
     k_reduce_parts<<<(int)((mn + 255) / 256), 256, 0, s>>>(M, N, nz, sym ? 1 : 0, part.p, C, ldc); HC_COUNT();
     HC_CHECK_LAUNCH();
-    HC_CUDA(cudaStreamSynchronize(s));   // the partial buffer is freed on return
+    HC_CUDA(cudaStreamSynchronize(s));   // the partial buffer is reused by the next call
   }
 }
 
