@@ -1122,7 +1122,8 @@ static void build_block(const Operator& op, const std::vector<uint8_t>& lab, int
     }
     upload(L.parent, parent);
     // prolongator pattern: parent(i) plus (smoothed) the parents of row i's columns
-    const bool smooth = level < (field == 0 ? cfg.sa_levels_c : cfg.sa_levels) ||
+    const int sa_c = cfg.sa_levels_c >= 0 ? cfg.sa_levels_c : (nvox <= 2000000LL ? 1 : 0);
+    const bool smooth = level < (field == 0 ? sa_c : cfg.sa_levels) ||
                         (field != 0 && (cfg.sa_any ? level >= cfg.sa_levels : level == cfg.sa_levels) &&
                          n >= cfg.sa_rows_min && n <= cfg.sa_rows);
     // filtered smoothing: the prolongator reaches only the aggregates of strong (same-phase

@@ -118,7 +118,11 @@ struct Amg {
   int coarse_max = 0;         // 0: by grid size, clamp(n_vox / 128, 1600, 4000) (HC_AMG_COARSE_MAX)
   int nu = 1;                // smoothing sweeps on the fine level (measured: 1 beats 2 on the medium cell)
   int nu_c = 2;              // smoothing sweeps on the CSR levels
-  int sa_levels_c = 0;       // smoothed transfers of the c block (plain aggregation suffices)
+  // smoothed transfers of the c block: -1 = by grid size, the first transfer on grids of at most 2 M
+  // voxels (on top of the dense coarsest level: medium cell 13.6 -> 11.9 ms per step, 32.5 -> 27.1
+  // iterations; tiny 2.90 -> 2.59 ms; batched 265 -> 315 cell-steps/s; the large cell's denser c level 1
+  // costs more than its 36.4 -> 33.8 iterations save: 59.5 -> 62.5 ms, so plain aggregation there)
+  int sa_levels_c = -1;
   double omega = 0.9;        // Jacobi smoothing weight
   // per-sweep weights (default omega): CSR-level zero-guess pre-sweep, first / second post-sweep;
   // fine-level pre (zero-guess) and post sweeps
